@@ -1,0 +1,126 @@
+/*
+ * cwgpu.h -- C ABI of the B200-native constant-weight PIR server answer.
+ *
+ * Drop-in boundary for the reference's server answer
+ *   std::vector<CipherValue> process_query(const HeBackend&, const PackedQuery&,
+ *                                          const PirDatabase&)
+ *   (/root/reference/proj/core/include/cwpir/pir.hpp:114-117, pir.cpp:337-347)
+ * plus the stage entry points its tests exercise.  Plain pointers and sizes only;
+ * no exceptions cross this boundary: every call returns CWG_OK (0) or a negative
+ * status, and cwg_last_error() returns the thread's last message, worded like the
+ * reference's exceptions (he_error / std::invalid_argument, he.hpp:16-18).
+ *
+ * Array layouts (little-endian u64, canonical residues):
+ *   ciphertext      [comps][L][N]       coefficient form          (he.hpp:56-65)
+ *   key-switch key  [D][2][L][N]        rows[d][k][i], reference NTT form (bfv.hpp:37-40,
+ *                                       bfv.cpp:394-402)
+ *   galois keys     [n_galois][Dg][2][L][N]  for exponents galois_g[a]
+ *   query           [h][2][L][N]        PackedQuery::cts (expansion.hpp:21-25)
+ *   positions       [n][k]              Codeword::positions(), ascending (cw_code.hpp:40)
+ *   payload         [n][s][N]           PirDatabase::chunk(i, j) coefficients < t
+ *   response        [s][2][L][N]
+ */
+#ifndef CWGPU_H
+#define CWGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CWG_OK 0
+#define CWG_EINVAL (-1) /* std::invalid_argument in the reference */
+#define CWG_EHE (-2)    /* he_error in the reference (e.g. missing Galois key) */
+#define CWG_ECUDA (-3)  /* CUDA runtime failure */
+#define CWG_ESTATE (-4) /* call out of order (e.g. answer before cwg_load_db) */
+
+#define CWG_OP_FOLKLORE 0u   /* product of the k selected bits (pir.cpp:287-302) */
+#define CWG_OP_ARITH 1u      /* prod_{i<k} (k' - i) / k!   (eq_circuits.cpp:105-127) */
+
+typedef struct cwg_ctx cwg_ctx;
+
+typedef struct cwg_info {
+    uint32_t N, L, J, Mm, Dr, Dg, q_bits, aux_bits;
+    uint64_t n_total, row_begin, n_local;
+    uint32_t s, k, m;
+} cwg_info;
+
+typedef struct cwg_timings {
+    double total_ms;   /* cwg_answer entry to return (includes H2D / D2H) */
+    double h2d_ms;     /* keys + query upload */
+    double expand_ms;  /* expand_query */
+    double select_ms;  /* aux lift + per-row equality (tensor, INTT, exact rounding, NTT) */
+    double mac_ms;     /* payload multiply-accumulate (DB streamed from HBM) */
+    double finish_ms;  /* accumulator reduce, INTT, basis conversion, relinearisation */
+    double d2h_ms;
+    uint64_t kernel_launches;
+    uint64_t exact_fallbacks; /* coefficients decided by the multiword slow path */
+} cwg_timings;
+
+const char* cwg_last_error(void);
+
+/* BfvContext equivalent (bfv.cpp:67-129) on one device.  q: L chain primes
+ * (each 2^32 < q_i < 2^60, NTT-friendly), t: plaintext prime, digit widths as
+ * HeParams::relin_digit_bits / galois_digit_bits (0 = one digit per prime). */
+cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint32_t relin_digit_bits,
+                    uint32_t galois_digit_bits, int device);
+void cwg_destroy(cwg_ctx* ctx);
+int cwg_get_info(const cwg_ctx* ctx, cwg_info* out);
+
+/* PirDatabase::setup + prepare_for (pir.cpp:214-264): rows [row_begin, row_begin+n_local)
+ * of an n_total-row database are made resident in NTT form on this device.
+ * positions: [n_local][k]; payload: [n_local][s][N] (NULL for a selection-only database,
+ * then s must be 0).  m: code length. */
+int cwg_load_db(cwg_ctx* ctx, uint64_t n_total, uint64_t row_begin, uint64_t n_local, uint32_t s,
+                uint32_t k, uint32_t m, const uint32_t* positions, const uint64_t* payload);
+
+/* Evaluation keys (EvalKeySet, bfv.hpp:42-51).  Kept resident until replaced. */
+int cwg_set_keys(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+                 const uint64_t* galois);
+
+/* process_query (pir.cpp:337-347): expand_query -> selection -> inner product ->
+ * finalize.  Keys may be passed per call (relin != NULL uploads them, as the
+ * reference server receives them with every query, server.cpp:63-68) or NULL to use
+ * the resident set.  query: [h][2][L][N] with compression c and code length m.
+ * out: [s][2][L][N].  t (optional) receives stage timings. */
+int cwg_answer(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+               const uint64_t* galois, uint32_t h, uint32_t c, uint32_t m, const uint64_t* query,
+               uint32_t op, uint64_t* out, cwg_timings* t);
+
+/* Row-sharded form (one process per GPU): the partial NTT-domain accumulators of this
+ * device's rows, written to DEVICE memory (cwg_partial_words() u64 words, each < 2^31,
+ * summable with a plain uint64 reduction), then cwg_finish on the root with the summed
+ * partials (device pointer) produces the response exactly as cwg_answer would. */
+uint64_t cwg_partial_words(const cwg_ctx* ctx);
+int cwg_answer_partial(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+                       const uint64_t* galois, uint32_t h, uint32_t c, uint32_t m, const uint64_t* query,
+                       uint32_t op, uint64_t* dev_partial, cwg_timings* t);
+int cwg_finish(cwg_ctx* ctx, const uint64_t* dev_partial_sum, uint32_t op, uint64_t* out, cwg_timings* t);
+
+/* compute_selection_vector (pir.cpp:277-312) without a payload (config 2): sel is
+ * [n_local][3][L][N]; comps[r] receives 2 or 3 (a 2-component row leaves slot 2 zero). */
+int cwg_select(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+               const uint64_t* galois, uint32_t h, uint32_t c, uint32_t m, const uint64_t* query,
+               uint32_t op, uint64_t* sel, uint32_t* comps, cwg_timings* t);
+
+/* ---- stage entry points (the reference's unit-test surface) ---- */
+/* RingContext::ntt_forward/inverse (ring.cpp:78-144) on `count` polys of chain prime
+ * idx (chain=1) or of aux prime idx (chain=0; our internal basis). */
+int cwg_ntt(cwg_ctx* ctx, int chain, uint32_t idx, uint64_t* data, uint32_t count, int inverse);
+/* expand_query (expansion.cpp:67-83) with the resident keys: out [m][2][L][N]. */
+int cwg_expand(cwg_ctx* ctx, uint32_t h, uint32_t c, uint32_t m, const uint64_t* query, uint64_t* out);
+/* BfvBackend::mul_lazy (bfv.cpp:761-857) of count pairs of 2-comp ciphertexts: out [count][3][L][N]. */
+int cwg_mul_lazy(cwg_ctx* ctx, uint32_t count, const uint64_t* a, const uint64_t* b, uint64_t* out);
+/* BfvBackend::finalize / relinearize (bfv.cpp:859-875) with the resident relin key. */
+int cwg_relinearize(cwg_ctx* ctx, uint32_t count, const uint64_t* ct3, uint64_t* out2);
+/* BfvBackend::substitute (bfv.cpp:694-712) with the resident Galois key for g. */
+int cwg_substitute(cwg_ctx* ctx, uint32_t count, const uint64_t* ct, uint64_t g, uint64_t* out);
+
+/* Kernel launch counter (all launches by this library since cwg_create). */
+uint64_t cwg_kernel_launches(const cwg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CWGPU_H */

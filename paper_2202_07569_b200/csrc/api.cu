@@ -1,0 +1,1083 @@
+// Context, device tables, orchestration and the C ABI (include/cwgpu.h).
+//
+// Orchestration mirrors process_query (reference pir.cpp:337-347):
+//   expand_query (expansion.cpp:67-83)      -> expand()
+//   compute_selection_vector (pir.cpp:277)   -> select_tile() per row tile (sel never
+//                                               materialised beyond one tile)
+//   inner_product / weighted_sum             -> k_mac per tile into NTT-domain accumulators
+//   finalize (pir.cpp:345)                   -> finish()
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cwgpu.h"
+#include "kernels.cuh"
+#include "params.h"
+
+namespace cwgpu {
+
+struct he_err : std::runtime_error { using std::runtime_error::runtime_error; };
+struct cuda_err : std::runtime_error { using std::runtime_error::runtime_error; };
+struct state_err : std::runtime_error { using std::runtime_error::runtime_error; };
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) throw cuda_err(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void ensure(size_t b) {
+        if (b <= bytes && p) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        CK(cudaMalloc(&p, std::max<size_t>(b, 16)));
+        bytes = std::max<size_t>(b, 16);
+    }
+    template <class T>
+    T* get(size_t count) {
+        ensure(count * sizeof(T));
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* ptr() const { return static_cast<T*>(p); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    std::mutex mu;
+    ChainParams cp;
+    AuxBasis ab;
+    u64 aux_n = 0;
+    DevTab T{};
+    DevBuf tab;
+    unsigned long long* d_fb = nullptr;
+    // database
+    bool db_loaded = false;
+    u64 n_total = 0, row_begin = 0, n_local = 0;
+    u32 s = 0, k = 0, m = 0;
+    std::vector<u32> h_pos;
+    DevBuf pos_rows;  // [n_local][k]
+    DevBuf pos_cols;  // [k][n_local]
+    DevBuf db;        // [n_local][s][Mm][N] u32 NTT form (MAC basis)
+    std::vector<u64> h_payload;  // kept to rebuild the NTT form if the basis changes
+    // keys
+    bool have_keys = false;
+    DevBuf relin, galois;
+    std::vector<u64> galois_g;
+    // scratch
+    DevBuf query, exA, exB, digits, dntt, ks, prep, Dbuf, chain3, node2, acc_lo, acc_hi, partial, X, resp3,
+        out2, tmp_idx, lift_tmp;
+    u64 launches = 0;
+    cudaEvent_t ev[8];
+};
+
+thread_local std::string g_err;
+
+// ------------------------------------------------------------------ launches
+template <class K, class... A>
+static void launch(Ctx& c, K kern, size_t grid, unsigned block, size_t smem, A... args) {
+    if (grid == 0) return;
+    kern<<<(unsigned)grid, block, smem, c.st>>>(args...);
+    CK(cudaGetLastError());
+    ++c.launches;
+}
+
+static size_t blocks(size_t n, unsigned b) { return (n + b - 1) / b; }
+
+static unsigned ntt_block(u32 N) { return std::min<u32>(512, N / 2); }
+
+// ------------------------------------------------------------------ tables
+struct Blob {
+    std::vector<unsigned char> b;
+    template <class T>
+    size_t add(const std::vector<T>& v) {
+        size_t off = (b.size() + 255) & ~size_t(255);
+        b.resize(off + v.size() * sizeof(T) + 1);
+        if (!v.empty()) std::memcpy(b.data() + off, v.data(), v.size() * sizeof(T));
+        return off;
+    }
+};
+
+static u32 inv32_neg(u32 a) {  // -a^-1 mod 2^32
+    u32 x = a;
+    for (int i = 0; i < 5; ++i) x *= 2 - a * x;
+    return (u32)(0u - x);
+}
+
+static u32 shoup32h(u32 w, u32 p) { return (u32)(((u64)w << 32) / p); }
+static u64 shoup64h(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+
+static void build_tables(Ctx& c) {
+    const ChainParams& cp = c.cp;
+    const AuxBasis& ab = c.ab;
+    const u32 N = cp.N, L = cp.L, J = ab.J, Mm = ab.Mm;
+    Blob blob;
+    DevTab T{};
+    T.N = N;
+    T.logN = cp.logN;
+    T.L = L;
+    T.J = J;
+    T.Mm = Mm;
+    T.Dr = cp.Dr;
+    T.Dg = cp.Dg;
+    T.relin_bits = cp.relin_bits;
+    T.galois_bits = cp.galois_bits;
+    T.t = cp.t;
+    T.gbits = 6;
+    const Big& Q = cp.Q;
+    T.QW = (cp.q_bits + 31) / 32;
+    if (T.QW > (u32)kQW) throw std::invalid_argument("cwgpu: modulus too wide");
+    // chain
+    std::vector<u64> q(L), mu96(L), gh(L), gl(L), muq(L), muq_s(L), ninv(L), ninv_s(L), delta(L);
+    std::vector<u64> crp, crps, cirp, cirps;
+    std::vector<u32> qov;
+    Big dq = Q.div_u64(cp.t);
+    for (u32 i = 0; i < L; ++i) {
+        const u64 qi = cp.q[i];
+        q[i] = qi;
+        mu96[i] = (u64)(((u128)1 << 96) / qi);
+        const u128 G = (~(u128)0) / qi;
+        gh[i] = (u64)(G >> 64);
+        gl[i] = (u64)G;
+        Big ov = Q.div_u64(qi);
+        muq[i] = invmod64(ov.mod_u64(qi), qi);
+        muq_s[i] = shoup64h(muq[i], qi);
+        ninv[i] = invmod64(N % qi, qi);
+        ninv_s[i] = shoup64h(ninv[i], qi);
+        delta[i] = dq.mod_u64(qi);
+        NttTables nt = make_ntt_tables(N, qi, 64);
+        crp.insert(crp.end(), nt.rp.begin(), nt.rp.end());
+        crps.insert(crps.end(), nt.rps.begin(), nt.rps.end());
+        cirp.insert(cirp.end(), nt.irp.begin(), nt.irp.end());
+        cirps.insert(cirps.end(), nt.irps.begin(), nt.irps.end());
+        auto l = ov.limbs32(T.QW);
+        qov.insert(qov.end(), l.begin(), l.end());
+    }
+    std::vector<u32> qw = Q.limbs32(T.QW);
+    // aux
+    std::vector<u32> a(J), apinv(J), a2_64(J), ninvA(J), ninvA_s(J), ninvRA(J), ninvRA_s(J);
+    std::vector<u64> abar(J), aF(J);
+    std::vector<u32> arp, arps, airp, airps;
+    Big A(1);
+    for (u32 j = 0; j < J; ++j) A = A.mul_u64(ab.a[j]);
+    Big M(1);
+    for (u32 k = 0; k < Mm; ++k) M = M.mul_u64(ab.a[k]);
+    T.AW = (A.bits() + 31) / 32;
+    if (T.AW > (u32)kAW) throw std::invalid_argument("cwgpu: aux basis too wide");
+    std::vector<u32> chat(J), chat_s(J), frac96(3 * J), Imod((size_t)J * Mm), Aov;
+    std::vector<u64> ImodQ((size_t)J * L);
+    std::vector<u32> liftV_m((size_t)L * J), liftV2_m((size_t)L * J), liftW_m(J), liftV_n((size_t)L * J),
+        liftV2_n((size_t)L * J), liftW_n(J);
+    for (u32 j = 0; j < J; ++j) {
+        const u32 p = (u32)ab.a[j];
+        a[j] = p;
+        apinv[j] = inv32_neg(p);
+        abar[j] = (~0ull) / p;
+        a2_64[j] = (u32)(((u128)1 << 64) % p);
+        aF[j] = (1ull << (64 - T.gbits)) / p;
+        ninvA[j] = (u32)invmod64(N % p, p);
+        ninvA_s[j] = shoup32h(ninvA[j], p);
+        const u64 r32 = (1ull << 32) % p;
+        ninvRA[j] = (u32)invmod64(mulmod64(N % p, r32, p), p);
+        ninvRA_s[j] = shoup32h(ninvRA[j], p);
+        NttTables nt = make_ntt_tables(N, p, 32);
+        for (u32 x = 0; x < N; ++x) {
+            arp.push_back((u32)nt.rp[x]);
+            arps.push_back((u32)nt.rps[x]);
+            airp.push_back((u32)nt.irp[x]);
+            airps.push_back((u32)nt.irps[x]);
+        }
+        Big Aj = A.div_u64(p);
+        chat[j] = (u32)invmod64(Aj.mod_u64(p), p);
+        chat_s[j] = shoup32h(chat[j], p);
+        // t (A/a_j) = I_j q + R_j ; frac96 = floor(R_j 2^96 / q)
+        Big tA = Aj.mul_u64(cp.t), I, R;
+        Big::divmod(tA, Q, I, R);
+        Big f, fr;
+        Big::divmod(R.shl(96), Q, f, fr);
+        for (int w = 0; w < 3; ++w) frac96[3 * j + w] = (u32)(f.limb(w / 2) >> (32 * (w % 2)));
+        for (u32 k = 0; k < Mm; ++k) Imod[(size_t)j * Mm + k] = (u32)I.mod_u64(ab.a[k]);
+        for (u32 i = 0; i < L; ++i) ImodQ[(size_t)j * L + i] = I.mod_u64(cp.q[i]);
+        auto l = Aj.limbs32(T.AW);
+        Aov.insert(Aov.end(), l.begin(), l.end());
+        // chain -> aux lift constants
+        const u64 qmod = Q.mod_u64(p);
+        liftW_n[j] = (u32)qmod;
+        liftW_m[j] = (u32)mulmod64(qmod, r32, p);
+        for (u32 i = 0; i < L; ++i) {
+            const u64 v = Q.div_u64(cp.q[i]).mod_u64(p);
+            const u64 v2 = mulmod64(v, (1ull << 30) % p, p);
+            liftV_n[(size_t)i * J + j] = (u32)v;
+            liftV2_n[(size_t)i * J + j] = (u32)v2;
+            liftV_m[(size_t)i * J + j] = (u32)mulmod64(v, r32, p);
+            liftV2_m[(size_t)i * J + j] = (u32)mulmod64(v2, r32, p);
+        }
+    }
+    std::vector<u32> fracA(3), IAmod(Mm);
+    std::vector<u64> IAmodQ(L);
+    {
+        Big tA = A.mul_u64(cp.t), I, R, f, fr;
+        Big::divmod(tA, Q, I, R);
+        Big::divmod(R.shl(96), Q, f, fr);
+        for (int w = 0; w < 3; ++w) fracA[w] = (u32)(f.limb(w / 2) >> (32 * (w % 2)));
+        for (u32 k = 0; k < Mm; ++k) IAmod[k] = (u32)I.mod_u64(ab.a[k]);
+        for (u32 i = 0; i < L; ++i) IAmodQ[i] = I.mod_u64(cp.q[i]);
+    }
+    std::vector<u32> Aw = A.limbs32(T.AW);
+    // MAC basis -> chain
+    std::vector<u32> mhat(Mm), mhat_s(Mm);
+    std::vector<u64> mF(Mm), Mconv((size_t)Mm * L), MnegQ(L);
+    for (u32 k = 0; k < Mm; ++k) {
+        const u32 p = (u32)ab.a[k];
+        Big Mk = M.div_u64(p);
+        mhat[k] = (u32)invmod64(Mk.mod_u64(p), p);
+        mhat_s[k] = shoup32h(mhat[k], p);
+        mF[k] = aF[k];
+        for (u32 i = 0; i < L; ++i) Mconv[(size_t)k * L + i] = Mk.mod_u64(cp.q[i]);
+    }
+    for (u32 i = 0; i < L; ++i) {
+        const u64 mm = M.mod_u64(cp.q[i]);
+        MnegQ[i] = mm ? cp.q[i] - mm : 0;
+    }
+
+#define ADD(name) const size_t o_##name = blob.add(name)
+    ADD(q); ADD(mu96); ADD(gh); ADD(gl); ADD(muq); ADD(muq_s); ADD(ninv); ADD(ninv_s); ADD(delta);
+    ADD(crp); ADD(crps); ADD(cirp); ADD(cirps); ADD(qw); ADD(qov);
+    ADD(a); ADD(apinv); ADD(abar); ADD(a2_64); ADD(ninvA); ADD(ninvA_s); ADD(ninvRA); ADD(ninvRA_s);
+    ADD(arp); ADD(arps); ADD(airp); ADD(airps);
+    ADD(liftV_m); ADD(liftV2_m); ADD(liftW_m); ADD(liftV_n); ADD(liftV2_n); ADD(liftW_n);
+    ADD(chat); ADD(chat_s); ADD(aF); ADD(frac96); ADD(fracA); ADD(Imod); ADD(IAmod); ADD(ImodQ); ADD(IAmodQ);
+    ADD(Aw); ADD(Aov); ADD(mhat); ADD(mhat_s); ADD(mF); ADD(Mconv); ADD(MnegQ);
+#undef ADD
+    c.tab.ensure(blob.b.size());
+    CK(cudaMemcpy(c.tab.p, blob.b.data(), blob.b.size(), cudaMemcpyHostToDevice));
+    unsigned char* base = static_cast<unsigned char*>(c.tab.p);
+#define P64(field, name) T.field = reinterpret_cast<const u64*>(base + o_##name)
+#define P32(field, name) T.field = reinterpret_cast<const u32*>(base + o_##name)
+    P64(q, q); P64(q_mu96, mu96); P64(q_gh, gh); P64(q_gl, gl); P64(muq, muq); P64(muq_s, muq_s);
+    P64(ninv, ninv); P64(ninv_s, ninv_s); P64(delta, delta); P64(crp, crp); P64(crps, crps); P64(cirp, cirp);
+    P64(cirps, cirps); P32(qw, qw); P32(qov, qov);
+    P32(a, a); P32(apinv, apinv); P64(abar, abar); P32(a2_64, a2_64); P32(ninvA, ninvA); P32(ninvA_s, ninvA_s);
+    P32(ninvRA, ninvRA); P32(ninvRA_s, ninvRA_s); P32(arp, arp); P32(arps, arps); P32(airp, airp); P32(airps, airps);
+    P32(liftV_m, liftV_m); P32(liftV2_m, liftV2_m); P32(liftW_m, liftW_m); P32(liftV_n, liftV_n);
+    P32(liftV2_n, liftV2_n); P32(liftW_n, liftW_n);
+    P32(chat, chat); P32(chat_s, chat_s); P64(aF, aF); P32(frac96, frac96); P32(fracA, fracA); P32(Imod, Imod);
+    P32(IAmod, IAmod); P64(ImodQ, ImodQ); P64(IAmodQ, IAmodQ); P32(Aw, Aw); P32(Aov, Aov);
+    P32(mhat, mhat); P32(mhat_s, mhat_s); P64(mF, mF); P64(Mconv, Mconv); P64(MnegQ, MnegQ);
+#undef P64
+#undef P32
+    T.fallbacks = c.d_fb;
+    c.T = T;
+}
+
+static void set_smem_limits(u32 N) {
+    const int s64 = (int)(N * sizeof(u64)), s32 = (int)(N * sizeof(u32));
+    CK(cudaFuncSetAttribute(k_ntt64<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64));
+    CK(cudaFuncSetAttribute(k_ntt64<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64));
+    CK(cudaFuncSetAttribute(k_ntt64<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64));
+    CK(cudaFuncSetAttribute(k_ntt32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
+    CK(cudaFuncSetAttribute(k_ntt32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
+    CK(cudaFuncSetAttribute(k_tensor_intt, cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
+}
+
+static void ensure_aux(Ctx& c, u64 n_total) {
+    n_total = std::max<u64>(n_total, 1);
+    if (c.aux_n == n_total && c.ab.J) return;
+    AuxBasis nb = choose_aux_basis(c.cp, n_total);
+    const bool same = c.ab.J && nb.a == c.ab.a && nb.Mm == c.ab.Mm;
+    c.aux_n = n_total;
+    if (same) return;
+    c.ab = nb;
+    build_tables(c);
+}
+
+// ------------------------------------------------------------------ NTT launchers
+static void ntt64(Ctx& c, u64* data, u32 npolys, bool inverse) {
+    const u32 N = c.cp.N;
+    if (inverse)
+        launch(c, k_ntt64<true, false>, npolys, ntt_block(N), N * 8, data, (const u64*)nullptr, c.T);
+    else
+        launch(c, k_ntt64<false, false>, npolys, ntt_block(N), N * 8, data, (const u64*)nullptr, c.T);
+}
+
+static void ntt32(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale) {
+    const u32 N = c.cp.N;
+    if (inverse)
+        launch(c, k_ntt32<true>, npolys, ntt_block(N), N * 4, base, c.T, gs, stride, off, scale);
+    else
+        launch(c, k_ntt32<false>, npolys, ntt_block(N), N * 4, base, c.T, gs, stride, off, scale);
+}
+
+// ------------------------------------------------------------------ key switching
+/// ks[b] (2 comps, coefficient form) = key_switch(poly_b) for B polys at polys + b*stride
+/// through automorphism ginv (0 = none) (bfv.cpp:343-372).
+static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B, const u64* key, u32 bits,
+                       u32 D, u64* ks) {
+    const u32 N = c.cp.N, L = c.cp.L;
+    u64* dig = c.digits.get<u64>((size_t)B * D * N);
+    u64* dn = c.dntt.get<u64>((size_t)B * D * L * N);
+    launch(c, k_decompose, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv, B, bits, D, c.T, dig);
+    launch(c, k_ntt64<false, true>, (size_t)B * D * L, ntt_block(N), N * 8, dn, (const u64*)dig, c.T);
+    launch(c, k_ks_mac, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u64*)dn, key, B, D, c.T, ks);
+    ntt64(c, ks, B * 2 * L, true);
+}
+
+static size_t ks_chunk(const Ctx& c, u32 D) {
+    // bound the digit / digit-NTT scratch to ~1.5 GB
+    const size_t per = (size_t)D * (c.cp.L + 1) * c.cp.N * 8 + 2 * (size_t)c.cp.L * c.cp.N * 8;
+    return std::max<size_t>(1, (size_t(1536) << 20) / per);
+}
+
+/// relinearize count 3-comp cts (stride 3LN) into out2 [count][2][L][N].
+static void relinearize(Ctx& c, const u64* ct3, u32 count, u64* out2) {
+    const size_t LN = (size_t)c.cp.L * c.cp.N;
+    const size_t chunk = ks_chunk(c, c.cp.Dr);
+    for (u32 b0 = 0; b0 < count; b0 += (u32)chunk) {
+        const u32 B = (u32)std::min<size_t>(chunk, count - b0);
+        u64* ks = c.ks.get<u64>((size_t)B * 2 * LN);
+        key_switch(c, ct3 + (size_t)b0 * 3 * LN + 2 * LN, 3 * LN, 0, B, c.relin.ptr<u64>(), c.cp.relin_bits,
+                   c.cp.Dr, ks);
+        launch(c, k_relin_add, blocks((size_t)B * 2 * LN, 256), 256, 0, ct3 + (size_t)b0 * 3 * LN, 3 * LN,
+               (const u64*)ks, B, c.T, out2 + (size_t)b0 * 2 * LN);
+    }
+}
+
+static u64 inv_mod_2n(u64 g, u64 twoN) {
+    for (u64 x = 1; x < twoN; x += 2)
+        if ((x * g) % twoN == 1) return x;
+    throw std::logic_error("no inverse");
+}
+
+static const u64* galois_key(Ctx& c, u64 g) {
+    for (size_t a = 0; a < c.galois_g.size(); ++a)
+        if (c.galois_g[a] == g)
+            return c.galois.ptr<u64>() + a * (size_t)c.cp.Dg * 2 * c.cp.L * c.cp.N;
+    throw he_err("missing Galois key for requested exponent");
+}
+
+/// expand_query (expansion.cpp:67-83): query [h][2][L][N] on device -> entries [h * 2^c].
+/// Returns a pointer to the final level buffer (first m entries are the result).
+static u64* expand(Ctx& c, const u64* dquery, u32 h, u32 comp, u32 m) {
+    const u32 N = c.cp.N, L = c.cp.L;
+    const size_t per = 2 * (size_t)L * N;
+    if ((u64(1) << comp) > N) throw std::invalid_argument("compression factor exceeds log2(N)");
+    if ((size_t)h << comp < m) throw std::invalid_argument("packed query too short for code length");
+    const size_t full = (size_t)h << comp;
+    u64* cur = c.exA.get<u64>(full * per);
+    u64* nxt = c.exB.get<u64>(full * per);
+    CK(cudaMemcpyAsync(cur, dquery, (size_t)h * per * 8, cudaMemcpyDeviceToDevice, c.st));
+    const size_t chunk = ks_chunk(c, c.cp.Dg);
+    for (u32 a = 0; a < comp; ++a) {
+        const u64 g = N / (u64(1) << a) + 1;
+        const u64 ginv = inv_mod_2n(g, 2 * (u64)N);
+        const u64* key = galois_key(c, g);
+        const u32 Bq = 1u << a;  // entries per query at this level
+        for (u32 qi = 0; qi < h; ++qi) {
+            const u64* in = cur + (size_t)qi * Bq * per;
+            u64* out = nxt + (size_t)qi * 2 * Bq * per;
+            for (u32 b0 = 0; b0 < Bq; b0 += (u32)chunk) {
+                const u32 B = (u32)std::min<size_t>(chunk, Bq - b0);
+                u64* ks = c.ks.get<u64>((size_t)B * per);
+                key_switch(c, in + (size_t)b0 * per + (size_t)L * N, per, ginv, B, key, c.cp.galois_bits,
+                           c.cp.Dg, ks);
+                // combine: in/out bases shifted to the chunk, partner offset Bq
+                launch(c, k_expand_combine, blocks((size_t)B * L * N, 256), 256, 0, in + (size_t)b0 * per,
+                       (const u64*)ks, B, Bq, ginv, (u32)(1u << a), c.T, out + (size_t)b0 * per);
+            }
+        }
+        std::swap(cur, nxt);
+    }
+    return cur;
+}
+
+// ------------------------------------------------------------------ per-row selection
+/// Lift count 2-comp chain cts (at src + sel[x]*stride) to the aux basis (Montgomery) and NTT:
+/// out [count][2][J][N].
+static void prepare(Ctx& c, const u64* src, size_t stride, const u32* sel, u32 count, u32* out) {
+    const u32 N = c.cp.N, J = c.ab.J;
+    launch(c, k_lift, blocks((size_t)count * 2 * N, 256), 256, 0, src, stride, sel, count, J, 1, c.T, out, J);
+    ntt32(c, out, count * 2 * J, J, J, 0, false, 0);
+}
+
+/// Tensor + INTT + exact rounding for P products of prepared operands.
+/// to_mac: D planes k < Mm become the NTT-form MAC-basis selection values (in c.Dbuf);
+/// else the 3-comp chain products are written to chain_out [P][3][L][N].
+static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* prepB, const u32* idxB, u32 P,
+                         bool to_mac, u64* chain_out) {
+    const u32 N = c.cp.N, J = c.ab.J;
+    u32* D = c.Dbuf.get<u32>((size_t)P * 3 * J * N);
+    launch(c, k_tensor_intt, (size_t)P * J, ntt_block(N), N * 4, prepA, idxA, prepB, idxB, P, c.T, D);
+    if (to_mac) {
+        launch(c, k_round_mac, blocks((size_t)P * 3 * N, 128), 128, 0, D, P, c.T);
+        ntt32(c, D, P * 3 * c.ab.Mm, c.ab.Mm, J, 0, false, 0);
+    } else {
+        launch(c, k_round_chain, blocks((size_t)P * 3 * N, 128), 128, 0, (const u32*)D, P, c.T, chain_out);
+    }
+    return D;
+}
+
+/// Selection values for rows [r0, r0+R) of the resident DB.  Returns the Z buffer and sets
+/// nc / zstride (Z + ((r*nc + comp)*zstride + k)*N in NTT form, MAC basis).
+/// If chain_sel != nullptr the selection ciphertexts are written there instead
+/// ([R][3][L][N], comps[r]) and no MAC-basis values are produced (config 2).
+static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64 r0, u32 R, u32& nc, u32& zstride,
+                        u64* chain_sel) {
+    const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J, Mm = c.ab.Mm, k = c.k;
+    const size_t LN = (size_t)L * N;
+    const u32* pcol = c.pos_cols.ptr<u32>();
+    auto col = [&](u32 p) { return pcol + (size_t)p * c.n_local + r0; };
+    if (op == CWG_OP_FOLKLORE && k == 1) {
+        if (chain_sel) {
+            u64* tmp = c.node2.get<u64>((size_t)R * 2 * LN);
+            launch(c, k_gather_ct, blocks((size_t)R * 2 * LN, 256), 256, 0, entries, col(0), R, 2 * LN, tmp);
+            for (u32 r = 0; r < R; ++r)
+                CK(cudaMemcpyAsync(chain_sel + (size_t)r * 3 * LN, tmp + (size_t)r * 2 * LN, 2 * LN * 8,
+                                   cudaMemcpyDeviceToDevice, c.st));
+            nc = 2;
+            return nullptr;
+        }
+        u32* Z = c.lift_tmp.get<u32>((size_t)R * 2 * Mm * N);
+        launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, entries, 2 * LN, col(0), R, Mm, 0, c.T, Z, Mm);
+        ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
+        nc = 2;
+        zstride = Mm;
+        return Z;
+    }
+    if (op == CWG_OP_FOLKLORE && k == 2) {
+        if (chain_sel) {
+            mul_prepared(c, prep, col(0), prep, col(1), R, false, chain_sel);
+            nc = 3;
+            return nullptr;
+        }
+        u32* D = mul_prepared(c, prep, col(0), prep, col(1), R, true, nullptr);
+        nc = 3;
+        zstride = J;
+        return D;
+    }
+    // ---- general product trees (k >= 3 folklore, arithmetic operator)
+    // nodes: [R][cnt][2][L][N] 2-comp chain ciphertexts
+    u32 cnt = 0;
+    u64* nodes = nullptr;
+    if (op == CWG_OP_FOLKLORE) {
+        // leaves: pairs (pos[2p], pos[2p+1]) -> mul_lazy_prepared -> finalize (pir.cpp:294-300)
+        const u32 np = k / 2;
+        cnt = np + (k % 2);
+        nodes = c.node2.get<u64>((size_t)R * cnt * 2 * LN);
+        std::vector<u32> ia((size_t)R * np), ib((size_t)R * np);
+        for (u32 r = 0; r < R; ++r)
+            for (u32 p = 0; p < np; ++p) {
+                ia[(size_t)r * np + p] = c.h_pos[(r0 + r) * k + 2 * p];
+                ib[(size_t)r * np + p] = c.h_pos[(r0 + r) * k + 2 * p + 1];
+            }
+        u32* di = c.tmp_idx.get<u32>((size_t)2 * R * np + 2 * R);
+        CK(cudaMemcpyAsync(di, ia.data(), ia.size() * 4, cudaMemcpyHostToDevice, c.st));
+        CK(cudaMemcpyAsync(di + ia.size(), ib.data(), ib.size() * 4, cudaMemcpyHostToDevice, c.st));
+        u64* c3 = c.chain3.get<u64>((size_t)R * np * 3 * LN);
+        mul_prepared(c, prep, di, prep, di + ia.size(), R * np, false, c3);
+        // relinearize into the node slots: node (r, p) = leaf r*np + p
+        u64* leaf2 = c.out2.get<u64>((size_t)R * np * 2 * LN);
+        relinearize(c, c3, R * np, leaf2);
+        for (u32 r = 0; r < R; ++r) {
+            CK(cudaMemcpyAsync(nodes + ((size_t)r * cnt) * 2 * LN, leaf2 + (size_t)r * np * 2 * LN,
+                               (size_t)np * 2 * LN * 8, cudaMemcpyDeviceToDevice, c.st));
+            if (k % 2) {
+                const u32 e = c.h_pos[(r0 + r) * k + k - 1];
+                CK(cudaMemcpyAsync(nodes + ((size_t)r * cnt + np) * 2 * LN, entries + (size_t)e * 2 * LN,
+                                   2 * LN * 8, cudaMemcpyDeviceToDevice, c.st));
+            }
+        }
+    } else {
+        cnt = k;
+        nodes = c.node2.get<u64>((size_t)R * cnt * 2 * LN);
+        launch(c, k_arith_factors, blocks((size_t)R * 2 * LN, 256), 256, 0, entries,
+               c.pos_rows.ptr<u32>() + (size_t)r0 * k, R, k, c.T, nodes);
+    }
+    const bool lazy_root = (op == CWG_OP_FOLKLORE);
+    // product_tree (eq_circuits.cpp:53-69)
+    while (cnt > 1) {
+        const bool last = cnt == 2;
+        const u32 np = cnt / 2, ncnt = np + (cnt % 2);
+        // prepare every node of every row (entries keep their own prepared buffer)
+        u32* np_prep = c.lift_tmp.get<u32>((size_t)R * cnt * 2 * J * N);
+        prepare(c, nodes, 2 * LN, nullptr, R * cnt, np_prep);
+        std::vector<u32> ia((size_t)R * np), ib((size_t)R * np);
+        for (u32 r = 0; r < R; ++r)
+            for (u32 p = 0; p < np; ++p) {
+                ia[(size_t)r * np + p] = r * cnt + 2 * p;
+                ib[(size_t)r * np + p] = r * cnt + 2 * p + 1;
+            }
+        u32* di = c.tmp_idx.get<u32>((size_t)2 * R * np + 2);
+        CK(cudaMemcpyAsync(di, ia.data(), ia.size() * 4, cudaMemcpyHostToDevice, c.st));
+        CK(cudaMemcpyAsync(di + ia.size(), ib.data(), ib.size() * 4, cudaMemcpyHostToDevice, c.st));
+        if (last && lazy_root) {
+            if (chain_sel) {
+                mul_prepared(c, np_prep, di, np_prep, di + ia.size(), R, false, chain_sel);
+                nc = 3;
+                return nullptr;
+            }
+            u32* D = mul_prepared(c, np_prep, di, np_prep, di + ia.size(), R, true, nullptr);
+            nc = 3;
+            zstride = J;
+            return D;
+        }
+        u64* c3 = c.chain3.get<u64>((size_t)R * np * 3 * LN);
+        mul_prepared(c, np_prep, di, np_prep, di + ia.size(), R * np, false, c3);
+        u64* nn = c.out2.get<u64>((size_t)R * ncnt * 2 * LN);
+        u64* rl = c.resp3.get<u64>((size_t)R * np * 2 * LN);
+        relinearize(c, c3, R * np, rl);
+        for (u32 r = 0; r < R; ++r) {
+            CK(cudaMemcpyAsync(nn + (size_t)r * ncnt * 2 * LN, rl + (size_t)r * np * 2 * LN, (size_t)np * 2 * LN * 8,
+                               cudaMemcpyDeviceToDevice, c.st));
+            if (cnt % 2)
+                CK(cudaMemcpyAsync(nn + ((size_t)r * ncnt + np) * 2 * LN, nodes + ((size_t)r * cnt + cnt - 1) * 2 * LN,
+                                   2 * LN * 8, cudaMemcpyDeviceToDevice, c.st));
+        }
+        CK(cudaMemcpyAsync(nodes, nn, (size_t)R * ncnt * 2 * LN * 8, cudaMemcpyDeviceToDevice, c.st));
+        cnt = ncnt;
+    }
+    // root is a 2-comp ciphertext: arithmetic operator -> plain_mul((k!)^-1) (eq_circuits.cpp:126)
+    if (op == CWG_OP_ARITH) {
+        u64 f = 1;
+        for (u32 i = 2; i <= k; ++i) f = mulmod64(f, i % c.cp.t, c.cp.t);
+        if (f == 0) throw std::invalid_argument("k! is not invertible mod t");
+        const u64 kinv = invmod64(f, c.cp.t);
+        launch(c, k_scale_const, blocks((size_t)R * 2 * LN, 256), 256, 0, nodes, R, kinv, c.T);
+    }
+    if (chain_sel) {
+        for (u32 r = 0; r < R; ++r)
+            CK(cudaMemcpyAsync(chain_sel + (size_t)r * 3 * LN, nodes + (size_t)r * 2 * LN, 2 * LN * 8,
+                               cudaMemcpyDeviceToDevice, c.st));
+        nc = 2;
+        return nullptr;
+    }
+    u32* Z = c.Dbuf.get<u32>((size_t)R * 2 * Mm * N);
+    launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, (const u64*)nodes, 2 * LN, (const u32*)nullptr, R, Mm,
+           0, c.T, Z, Mm);
+    ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
+    nc = 2;
+    zstride = Mm;
+    return Z;
+}
+
+static u32 tile_rows(const Ctx& c) {
+    // bound the per-tile aux buffer (P x 3 x J x N u32) to ~256 MB and tree scratch
+    const size_t per = (size_t)3 * c.ab.J * c.cp.N * 4 * std::max<u32>(1, c.k / 2);
+    size_t r = std::max<size_t>(4, (size_t(256) << 20) / per);
+    if (c.k > 2) r = std::min<size_t>(r, 64);
+    return (u32)std::min<size_t>(r, 512);
+}
+
+// ------------------------------------------------------------------ answer
+struct Timer {
+    Ctx& c;
+    bool on;
+    std::vector<std::pair<int, cudaEvent_t>> marks;
+    Timer(Ctx& cc, bool enabled) : c(cc), on(enabled) {}
+    ~Timer() {
+        for (auto& m : marks) cudaEventDestroy(m.second);
+    }
+    void mark(int tag) {
+        if (!on) return;
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(e, c.st));
+        marks.push_back({tag, e});
+    }
+    /// sum of elapsed times over consecutive marks whose END mark carries `tag`
+    double sum(int tag) const {
+        double s = 0;
+        for (size_t i = 1; i < marks.size(); ++i) {
+            if (marks[i].first != tag) continue;
+            float f = 0;
+            CK(cudaEventElapsedTime(&f, marks[i - 1].second, marks[i].second));
+            s += f;
+        }
+        return s;
+    }
+};
+enum { TM_START = 0, TM_H2D, TM_EXPAND, TM_SELECT, TM_MAC, TM_FINISH, TM_D2H };
+
+static void upload_keys(Ctx& c, const u64* relin, u32 n_galois, const u64* gg, const u64* galois) {
+    const size_t LN = (size_t)c.cp.L * c.cp.N;
+    const size_t rw = (size_t)c.cp.Dr * 2 * LN, gw = (size_t)c.cp.Dg * 2 * LN;
+    CK(cudaMemcpyAsync(c.relin.get<u64>(rw), relin, rw * 8, cudaMemcpyHostToDevice, c.st));
+    if (n_galois)
+        CK(cudaMemcpyAsync(c.galois.get<u64>(gw * n_galois), galois, gw * n_galois * 8, cudaMemcpyHostToDevice, c.st));
+    c.galois_g.assign(gg, gg + n_galois);
+    c.have_keys = true;
+}
+
+/// expand + select + MAC; leaves the reduced partial accumulators [s][3][Mm][N] u64
+/// in dev_partial; returns the response component count (2 or 3).
+static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 op, u64* dev_partial, Timer& tm) {
+    if (!c.db_loaded) throw state_err("no database loaded");
+    if (m != c.m) throw std::invalid_argument("query code length does not match the database");  // pir.cpp:339-341
+    if (c.s == 0) throw state_err("database has no payload (selection-only); use cwg_select");
+    if (!c.have_keys) throw he_err("evaluation keys not set");
+    if (op != CWG_OP_FOLKLORE && op != CWG_OP_ARITH) throw std::invalid_argument("unknown equality operator");
+    if (op == CWG_OP_ARITH && c.k < 2) throw std::invalid_argument("arithmetic operator needs k >= 2");
+    const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J, Mm = c.ab.Mm;
+    const size_t LN = (size_t)L * N;
+    u64* dq = c.query.get<u64>((size_t)h * 2 * LN);
+    CK(cudaMemcpyAsync(dq, query, (size_t)h * 2 * LN * 8, cudaMemcpyHostToDevice, c.st));
+    tm.mark(TM_H2D);
+    u64* entries = expand(c, dq, h, comp, m);
+    tm.mark(TM_EXPAND);
+    u32* prep = nullptr;
+    if (op == CWG_OP_FOLKLORE && c.k >= 2) {
+        prep = c.prep.get<u32>((size_t)m * 2 * J * N);
+        prepare(c, entries, 2 * LN, nullptr, m, prep);
+    }
+    const size_t accw = (size_t)c.s * 3 * Mm * N;
+    u64* alo = c.acc_lo.get<u64>(accw);
+    u64* ahi = c.acc_hi.get<u64>(accw);
+    CK(cudaMemsetAsync(alo, 0, accw * 8, c.st));
+    CK(cudaMemsetAsync(ahi, 0, accw * 8, c.st));
+    const u32 R = tile_rows(c);
+    u32 nc_all = 2;
+    for (u64 r0 = 0; r0 < c.n_local; r0 += R) {
+        const u32 Rt = (u32)std::min<u64>(R, c.n_local - r0);
+        u32 nc = 0, zs = 0;
+        u32* Z = select_tile(c, entries, prep, op, r0, Rt, nc, zs, nullptr);
+        nc_all = std::max(nc_all, nc);
+        tm.mark(TM_SELECT);
+        launch(c, k_mac, blocks((size_t)c.s * Mm * N, 128), 128, 0, (const u32*)Z, nc, zs,
+               (const u32*)(c.db.ptr<u32>() + (size_t)r0 * c.s * Mm * N), Rt, c.s, c.T, alo, ahi);
+        tm.mark(TM_MAC);
+    }
+    launch(c, k_acc_reduce, blocks(accw, 256), 256, 0, (const u64*)alo, (const u64*)ahi, accw, c.T, dev_partial);
+    tm.mark(TM_MAC);
+    return nc_all;
+}
+
+/// summed partials -> responses: mod a_k, INTT, M -> chain, finalize (pir.cpp:345).
+static void finish(Ctx& c, const u64* dev_partial, u32 nc, u64* out_host, Timer& tm) {
+    const u32 N = c.cp.N, L = c.cp.L, Mm = c.ab.Mm;
+    const size_t LN = (size_t)L * N;
+    const size_t accw = (size_t)c.s * 3 * Mm * N;
+    u32* X = c.X.get<u32>(accw);
+    launch(c, k_partial_mod, blocks(accw, 256), 256, 0, dev_partial, accw, c.T, X);
+    ntt32(c, X, c.s * 3 * Mm, Mm, Mm, 0, true, 0);
+    u64* r3 = c.resp3.get<u64>((size_t)c.s * 3 * LN);
+    launch(c, k_mac_to_chain, blocks((size_t)c.s * 3 * N, 128), 128, 0, (const u32*)X, c.s * 3, c.T, r3);
+    u64* o2 = c.out2.get<u64>((size_t)c.s * 2 * LN);
+    if (nc == 3) {
+        relinearize(c, r3, c.s, o2);
+    } else {
+        for (u32 j = 0; j < c.s; ++j)
+            CK(cudaMemcpyAsync(o2 + (size_t)j * 2 * LN, r3 + (size_t)j * 3 * LN, 2 * LN * 8, cudaMemcpyDeviceToDevice,
+                               c.st));
+    }
+    tm.mark(TM_FINISH);
+    CK(cudaMemcpyAsync(out_host, o2, (size_t)c.s * 2 * LN * 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    tm.mark(TM_D2H);
+}
+
+static void fill_timings(Ctx& c, Timer& tm, cwg_timings* t, double total_ms) {
+    if (!t) return;
+    CK(cudaStreamSynchronize(c.st));
+    t->total_ms = total_ms;
+    t->h2d_ms = tm.sum(TM_H2D);
+    t->expand_ms = tm.sum(TM_EXPAND);
+    t->select_ms = tm.sum(TM_SELECT);
+    t->mac_ms = tm.sum(TM_MAC);
+    t->finish_ms = tm.sum(TM_FINISH);
+    t->d2h_ms = tm.sum(TM_D2H);
+    t->kernel_launches = c.launches;
+    unsigned long long fb = 0;
+    CK(cudaMemcpy(&fb, c.d_fb, 8, cudaMemcpyDeviceToHost));
+    t->exact_fallbacks = fb;
+}
+
+// ------------------------------------------------------------------ database
+static void load_db(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s, u32 k, u32 m, const u32* positions,
+                    const u64* payload) {
+    if (n_local == 0 || n_total == 0) throw std::invalid_argument("empty database");
+    if (row_begin + n_local > n_total) throw std::invalid_argument("row range outside the database");
+    if (k < 1) throw std::invalid_argument("hamming weight must be >= 1");
+    if (k > 64) throw std::invalid_argument("cwgpu: hamming weight above 64 is not supported");
+    if (c.cp.t <= k) throw std::invalid_argument("plaintext modulus must exceed the Hamming weight");
+    if (s > 0 && !payload) throw std::invalid_argument("payload missing");
+    const u32 N = c.cp.N;
+    for (u64 r = 0; r < n_local; ++r) {
+        for (u32 p = 0; p < k; ++p) {
+            const u32 v = positions[r * k + p];
+            if (v >= m) throw std::invalid_argument("codeword position outside the code length");
+            if (p && v <= positions[r * k + p - 1]) throw std::invalid_argument("codeword positions must ascend");
+        }
+    }
+    ensure_aux(c, n_total);
+    const u32 Mm = c.ab.Mm;
+    c.n_total = n_total;
+    c.row_begin = row_begin;
+    c.n_local = n_local;
+    c.s = s;
+    c.k = k;
+    c.m = m;
+    c.h_pos.assign(positions, positions + n_local * k);
+    std::vector<u32> cols((size_t)k * n_local);
+    for (u64 r = 0; r < n_local; ++r)
+        for (u32 p = 0; p < k; ++p) cols[(size_t)p * n_local + r] = positions[r * k + p];
+    CK(cudaMemcpy(c.pos_rows.get<u32>(n_local * k), positions, n_local * k * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c.pos_cols.get<u32>(n_local * k), cols.data(), cols.size() * 4, cudaMemcpyHostToDevice));
+    if (s > 0) {
+        // prepare_plain (bfv.cpp:933-942) into the MAC basis: coefficients < t lifted unchanged,
+        // NTT per MAC prime; staged in chunks of rows.
+        for (u64 i = 0; i < n_local * s * N; ++i)
+            if (payload[i] >= c.cp.t) throw std::invalid_argument("plain operand not reduced mod t");
+        u32* dbp = c.db.get<u32>(n_local * s * Mm * N);
+        const u64 chunk = std::max<u64>(1, (u64(256) << 20) / ((u64)s * N * 8));
+        u64* stage = c.chain3.get<u64>(std::min(chunk, n_local) * s * N);
+        for (u64 r0 = 0; r0 < n_local; r0 += chunk) {
+            const u64 R = std::min(chunk, n_local - r0);
+            CK(cudaMemcpyAsync(stage, payload + r0 * s * N, R * s * N * 8, cudaMemcpyHostToDevice, c.st));
+            u32* dst = dbp + r0 * s * Mm * N;
+            launch(c, k_db_spread, blocks(R * s * Mm * N, 256), 256, 0, (const u64*)stage, R * s, c.T, dst);
+            ntt32(c, dst, (u32)(R * s * Mm), Mm, Mm, 0, false, 0);
+        }
+        CK(cudaStreamSynchronize(c.st));
+    }
+    c.db_loaded = true;
+}
+
+}  // namespace cwgpu
+
+// ================================================================== C ABI
+using namespace cwgpu;
+
+struct cwg_ctx {
+    Ctx c;
+};
+
+template <class F>
+static int guarded(F&& f) {
+    try {
+        f();
+        return CWG_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return CWG_EINVAL;
+    } catch (const he_err& e) {
+        g_err = e.what();
+        return CWG_EHE;
+    } catch (const cuda_err& e) {
+        g_err = e.what();
+        return CWG_ECUDA;
+    } catch (const state_err& e) {
+        g_err = e.what();
+        return CWG_ESTATE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return CWG_EINVAL;
+    }
+}
+
+extern "C" {
+
+const char* cwg_last_error(void) { return g_err.c_str(); }
+
+cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint32_t relin_digit_bits,
+                    uint32_t galois_digit_bits, int device) {
+    cwg_ctx* h = nullptr;
+    int rc = guarded([&] {
+        auto ctx = std::make_unique<cwg_ctx>();
+        Ctx& c = ctx->c;
+        c.cp = make_chain(N, t, std::vector<u64>(q, q + L), relin_digit_bits, galois_digit_bits);
+        if (N > 16384) throw std::invalid_argument("cwgpu: ring degree above 16384 is not supported");
+        c.device = device;
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+        CK(cudaMalloc(&c.d_fb, 8));
+        CK(cudaMemset(c.d_fb, 0, 8));
+        set_smem_limits(N);
+        ensure_aux(c, 1);
+        h = ctx.release();
+    });
+    return rc == CWG_OK ? h : nullptr;
+}
+
+void cwg_destroy(cwg_ctx* h) {
+    if (!h) return;
+    Ctx& c = h->c;
+    cudaSetDevice(c.device);
+    cudaStreamSynchronize(c.st);
+    for (DevBuf* b : {&c.tab, &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
+                      &c.digits, &c.dntt, &c.ks, &c.prep, &c.Dbuf, &c.chain3, &c.node2, &c.acc_lo, &c.acc_hi,
+                      &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp})
+        b->release();
+    if (c.d_fb) cudaFree(c.d_fb);
+    if (c.st) cudaStreamDestroy(c.st);
+    delete h;
+}
+
+int cwg_get_info(const cwg_ctx* h, cwg_info* out) {
+    return guarded([&] {
+        const Ctx& c = h->c;
+        out->N = c.cp.N;
+        out->L = c.cp.L;
+        out->J = c.ab.J;
+        out->Mm = c.ab.Mm;
+        out->Dr = c.cp.Dr;
+        out->Dg = c.cp.Dg;
+        out->q_bits = c.cp.q_bits;
+        Big A(1);
+        for (u64 a : c.ab.a) A = A.mul_u64(a);
+        out->aux_bits = A.bits();
+        out->n_total = c.n_total;
+        out->row_begin = c.row_begin;
+        out->n_local = c.n_local;
+        out->s = c.s;
+        out->k = c.k;
+        out->m = c.m;
+    });
+}
+
+int cwg_load_db(cwg_ctx* h, uint64_t n_total, uint64_t row_begin, uint64_t n_local, uint32_t s, uint32_t k,
+                uint32_t m, const uint32_t* positions, const uint64_t* payload) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->c.mu);
+        CK(cudaSetDevice(h->c.device));
+        load_db(h->c, n_total, row_begin, n_local, s, k, m, positions, payload);
+    });
+}
+
+int cwg_set_keys(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+                 const uint64_t* galois) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->c.mu);
+        CK(cudaSetDevice(h->c.device));
+        upload_keys(h->c, relin, n_galois, galois_g, galois);
+        CK(cudaStreamSynchronize(h->c.st));
+    });
+}
+
+uint64_t cwg_partial_words(const cwg_ctx* h) {
+    const Ctx& c = h->c;
+    return (uint64_t)c.s * 3 * c.ab.Mm * c.cp.N;
+}
+
+int cwg_answer_partial(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+                       const uint64_t* galois, uint32_t nq, uint32_t comp, uint32_t m, const uint64_t* query,
+                       uint32_t op, uint64_t* dev_partial, cwg_timings* t) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        auto t0 = std::chrono::steady_clock::now();
+        Timer tm(c, t != nullptr);
+        tm.mark(TM_START);
+        if (relin) upload_keys(c, relin, n_galois, galois_g, galois);
+        answer_partial(c, nq, comp, m, query, op, dev_partial, tm);
+        CK(cudaStreamSynchronize(c.st));
+        fill_timings(c, tm, t,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    });
+}
+
+int cwg_finish(cwg_ctx* h, const uint64_t* dev_partial_sum, uint32_t op, uint64_t* out, cwg_timings* t) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        if (!c.db_loaded || c.s == 0) throw state_err("no database loaded");
+        if (!c.have_keys) throw he_err("evaluation keys not set");
+        auto t0 = std::chrono::steady_clock::now();
+        Timer tm(c, t != nullptr);
+        tm.mark(TM_START);
+        const u32 nc = (op == CWG_OP_FOLKLORE && c.k >= 2) ? 3 : 2;
+        finish(c, dev_partial_sum, nc, out, tm);
+        fill_timings(c, tm, t,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    });
+}
+
+int cwg_answer(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g, const uint64_t* galois,
+               uint32_t nq, uint32_t comp, uint32_t m, const uint64_t* query, uint32_t op, uint64_t* out,
+               cwg_timings* t) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        auto t0 = std::chrono::steady_clock::now();
+        Timer tm(c, t != nullptr);
+        tm.mark(TM_START);
+        if (relin) upload_keys(c, relin, n_galois, galois_g, galois);
+        u64* part = c.partial.get<u64>((size_t)c.s * 3 * c.ab.Mm * c.cp.N);
+        const u32 nc = answer_partial(c, nq, comp, m, query, op, part, tm);
+        finish(c, part, nc, out, tm);
+        fill_timings(c, tm, t,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    });
+}
+
+int cwg_select(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g, const uint64_t* galois,
+               uint32_t nq, uint32_t comp, uint32_t m, const uint64_t* query, uint32_t op, uint64_t* sel,
+               uint32_t* comps, cwg_timings* t) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        if (!c.db_loaded) throw state_err("no database loaded");
+        if (m != c.m) throw std::invalid_argument("expanded query length must equal the code length");
+        auto t0 = std::chrono::steady_clock::now();
+        Timer tm(c, t != nullptr);
+        tm.mark(TM_START);
+        if (relin) upload_keys(c, relin, n_galois, galois_g, galois);
+        if (!c.have_keys) throw he_err("evaluation keys not set");
+        const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J;
+        const size_t LN = (size_t)L * N;
+        u64* dq = c.query.get<u64>((size_t)nq * 2 * LN);
+        CK(cudaMemcpyAsync(dq, query, (size_t)nq * 2 * LN * 8, cudaMemcpyHostToDevice, c.st));
+        tm.mark(TM_H2D);
+        u64* entries = expand(c, dq, nq, comp, m);
+        tm.mark(TM_EXPAND);
+        u32* prep = nullptr;
+        if (op == CWG_OP_FOLKLORE && c.k >= 2) {
+            prep = c.prep.get<u32>((size_t)m * 2 * J * N);
+            prepare(c, entries, 2 * LN, nullptr, m, prep);
+        }
+        const u32 R = tile_rows(c);
+        u64* dsel = c.partial.get<u64>((size_t)R * 3 * LN);
+        for (u64 r0 = 0; r0 < c.n_local; r0 += R) {
+            const u32 Rt = (u32)std::min<u64>(R, c.n_local - r0);
+            CK(cudaMemsetAsync(dsel, 0, (size_t)Rt * 3 * LN * 8, c.st));
+            u32 nc = 0, zs = 0;
+            select_tile(c, entries, prep, op, r0, Rt, nc, zs, dsel);
+            tm.mark(TM_SELECT);
+            CK(cudaMemcpyAsync(sel + r0 * 3 * LN, dsel, (size_t)Rt * 3 * LN * 8, cudaMemcpyDeviceToHost, c.st));
+            CK(cudaStreamSynchronize(c.st));
+            for (u32 r = 0; r < Rt; ++r) comps[r0 + r] = nc;
+            tm.mark(TM_D2H);
+        }
+        fill_timings(c, tm, t,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    });
+}
+
+int cwg_ntt(cwg_ctx* h, int chain, uint32_t idx, uint64_t* data, uint32_t count, int inverse) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        const u32 N = c.cp.N;
+        if (chain) {
+            if (idx >= c.cp.L) throw std::invalid_argument("prime index out of range");
+            // lay the polys out as p = x*L + idx so that prime(p) = idx
+            u64* d = c.exA.get<u64>((size_t)count * c.cp.L * N);
+            for (u32 x = 0; x < count; ++x)
+                CK(cudaMemcpyAsync(d + ((size_t)x * c.cp.L + idx) * N, data + (size_t)x * N, N * 8,
+                                   cudaMemcpyHostToDevice, c.st));
+            ntt64(c, d, count * c.cp.L, inverse != 0);
+            for (u32 x = 0; x < count; ++x)
+                CK(cudaMemcpyAsync(data + (size_t)x * N, d + ((size_t)x * c.cp.L + idx) * N, N * 8,
+                                   cudaMemcpyDeviceToHost, c.st));
+        } else {
+            if (idx >= c.ab.J) throw std::invalid_argument("prime index out of range");
+            std::vector<u32> tmp((size_t)count * N);
+            for (size_t x = 0; x < tmp.size(); ++x) tmp[x] = (u32)data[x];
+            u32* d = c.lift_tmp.get<u32>(tmp.size());
+            CK(cudaMemcpyAsync(d, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, c.st));
+            // group size 1, stride 1, offset idx: poly p at (p + idx) * N uses prime idx
+            ntt32(c, d - (size_t)idx * N, count, 1, 1, idx, inverse != 0, 0);
+            CK(cudaMemcpyAsync(tmp.data(), d, tmp.size() * 4, cudaMemcpyDeviceToHost, c.st));
+            CK(cudaStreamSynchronize(c.st));
+            for (size_t x = 0; x < tmp.size(); ++x) data[x] = tmp[x];
+        }
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int cwg_expand(cwg_ctx* h, uint32_t nq, uint32_t comp, uint32_t m, const uint64_t* query, uint64_t* out) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        if (!c.have_keys) throw he_err("evaluation keys not set");
+        const size_t per = 2 * (size_t)c.cp.L * c.cp.N;
+        u64* dq = c.query.get<u64>(nq * per);
+        CK(cudaMemcpyAsync(dq, query, nq * per * 8, cudaMemcpyHostToDevice, c.st));
+        u64* e = expand(c, dq, nq, comp, m);
+        CK(cudaMemcpyAsync(out, e, (size_t)m * per * 8, cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int cwg_mul_lazy(cwg_ctx* h, uint32_t count, const uint64_t* a, const uint64_t* b, uint64_t* out) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        const u32 N = c.cp.N, J = c.ab.J;
+        const size_t per = 2 * (size_t)c.cp.L * N;
+        u64* d = c.exA.get<u64>(2 * (size_t)count * per);
+        CK(cudaMemcpyAsync(d, a, count * per * 8, cudaMemcpyHostToDevice, c.st));
+        CK(cudaMemcpyAsync(d + count * per, b, count * per * 8, cudaMemcpyHostToDevice, c.st));
+        u32* pr = c.prep.get<u32>((size_t)2 * count * 2 * J * N);
+        prepare(c, d, per, nullptr, 2 * count, pr);
+        u64* o = c.chain3.get<u64>((size_t)count * 3 * c.cp.L * N);
+        mul_prepared(c, pr, nullptr, pr + (size_t)count * 2 * J * N, nullptr, count, false, o);
+        CK(cudaMemcpyAsync(out, o, (size_t)count * 3 * c.cp.L * N * 8, cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int cwg_relinearize(cwg_ctx* h, uint32_t count, const uint64_t* ct3, uint64_t* out2) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        if (!c.have_keys) throw he_err("evaluation keys not set");
+        const size_t LN = (size_t)c.cp.L * c.cp.N;
+        u64* d = c.chain3.get<u64>(count * 3 * LN);
+        CK(cudaMemcpyAsync(d, ct3, count * 3 * LN * 8, cudaMemcpyHostToDevice, c.st));
+        u64* o = c.out2.get<u64>(count * 2 * LN);
+        relinearize(c, d, count, o);
+        CK(cudaMemcpyAsync(out2, o, count * 2 * LN * 8, cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int cwg_substitute(cwg_ctx* h, uint32_t count, const uint64_t* ct, uint64_t g, uint64_t* out) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> lk(c.mu);
+        CK(cudaSetDevice(c.device));
+        if (!c.have_keys) throw he_err("evaluation keys not set");
+        const u32 N = c.cp.N, L = c.cp.L;
+        if (g % 2 == 0 || g >= 2 * (u64)N) throw std::invalid_argument("automorphism exponent must be odd in (0, 2N)");
+        const u64* key = galois_key(c, g);
+        const size_t per = 2 * (size_t)L * N;
+        u64* d = c.exA.get<u64>(count * per);
+        CK(cudaMemcpyAsync(d, ct, count * per * 8, cudaMemcpyHostToDevice, c.st));
+        u64* ks = c.ks.get<u64>(count * per);
+        const u64 ginv = inv_mod_2n(g, 2 * (u64)N);
+        key_switch(c, d + (size_t)L * N, per, ginv, count, key, c.cp.galois_bits, c.cp.Dg, ks);
+        u64* o = c.out2.get<u64>(count * per);
+        launch(c, k_subst_combine, blocks((size_t)count * L * N, 256), 256, 0, (const u64*)d, (const u64*)ks, count,
+               ginv, c.T, o);
+        CK(cudaMemcpyAsync(out, o, count * per * 8, cudaMemcpyDeviceToHost, c.st));
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+uint64_t cwg_kernel_launches(const cwg_ctx* h) { return h->c.launches; }
+
+}  // extern "C"

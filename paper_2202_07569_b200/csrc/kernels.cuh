@@ -1,0 +1,892 @@
+// sm_100a kernels for the constant-weight PIR server answer.
+//
+// Reference functions replaced (all under /root/reference/proj/core/src):
+//   k_ntt64 / ntt64 smem     RingContext::ntt_forward / ntt_inverse   ring.cpp:78-144
+//   k_ntt32                  same transform over the 31-bit aux / MAC primes (our basis)
+//   k_decompose              decompose_digits + crt_q                 bfv.cpp:316-339, 197-209
+//   k_ks_mac                 key_switch accumulation                  bfv.cpp:352-363
+//   k_expand_combine         expand_one node update                   expansion.cpp:55-59,
+//                            automorphism / monomial_mul              ring.cpp:296-331
+//   k_lift                   to_aux_basis                             bfv.cpp:718-744
+//   k_tensor_intt            mul_lazy_prepared tensor + INTT          bfv.cpp:776-791
+//   k_round_mac/_chain       exact scale-and-round t/q                bfv.cpp:811-849
+//   k_mac                    weighted_sum                             bfv.cpp:944-986
+//   k_relin_add              relinearize                              bfv.cpp:859-869
+#pragma once
+#include "devtab.h"
+#include "modarith.cuh"
+
+namespace cwgpu {
+
+typedef long long i64;
+
+// ============================================================== NTT in shared memory
+// Chain primes: Harvey lazy butterflies exactly as ring.cpp:78-144 ([0,4q) ranges).
+__device__ __forceinline__ void ntt64_fwd_smem(u64* sm, u32 N, u32 logN, const u64* rp, const u64* rps, u64 q) {
+    const u64 tq = 2 * q;
+    u32 logt = logN - 1;
+    for (u32 m = 1; m < N; m <<= 1, --logt) {
+        const u32 t = 1u << logt;
+        for (u32 k = threadIdx.x; k < (N >> 1); k += blockDim.x) {
+            const u32 ii = k >> logt, jj = k & (t - 1);
+            const u32 lo = (ii << (logt + 1)) + jj, hi = lo + t;
+            const u64 w = __ldg(rp + m + ii), ws = __ldg(rps + m + ii);
+            u64 u = sm[lo];
+            if (u >= tq) u -= tq;
+            const u64 v = shoup64(sm[hi], w, ws, q);
+            sm[lo] = u + v;
+            sm[hi] = u - v + tq;
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void ntt64_inv_smem(u64* sm, u32 N, u32 logN, const u64* rp, const u64* rps, u64 q) {
+    const u64 tq = 2 * q;
+    u32 logt = 0;
+    for (u32 m = N; m > 1; m >>= 1, ++logt) {
+        const u32 h = m >> 1, t = 1u << logt;
+        for (u32 k = threadIdx.x; k < (N >> 1); k += blockDim.x) {
+            const u32 ii = k >> logt, jj = k & (t - 1);
+            const u32 lo = (ii << (logt + 1)) + jj, hi = lo + t;
+            const u64 w = __ldg(rp + h + ii), ws = __ldg(rps + h + ii);
+            const u64 u = sm[lo], v = sm[hi];
+            u64 s = u + v;
+            if (s >= tq) s -= tq;
+            sm[lo] = s;
+            sm[hi] = shoup64(u - v + tq, w, ws, q);
+        }
+        __syncthreads();
+    }
+}
+
+// 31-bit primes: values kept in [0, 2p) (2p < 2^32).
+__device__ __forceinline__ void ntt32_fwd_smem(u32* sm, u32 N, u32 logN, const u32* rp, const u32* rps, u32 p) {
+    u32 logt = logN - 1;
+    for (u32 m = 1; m < N; m <<= 1, --logt) {
+        const u32 t = 1u << logt;
+        for (u32 k = threadIdx.x; k < (N >> 1); k += blockDim.x) {
+            const u32 ii = k >> logt, jj = k & (t - 1);
+            const u32 lo = (ii << (logt + 1)) + jj, hi = lo + t;
+            const u32 w = __ldg(rp + m + ii), ws = __ldg(rps + m + ii);
+            const u32 u = red32(sm[lo], p);
+            const u32 v = red32(shoup32(sm[hi], w, ws, p), p);
+            sm[lo] = u + v;
+            sm[hi] = u - v + p;
+        }
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void ntt32_inv_smem(u32* sm, u32 N, u32 logN, const u32* rp, const u32* rps, u32 p) {
+    u32 logt = 0;
+    for (u32 m = N; m > 1; m >>= 1, ++logt) {
+        const u32 h = m >> 1, t = 1u << logt;
+        for (u32 k = threadIdx.x; k < (N >> 1); k += blockDim.x) {
+            const u32 ii = k >> logt, jj = k & (t - 1);
+            const u32 lo = (ii << (logt + 1)) + jj, hi = lo + t;
+            const u32 w = __ldg(rp + h + ii), ws = __ldg(rps + h + ii);
+            const u32 u = red32(sm[lo], p), v = red32(sm[hi], p);
+            sm[lo] = u + v;
+            sm[hi] = shoup32(u - v + p, w, ws, p);
+        }
+        __syncthreads();
+    }
+}
+
+/// Batched 64-bit NTT over chain primes; poly p uses prime p % L.
+/// SRC_DIGITS: input row (p / L) of a digit array, reduced mod q_i (bfv.cpp:355-358).
+template <bool INV, bool SRC_DIGITS>
+__global__ void k_ntt64(u64* __restrict__ dst, const u64* __restrict__ src, DevTab T) {
+    extern __shared__ u64 sm64[];
+    const u32 N = T.N;
+    const u32 p = blockIdx.x, i = p % T.L;
+    const u64 q = T.q[i];
+    const u64* s = SRC_DIGITS ? src + (size_t)(p / T.L) * N : dst + (size_t)p * N;
+    for (u32 x = threadIdx.x; x < N; x += blockDim.x) {
+        u64 v = s[x];
+        if (SRC_DIGITS && v >= q) v %= q;
+        sm64[x] = v;
+    }
+    __syncthreads();
+    u64* o = dst + (size_t)p * N;
+    if (!INV) {
+        ntt64_fwd_smem(sm64, N, T.logN, T.crp + (size_t)i * N, T.crps + (size_t)i * N, q);
+        const u64 tq = 2 * q;
+        for (u32 x = threadIdx.x; x < N; x += blockDim.x) {
+            u64 v = sm64[x];
+            if (v >= tq) v -= tq;
+            if (v >= q) v -= q;
+            o[x] = v;
+        }
+    } else {
+        ntt64_inv_smem(sm64, N, T.logN, T.cirp + (size_t)i * N, T.cirps + (size_t)i * N, q);
+        const u64 ni = T.ninv[i], nis = T.ninv_s[i];
+        for (u32 x = threadIdx.x; x < N; x += blockDim.x) {
+            u64 v = shoup64(sm64[x], ni, nis, q);
+            if (v >= q) v -= q;
+            o[x] = v;
+        }
+    }
+}
+
+/// Batched 32-bit NTT over aux primes. Poly p: group g = p / gs, prime j = off + p % gs,
+/// address (g * stride + j) * N.  scale: 0 = N^-1, 1 = (N 2^32)^-1 (Montgomery undo).
+template <bool INV>
+__global__ void k_ntt32(u32* __restrict__ base, DevTab T, u32 gs, u32 stride, u32 off, int scale) {
+    extern __shared__ u32 sm32[];
+    const u32 N = T.N;
+    const u32 p = blockIdx.x, g = p / gs, j = off + p % gs;
+    const u32 pr = T.a[j];
+    u32* d = base + ((size_t)g * stride + j) * N;
+    for (u32 x = threadIdx.x; x < N; x += blockDim.x) sm32[x] = d[x];
+    __syncthreads();
+    if (!INV) {
+        ntt32_fwd_smem(sm32, N, T.logN, T.arp + (size_t)j * N, T.arps + (size_t)j * N, pr);
+        for (u32 x = threadIdx.x; x < N; x += blockDim.x) d[x] = red32(sm32[x], pr);
+    } else {
+        ntt32_inv_smem(sm32, N, T.logN, T.airp + (size_t)j * N, T.airps + (size_t)j * N, pr);
+        const u32 ni = scale ? T.ninvRA[j] : T.ninvA[j], nis = scale ? T.ninvRA_s[j] : T.ninvA_s[j];
+        for (u32 x = threadIdx.x; x < N; x += blockDim.x) d[x] = red32(shoup32(sm32[x], ni, nis, pr), pr);
+    }
+}
+
+// ============================================================== multiword helpers (32-bit limbs)
+// X (kQW+2 limbs) += y * src (n limbs) << (32 * OFF)
+template <u32 OFF>
+__device__ __forceinline__ void mw_mac(u32* X, const u32* src, u32 n, u32 y) {
+    constexpr u32 off = OFF;
+    u64 c = 0;
+#pragma unroll
+    for (u32 k = 0; k < kQW; ++k) {
+        if (k < n) {
+            u64 cur = (u64)X[k + off] + (u64)y * __ldg(src + k) + c;
+            X[k + off] = (u32)cur;
+            c = cur >> 32;
+        }
+    }
+#pragma unroll
+    for (u32 k = 0; k < kQW + 2; ++k) {
+        if (k >= n + off && c) {
+            u64 cur = (u64)X[k] + c;
+            X[k] = (u32)cur;
+            c = cur >> 32;
+        }
+    }
+}
+
+// X -= y * src (n limbs); caller guarantees no underflow.
+__device__ __forceinline__ void mw_msub(u32* X, const u32* src, u32 n, u32 y) {
+    u64 c = 0;
+    u32 br = 0;
+#pragma unroll
+    for (u32 k = 0; k < kQW + 2; ++k) {
+        u64 pk = (k < n ? (u64)y * __ldg(src + k) : 0) + c;
+        c = pk >> 32;
+        const u32 pl = (u32)pk, x = X[k];
+        const u32 r1 = x - pl;
+        const u32 b1 = x < pl;
+        const u32 r2 = r1 - br;
+        const u32 b2 = r1 < br;
+        X[k] = r2;
+        br = b1 | b2;
+    }
+}
+
+// X >= src (n limbs)?
+__device__ __forceinline__ bool mw_ge(const u32* X, const u32* src, u32 n) {
+    int res = 1;  // equal -> ge
+#pragma unroll
+    for (int k = kQW + 1; k >= 0; --k) {
+        const u32 s = (u32)k < n ? __ldg(src + k) : 0u;
+        if (res == 1 && X[k] != s) res = X[k] > s ? 2 : 0;
+    }
+    return res != 0;
+}
+
+/// CRT of chain residues y_i (already multiplied by (q/q_i)^-1) into the integer
+/// x = sum y_i (q/q_i) - alpha q in [0, q) (32-bit limbs), alpha from the fractional
+/// estimate (an underestimate by at most one) then corrected (crt_q, bfv.cpp:197-209).
+/// Returns alpha.
+__device__ __forceinline__ u32 crt_exact(const u64* y, u32 alpha_est, const DevTab& T, u32* X) {
+#pragma unroll
+    for (u32 k = 0; k < kQW + 2; ++k) X[k] = 0;
+    for (u32 i = 0; i < T.L; ++i) {
+        mw_mac<0>(X, T.qov + (size_t)i * T.QW, T.QW, (u32)y[i]);
+        mw_mac<1>(X, T.qov + (size_t)i * T.QW, T.QW, (u32)(y[i] >> 32));
+    }
+    mw_msub(X, T.qw, T.QW, alpha_est);
+    if (mw_ge(X, T.qw, T.QW)) {
+        mw_msub(X, T.qw, T.QW, 1u);
+        return alpha_est + 1;
+    }
+    return alpha_est;
+}
+
+/// y_i = res_i (q/q_i)^-1 mod q_i and the fractional sum of y_i / q_i
+/// (integer part in *ip, 64-bit fraction returned; underestimate by < 2L units).
+__device__ __forceinline__ u64 crt_prepare(const u64* res, const DevTab& T, u64* y, u32* ip) {
+    u64 lo = 0;
+    u32 carry = 0;
+    for (u32 i = 0; i < T.L; ++i) {
+        const u64 q = T.q[i];
+        y[i] = red64(shoup64(res[i], T.muq[i], T.muq_s[i], q), q);
+        const u64 f = frac64(y[i], T.q_gh[i], T.q_gl[i]);
+        lo += f;
+        carry += (lo < f);
+    }
+    *ip = carry;
+    return lo;
+}
+
+/// rho = round(sum y_i / q_i): x > floor(q/2) decides (bfv.cpp:731).  Exact: the
+/// fractional estimate decides unless it lies within its error band below 1/2.
+__device__ __noinline__ u32 crt_round_exact(const u64* y, u32 ip, const DevTab& T) {
+    u32 X[kQW + 2];
+    const u32 alpha = crt_exact(y, ip, T, X);
+    u32 c = 0;  // X <- 2X
+#pragma unroll
+    for (u32 k = 0; k < kQW + 2; ++k) {
+        const u32 nv = (X[k] << 1) | c;
+        c = X[k] >> 31;
+        X[k] = nv;
+    }
+    atomicAdd(T.fallbacks, 1ull);
+    return alpha + (mw_ge(X, T.qw, T.QW) ? 1u : 0u);  // 2X >= q <=> 2X > q (q odd)
+}
+
+__device__ __forceinline__ u32 crt_round(const u64* y, u32 ip, u64 frac, const DevTab& T) {
+    if (frac >= (1ull << 63)) return ip + 1;
+    if (frac < (1ull << 63) - 2ull * T.L - 2ull) return ip;
+    return crt_round_exact(y, ip, T);
+}
+
+// ============================================================== expansion / key switching
+/// Digit decomposition (bfv.cpp:316-339) of B polys (each L x N at polys + b*stride),
+/// optionally through the automorphism with inverse exponent ginv (0 = identity).
+/// digits: [B][D][N].
+__global__ void k_decompose(const u64* __restrict__ polys, size_t stride, u64 ginv, u32 B, u32 bits,
+                            u32 D, DevTab T, u64* __restrict__ digits) {
+    const u32 N = T.N;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)B * N) return;
+    const u32 b = (u32)(idx / N), n = (u32)(idx % N);
+    const u64* pb = polys + (size_t)b * stride;
+    u32 src = n;
+    bool neg = false;
+    if (ginv) {
+        const u32 s = (u32)(((u64)n * ginv) & (2 * N - 1));
+        neg = s >= N;
+        src = neg ? s - N : s;
+    }
+    u64 res[kMaxL];
+    for (u32 i = 0; i < T.L; ++i) {
+        u64 v = pb[(size_t)i * N + src];
+        if (neg && v) v = T.q[i] - v;
+        res[i] = v;
+    }
+    u64* out = digits + (size_t)b * D * N + n;
+    if (bits == 0) {  // one RNS digit per chain prime (bfv.cpp:320-323)
+        for (u32 d = 0; d < D; ++d) out[(size_t)d * N] = res[d];
+        return;
+    }
+    u64 y[kMaxL];
+    u32 ip;
+    crt_prepare(res, T, y, &ip);
+    u32 X[kQW + 2];
+    crt_exact(y, ip, T, X);
+    const u64 mask = (bits == 64) ? ~0ull : ((1ull << bits) - 1);
+    for (u32 d = 0; d < D; ++d) {
+        const u32 bit = d * bits, limb = bit >> 5, off = bit & 31;
+        u64 v = 0;
+        // gather 96 bits starting at limb
+        u32 l0 = 0, l1 = 0, l2 = 0;
+#pragma unroll
+        for (u32 k = 0; k < kQW + 2; ++k) {
+            if (k == limb) l0 = X[k];
+            if (k == limb + 1) l1 = X[k];
+            if (k == limb + 2) l2 = X[k];
+        }
+        const u64 lo64 = ((u64)l1 << 32) | l0;
+        v = lo64 >> off;
+        if (off) v |= ((u64)l2 << (64 - off));
+        out[(size_t)d * N] = v & mask;
+    }
+}
+
+/// ks[b][k][i][n] = sum_d dntt[b][d][i][n] * key[d][k][i][n] mod q_i (key_switch MAC).
+__global__ void k_ks_mac(const u64* __restrict__ dntt, const u64* __restrict__ key, u32 B, u32 D, DevTab T,
+                         u64* __restrict__ ks) {
+    const u32 N = T.N, L = T.L;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t per = (size_t)2 * L * N;
+    if (idx >= (size_t)B * per) return;
+    const u32 b = (u32)(idx / per);
+    const u32 rem = (u32)(idx % per);
+    const u32 k = rem / (L * N), i = (rem / N) % L, n = rem % N;
+    u64 hi = 0, lo = 0;
+    const u64* dp = dntt + ((size_t)b * D * L + i) * N + n;
+    const u64* kp = key + ((size_t)k * L + i) * N + n;
+    for (u32 d = 0; d < D; ++d) mac128(hi, lo, dp[(size_t)d * L * N], __ldg(kp + (size_t)d * 2 * L * N));
+    ks[idx] = reduce128(hi, lo, T.q[i], T.q_mu96[i]);
+}
+
+/// One expansion level node update for all B ciphertexts (expansion.cpp:55-59):
+///   sub = (auto_g(c0) + ks0, ks1)
+///   out[b]     = ct_b + sub
+///   out[b + partner] = x^(-2^a) (ct_b - sub)   (partner = 2^a)
+__global__ void k_expand_combine(const u64* __restrict__ in, const u64* __restrict__ ks, u32 B, u32 partner,
+                                 u64 ginv, u32 shift, DevTab T, u64* __restrict__ out) {
+    const u32 N = T.N, L = T.L;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)B * L * N) return;
+    const u32 b = (u32)(idx / ((size_t)L * N));
+    const u32 i = (u32)((idx / N) % L), e = (u32)(idx % N);
+    const u64 q = T.q[i];
+    const size_t LN = (size_t)L * N;
+    const u64* c0 = in + (size_t)b * 2 * LN + (size_t)i * N;
+    const u64* c1 = c0 + LN;
+    const u64* k0 = ks + (size_t)b * 2 * LN + (size_t)i * N;
+    const u64* k1 = k0 + LN;
+    auto auto_c0 = [&](u32 x) -> u64 {
+        const u32 s = (u32)(((u64)x * ginv) & (2 * N - 1));
+        if (s < N) return c0[s];
+        const u64 v = c0[s - N];
+        return v ? q - v : 0;
+    };
+    auto addq = [&](u64 a, u64 c) { u64 s = a + c; return s >= q ? s - q : s; };
+    auto subq = [&](u64 a, u64 c) { return a >= c ? a - c : a + q - c; };
+    // out[b] at e
+    const u64 s0e = addq(auto_c0(e), k0[e]), s1e = k1[e];
+    u64* o0 = out + (size_t)b * 2 * LN + (size_t)i * N;
+    o0[e] = addq(c0[e], s0e);
+    o0[LN + e] = addq(c1[e], s1e);
+    // out[b + B] at e: source index x = (e + 2^a) mod 2N
+    const u32 sm = (e + shift) & (2 * N - 1);
+    const bool neg = sm >= N;
+    const u32 x = neg ? sm - N : sm;
+    const u64 s0x = addq(auto_c0(x), k0[x]), s1x = k1[x];
+    u64 v0 = subq(c0[x], s0x), v1 = subq(c1[x], s1x);
+    if (neg) {
+        v0 = v0 ? q - v0 : 0;
+        v1 = v1 ? q - v1 : 0;
+    }
+    u64* o1 = out + (size_t)(b + partner) * 2 * LN + (size_t)i * N;
+    o1[e] = v0;
+    o1[LN + e] = v1;
+}
+
+/// out2 = (c0 + ks0, c1 + ks1) for B ciphertexts; ct3 stride 3LN, ks stride 2LN (relinearize).
+__global__ void k_relin_add(const u64* __restrict__ ct3, size_t ct_stride, const u64* __restrict__ ks, u32 B,
+                            DevTab T, u64* __restrict__ out2) {
+    const u32 N = T.N, L = T.L;
+    const size_t LN = (size_t)L * N;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)B * 2 * LN) return;
+    const size_t b = idx / (2 * LN), r = idx % (2 * LN);
+    const u32 i = (u32)((r / N) % L);
+    const u64 q = T.q[i];
+    u64 s = ct3[b * ct_stride + r] + ks[idx];
+    out2[idx] = s >= q ? s - q : s;
+}
+
+// ============================================================== aux / MAC lift
+/// Centred lift of chain ciphertexts into aux residues (to_aux_basis, bfv.cpp:718-744):
+/// for count ciphertexts (2 comps each, ct c at src + sel(c) * src_stride),
+/// out[c][k][j][n] for j < nj, constants mont (x 2^32, tensor operands) or plain.
+__global__ void k_lift(const u64* __restrict__ src, size_t src_stride, const u32* __restrict__ sel, u32 count,
+                       u32 nj, int mont, DevTab T, u32* __restrict__ out, u32 out_stride_j) {
+    const u32 N = T.N, L = T.L;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)count * 2 * N) return;
+    const u32 c = (u32)(idx / (2 * N)), k = (u32)((idx / N) % 2), n = (u32)(idx % N);
+    const u64* s = src + (size_t)(sel ? sel[c] : c) * src_stride + (size_t)k * L * N + n;
+    u64 res[kMaxL], y[kMaxL];
+    for (u32 i = 0; i < L; ++i) res[i] = s[(size_t)i * N];
+    u32 ip;
+    const u64 fr = crt_prepare(res, T, y, &ip);
+    const u32 rho = crt_round(y, ip, fr, T);
+    const u32* V = mont ? T.liftV_m : T.liftV_n;
+    const u32* V2 = mont ? T.liftV2_m : T.liftV2_n;
+    const u32* W = mont ? T.liftW_m : T.liftW_n;
+    u32* o = out + ((size_t)c * 2 + k) * out_stride_j * N + n;
+    for (u32 j = 0; j < nj; ++j) {
+        const u32 a = T.a[j];
+        u64 accA = 0, accB = (u64)rho * (a - W[j]);
+        for (u32 i = 0; i < L; ++i) {
+            accA += (u64)(u32)(y[i] & ((1u << 30) - 1)) * V[i * T.J + j];
+            accB += (u64)(u32)(y[i] >> 30) * V2[i * T.J + j];
+        }
+        const u64 ab = T.abar[j];
+        o[(size_t)j * N] = red32(bar64(accA, a, ab) + bar64(accB, a, ab), a);
+    }
+}
+
+// ============================================================== tensor + INTT (aux)
+/// Tensor product of prepared operands (mul_lazy_prepared, bfv.cpp:776-791) for P
+/// products and one aux prime per CTA, then INTT; D[p][comp][j][N] normal form.
+__global__ void k_tensor_intt(const u32* __restrict__ prepA, const u32* __restrict__ idxA,
+                              const u32* __restrict__ prepB, const u32* __restrict__ idxB, u32 P, DevTab T,
+                              u32* __restrict__ D) {
+    extern __shared__ u32 sm32[];
+    const u32 N = T.N, J = T.J;
+    const u32 pr = blockIdx.x / J, j = blockIdx.x % J;
+    const u32 p = T.a[j], pinv = T.apinv[j];
+    const size_t per = (size_t)2 * J * N;
+    const u32* A = prepA + (size_t)(idxA ? idxA[pr] : pr) * per + (size_t)j * N;
+    const u32* B = prepB + (size_t)(idxB ? idxB[pr] : pr) * per + (size_t)j * N;
+    const size_t o1 = (size_t)J * N;
+    for (u32 comp = 0; comp < 3; ++comp) {
+        for (u32 x = threadIdx.x; x < N; x += blockDim.x) {
+            u32 d;
+            if (comp == 0) {
+                d = red32(mont32(A[x], B[x], p, pinv), p);
+            } else if (comp == 1) {
+                d = red32(mont32(A[x], B[o1 + x], p, pinv), p) + red32(mont32(A[o1 + x], B[x], p, pinv), p);
+            } else {
+                d = red32(mont32(A[o1 + x], B[o1 + x], p, pinv), p);
+            }
+            sm32[x] = d;
+        }
+        __syncthreads();
+        ntt32_inv_smem(sm32, N, T.logN, T.airp + (size_t)j * N, T.airps + (size_t)j * N, p);
+        const u32 ni = T.ninvRA[j], nis = T.ninvRA_s[j];
+        u32* out = D + (((size_t)pr * 3 + comp) * J + j) * N;
+        for (u32 x = threadIdx.x; x < N; x += blockDim.x) out[x] = red32(shoup32(sm32[x], ni, nis, p), p);
+        __syncthreads();
+    }
+}
+
+// ============================================================== exact scale-and-round
+struct HpsState {
+    u32 w[kMaxJ];
+    u32 gamma;
+    i64 rho;       // round(sum w_j F_j - gamma F_A)
+    bool exact;    // fast path decided
+};
+
+/// HPS scaling: r = sum_j w_j I_j - gamma I_A + round(sum_j w_j F_j - gamma F_A), with
+/// t (A/a_j) = I_j q + F_j q.  Returns false when the 96-bit fractional estimate cannot
+/// decide the rounding (then the exact multiword path runs).
+__device__ __forceinline__ bool hps_prepare(const u32* __restrict__ Dp, size_t jstride, const DevTab& T, HpsState& h) {
+    const u32 J = T.J;
+    u64 gs = 0;
+    u32 s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
+    for (u32 j = 0; j < J; ++j) {
+        const u32 a = T.a[j];
+        const u32 w = red32(shoup32(Dp[(size_t)j * jstride], T.chat[j], T.chat_s[j], a), a);
+        h.w[j] = w;
+        gs += (u64)w * T.aF[j];
+        const u32 f0 = T.frac96[3 * j], f1 = T.frac96[3 * j + 1], f2 = T.frac96[3 * j + 2];
+        asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
+            "madc.lo.cc.u32 %1, %5, %7, %1;\n\t"
+            "madc.lo.cc.u32 %2, %5, %8, %2;\n\t"
+            "addc.cc.u32    %3, %3, 0;\n\t"
+            "addc.u32       %4, %4, 0;\n\t"
+            "mad.hi.cc.u32  %1, %5, %6, %1;\n\t"
+            "madc.hi.cc.u32 %2, %5, %7, %2;\n\t"
+            "madc.hi.cc.u32 %3, %5, %8, %3;\n\t"
+            "addc.u32       %4, %4, 0;\n\t"
+            : "+r"(s0), "+r"(s1), "+r"(s2), "+r"(s3), "+r"(s4)
+            : "r"(w), "r"(f0), "r"(f1), "r"(f2));
+    }
+    const u32 gsh = 64 - T.gbits;
+    const u32 gamma = (u32)((gs + (1ull << (gsh - 1))) >> gsh);
+    h.gamma = gamma;
+    // subtract gamma * fracA (96-bit) as a 128-bit value
+    {
+        const u32 f0 = T.fracA[0], f1 = T.fracA[1], f2 = T.fracA[2];
+        const u64 p0 = (u64)gamma * f0, p1 = (u64)gamma * f1, p2 = (u64)gamma * f2;
+        // P = p0 + p1 << 32 + p2 << 64
+        u32 q0 = (u32)p0;
+        u64 t1 = (p0 >> 32) + (u32)p1;
+        u32 q1 = (u32)t1;
+        u64 t2 = (t1 >> 32) + (p1 >> 32) + (u32)p2;
+        u32 q2 = (u32)t2;
+        u64 t3 = (t2 >> 32) + (p2 >> 32);
+        u32 q3 = (u32)t3;
+        asm("sub.cc.u32  %0, %0, %5;\n\t"
+            "subc.cc.u32 %1, %1, %6;\n\t"
+            "subc.cc.u32 %2, %2, %7;\n\t"
+            "subc.cc.u32 %3, %3, %8;\n\t"
+            "subc.u32    %4, %4, 0;\n\t"
+            : "+r"(s0), "+r"(s1), "+r"(s2), "+r"(s3), "+r"(s4)
+            : "r"(q0), "r"(q1), "r"(q2), "r"(q3));
+    }
+    // + 1/2
+    asm("add.cc.u32  %0, %0, 0x80000000;\n\t"
+        "addc.cc.u32 %1, %1, 0;\n\t"
+        "addc.u32    %2, %2, 0;\n\t"
+        : "+r"(s2), "+r"(s3), "+r"(s4));
+    h.rho = (i64)(((u64)s4 << 32) | s3);
+    // estimate error in (-J, J 2^31) units of 2^-96: undecidable near a wrap of the low 96 bits
+    const bool bad = (s2 == 0u && s1 == 0u) || (s2 == 0xffffffffu && s1 >= 0xffffff00u);
+    h.exact = !bad;
+    return !bad;
+}
+
+/// Exact slow path: D = sum_j w_j (A/a_j) - gamma A (signed), r = sign(D) round(|D| t / q)
+/// by long division (bfv.cpp:811-849). Writes the magnitude limbs into R and returns sign.
+__device__ __noinline__ bool round_exact(const HpsState& h, const DevTab& T, u32* R /*kAW+2*/) {
+    u32 Dm[kAW + 2];
+    for (u32 k = 0; k < kAW + 2; ++k) Dm[k] = 0;
+    for (u32 j = 0; j < T.J; ++j) {
+        u64 c = 0;
+        const u32* src = T.Aov + (size_t)j * T.AW;
+        for (u32 k = 0; k < T.AW; ++k) {
+            u64 cur = (u64)Dm[k] + (u64)h.w[j] * src[k] + c;
+            Dm[k] = (u32)cur;
+            c = cur >> 32;
+        }
+        for (u32 k = T.AW; k < kAW + 2 && c; ++k) {
+            u64 cur = (u64)Dm[k] + c;
+            Dm[k] = (u32)cur;
+            c = cur >> 32;
+        }
+    }
+    // Dm - gamma * A ; if negative, negate
+    u32 G[kAW + 2];
+    {
+        u64 c = 0;
+        for (u32 k = 0; k < kAW + 2; ++k) {
+            u64 cur = (k < T.AW ? (u64)h.gamma * T.Aw[k] : 0) + c;
+            G[k] = (u32)cur;
+            c = cur >> 32;
+        }
+    }
+    bool neg = false;
+    {
+        int cmp = 0;
+        for (int k = kAW + 1; k >= 0 && !cmp; --k)
+            if (Dm[k] != G[k]) cmp = Dm[k] > G[k] ? 1 : -1;
+        neg = cmp < 0;
+        const u32* X = neg ? G : Dm;
+        const u32* Y = neg ? Dm : G;
+        u32 br = 0;
+        for (u32 k = 0; k < kAW + 2; ++k) {
+            u64 need = (u64)Y[k] + br;
+            u64 cur = X[k];
+            Dm[k] = (u32)(cur - need);
+            br = cur < need;
+        }
+    }
+    // |D| * t
+    {
+        u64 c = 0;
+        for (u32 k = 0; k < kAW + 2; ++k) {
+            u64 cur = (u64)Dm[k] * (u32)T.t + c;
+            Dm[k] = (u32)cur;
+            c = cur >> 32;
+        }
+    }
+    // long division by q, bitwise
+    u32 Rm[kQW + 2];
+    for (u32 k = 0; k < kQW + 2; ++k) Rm[k] = 0;
+    for (u32 k = 0; k < kAW + 2; ++k) R[k] = 0;
+    for (int bit = 32 * (kAW + 2) - 1; bit >= 0; --bit) {
+        u32 c = (Dm[bit >> 5] >> (bit & 31)) & 1u;
+        for (u32 k = 0; k < kQW + 2; ++k) {
+            u32 nv = (Rm[k] << 1) | c;
+            c = Rm[k] >> 31;
+            Rm[k] = nv;
+        }
+        if (mw_ge(Rm, T.qw, T.QW)) {
+            mw_msub(Rm, T.qw, T.QW, 1u);
+            R[bit >> 5] |= 1u << (bit & 31);
+        }
+    }
+    // round half up on the magnitude: 2 rem >= q
+    {
+        u32 c = 0;
+        for (u32 k = 0; k < kQW + 2; ++k) {
+            u32 nv = (Rm[k] << 1) | c;
+            c = Rm[k] >> 31;
+            Rm[k] = nv;
+        }
+        if (mw_ge(Rm, T.qw, T.QW)) {
+            for (u32 k = 0; k < kAW + 2; ++k)
+                if (++R[k]) break;
+        }
+    }
+    atomicAdd(T.fallbacks, 1ull);
+    return neg;
+}
+
+__device__ __forceinline__ u32 mag_mod32(const u32* R, u32 a, u64 abar) {
+    u32 r = 0;
+    for (int k = kAW + 1; k >= 0; --k) r = bar64(((u64)r << 32) | R[k], a, abar);
+    return r;
+}
+
+__device__ __forceinline__ u64 mag_mod64(const u32* R, u64 q, u64 mu96) {
+    u64 r = 0;
+    for (int k = kAW + 1; k >= 0; --k) r = reduce96((u32)(r >> 32), (r << 32) | R[k], q, mu96);
+    return r;
+}
+
+/// Round t*D/q for P products x 3 comps x N coefficients; writes r mod a_k (k < Mm) in place
+/// into D[p][comp][k][n] (the lazy root's selection value in the MAC basis).
+__global__ void k_round_mac(u32* __restrict__ D, u32 P, DevTab T) {
+    const u32 N = T.N, J = T.J;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)P * 3 * N) return;
+    const size_t pc = idx / N;
+    const u32 n = (u32)(idx % N);
+    u32* Dp = D + pc * J * N + n;
+    HpsState h;
+    if (hps_prepare(Dp, N, T, h)) {
+        for (u32 k = 0; k < T.Mm; ++k) {
+            const u32 a = T.a[k];
+            const u64 ab = T.abar[k];
+            u64 lo = 0, hi = 0;
+            u32 j = 0;
+            for (; j + 4 <= J; j += 4) {  // 4 products < 2^64
+                u64 g = (u64)h.w[j] * T.Imod[(size_t)j * T.Mm + k];
+                g += (u64)h.w[j + 1] * T.Imod[(size_t)(j + 1) * T.Mm + k];
+                g += (u64)h.w[j + 2] * T.Imod[(size_t)(j + 2) * T.Mm + k];
+                g += (u64)h.w[j + 3] * T.Imod[(size_t)(j + 3) * T.Mm + k];
+                lo += g;
+                hi += (lo < g);
+            }
+            u64 g = 0;
+            for (; j < J; ++j) g += (u64)h.w[j] * T.Imod[(size_t)j * T.Mm + k];
+            lo += g;
+            hi += (lo < g);
+            u32 rm = h.rho >= 0 ? bar64((u64)h.rho, a, ab) : bar64((u64)(-h.rho), a, ab);
+            if (h.rho < 0 && rm) rm = a - rm;
+            const u64 tot = (u64)bar64(lo, a, ab) + hi * T.a2_64[k] + (u64)h.gamma * (a - T.IAmod[k]) + rm;
+            Dp[(size_t)k * N] = bar64(tot, a, ab);
+        }
+    } else {
+        u32 R[kAW + 2];
+        const bool neg = round_exact(h, T, R);
+        for (u32 k = 0; k < T.Mm; ++k) {
+            const u32 a = T.a[k];
+            u32 r = mag_mod32(R, a, T.abar[k]);
+            if (neg && r) r = a - r;
+            Dp[(size_t)k * N] = r;
+        }
+    }
+}
+
+/// Round t*D/q into the chain: out[p][comp][i][n] = r mod q_i (mul_lazy_prepared output).
+__global__ void k_round_chain(const u32* __restrict__ D, u32 P, DevTab T, u64* __restrict__ out) {
+    const u32 N = T.N, J = T.J, L = T.L;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)P * 3 * N) return;
+    const size_t pc = idx / N;
+    const u32 n = (u32)(idx % N);
+    const u32* Dp = D + pc * J * N + n;
+    u64* o = out + pc * L * N + n;
+    HpsState h;
+    if (hps_prepare(Dp, N, T, h)) {
+        for (u32 i = 0; i < L; ++i) {
+            const u64 q = T.q[i];
+            u64 hi = 0, lo = 0;
+            for (u32 j = 0; j < J; ++j) mac128(hi, lo, h.w[j], T.ImodQ[(size_t)j * L + i]);
+            mac128(hi, lo, h.gamma, q - T.IAmodQ[i]);
+            u64 r = reduce128(hi, lo, q, T.q_mu96[i]);
+            // + rho (signed, |rho| < 2^40 < q)
+            if (h.rho >= 0) {
+                r += (u64)h.rho;
+                r = red64(r, q);
+            } else {
+                const u64 m = (u64)(-h.rho);
+                r = r >= m ? r - m : r + q - m;
+            }
+            o[(size_t)i * N] = r;
+        }
+    } else {
+        u32 R[kAW + 2];
+        const bool neg = round_exact(h, T, R);
+        for (u32 i = 0; i < L; ++i) {
+            const u64 q = T.q[i];
+            u64 r = mag_mod64(R, q, T.q_mu96[i]);
+            if (neg && r) r = q - r;
+            o[(size_t)i * N] = r;
+        }
+    }
+}
+
+// ============================================================== payload MAC
+/// acc[sj][comp][k][n] (lo, hi planes) += sum_{r < R} Z[r][comp][k][n] * DB[row0 + r][sj][k][n]
+/// Z layout: Z + ((r * nc + comp) * zstride + k) * N. DB: [rows][s][Mm][N] u32 (NTT form, mod a_k).
+__global__ void k_mac(const u32* __restrict__ Z, u32 nc, u32 zstride, const u32* __restrict__ DB, u32 R, u32 s,
+                      DevTab T, u64* __restrict__ acc_lo, u64* __restrict__ acc_hi) {
+    const u32 N = T.N, Mm = T.Mm;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)s * Mm * N) return;
+    const u32 sj = (u32)(idx / ((size_t)Mm * N));
+    const u32 k = (u32)((idx / N) % Mm), n = (u32)(idx % N);
+    u64 lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (u32 c = 0; c < nc; ++c) {
+        const size_t o = (((size_t)sj * 3 + c) * Mm + k) * N + n;
+        lo[c] = acc_lo[o];
+        hi[c] = acc_hi[o];
+    }
+    const size_t dbs = (size_t)s * Mm * N;
+    const u32* dbp = DB + ((size_t)sj * Mm + k) * N + n;
+    u32 r = 0;
+    for (; r + 4 <= R; r += 4) {
+        const u32 d0 = __ldg(dbp + (size_t)r * dbs), d1 = __ldg(dbp + (size_t)(r + 1) * dbs);
+        const u32 d2 = __ldg(dbp + (size_t)(r + 2) * dbs), d3 = __ldg(dbp + (size_t)(r + 3) * dbs);
+        for (u32 c = 0; c < nc; ++c) {
+            const u32* zp = Z + ((size_t)c * zstride + k) * N + n;
+            const size_t zs = (size_t)nc * zstride * N;
+            u64 g = (u64)zp[(size_t)r * zs] * d0;
+            g += (u64)zp[(size_t)(r + 1) * zs] * d1;
+            g += (u64)zp[(size_t)(r + 2) * zs] * d2;
+            g += (u64)zp[(size_t)(r + 3) * zs] * d3;
+            lo[c] += g;
+            hi[c] += (lo[c] < g);
+        }
+    }
+    for (; r < R; ++r) {
+        const u32 d0 = __ldg(dbp + (size_t)r * dbs);
+        for (u32 c = 0; c < nc; ++c) {
+            const u64 g = (u64)Z[(((size_t)r * nc + c) * zstride + k) * N + n] * d0;
+            lo[c] += g;
+            hi[c] += (lo[c] < g);
+        }
+    }
+    for (u32 c = 0; c < nc; ++c) {
+        const size_t o = (((size_t)sj * 3 + c) * Mm + k) * N + n;
+        acc_lo[o] = lo[c];
+        acc_hi[o] = hi[c];
+    }
+}
+
+/// partial[x] = (hi 2^64 + lo) mod a_k (values < 2^31 stored as u64, summable across GPUs).
+__global__ void k_acc_reduce(const u64* __restrict__ acc_lo, const u64* __restrict__ acc_hi, size_t total,
+                             DevTab T, u64* __restrict__ partial) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    const u32 k = (u32)((idx / T.N) % T.Mm);
+    const u32 a = T.a[k];
+    const u64 ab = T.abar[k];
+    const u64 v = (u64)bar64(acc_lo[idx], a, ab) + (u64)bar64(acc_hi[idx], a, ab) * T.a2_64[k];
+    partial[idx] = bar64(v, a, ab);
+}
+
+/// Summed partials -> u32 residues mod a_k (in place into a u32 plane array).
+__global__ void k_partial_mod(const u64* __restrict__ partial, size_t total, DevTab T, u32* __restrict__ X) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    const u32 k = (u32)((idx / T.N) % T.Mm);
+    X[idx] = bar64(partial[idx], T.a[k], T.abar[k]);
+}
+
+/// MAC basis -> chain: X (coefficient form, centred |X| < M/2) -> out[g][i][n] mod q_i.
+/// X layout [G][Mm][N]; out layout [G][L][N].
+__global__ void k_mac_to_chain(const u32* __restrict__ X, u32 G, DevTab T, u64* __restrict__ out) {
+    const u32 N = T.N, Mm = T.Mm, L = T.L;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)G * N) return;
+    const size_t g = idx / N;
+    const u32 n = (u32)(idx % N);
+    u32 v[kMaxJ];
+    u64 gs = 0;
+    for (u32 k = 0; k < Mm; ++k) {
+        const u32 a = T.a[k];
+        v[k] = red32(shoup32(X[(g * Mm + k) * N + n], T.mhat[k], T.mhat_s[k], a), a);
+        gs += (u64)v[k] * T.mF[k];
+    }
+    const u32 gsh = 64 - T.gbits;
+    const u32 gamma = (u32)((gs + (1ull << (gsh - 1))) >> gsh);
+    for (u32 i = 0; i < L; ++i) {
+        const u64 q = T.q[i];
+        u64 hi = 0, lo = 0;
+        for (u32 k = 0; k < Mm; ++k) mac128(hi, lo, v[k], T.Mconv[(size_t)k * L + i]);
+        mac128(hi, lo, gamma, T.MnegQ[i]);
+        out[(g * L + i) * N + n] = reduce128(hi, lo, q, T.q_mu96[i]);
+    }
+}
+
+// ============================================================== row-level helpers
+/// Arithmetic-operator factors: for row r, inner = sum of its k selected
+/// entries; factor f = inner + Delta (t - f) on c0's constant coefficient (add_plain,
+/// bfv.cpp:641-649). out[r][f][2][L][N].
+__global__ void k_arith_factors(const u64* __restrict__ entries, const u32* __restrict__ pos, u32 R, u32 k,
+                                DevTab T, u64* __restrict__ out) {
+    const u32 N = T.N, L = T.L;
+    const size_t LN = (size_t)L * N;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)R * 2 * LN) return;
+    const u32 r = (u32)(idx / (2 * LN));
+    const size_t rem = idx % (2 * LN);
+    const u32 comp = (u32)(rem / LN), i = (u32)((rem / N) % L), n = (u32)(rem % N);
+    const u64 q = T.q[i];
+    u64 s = 0;
+    for (u32 p = 0; p < k; ++p) {
+        s += entries[(size_t)pos[(size_t)r * k + p] * 2 * LN + rem];
+        if (s >= q) s -= q;
+    }
+    for (u32 f = 0; f < k; ++f) {
+        u64 v = s;
+        if (f > 0 && comp == 0 && n == 0) {
+            const u64 m = (T.t - f) % q;
+            // Delta * m mod q_i (small m < 2^31): via 128-bit reduce
+            const u64 dl = T.delta[i];
+            const u64 pl = dl * m, ph = __umul64hi(dl, m);
+            v += reduce128(ph, pl, q, T.q_mu96[i]);
+            if (v >= q) v -= q;
+        }
+        out[(((size_t)r * k + f) * 2) * LN + rem] = v;
+    }
+}
+
+/// Multiply every coefficient of B 2-comp ciphertexts by c mod q_i (plain_mul by a
+/// constant polynomial, bfv.cpp:664-680).
+__global__ void k_scale_const(u64* __restrict__ ct, u32 B, u64 c, DevTab T) {
+    const u32 N = T.N, L = T.L;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)B * 2 * L * N) return;
+    const u32 i = (u32)((idx / N) % L);
+    const u64 q = T.q[i];
+    const u64 cm = c % q;
+    const u64 pl = ct[idx] * cm, ph = __umul64hi(ct[idx], cm);
+    ct[idx] = reduce128(ph, pl, q, T.q_mu96[i]);
+}
+
+/// Gather 2-comp ciphertexts: out[x] = src[sel[x]] (each 2LN words).
+__global__ void k_gather_ct(const u64* __restrict__ src, const u32* __restrict__ sel, u32 count, size_t per,
+                            u64* __restrict__ out) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)count * per) return;
+    const size_t x = idx / per, o = idx % per;
+    out[idx] = src[(size_t)sel[x] * per + o];
+}
+
+}  // namespace cwgpu
+
+namespace cwgpu {
+/// DB staging: payload rows [R][N] (< t) -> [R][Mm][N] (lifted unchanged into each MAC prime,
+/// prepare_plain, bfv.cpp:933-942; the NTT follows).
+__global__ void k_db_spread(const u64* __restrict__ src, u64 rows, DevTab T, u32* __restrict__ dst) {
+    const u32 N = T.N, Mm = T.Mm;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)rows * Mm * N) return;
+    const size_t r = idx / ((size_t)Mm * N);
+    const u32 n = (u32)(idx % N);
+    dst[idx] = (u32)src[r * N + n];  // t < 2^31 < a_k
+}
+
+/// substitute (bfv.cpp:694-712): out = (auto_g(c0) + ks0, ks1).
+__global__ void k_subst_combine(const u64* __restrict__ in, const u64* __restrict__ ks, u32 B, u64 ginv, DevTab T,
+                                u64* __restrict__ out) {
+    const u32 N = T.N, L = T.L;
+    const size_t LN = (size_t)L * N;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)B * LN) return;
+    const size_t b = idx / LN;
+    const u32 i = (u32)((idx / N) % L), e = (u32)(idx % N);
+    const u64 q = T.q[i];
+    const u64* c0 = in + b * 2 * LN + (size_t)i * N;
+    const u32 s = (u32)(((u64)e * ginv) & (2 * N - 1));
+    u64 v = s < N ? c0[s] : (c0[s - N] ? q - c0[s - N] : 0);
+    v += ks[b * 2 * LN + (size_t)i * N + e];
+    if (v >= q) v -= q;
+    out[b * 2 * LN + (size_t)i * N + e] = v;
+    out[b * 2 * LN + LN + (size_t)i * N + e] = ks[b * 2 * LN + LN + (size_t)i * N + e];
+}
+}  // namespace cwgpu
