@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark: constant-weight PIR server answer on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cwgpu|reference] [--config C4]
+
+One step = one server answer (process_query, reference pir.cpp:337-347) over the
+whole database of the workload.  Default workload: config 4 (n = 65536 rows,
+N = 8192, 5 x 43/44-bit chain primes, t = 1032193, k = 2, m = 363, c = 9, s = 1;
+21.5 GB of NTT-form database), the configuration BASELINE's "1/2/4/8 B200" metric is
+quoted on.  Synthetic seeded inputs (no public dataset), keys and query from the
+client that reproduces the reference's seeded key generation.
+
+value       = database GB/s scanned (n*s*L*N*8 bytes / answer time), inputs resident
+              in HBM (keys, query, DB), device-timed with CUDA events, max over ranks.
+e2e         = the same metric through cwg_answer with host buffers: the query and the
+              evaluation keys (which the reference server receives with every query,
+              server.cpp:63-68) copied H2D and the response D2H inside the timed region.
+N > 1       = rows sharded contiguously (strong scaling), one NCCL sum of the
+              partial NTT-domain accumulators to rank 0, which finishes (cwg_finish).
+--impl reference = the reference C++ CPU implementation (oracle/_ref) on all host
+              cores, on a bounded row sample extrapolated to the full database.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-f", self.path], stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        load = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def make_inputs(cfg, rank, world, seed=1):
+    from paper_2202_07569_b200 import Client, configs
+
+    lo = rank * cfg.n // world
+    hi = (rank + 1) * cfg.n // world
+    positions = configs.db_positions(cfg, seed)
+    target = configs.query_row(cfg, seed)
+    client = Client(cfg.N, cfg.primes, cfg.t, seed=seed, galois_levels=cfg.c, relin_bits=cfg.relin_bits,
+                    galois_bits=cfg.galois_bits)
+    keys = client.keys()
+    query = client.pack_query(configs.codeword_bits(positions[target], cfg.m), cfg.c, first_index=1)
+    return client, keys, query, positions, target, lo, hi
+
+
+def cpu_reference_sample(cfg, keys, query, positions, seed=1, sample_rows=None):
+    """The reference's own CPU path (oracle/_ref) on a bounded row sample, extrapolated.
+
+    Times expand_query + prepare_cipher (fixed per query), selection + inner product on
+    `sample_rows` rows (linear in rows), finalize; returns the extrapolated full answer."""
+    import oracle
+    from paper_2202_07569_b200 import configs
+
+    ref = oracle.RefLib()
+    be = oracle.RefBackend(ref, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), relin_bits=cfg.relin_bits,
+                           galois_bits=cfg.galois_bits, keys=(keys.relin, keys.galois))
+    R = sample_rows or min(cfg.n, {"C1": 1024}.get(cfg.name, 512 if cfg.k <= 2 else 16))
+    db = configs.db_payload(cfg, seed, 0, R)
+    t0 = time.perf_counter()
+    _, st = be.answer(query, cfg.c, cfg.m, positions[:R], db, op=cfg.op, tile_rows=R)
+    wall = time.perf_counter() - t0
+    t_expand, t_select, t_inner, t_final, t_prep = [x / 1e3 for x in st]
+    per_row = (t_select - t_prep + t_inner) / R
+    full = t_expand + t_prep + per_row * cfg.n + t_final
+    return {"seconds_full": full, "sample_rows": R, "sample_wall_s": wall, "threads": ref.worker_threads(),
+            "stages_s": {"expand": t_expand, "prepare": t_prep, "select_per_row": (t_select - t_prep) / R,
+                         "inner_per_row": t_inner / R, "finalize": t_final}}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def workload_desc(cfg):
+    return (f"{cfg.name}: n={cfg.n} rows, N={cfg.N}, L={cfg.L} chain primes ({cfg.primes[0].bit_length()}-"
+            f"{cfg.primes[-1].bit_length()} bit), t={cfg.t}, k={cfg.k}, m={cfg.m}, c={cfg.c}, s={cfg.s}, "
+            f"op={'arith' if cfg.op else 'folklore'}")
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2202_07569_b200 import Client, configs
+
+    positions = configs.db_positions(cfg, 1)
+    target = configs.query_row(cfg, 1)
+    client = Client(cfg.N, cfg.primes, cfg.t, seed=1, galois_levels=cfg.c)
+    keys = client.keys()
+    query = client.pack_query(configs.codeword_bits(positions[target], cfg.m), cfg.c, first_index=1)
+    for _ in range(args.warmup):
+        cpu_reference_sample(cfg, keys, query, positions, sample_rows=args.cpu_sample_rows or 64)
+    runs = [cpu_reference_sample(cfg, keys, query, positions, sample_rows=args.cpu_sample_rows)
+            for _ in range(args.steps)]
+    secs = statistics.median(r["seconds_full"] for r in runs)
+    gbps = cfg.db_bytes() / secs / 1e9
+    line = {
+        "impl": "reference", "metric": "db_GBps_scanned", "value": gbps, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded)",
+        "config": {"workload": workload_desc(cfg), "db_bytes": cfg.db_bytes()},
+        "cpu_baseline": {"value": gbps, "unit": "GB/s", "cores": runs[0]["threads"], "kind": "reference",
+                         "sample": f"expand+prepare of the full query, selection+inner product on "
+                                   f"{runs[0]['sample_rows']} of {cfg.n} rows, extrapolated linearly in rows; "
+                                   f"CPU {cpu_model()}", "stages_s": runs[0]["stages_s"]},
+        "e2e": {"value": gbps, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "answer_ms": secs * 1e3,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cwgpu", choices=["cwgpu", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--rows", type=int, default=0, help="override n (quick runs only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-rows", type=int, default=0)
+    ap.add_argument("--no-verify", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "cwgpu" else args.warmup
+
+    from paper_2202_07569_b200 import configs
+
+    cfg = configs.config(args.config)
+    if args.rows:
+        cfg.n = args.rows
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+
+    from paper_2202_07569_b200 import Context
+    from paper_2202_07569_b200.cwgpu import CwgTimings as CwgTimings_type
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    client, keys, query, positions, target, lo, hi = make_inputs(cfg, rank, world)
+    payload = configs.db_payload(cfg, 1, lo, hi)
+    ctx = Context(cfg.N, cfg.primes, cfg.t, relin_bits=cfg.relin_bits, galois_bits=cfg.galois_bits, device=local)
+    t_load = time.perf_counter()
+    ctx.load_db(positions[lo:hi], payload, n_total=cfg.n, row_begin=lo, m=cfg.m)
+    t_load = time.perf_counter() - t_load
+    info = ctx.info()
+    ctx.set_keys(keys)
+    L, N = cfg.L, cfg.N
+    resp_words = cfg.s * 2 * L * N
+    ext = torch.cuda.ExternalStream(ctx.stream())
+
+    # device-resident inputs for `value`; pinned host buffers for `e2e`
+    dq = torch.from_numpy(query.view(np.int64)).cuda()
+    dout = torch.zeros(resp_words, dtype=torch.int64, device="cuda")
+    hq = torch.from_numpy(query.view(np.int64).copy()).pin_memory()
+    hrelin = torch.from_numpy(keys.relin.view(np.int64).reshape(-1).copy()).pin_memory()
+    hgal = torch.from_numpy(keys.galois.view(np.int64).reshape(-1).copy()).pin_memory()
+    hg = np.ascontiguousarray(keys.exponents(N))
+    hout = torch.zeros(resp_words, dtype=torch.int64).pin_memory()
+    import ctypes
+
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    key_ptrs = (ctypes.cast(hrelin.data_ptr(), u64p), keys.galois.shape[0], hg.ctypes.data_as(u64p),
+                ctypes.cast(hgal.data_ptr(), u64p))
+    h_q = query.shape[0]
+    partial = None
+    if world > 1:
+        partial = torch.zeros(ctx.partial_words(), dtype=torch.int64, device="cuda")
+
+    def step_value():
+        if world == 1:
+            ctx.answer_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, dout.data_ptr())
+        else:
+            ctx.answer_partial_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, partial.data_ptr())
+            dist.reduce(partial, dst=0)
+            if rank == 0:
+                ctx.finish(partial.data_ptr(), cfg.op, out=dout.data_ptr())
+
+    def step_e2e():
+        if world == 1:
+            ctx.answer_ptr(hq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, hout.data_ptr(), keys_ptrs=key_ptrs)
+        else:
+            ctx.answer_partial_ptr(hq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, partial.data_ptr(), keys_ptrs=key_ptrs)
+            dist.reduce(partial, dst=0)
+            if rank == 0:
+                ctx.finish(partial.data_ptr(), cfg.op, out=hout.data_ptr())
+
+    def timed(fn, steps):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        stream = ext if world == 1 else torch.cuda.current_stream()
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        if dist:
+            t = torch.tensor([ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            dist.barrier()
+        return ms
+
+    for _ in range(args.warmup):
+        step_value()
+    launches0 = ctx.kernel_launches()
+    clk = ClockSampler(local)
+    clk.start()
+    ms = timed(step_value, args.steps)
+    clocks = clk.stop()
+    launches = (ctx.kernel_launches() - launches0) // args.steps
+    for _ in range(1):
+        step_e2e()
+    ms_e2e = timed(step_e2e, args.steps)
+
+    # correctness of the benchmarked answer: the response decrypts to the selected row
+    verified = None
+    if rank == 0 and not args.no_verify:
+        resp = dout.cpu().numpy().view(np.uint64).reshape(cfg.s, 2, L, N)
+        trow = configs.db_payload(cfg, 1, target, target + 1)[0]
+        verified = all(np.array_equal(client.decrypt(resp[j]), trow[j]) for j in range(cfg.s))
+        hresp = hout.numpy().view(np.uint64).reshape(cfg.s, 2, L, N)
+        verified = verified and np.array_equal(hresp, resp)
+
+    # per-kernel device times (profiling pass, outside the timed region)
+    ctx.set_profiling(True)
+    tm = CwgTimings_type()
+    if world == 1:
+        ctx.answer_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, dout.data_ptr(), timings=tm)
+    else:
+        ctx.answer_partial_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, partial.data_ptr(), timings=tm)
+    kstats = ctx.kernel_stats()
+    ctx.set_profiling(False)
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+
+    hbm, peak_kind = peaks()
+    db_bytes = cfg.db_bytes()
+    value = db_bytes / (ms / 1e3) / 1e9
+    e2e = db_bytes / (ms_e2e / 1e3) / 1e9
+    # roofline of the payload MAC kernel (HBM-bound): algorithmic bytes = rows * s * L * N * 8 per
+    # launch (the NTT-form database words it streams), over the CUDA-event launch time.
+    mac_ms, mac_n = kstats.get("k_mac", (0.0, 0))
+    local_rows = hi - lo
+    bytes_per_launch = local_rows / max(mac_n, 1) * cfg.s * L * N * 8
+    mac_achieved = bytes_per_launch / (mac_ms / max(mac_n, 1) / 1e3) / 1e9 if mac_n else None
+    tot_prof = sum(v[0] for v in kstats.values())
+    dom = max(kstats.items(), key=lambda kv: kv[1][0]) if kstats else ("", (0, 0))
+    line = {
+        "metric": "db_GBps_scanned", "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded rows/keys/query)",
+        "config": {"workload": workload_desc(cfg), "db_bytes": db_bytes, "rows_per_gpu": local_rows,
+                   "parallelism": f"row-shard x{world}", "l2": "no flush: 21.5 GB DB >> 126 MB L2"
+                   if cfg.name == "C4" else "inputs larger than L2" if db_bytes > 2e8 else "small (L2-resident)",
+                   "aux_primes": info.J, "mac_primes": info.Mm},
+        "answer_ms": ms,
+        "e2e": {"value": e2e, "unit": "GB/s", "answer_ms": ms_e2e,
+                "h2d_bytes_per_step": int(query.nbytes + keys.relin.nbytes + keys.galois.nbytes),
+                "d2h_bytes_per_step": int(resp_words * 8)},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": {"kernel": "k_mac", "bound": "hbm", "achieved": mac_achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": (mac_achieved / hbm) if mac_achieved else None, "traffic": None,
+                     "peak_kind": peak_kind, "bytes_per_launch": bytes_per_launch,
+                     "share_of_step": mac_ms / tot_prof if tot_prof else None},
+        "kernels_ms_per_answer": {k: round(v[0], 3) for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
+        "dominant_kernel": {"name": dom[0], "share_of_step": dom[1][0] / tot_prof if tot_prof else None},
+        "stages_ms": {k: getattr(tm, k) for k in ("expand_ms", "select_ms", "mac_ms", "finish_ms")},
+        "exact_fallbacks": int(tm.exact_fallbacks),
+        "verified_decrypt": verified,
+        "db_load_s": t_load,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference_sample(cfg, keys, query, positions, sample_rows=args.cpu_sample_rows or None)
+            line["cpu_baseline"] = {
+                "value": db_bytes / cb["seconds_full"] / 1e9, "unit": "GB/s", "cores": cb["threads"],
+                "kind": "reference",
+                "sample": f"reference process_query composition (oracle/_ref): expand+prepare of the query and "
+                          f"selection+inner product on {cb['sample_rows']} of {cfg.n} rows, extrapolated linearly "
+                          f"in rows ({cb['seconds_full']:.1f} s full answer); CPU {cpu_model()}",
+                "answer_s": cb["seconds_full"], "stages_s": cb["stages_s"]}
+        except Exception as e:  # the baseline must not hide the GPU line
+            line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -83,7 +83,8 @@ int cwg_set_keys(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const u
  * finalize.  Keys may be passed per call (relin != NULL uploads them, as the
  * reference server receives them with every query, server.cpp:63-68) or NULL to use
  * the resident set.  query: [h][2][L][N] with compression c and code length m.
- * out: [s][2][L][N].  t (optional) receives stage timings. */
+ * out: [s][2][L][N].  query, out and the keys may be host (pageable or pinned) or device
+ * pointers (copies use cudaMemcpyDefault).  t (optional) receives stage timings. */
 int cwg_answer(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
                const uint64_t* galois, uint32_t h, uint32_t c, uint32_t m, const uint64_t* query,
                uint32_t op, uint64_t* out, cwg_timings* t);
@@ -119,6 +120,14 @@ int cwg_substitute(cwg_ctx* ctx, uint32_t count, const uint64_t* ct, uint64_t g,
 
 /* Kernel launch counter (all launches by this library since cwg_create). */
 uint64_t cwg_kernel_launches(const cwg_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) so callers can record events on it. */
+void* cwg_stream(const cwg_ctx* ctx);
+/* Per-kernel CUDA-event timing of every launch (adds overhead; off by default).  Turning it
+ * on or off clears the statistics; cwg_kernel_stats enumerates (idx = 0, 1, ...) name,
+ * summed device time and launch count, returning CWG_EINVAL past the end. */
+int cwg_set_profiling(cwg_ctx* ctx, int on);
+int cwg_kernel_stats(const cwg_ctx* ctx, uint32_t idx, char* name, uint32_t name_len, double* total_ms,
+                     uint64_t* count);
 
 #ifdef __cplusplus
 }

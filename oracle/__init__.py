@@ -248,7 +248,7 @@ class RefBackend:
         n, k = positions.shape
         s = db.shape[1]
         out = np.zeros((s, 2, self.L, self.N), np.uint64)
-        st = (ctypes.c_double * 4)()
+        st = (ctypes.c_double * 5)()
         self.ref._check(self.ref.lib.ref_answer(self.h, _p64(query), query.shape[0], c, m, n, k,
                                                 _p32(positions), s, _p64(db), op, tile_rows, _p64(out), st))
         return out, list(st)

@@ -359,7 +359,7 @@ int ref_weighted_sum(void* h, const std::uint64_t* cts, std::uint32_t comps, std
 ///        over row tiles of `tile_rows` and summed with be.add (bit-identical to the
 ///        untiled weighted_sum: INTT and mod-q addition are linear), then finalize
 ///        (pir.cpp:345).
-/// stage_ms (optional, 4 doubles): expand, select, inner, finalize wall times.
+/// stage_ms (optional, 5 doubles): expand, select (incl. prepare), inner, finalize, prepare wall times.
 int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint32_t c,
                std::uint32_t m, std::uint64_t n, std::uint32_t k, const std::uint32_t* positions,
                std::uint32_t s, const std::uint64_t* db, std::uint32_t op, std::uint64_t tile_rows,
@@ -386,7 +386,8 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
             prepared.resize(expanded.size());
             parallel_for(expanded.size(), [&](std::size_t j) { prepared[j] = be.prepare_cipher(expanded[j]); });
         }
-        t_select += ms_since(t1);
+        const double t_prepare = ms_since(t1);
+        t_select += t_prepare;
 
         u64 kfact_inv = 0;
         if (op == 1) {
@@ -459,6 +460,7 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
             stage_ms[1] = t_select;
             stage_ms[2] = t_inner;
             stage_ms[3] = ms_since(tf);
+            stage_ms[4] = t_prepare;
         }
     });
 }

@@ -227,8 +227,20 @@ def query_row(cfg: Config, seed: int = 1) -> int:
     return int(np.random.default_rng(seed + 7).integers(0, cfg.n))
 
 
-def db_payload(cfg: Config, seed: int = 1, rows=None) -> np.ndarray:
-    """Row payloads: s plaintexts of N coefficients uniform in [0, t) per row."""
-    n = cfg.n if rows is None else rows
-    rng = np.random.default_rng(seed + 99)
-    return rng.integers(0, cfg.t, (n, cfg.s, cfg.N), dtype=np.uint64)
+PAYLOAD_BLOCK = 1024
+
+
+def db_payload(cfg: Config, seed: int = 1, lo: int = 0, hi: int | None = None) -> np.ndarray:
+    """Payloads of rows [lo, hi): s plaintexts of N coefficients uniform in [0, t) per row.
+
+    Generated per 1024-row block from its own seeded stream, so any row shard is
+    reproducible on its own (identical bytes however the rows are split across GPUs)."""
+    hi = cfg.n if hi is None else hi
+    out = np.empty((hi - lo, cfg.s, cfg.N), dtype=np.uint64)
+    b0 = lo // PAYLOAD_BLOCK
+    for b in range(b0, -(-hi // PAYLOAD_BLOCK)):
+        r0, r1 = b * PAYLOAD_BLOCK, min((b + 1) * PAYLOAD_BLOCK, cfg.n)
+        blk = np.random.default_rng([seed, 99, b]).integers(0, cfg.t, (r1 - r0, cfg.s, cfg.N), dtype=np.uint64)
+        s0, s1 = max(r0, lo), min(r1, hi)
+        out[s0 - lo:s1 - lo] = blk[s0 - r0:s1 - r0]
+    return out

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -85,18 +86,51 @@ struct Ctx {
     DevBuf query, exA, exB, digits, dntt, ks, prep, Dbuf, chain3, node2, acc_lo, acc_hi, partial, X, resp3,
         out2, tmp_idx, lift_tmp;
     u64 launches = 0;
-    cudaEvent_t ev[8];
+    // per-kernel profiling (CUDA events around every launch; off in timed runs)
+    bool profiling = false;
+    std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
+    std::vector<std::pair<std::string, std::pair<double, u64>>> prof_stats;
 };
 
 thread_local std::string g_err;
 
 // ------------------------------------------------------------------ launches
 template <class K, class... A>
-static void launch(Ctx& c, K kern, size_t grid, unsigned block, size_t smem, A... args) {
+static void launch_named(Ctx& c, const char* name, K kern, size_t grid, unsigned block, size_t smem, A... args) {
     if (grid == 0) return;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c.profiling) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(cudaEventRecord(e0, c.st));
+    }
     kern<<<(unsigned)grid, block, smem, c.st>>>(args...);
     CK(cudaGetLastError());
     ++c.launches;
+    if (c.profiling) {
+        CK(cudaEventRecord(e1, c.st));
+        c.prof_pending.push_back({name, {e0, e1}});
+    }
+}
+#define launch(c, kern, ...) launch_named(c, #kern, kern, __VA_ARGS__)
+
+/// fold finished launch events into per-kernel totals (call after a stream sync)
+static void prof_collect(Ctx& c) {
+    for (auto& p : c.prof_pending) {
+        float f = 0;
+        CK(cudaEventElapsedTime(&f, p.second.first, p.second.second));
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+        std::string name(p.first);
+        auto it = std::find_if(c.prof_stats.begin(), c.prof_stats.end(), [&](auto& x) { return x.first == name; });
+        if (it == c.prof_stats.end()) {
+            c.prof_stats.push_back({name, {0.0, 0}});
+            it = c.prof_stats.end() - 1;
+        }
+        it->second.first += f;
+        it->second.second += 1;
+    }
+    c.prof_pending.clear();
 }
 
 static size_t blocks(size_t n, unsigned b) { return (n + b - 1) / b; }
@@ -312,17 +346,17 @@ static void ensure_aux(Ctx& c, u64 n_total) {
 static void ntt64(Ctx& c, u64* data, u32 npolys, bool inverse) {
     const u32 N = c.cp.N;
     if (inverse)
-        launch(c, k_ntt64<true, false>, npolys, ntt_block(N), N * 8, data, (const u64*)nullptr, c.T);
+        launch_named(c, "k_ntt64_inv", k_ntt64<true, false>, npolys, ntt_block(N), N * 8, data, (const u64*)nullptr, c.T);
     else
-        launch(c, k_ntt64<false, false>, npolys, ntt_block(N), N * 8, data, (const u64*)nullptr, c.T);
+        launch_named(c, "k_ntt64_fwd", k_ntt64<false, false>, npolys, ntt_block(N), N * 8, data, (const u64*)nullptr, c.T);
 }
 
 static void ntt32(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale) {
     const u32 N = c.cp.N;
     if (inverse)
-        launch(c, k_ntt32<true>, npolys, ntt_block(N), N * 4, base, c.T, gs, stride, off, scale);
+        launch_named(c, "k_ntt32_inv", k_ntt32<true>, npolys, ntt_block(N), N * 4, base, c.T, gs, stride, off, scale);
     else
-        launch(c, k_ntt32<false>, npolys, ntt_block(N), N * 4, base, c.T, gs, stride, off, scale);
+        launch_named(c, "k_ntt32_fwd", k_ntt32<false>, npolys, ntt_block(N), N * 4, base, c.T, gs, stride, off, scale);
 }
 
 // ------------------------------------------------------------------ key switching
@@ -334,7 +368,7 @@ static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
     u64* dig = c.digits.get<u64>((size_t)B * D * N);
     u64* dn = c.dntt.get<u64>((size_t)B * D * L * N);
     launch(c, k_decompose, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv, B, bits, D, c.T, dig);
-    launch(c, k_ntt64<false, true>, (size_t)B * D * L, ntt_block(N), N * 8, dn, (const u64*)dig, c.T);
+    launch_named(c, "k_ntt64_digits", k_ntt64<false, true>, (size_t)B * D * L, ntt_block(N), N * 8, dn, (const u64*)dig, c.T);
     launch(c, k_ks_mac, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u64*)dn, key, B, D, c.T, ks);
     ntt64(c, ks, B * 2 * L, true);
 }
@@ -617,9 +651,9 @@ enum { TM_START = 0, TM_H2D, TM_EXPAND, TM_SELECT, TM_MAC, TM_FINISH, TM_D2H };
 static void upload_keys(Ctx& c, const u64* relin, u32 n_galois, const u64* gg, const u64* galois) {
     const size_t LN = (size_t)c.cp.L * c.cp.N;
     const size_t rw = (size_t)c.cp.Dr * 2 * LN, gw = (size_t)c.cp.Dg * 2 * LN;
-    CK(cudaMemcpyAsync(c.relin.get<u64>(rw), relin, rw * 8, cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(c.relin.get<u64>(rw), relin, rw * 8, cudaMemcpyDefault, c.st));
     if (n_galois)
-        CK(cudaMemcpyAsync(c.galois.get<u64>(gw * n_galois), galois, gw * n_galois * 8, cudaMemcpyHostToDevice, c.st));
+        CK(cudaMemcpyAsync(c.galois.get<u64>(gw * n_galois), galois, gw * n_galois * 8, cudaMemcpyDefault, c.st));
     c.galois_g.assign(gg, gg + n_galois);
     c.have_keys = true;
 }
@@ -636,7 +670,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J, Mm = c.ab.Mm;
     const size_t LN = (size_t)L * N;
     u64* dq = c.query.get<u64>((size_t)h * 2 * LN);
-    CK(cudaMemcpyAsync(dq, query, (size_t)h * 2 * LN * 8, cudaMemcpyHostToDevice, c.st));
+    CK(cudaMemcpyAsync(dq, query, (size_t)h * 2 * LN * 8, cudaMemcpyDefault, c.st));  // host or device
     tm.mark(TM_H2D);
     u64* entries = expand(c, dq, h, comp, m);
     tm.mark(TM_EXPAND);
@@ -686,14 +720,15 @@ static void finish(Ctx& c, const u64* dev_partial, u32 nc, u64* out_host, Timer&
                                c.st));
     }
     tm.mark(TM_FINISH);
-    CK(cudaMemcpyAsync(out_host, o2, (size_t)c.s * 2 * LN * 8, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaMemcpyAsync(out_host, o2, (size_t)c.s * 2 * LN * 8, cudaMemcpyDefault, c.st));  // host or device
     CK(cudaStreamSynchronize(c.st));
     tm.mark(TM_D2H);
 }
 
 static void fill_timings(Ctx& c, Timer& tm, cwg_timings* t, double total_ms) {
-    if (!t) return;
     CK(cudaStreamSynchronize(c.st));
+    if (c.profiling) prof_collect(c);
+    if (!t) return;
     t->total_ms = total_ms;
     t->h2d_ms = tm.sum(TM_H2D);
     t->expand_ms = tm.sum(TM_EXPAND);
@@ -1079,5 +1114,29 @@ int cwg_substitute(cwg_ctx* h, uint32_t count, const uint64_t* ct, uint64_t g, u
 }
 
 uint64_t cwg_kernel_launches(const cwg_ctx* h) { return h->c.launches; }
+
+void* cwg_stream(const cwg_ctx* h) { return (void*)h->c.st; }
+
+int cwg_set_profiling(cwg_ctx* h, int on) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaStreamSynchronize(c.st));
+        prof_collect(c);
+        c.profiling = on != 0;
+        c.prof_stats.clear();
+    });
+}
+
+int cwg_kernel_stats(const cwg_ctx* h, uint32_t idx, char* name, uint32_t name_len, double* total_ms,
+                     uint64_t* count) {
+    const Ctx& c = h->c;
+    if (idx >= c.prof_stats.size()) return CWG_EINVAL;
+    const auto& e = c.prof_stats[idx];
+    std::snprintf(name, name_len, "%s", e.first.c_str());
+    *total_ms = e.second.first;
+    *count = e.second.second;
+    return CWG_OK;
+}
 
 }  // extern "C"

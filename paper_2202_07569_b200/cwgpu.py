@@ -35,6 +35,7 @@ EXPORTED_SYMBOLS = [
     "cwg_last_error", "cwg_create", "cwg_destroy", "cwg_get_info", "cwg_load_db", "cwg_set_keys",
     "cwg_answer", "cwg_partial_words", "cwg_answer_partial", "cwg_finish", "cwg_select", "cwg_ntt",
     "cwg_expand", "cwg_mul_lazy", "cwg_relinearize", "cwg_substitute", "cwg_kernel_launches",
+    "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats",
     "cwg_client_last_error", "cwg_client_create", "cwg_client_destroy", "cwg_client_digits",
     "cwg_client_export_keys", "cwg_client_encrypt", "cwg_client_pack_query", "cwg_client_decrypt",
 ]
@@ -104,6 +105,11 @@ def load_library(path: str = LIB_PATH):
     lib.cwg_substitute.argtypes = [ctypes.c_void_p, ctypes.c_uint32, _u64p, ctypes.c_uint64, _u64p]
     lib.cwg_kernel_launches.restype = ctypes.c_uint64
     lib.cwg_kernel_launches.argtypes = [ctypes.c_void_p]
+    lib.cwg_stream.restype = ctypes.c_void_p
+    lib.cwg_stream.argtypes = [ctypes.c_void_p]
+    lib.cwg_set_profiling.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.cwg_kernel_stats.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_char_p, ctypes.c_uint32,
+                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
     lib.cwg_client_last_error.restype = ctypes.c_char_p
     lib.cwg_client_create.restype = ctypes.c_void_p
     lib.cwg_client_create.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint64, ctypes.c_uint32,
@@ -235,6 +241,12 @@ class Context:
                                  ctypes.byref(timings) if timings is not None else None)
         _raise(self.lib, rc)
 
+    def answer_partial_ptr(self, query_ptr, h, c, m, op, dev_partial_ptr, keys_ptrs=(None, 0, None, None),
+                           timings=None):
+        rc = self.lib.cwg_answer_partial(self.h, *keys_ptrs, h, c, m, query_ptr, op, dev_partial_ptr,
+                                         ctypes.byref(timings) if timings is not None else None)
+        _raise(self.lib, rc)
+
     def partial_words(self) -> int:
         return int(self.lib.cwg_partial_words(self.h))
 
@@ -246,10 +258,12 @@ class Context:
         _raise(self.lib, rc)
 
     def finish(self, dev_partial_ptr, op=OP_FOLKLORE, out=None, timings=None):
-        info = self.info()
+        """cwg_finish; `out` may be an ndarray or a raw (host or device) pointer."""
         if out is None:
+            info = self.info()
             out = np.zeros((info.s, 2, self.L, self.N), np.uint64)
-        rc = self.lib.cwg_finish(self.h, dev_partial_ptr, op, out.ctypes.data,
+        ptr = out.ctypes.data if isinstance(out, np.ndarray) else int(out)
+        rc = self.lib.cwg_finish(self.h, dev_partial_ptr, op, ptr,
                                  ctypes.byref(timings) if timings is not None else None)
         _raise(self.lib, rc)
         return out
@@ -306,6 +320,23 @@ class Context:
 
     def kernel_launches(self) -> int:
         return int(self.lib.cwg_kernel_launches(self.h))
+
+    def stream(self) -> int:
+        """cudaStream_t of the context (for torch.cuda.ExternalStream / event timing)."""
+        return int(self.lib.cwg_stream(self.h))
+
+    def set_profiling(self, on: bool):
+        _raise(self.lib, self.lib.cwg_set_profiling(self.h, int(on)))
+
+    def kernel_stats(self) -> dict:
+        """{kernel: (total_ms, launches)} collected while profiling was on."""
+        out, i = {}, 0
+        buf = ctypes.create_string_buffer(128)
+        tot, cnt = ctypes.c_double(), ctypes.c_uint64()
+        while self.lib.cwg_kernel_stats(self.h, i, buf, 128, ctypes.byref(tot), ctypes.byref(cnt)) == CWG_OK:
+            out[buf.value.decode()] = (tot.value, cnt.value)
+            i += 1
+        return out
 
 
 class Client:
