@@ -104,6 +104,9 @@ class RefLib:
                                    ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, _u32p,
                                    ctypes.c_uint32, _u64p, ctypes.c_uint32, ctypes.c_uint64, _u64p,
                                    ctypes.POINTER(ctypes.c_double)]
+        lib.ref_answer_partial.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, ctypes.c_uint32,
+                                           ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, _u32p,
+                                           ctypes.c_uint32, _u64p, ctypes.c_uint32, _u64p]
         lib.ref_process_query_bytes.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, ctypes.c_uint32,
                                                 ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, _u8p,
                                                 ctypes.c_uint64, _u64p, _u32p, _u64p, _u32p]
@@ -252,6 +255,18 @@ class RefBackend:
         self.ref._check(self.ref.lib.ref_answer(self.h, _p64(query), query.shape[0], c, m, n, k,
                                                 _p32(positions), s, _p64(db), op, tile_rows, _p64(out), st))
         return out, list(st)
+
+    def answer_partial(self, query, c, m, positions, db, op=0):
+        """Un-finalized inner product of a row shard: [s][3][L][N]."""
+        query = np.ascontiguousarray(query, dtype=np.uint64)
+        positions = np.ascontiguousarray(positions, dtype=np.uint32)
+        db = np.ascontiguousarray(db, dtype=np.uint64)
+        n, k = positions.shape
+        s = db.shape[1]
+        out = np.zeros((s, 3, self.L, self.N), np.uint64)
+        self.ref._check(self.ref.lib.ref_answer_partial(self.h, _p64(query), query.shape[0], c, m, n, k,
+                                                        _p32(positions), s, _p64(db), op, _p64(out)))
+        return out
 
     def process_query_bytes(self, query, c, m, n, k, payloads):
         """The reference's own process_query on a PirDatabase::setup database."""

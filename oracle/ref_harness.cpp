@@ -36,6 +36,7 @@ using namespace cwpir;
 namespace {
 
 thread_local std::string g_err;
+thread_local bool g_partial = false;
 
 struct RefBackend {
     HeParams hp;
@@ -452,6 +453,10 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
         }
         auto tf = std::chrono::steady_clock::now();
         for (std::uint32_t j = 0; j < s; ++j) {
+            if (g_partial) {  // un-finalized inner product, [s][3][L][N]
+                write_ct(be, acc[j], out + j * 3 * L * N);
+                continue;
+            }
             CipherValue r = be.finalize(acc[j]);
             write_ct(be, r, out + j * per);
         }
@@ -463,6 +468,18 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
             stage_ms[4] = t_prepare;
         }
     });
+}
+
+/// ref_answer without the final relinearisation: the row shard's inner product
+/// (weighted_sum, bfv.cpp:944-986) as [s][3][L][N] (zero padded when 2-component).
+/// Summing these over row shards mod q and then finalize = the full answer (row sharding).
+int ref_answer_partial(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint32_t c,
+                       std::uint32_t m, std::uint64_t n, std::uint32_t k, const std::uint32_t* positions,
+                       std::uint32_t s, const std::uint64_t* db, std::uint32_t op, std::uint64_t* out) {
+    g_partial = true;
+    int rc = ref_answer(h, query, nq, c, m, n, k, positions, s, db, op, 0, out, nullptr);
+    g_partial = false;
+    return rc;
 }
 
 /// The reference's own process_query (pir.cpp:337-347) on a PirDatabase built by

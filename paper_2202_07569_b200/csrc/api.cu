@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -20,6 +21,7 @@
 
 #include "../../include/cwgpu.h"
 #include "kernels.cuh"
+#include "ntt_reg.cuh"
 #include "params.h"
 
 namespace cwgpu {
@@ -67,7 +69,9 @@ struct Ctx {
     AuxBasis ab;
     u64 aux_n = 0;
     DevTab T{};
-    DevBuf tab;
+    DevBuf tab, tab_self, round_tab;
+    u32 JM = 16;  // aux-prime count padded to a multiple of 8 (rounding kernel template)
+    int np_select = 3;  // register NTT polys per CTA (env CWGPU_NP)
     unsigned long long* d_fb = nullptr;
     // database
     bool db_loaded = false;
@@ -175,6 +179,7 @@ static void build_tables(Ctx& c) {
     T.galois_bits = cp.galois_bits;
     T.t = cp.t;
     T.gbits = 6;
+    T.force_exact = (std::getenv("CWGPU_FORCE_EXACT") && std::atoi(std::getenv("CWGPU_FORCE_EXACT"))) ? 1u : 0u;
     const Big& Q = cp.Q;
     T.QW = (cp.q_bits + 31) / 32;
     if (T.QW > (u32)kQW) throw std::invalid_argument("cwgpu: modulus too wide");
@@ -319,17 +324,48 @@ static void build_tables(Ctx& c) {
 #undef P32
     T.fallbacks = c.d_fb;
     c.T = T;
+    // HPS rounding tables for k_round_mac_t (padded to JM, ImodT transposed)
+    {
+        c.JM = std::max<u32>(8, (J + 7) / 8 * 8);
+        if (c.JM > 40) throw std::invalid_argument("cwgpu: too many aux primes for the rounding kernel");
+        std::vector<RoundJ> rj(c.JM);
+        for (u32 j = 0; j < c.JM; ++j) {
+            RoundJ x{};
+            if (j < J) {
+                x.a = a[j]; x.chat = chat[j]; x.chat_s = chat_s[j]; x.aF = aF[j];
+                x.f0 = frac96[3 * j + 1]; x.f1 = frac96[3 * j + 2];  // top 64 bits of the 96-bit fraction
+            } else {
+                x.a = 1;  // padded prime: w_j = 0
+            }
+            rj[j] = x;
+        }
+        std::vector<RoundK> rk(kMaxJ);
+        for (u32 k = 0; k < Mm; ++k) {
+            RoundK x{};
+            x.a = a[k];
+            x.gcoef = (a[k] - IAmod[k]) % a[k];
+            x.roff = (u32)((a[k] - (u32)(((u128)1 << 36) % a[k])) % a[k]);
+            x.c30 = (u32)((1ull << 30) % a[k]);
+            x.abar = abar[k];
+            rk[k] = x;
+        }
+        std::vector<u32> imT((size_t)Mm * c.JM, 0);
+        for (u32 k = 0; k < Mm; ++k)
+            for (u32 j = 0; j < J; ++j) imT[(size_t)k * c.JM + j] = Imod[(size_t)j * Mm + k];
+        const size_t bytes = sizeof(RoundJ) * c.JM + sizeof(RoundK) * kMaxJ + imT.size() * 4;
+        std::vector<unsigned char> blob(bytes);
+        std::memcpy(blob.data(), rj.data(), sizeof(RoundJ) * c.JM);
+        std::memcpy(blob.data() + sizeof(RoundJ) * c.JM, rk.data(), sizeof(RoundK) * kMaxJ);
+        std::memcpy(blob.data() + sizeof(RoundJ) * c.JM + sizeof(RoundK) * kMaxJ, imT.data(), imT.size() * 4);
+        c.round_tab.ensure(bytes);
+        CK(cudaMemcpy(c.round_tab.p, blob.data(), bytes, cudaMemcpyHostToDevice));
+    }
+    // device copy of the table itself (slow paths read it through T.self)
+    c.tab_self.ensure(sizeof(DevTab));
+    c.T.self = static_cast<const DevTab*>(c.tab_self.p);
+    CK(cudaMemcpy(c.tab_self.p, &c.T, sizeof(DevTab), cudaMemcpyHostToDevice));
 }
 
-static void set_smem_limits(u32 N) {
-    const int s64 = (int)(N * sizeof(u64)), s32 = (int)(N * sizeof(u32));
-    CK(cudaFuncSetAttribute(k_ntt64<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64));
-    CK(cudaFuncSetAttribute(k_ntt64<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64));
-    CK(cudaFuncSetAttribute(k_ntt64<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64));
-    CK(cudaFuncSetAttribute(k_ntt32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
-    CK(cudaFuncSetAttribute(k_ntt32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
-    CK(cudaFuncSetAttribute(k_tensor_intt, cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
-}
 
 static void ensure_aux(Ctx& c, u64 n_total) {
     n_total = std::max<u64>(n_total, 1);
@@ -351,8 +387,79 @@ static void ntt64(Ctx& c, u64* data, u32 npolys, bool inverse) {
         launch_named(c, "k_ntt64_fwd", k_ntt64<false, false>, npolys, ntt_block(N), N * 8, data, (const u64*)nullptr, c.T);
 }
 
+// Register-resident NTT kernels (ntt_reg.cuh) for 2^8 <= N <= 2^14; the shared-memory
+// radix-2 kernels remain for smaller rings.
+template <int LOGN>
+struct Reg32 {
+    static constexpr int NP = LOGN >= 14 ? 1 : 3;
+    static size_t smem(int np) { return (size_t)np * NttGeom<LOGN>::SMEM * 4; }
+    static void limits() {
+        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
+        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
+        CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(NP)));
+        CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem(NP)));
+        CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
+        CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
+    }
+    static void ntt(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale) {
+        if (inverse)
+            launch_named(c, "k_ntt32r_inv", k_ntt32r<LOGN, true>, npolys, NttGeom<LOGN>::T, smem(1), base, c.T, gs,
+                         stride, off, scale);
+        else
+            launch_named(c, "k_ntt32r_fwd", k_ntt32r<LOGN, false>, npolys, NttGeom<LOGN>::T, smem(1), base, c.T, gs,
+                         stride, off, scale);
+    }
+    static void sel3(Ctx& c, u32* D, u32 P) {
+        if (NP == 3 && c.np_select == 3)
+            launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN, NP>, (size_t)P * c.ab.Mm, NttGeom<LOGN>::T, smem(NP),
+                         D, c.T, c.ab.J);
+        else
+            launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN, 1>, (size_t)P * c.ab.Mm, NttGeom<LOGN>::T, smem(1), D,
+                         c.T, c.ab.J);
+    }
+    static void tensor(Ctx& c, const u32* pa, const u32* ia, const u32* pb, const u32* ib, u32 P, u32* D) {
+        if (NP == 3 && c.np_select == 3)
+            launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN, NP>, (size_t)P * c.ab.J, NttGeom<LOGN>::T,
+                         smem(NP), pa, ia, pb, ib, P, c.T, D);
+        else
+            launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN, 1>, (size_t)P * c.ab.J, NttGeom<LOGN>::T, smem(1),
+                         pa, ia, pb, ib, P, c.T, D);
+    }
+};
+
+#define REG32_DISPATCH(logn, call)            \
+    switch (logn) {                           \
+        case 8: Reg32<8>::call; break;        \
+        case 9: Reg32<9>::call; break;        \
+        case 10: Reg32<10>::call; break;      \
+        case 11: Reg32<11>::call; break;      \
+        case 12: Reg32<12>::call; break;      \
+        case 13: Reg32<13>::call; break;      \
+        case 14: Reg32<14>::call; break;      \
+        default: throw std::logic_error("no register NTT for this degree"); \
+    }
+
+static void set_smem_limits(u32 N) {
+    Reg32<8>::limits(); Reg32<9>::limits(); Reg32<10>::limits(); Reg32<11>::limits();
+    Reg32<12>::limits(); Reg32<13>::limits(); Reg32<14>::limits();
+    const int s64 = (int)(N * sizeof(u64)), s32 = (int)(N * sizeof(u32));
+    CK(cudaFuncSetAttribute(k_ntt64<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64));
+    CK(cudaFuncSetAttribute(k_ntt64<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64));
+    CK(cudaFuncSetAttribute(k_ntt64<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s64));
+    CK(cudaFuncSetAttribute(k_ntt32<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
+    CK(cudaFuncSetAttribute(k_ntt32<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
+    CK(cudaFuncSetAttribute(k_tensor_intt, cudaFuncAttributeMaxDynamicSharedMemorySize, s32));
+}
+
+static bool reg32_ok(u32 logN) { return logN >= 8 && logN <= 14; }
+
 static void ntt32(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale) {
     const u32 N = c.cp.N;
+    if (reg32_ok(c.cp.logN)) {
+        REG32_DISPATCH(c.cp.logN, ntt(c, base, npolys, gs, stride, off, inverse, scale));
+        return;
+    }
     if (inverse)
         launch_named(c, "k_ntt32_inv", k_ntt32<true>, npolys, ntt_block(N), N * 4, base, c.T, gs, stride, off, scale);
     else
@@ -457,10 +564,28 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
                          bool to_mac, u64* chain_out) {
     const u32 N = c.cp.N, J = c.ab.J;
     u32* D = c.Dbuf.get<u32>((size_t)P * 3 * J * N);
-    launch(c, k_tensor_intt, (size_t)P * J, ntt_block(N), N * 4, prepA, idxA, prepB, idxB, P, c.T, D);
+    if (reg32_ok(c.cp.logN)) {
+        REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D));
+    } else {
+        launch(c, k_tensor_intt, (size_t)P * J, ntt_block(N), N * 4, prepA, idxA, prepB, idxB, P, c.T, D);
+    }
     if (to_mac) {
-        launch(c, k_round_mac, blocks((size_t)P * 3 * N, 128), 128, 0, D, P, c.T);
-        ntt32(c, D, P * 3 * c.ab.Mm, c.ab.Mm, J, 0, false, 0);
+        const size_t items = (size_t)P * 3 * N;
+        const size_t grid = std::min<size_t>(blocks(items, 256), 148 * 8);
+        const size_t sm = sizeof(RoundJ) * c.JM + sizeof(RoundK) * kMaxJ + (size_t)c.ab.Mm * c.JM * 4;
+        const RoundJ* rj = c.round_tab.ptr<RoundJ>();
+        const RoundK* rk = reinterpret_cast<const RoundK*>(rj + c.JM);
+        const u32* im = reinterpret_cast<const u32*>(rk + kMaxJ);
+        if (c.JM == 8) launch_named(c, "k_round_mac", k_round_mac_t<8>, grid, 256, sm, D, P, c.T, rj, rk, im);
+        else if (c.JM == 16) launch_named(c, "k_round_mac", k_round_mac_t<16>, grid, 256, sm, D, P, c.T, rj, rk, im);
+        else if (c.JM == 24) launch_named(c, "k_round_mac", k_round_mac_t<24>, grid, 256, sm, D, P, c.T, rj, rk, im);
+        else if (c.JM == 32) launch_named(c, "k_round_mac", k_round_mac_t<32>, grid, 256, sm, D, P, c.T, rj, rk, im);
+        else launch_named(c, "k_round_mac", k_round_mac_t<40>, grid, 256, sm, D, P, c.T, rj, rk, im);
+        if (reg32_ok(c.cp.logN)) {
+            REG32_DISPATCH(c.cp.logN, sel3(c, D, P));
+        } else {
+            ntt32(c, D, P * 3 * c.ab.Mm, c.ab.Mm, J, 0, false, 0);
+        }
     } else {
         launch(c, k_round_chain, blocks((size_t)P * 3 * N, 128), 128, 0, (const u32*)D, P, c.T, chain_out);
     }
@@ -615,6 +740,7 @@ static u32 tile_rows(const Ctx& c) {
     const size_t per = (size_t)3 * c.ab.J * c.cp.N * 4 * std::max<u32>(1, c.k / 2);
     size_t r = std::max<size_t>(4, (size_t(256) << 20) / per);
     if (c.k > 2) r = std::min<size_t>(r, 64);
+    if (const char* e = std::getenv("CWGPU_TILE_ROWS")) r = std::max(1, std::atoi(e));
     return (u32)std::min<size_t>(r, 512);
 }
 
@@ -843,6 +969,7 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         CK(cudaMalloc(&c.d_fb, 8));
         CK(cudaMemset(c.d_fb, 0, 8));
         set_smem_limits(N);
+        if (const char* e = std::getenv("CWGPU_NP")) c.np_select = std::atoi(e) == 1 ? 1 : 3;
         ensure_aux(c, 1);
         h = ctx.release();
     });
@@ -854,7 +981,7 @@ void cwg_destroy(cwg_ctx* h) {
     Ctx& c = h->c;
     cudaSetDevice(c.device);
     cudaStreamSynchronize(c.st);
-    for (DevBuf* b : {&c.tab, &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
+    for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
                       &c.digits, &c.dntt, &c.ks, &c.prep, &c.Dbuf, &c.chain3, &c.node2, &c.acc_lo, &c.acc_hi,
                       &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp})
         b->release();

@@ -12,6 +12,8 @@ constexpr int kAW = 44;     // 32-bit limbs for A (<= 40 * 31 bits) + headroom
 
 struct DevTab {
     std::uint32_t N, logN, L, J, Mm, Dr, Dg, relin_bits, galois_bits, QW, AW, gbits;
+    std::uint32_t force_exact;  // test knob (env CWGPU_FORCE_EXACT): every rounding / centring decision
+                                // takes the exact multiword path
     std::uint64_t t;
     // ---- chain primes q_i (bfv.cpp:31-129 restated) ----
     const std::uint64_t* q;        // [L]
@@ -71,6 +73,8 @@ struct DevTab {
     const std::uint64_t* MnegQ;    // [L] (-M) mod q_i
     // ---- diagnostics ----
     unsigned long long* fallbacks;  // exact-path counter (device)
+    const DevTab* self;             // device-memory copy of this table (slow paths take it by
+                                    // reference so kernels never spill the parameter block)
 };
 
 }  // namespace cwgpu

@@ -256,9 +256,10 @@ __device__ __noinline__ u32 crt_round_exact(const u64* y, u32 ip, const DevTab& 
 }
 
 __device__ __forceinline__ u32 crt_round(const u64* y, u32 ip, u64 frac, const DevTab& T) {
+    if (T.force_exact) return crt_round_exact(y, ip, *T.self);
     if (frac >= (1ull << 63)) return ip + 1;
     if (frac < (1ull << 63) - 2ull * T.L - 2ull) return ip;
-    return crt_round_exact(y, ip, T);
+    return crt_round_exact(y, ip, *T.self);
 }
 
 // ============================================================== expansion / key switching
@@ -520,7 +521,7 @@ __device__ __forceinline__ bool hps_prepare(const u32* __restrict__ Dp, size_t j
         : "+r"(s2), "+r"(s3), "+r"(s4));
     h.rho = (i64)(((u64)s4 << 32) | s3);
     // estimate error in (-J, J 2^31) units of 2^-96: undecidable near a wrap of the low 96 bits
-    const bool bad = (s2 == 0u && s1 == 0u) || (s2 == 0xffffffffu && s1 >= 0xffffff00u);
+    const bool bad = (s2 == 0u && s1 == 0u) || (s2 == 0xffffffffu && s1 >= 0xffffff00u) || T.force_exact;
     h.exact = !bad;
     return !bad;
 }
@@ -630,8 +631,8 @@ __global__ void k_round_mac(u32* __restrict__ D, u32 P, DevTab T) {
     const u32 N = T.N, J = T.J;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)P * 3 * N) return;
-    const size_t pc = idx / N;
-    const u32 n = (u32)(idx % N);
+    const size_t pc = idx >> T.logN;
+    const u32 n = (u32)(idx & (N - 1));
     u32* Dp = D + pc * J * N + n;
     HpsState h;
     if (hps_prepare(Dp, N, T, h)) {
@@ -659,7 +660,7 @@ __global__ void k_round_mac(u32* __restrict__ D, u32 P, DevTab T) {
         }
     } else {
         u32 R[kAW + 2];
-        const bool neg = round_exact(h, T, R);
+        const bool neg = round_exact(h, *T.self, R);
         for (u32 k = 0; k < T.Mm; ++k) {
             const u32 a = T.a[k];
             u32 r = mag_mod32(R, a, T.abar[k]);
@@ -674,8 +675,8 @@ __global__ void k_round_chain(const u32* __restrict__ D, u32 P, DevTab T, u64* _
     const u32 N = T.N, J = T.J, L = T.L;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)P * 3 * N) return;
-    const size_t pc = idx / N;
-    const u32 n = (u32)(idx % N);
+    const size_t pc = idx >> T.logN;
+    const u32 n = (u32)(idx & (N - 1));
     const u32* Dp = D + pc * J * N + n;
     u64* o = out + pc * L * N + n;
     HpsState h;
@@ -698,7 +699,7 @@ __global__ void k_round_chain(const u32* __restrict__ D, u32 P, DevTab T, u64* _
         }
     } else {
         u32 R[kAW + 2];
-        const bool neg = round_exact(h, T, R);
+        const bool neg = round_exact(h, *T.self, R);
         for (u32 i = 0; i < L; ++i) {
             const u64 q = T.q[i];
             u64 r = mag_mod64(R, q, T.q_mu96[i]);
@@ -716,8 +717,8 @@ __global__ void k_mac(const u32* __restrict__ Z, u32 nc, u32 zstride, const u32*
     const u32 N = T.N, Mm = T.Mm;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)s * Mm * N) return;
-    const u32 sj = (u32)(idx / ((size_t)Mm * N));
-    const u32 k = (u32)((idx / N) % Mm), n = (u32)(idx % N);
+    const u32 plane = (u32)(idx >> T.logN);
+    const u32 sj = plane / Mm, k = plane % Mm, n = (u32)(idx & (N - 1));
     u64 lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
     for (u32 c = 0; c < nc; ++c) {
         const size_t o = (((size_t)sj * 3 + c) * Mm + k) * N + n;

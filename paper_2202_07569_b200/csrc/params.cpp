@@ -300,9 +300,10 @@ AuxBasis choose_aux_basis(const ChainParams& cp, u64 n_rows_total) {
     Big selb = cp.Q.mul_u64(cp.t).mul_u64(cp.N).div_u64(2) + Big(1);
     Big needM = selb.mul_u64(cp.t - 1).mul_u64(cp.N).mul_u64(std::max<u64>(n_rows_total, 1)).mul_u64(128);
     AuxBasis ab;
-    // 31-bit NTT-friendly primes, descending below 2^31.
+    // 30-bit NTT-friendly primes, descending below 2^30: 4p < 2^32 allows Harvey-style lazy
+    // butterflies in 32-bit words and 16 residue products fit one u64 accumulator.
     const u64 step = 2 * u64(cp.N);
-    u64 p = (u64(1) << 31);
+    u64 p = (u64(1) << 30);
     Big prod(1);
     u32 J = 0, Mm = 0;
     while (prod.cmp(needA) <= 0 || prod.cmp(needM) <= 0) {

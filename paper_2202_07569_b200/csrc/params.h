@@ -7,7 +7,7 @@
 // arrive in that layout).
 //
 // The tensor / MAC basis is OUR choice ("the choice of aux primes is
-// free"): 31-bit NTT primes instead of the reference's 59-bit ones, sized so that
+// free"): 30-bit NTT primes instead of the reference's 59-bit ones, sized so that
 //   A = prod a_j  >  2^6 * N * q^2                 (exact tensor, bfv.cpp:103-108)
 //   M = prod_{j<Mm} a_j > 2^6 * 2 * |sum_r DB_r * sel_r|   (exact payload MAC)
 // and the exact t/q rounding is computed by HPS-style scaling with an exact

@@ -51,13 +51,13 @@ def test_ntt_chain_matches_ringcontext(gpu, reflib, N, L, bits):
 
 @pytest.mark.parametrize("N", [1024, 8192, 16384])
 def test_ntt_aux_matches_ringcontext(gpu, reflib, N):
-    """The 31-bit aux/MAC primes use the same negacyclic convention."""
+    """The 30-bit aux/MAC primes use the same negacyclic convention."""
     from paper_2202_07569_b200 import configs
 
     _, primes, t = small_params(N, 3, 40, 65537)
     ctx = _ctx(N, primes, t)
     J = ctx.info().J
-    aux = configs.find_ntt_primes_below((1 << 31) - 1, 2 * N, J)
+    aux = configs.find_ntt_primes_below((1 << 30) - 1, 2 * N, J)
     r = np.random.default_rng(1)
     for j in (0, J - 1):
         a = r.integers(0, aux[j], (2, N), dtype=np.uint64)
@@ -220,3 +220,43 @@ def test_errors_match_reference_messages(gpu):
     q = np.zeros((1, 2, 3, N), np.uint64)
     with pytest.raises(ValueError, match="query code length does not match the database"):
         ctx.answer(q, 3, 6)
+
+
+def test_exact_fallback_paths_match(gpu, reflib):
+    """Every rounding / centring decision forced through the exact multiword path
+    (round_exact, crt_round_exact) in a subprocess with CWGPU_FORCE_EXACT=1."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import numpy as np, sys
+sys.path.insert(0, %r)
+sys.path.insert(0, %r)
+from conftest import small_params
+from oracle import RefLib, RefBackend
+from paper_2202_07569_b200 import Context, configs, Keys
+ref = RefLib()
+N, primes, t = small_params(1024, 3, 36, 12289)
+be = RefBackend(ref, N, t, np.array(primes, np.uint64), seed=31, galois_levels=4)
+r = np.random.default_rng(5)
+a = np.stack([np.stack([r.integers(0, p, N, dtype=np.uint64) for p in primes]) for _ in range(2)])
+b = np.stack([np.stack([r.integers(0, p, N, dtype=np.uint64) for p in primes]) for _ in range(2)])
+ctx = Context(N, primes, t)
+assert np.array_equal(ctx.mul_lazy(a, b), be.mul_lazy(a, b))
+n, k, m, c = 20, 2, 7, 3
+pos = configs.perfect_map(np.arange(n), m, k)
+q = be.pack_query(configs.codeword_bits(pos[4], m), c)
+db = r.integers(0, t, (n, 1, N), dtype=np.uint64)
+want, _ = be.answer(q, c, m, pos, db)
+rk, gk = be.export_keys()
+ctx.load_db(pos, db, m=m)
+got, tm = ctx.answer(q, c, m, keys=Keys(rk, gk), timings=True)
+assert np.array_equal(got, want)
+assert tm["exact_fallbacks"] > 0
+print("ok", tm["exact_fallbacks"])
+''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CWGPU_FORCE_EXACT="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "ok" in out.stdout
