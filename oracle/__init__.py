@@ -104,6 +104,8 @@ class RefLib:
                                    ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, _u32p,
                                    ctypes.c_uint32, _u64p, ctypes.c_uint32, ctypes.c_uint64, _u64p,
                                    ctypes.POINTER(ctypes.c_double)]
+        lib.ref_select.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                   ctypes.c_uint64, ctypes.c_uint32, _u32p, _u64p, _u32p]
         lib.ref_answer_partial.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, ctypes.c_uint32,
                                            ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, _u32p,
                                            ctypes.c_uint32, _u64p, ctypes.c_uint32, _u64p]
@@ -255,6 +257,17 @@ class RefBackend:
         self.ref._check(self.ref.lib.ref_answer(self.h, _p64(query), query.shape[0], c, m, n, k,
                                                 _p32(positions), s, _p64(db), op, tile_rows, _p64(out), st))
         return out, list(st)
+
+    def select(self, query, c, m, positions):
+        """compute_selection_vector per row: ([n][3][L][N], comps[n])."""
+        query = np.ascontiguousarray(query, dtype=np.uint64)
+        positions = np.ascontiguousarray(positions, dtype=np.uint32)
+        n, k = positions.shape
+        sel = np.zeros((n, 3, self.L, self.N), np.uint64)
+        comps = np.zeros(n, np.uint32)
+        self.ref._check(self.ref.lib.ref_select(self.h, _p64(query), query.shape[0], c, m, n, k, _p32(positions),
+                                                _p64(sel), _p32(comps)))
+        return sel, comps
 
     def answer_partial(self, query, c, m, positions, db, op=0):
         """Un-finalized inner product of a row shard: [s][3][L][N]."""

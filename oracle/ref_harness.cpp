@@ -470,6 +470,50 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
     });
 }
 
+/// compute_selection_vector's BFV branch (pir.cpp:287-302) for caller-given codewords
+/// (config 2 draws them at random, with duplicates, so PirDatabase::setup cannot be used).
+/// sel: [n][3][L][N] (2-component rows zero padded), comps[n].
+int ref_select(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint32_t c, std::uint32_t m,
+               std::uint64_t n, std::uint32_t k, const std::uint32_t* positions, std::uint64_t* sel,
+               std::uint32_t* comps) {
+    return guarded([&] {
+        auto* rb = static_cast<RefBackend*>(h);
+        const BfvBackend& be = *rb->be;
+        const std::size_t N = rb->hp.degree, L = rb->hp.coeff_primes.size();
+        const std::size_t per = 2 * L * N;
+        PackedQuery pq;
+        pq.compression = c;
+        pq.code_length = m;
+        for (std::uint32_t i = 0; i < nq; ++i) pq.cts.push_back(read_ct(be, query + i * per, 2));
+        auto expanded = expand_query(be, pq);
+        std::vector<BfvBackend::PreparedCipher> prepared;
+        if (k >= 2) {
+            prepared.resize(expanded.size());
+            parallel_for(expanded.size(), [&](std::size_t j) { prepared[j] = be.prepare_cipher(expanded[j]); });
+        }
+        parallel_for(n, [&](std::size_t i) {
+            std::vector<unsigned> pos(positions + i * k, positions + (i + 1) * k);
+            CipherValue out;
+            if (k == 1) {
+                out = expanded[pos[0]];
+            } else {
+                std::vector<CipherValue> nodes;
+                for (std::size_t p = 0; p + 1 < pos.size(); p += 2) {
+                    const bool root = pos.size() == 2;
+                    CipherValue prod = be.mul_lazy_prepared(prepared[pos[p]], prepared[pos[p + 1]]);
+                    if (!root) prod = be.finalize(prod);
+                    nodes.push_back(std::move(prod));
+                }
+                if (pos.size() % 2) nodes.push_back(expanded[pos.back()]);
+                out = product_tree(be, std::move(nodes), /*lazy_root=*/true);
+            }
+            std::memset(sel + i * 3 * L * N, 0, 3 * L * N * 8);
+            write_ct(be, out, sel + i * 3 * L * N);
+            comps[i] = static_cast<std::uint32_t>(out.comps.size());
+        });
+    });
+}
+
 /// ref_answer without the final relinearisation: the row shard's inner product
 /// (weighted_sum, bfv.cpp:944-986) as [s][3][L][N] (zero padded when 2-component).
 /// Summing these over row shards mod q and then finalize = the full answer (row sharding).

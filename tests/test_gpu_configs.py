@@ -1,0 +1,59 @@
+"""BASELINE.json configurations at their full cryptographic parameters (N, chain, t, k, m,
+c, s, operator) against the reference, with the row count reduced so the reference
+finishes in seconds.  Full row counts are checked by test_golden.py (reference answer
+hashes) and by bench.py (decryption of the selected row)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(reflib, cfg, rows, seed=1, select_only=False):
+    from oracle import RefBackend
+    from paper_2202_07569_b200 import Client, Context, configs
+
+    client = Client(cfg.N, cfg.primes, cfg.t, seed=seed, galois_levels=cfg.c)
+    keys = client.keys()
+    pos = configs.db_positions(cfg, seed)[:rows]
+    target = rows // 3
+    q = client.pack_query(configs.codeword_bits(pos[target], cfg.m), cfg.c, first_index=1)
+    be = RefBackend(reflib, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), keys=(keys.relin, keys.galois))
+    ctx = Context(cfg.N, cfg.primes, cfg.t)
+    if select_only:
+        want, wc = be.select(q, cfg.c, cfg.m, pos)
+        ctx.load_db(pos, None, m=cfg.m)
+        got, gc = ctx.select(q, cfg.c, cfg.m, keys=keys)
+        assert np.array_equal(gc, wc)
+        assert np.array_equal(got, want)
+        return client, got, pos, target
+    db = configs.db_payload(cfg, seed, 0, rows)
+    want, _ = be.answer(q, cfg.c, cfg.m, pos, db, op=cfg.op)
+    ctx.load_db(pos, db, n_total=rows, m=cfg.m)
+    got = ctx.answer(q, cfg.c, cfg.m, op=cfg.op, keys=keys)
+    assert np.array_equal(got, want)
+    for j in range(cfg.s):
+        assert np.array_equal(client.decrypt(got[j]), db[target, j])
+    return client, got, pos, target
+
+
+@pytest.mark.parametrize("name,rows", [("C3", 12), ("C4", 40)])
+def test_config_full_params_reduced_rows(gpu, reflib, name, rows):
+    from paper_2202_07569_b200 import configs
+
+    _run(reflib, configs.config(name), rows)
+
+
+def test_config5_keyword_arith_reduced_rows(gpu, reflib):
+    """Config 5: N = 16384, 8 x 50-bit primes (400-bit q), t = 786433, arithmetic operator
+    k = 4 over CW(569, 4) keyword codewords, s = 2, c = 10 (1023 substitutions)."""
+    from paper_2202_07569_b200 import configs
+
+    _run(reflib, configs.config("C5"), 6)
+
+
+@pytest.mark.parametrize("k", [2, 16])
+def test_config2_full_params_reduced_rows(gpu, reflib, k):
+    from paper_2202_07569_b200 import configs
+
+    cfg = configs.config(f"C2-k{k}")
+    client, sel, pos, target = _run(reflib, cfg, 10, select_only=True)

@@ -260,3 +260,32 @@ print("ok", tm["exact_fallbacks"])
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ok" in out.stdout
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
+def test_select_config2_style(gpu, reflib, k):
+    """compute_selection_vector (pir.cpp:277-312) for config 2's operator sweep: random
+    codewords of weight k (1 in 4 equal to the query's), folklore product tree of depth
+    ceil(log2 k) with lazy root."""
+    from paper_2202_07569_b200 import configs
+
+    N, primes, t = small_params(2048, 4, 50, 65537)
+    n = 12
+    m = configs.min_code_length(64, k) if k > 1 else 40
+    c = configs.default_compression(N, m)
+    be = _ref_backend(reflib, N, primes, t, seed=40 + k, levels=c)
+    keys = _keys(be)
+    r = np.random.default_rng(k)
+    pos = configs.perfect_map(r.integers(0, configs.comb(m, k), n), m, k)
+    pos[r.random(n) < 0.25] = pos[3]
+    q = be.pack_query(configs.codeword_bits(pos[3], m), c)
+    want, wcomps = be.select(q, c, m, pos)
+    ctx = _ctx(N, primes, t)
+    ctx.load_db(pos, None, m=m)
+    got, comps = ctx.select(q, c, m, keys=keys)
+    assert np.array_equal(comps, wcomps)
+    assert np.array_equal(got, want)
+    # matching rows decrypt to 1 (the selection bit), others to 0
+    for i in range(n):
+        bit = int(np.array_equal(pos[i], pos[3]))
+        assert be.decrypt(got[i][: comps[i]])[0] == bit
