@@ -118,6 +118,8 @@ int cwg_relinearize(cwg_ctx* ctx, uint32_t count, const uint64_t* ct3, uint64_t*
 /* BfvBackend::substitute (bfv.cpp:694-712) with the resident Galois key for g. */
 int cwg_substitute(cwg_ctx* ctx, uint32_t count, const uint64_t* ct, uint64_t g, uint64_t* out);
 
+/* Microbenchmark of internal kernel variants (N = 8192 only); ms per launch over npolys. */
+int cwg_bench_kernel(cwg_ctx* ctx, int which, uint32_t npolys, int iters, float* ms_per_launch);
 /* Kernel launch counter (all launches by this library since cwg_create). */
 uint64_t cwg_kernel_launches(const cwg_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) so callers can record events on it. */

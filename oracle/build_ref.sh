@@ -48,3 +48,14 @@ pids="$pids $!"
 for p in $pids; do wait "$p"; done
 $CXX -shared -pthread -o "$OUT/libcwpir_ref.so" "$OUT"/obj/*.o
 echo "built $OUT/libcwpir_ref.so"
+
+# Drop-in shim (integration/cwgpu_process_query.cpp) + its test harness, linked against the
+# product library when it has been built.
+LIBCWGPU="$HERE/../paper_2202_07569_b200/libcwgpu.so"
+if [ -f "$LIBCWGPU" ]; then
+    $CXX $FLAGS -I"$HERE/../include" -c "$HERE/../integration/cwgpu_process_query.cpp" -o "$OUT/obj_dropin_shim.o"
+    $CXX $FLAGS -c "$HERE/dropin_test.cpp" -o "$OUT/obj_dropin_test.o"
+    $CXX -shared -pthread -o "$OUT/libcwgpu_dropin.so" "$OUT/obj_dropin_shim.o" "$OUT/obj_dropin_test.o" \
+        "$OUT"/obj/*.o -L"$(dirname "$LIBCWGPU")" -lcwgpu -Wl,-rpath,'$ORIGIN/../../paper_2202_07569_b200'
+    echo "built $OUT/libcwgpu_dropin.so"
+fi

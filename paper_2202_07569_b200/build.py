@@ -9,7 +9,6 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libcwgpu.so")
 SOURCES = ["api.cu", "params.cpp", "client.cpp"]
-HEADERS = ["devtab.h", "kernels.cuh", "modarith.cuh", "params.h", "client.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-lineinfo", "-O3", "-std=c++17",
@@ -20,7 +19,7 @@ NVCC_FLAGS = [
 
 def _inputs():
     inc = os.path.join(os.path.dirname(HERE), "include")
-    files = [os.path.join(CSRC, f) for f in SOURCES + HEADERS if os.path.exists(os.path.join(CSRC, f))]
+    files = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]  # every source and header
     files += [os.path.join(inc, f) for f in os.listdir(inc)]
     return files
 

@@ -340,18 +340,21 @@ static void build_tables(Ctx& c) {
             rj[j] = x;
         }
         std::vector<RoundK> rk(kMaxJ);
+        auto mf = [](u64 x, u32 p) { return (u32)((((u128)(x % p)) << 32) % p); };  // Montgomery form
         for (u32 k = 0; k < Mm; ++k) {
             RoundK x{};
             x.a = a[k];
-            x.gcoef = (a[k] - IAmod[k]) % a[k];
-            x.roff = (u32)((a[k] - (u32)(((u128)1 << 36) % a[k])) % a[k]);
-            x.c30 = (u32)((1ull << 30) % a[k]);
+            x.pinv = apinv[k];
+            x.gcoef = mf((a[k] - IAmod[k]) % a[k], a[k]);
+            x.roff = mf((a[k] - (u32)(((u128)1 << 36) % a[k])) % a[k], a[k]);
+            x.c0 = mf(1, a[k]);
+            x.c30 = mf(1ull << 30, a[k]);
             x.abar = abar[k];
             rk[k] = x;
         }
         std::vector<u32> imT((size_t)Mm * c.JM, 0);
         for (u32 k = 0; k < Mm; ++k)
-            for (u32 j = 0; j < J; ++j) imT[(size_t)k * c.JM + j] = Imod[(size_t)j * Mm + k];
+            for (u32 j = 0; j < J; ++j) imT[(size_t)k * c.JM + j] = mf(Imod[(size_t)j * Mm + k], a[k]);
         const size_t bytes = sizeof(RoundJ) * c.JM + sizeof(RoundK) * kMaxJ + imT.size() * 4;
         std::vector<unsigned char> blob(bytes);
         std::memcpy(blob.data(), rj.data(), sizeof(RoundJ) * c.JM);
@@ -806,10 +809,8 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         prepare(c, entries, 2 * LN, nullptr, m, prep);
     }
     const size_t accw = (size_t)c.s * 3 * Mm * N;
-    u64* alo = c.acc_lo.get<u64>(accw);
-    u64* ahi = c.acc_hi.get<u64>(accw);
-    CK(cudaMemsetAsync(alo, 0, accw * 8, c.st));
-    CK(cudaMemsetAsync(ahi, 0, accw * 8, c.st));
+    auto* acc = reinterpret_cast<unsigned long long*>(c.acc_lo.get<u64>(accw));
+    CK(cudaMemsetAsync(acc, 0, accw * 8, c.st));
     const u32 R = tile_rows(c);
     u32 nc_all = 2;
     for (u64 r0 = 0; r0 < c.n_local; r0 += R) {
@@ -818,11 +819,22 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         u32* Z = select_tile(c, entries, prep, op, r0, Rt, nc, zs, nullptr);
         nc_all = std::max(nc_all, nc);
         tm.mark(TM_SELECT);
-        launch(c, k_mac, blocks((size_t)c.s * Mm * N, 128), 128, 0, (const u32*)Z, nc, zs,
-               (const u32*)(c.db.ptr<u32>() + (size_t)r0 * c.s * Mm * N), Rt, c.s, c.T, alo, ahi);
+        // rows per chunk: enough threads to cover the GPU several times, >= 16 rows each
+        const size_t per_chunk_threads = (size_t)c.s * Mm * (N / 4);
+        u32 chunks = (u32)std::max<size_t>(1, std::min<size_t>((size_t)(Rt + 15) / 16, (148 * 2048 * 2) / per_chunk_threads + 1));
+        const u32 chunk = (Rt + chunks - 1) / chunks;
+        chunks = (Rt + chunk - 1) / chunk;
+        const u32* dbt = c.db.ptr<u32>() + (size_t)r0 * c.s * Mm * N;
+        const size_t threads = (size_t)c.s * Mm * ((N / 4 + 255) / 256) * 256 * chunks;
+        if (nc == 3)
+            launch_named(c, "k_mac", k_mac2<3>, blocks(threads, 256), 256, 0, (const u32*)Z, zs, dbt, Rt, c.s, chunk,
+                         c.T, acc);
+        else
+            launch_named(c, "k_mac", k_mac2<2>, blocks(threads, 256), 256, 0, (const u32*)Z, zs, dbt, Rt, c.s, chunk,
+                         c.T, acc);
         tm.mark(TM_MAC);
     }
-    launch(c, k_acc_reduce, blocks(accw, 256), 256, 0, (const u64*)alo, (const u64*)ahi, accw, c.T, dev_partial);
+    launch(c, k_acc_mod, blocks(accw, 256), 256, 0, (const unsigned long long*)acc, accw, c.T, dev_partial);
     tm.mark(TM_MAC);
     return nc_all;
 }
@@ -1267,3 +1279,57 @@ int cwg_kernel_stats(const cwg_ctx* h, uint32_t idx, char* name, uint32_t name_l
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ microbenchmarks
+#include "ntt_bench.cuh"
+
+namespace {
+template <int NP, int MINB, bool INV>
+float bench_ntt_variant(cwgpu::Ctx& c, u32* buf, u32 npolys, int iters) {
+    using namespace cwgpu;
+    constexpr int LOGN = 13;
+    const size_t sm = (size_t)NP * NttGeom<LOGN>::SMEM * 4;
+    CK(cudaFuncSetAttribute(k_ntt_bench<LOGN, NP, MINB, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const u32 grid = npolys / NP;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    k_ntt_bench<LOGN, NP, MINB, INV><<<grid, NttGeom<LOGN>::T, sm, c.st>>>(buf, c.T);
+    CK(cudaEventRecord(e0, c.st));
+    for (int i = 0; i < iters; ++i) k_ntt_bench<LOGN, NP, MINB, INV><<<grid, NttGeom<LOGN>::T, sm, c.st>>>(buf, c.T);
+    CK(cudaEventRecord(e1, c.st));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms / iters;
+}
+}  // namespace
+
+extern "C" int cwg_bench_kernel(cwg_ctx* h, int which, uint32_t npolys, int iters, float* ms_per_launch) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        if (c.cp.logN != 13) throw std::invalid_argument("bench variants are compiled for N = 8192");
+        npolys = npolys / 6 * 6;
+        u32* buf = c.lift_tmp.get<u32>((size_t)npolys * c.cp.N);
+        CK(cudaMemsetAsync(buf, 0x1a, (size_t)npolys * c.cp.N * 4, c.st));
+        float ms = 0;
+        switch (which) {
+            case 0: ms = bench_ntt_variant<1, 1, false>(c, buf, npolys, iters); break;
+            case 1: ms = bench_ntt_variant<1, 2, false>(c, buf, npolys, iters); break;
+            case 2: ms = bench_ntt_variant<1, 3, false>(c, buf, npolys, iters); break;
+            case 3: ms = bench_ntt_variant<3, 1, false>(c, buf, npolys, iters); break;
+            case 4: ms = bench_ntt_variant<2, 1, false>(c, buf, npolys, iters); break;
+            case 5: ms = bench_ntt_variant<3, 1, true>(c, buf, npolys, iters); break;
+            case 6: ms = bench_ntt_variant<1, 2, true>(c, buf, npolys, iters); break;
+            case 7: ms = bench_ntt_variant<1, 4, false>(c, buf, npolys, iters); break;
+            case 8: ms = bench_ntt_variant<2, 2, false>(c, buf, npolys, iters); break;
+            default: throw std::invalid_argument("unknown benchmark variant");
+        }
+        *ms_per_launch = ms;
+    });
+}

@@ -17,15 +17,16 @@
 
 namespace cwgpu {
 
-// one pad word per 16: conflict-free (<= 1 collision per warp) for every window mapping
-__device__ __forceinline__ u32 pidx(u32 x) { return x + (x >> 4); }
+// XOR swizzle inside each 32-word row, y = x >> 5: bank(x) = x ^ (y ^ (y << 1)) mod 32 is conflict-free
+// for every transpose window of 2^8 <= N <= 2^14 (checked exhaustively) and needs no padding
+__device__ __forceinline__ u32 pidx(u32 x) { const u32 y = x >> 5; return x ^ ((y ^ (y << 1)) & 31u); }
 
 template <int LOGN>
 struct NttGeom {
     static constexpr int N = 1 << LOGN;
     static constexpr int T = N / 16;
     static constexpr int NW = (LOGN + 3) / 4;       // windows
-    static constexpr int SMEM = N + N / 16 + 8;     // padded u32 words
+    static constexpr int SMEM = N;                  // u32 words per polynomial (swizzled, unpadded)
 };
 
 /// window w (low bit) mapping: x = (tid >> w) << (w + 4) | r << w | (tid & (2^w - 1))
@@ -56,6 +57,24 @@ __device__ __forceinline__ void load_tw(const u32* __restrict__ tp, const u32* _
     }
 }
 
+/// Twiddles of one 4-bit window: stage slot j (register bit) needs 2^(3-j) consecutive
+/// table entries starting at (N >> (b+1)) + (high << (3-j)), b = w + j.  Loaded for the whole
+/// window before its transpose so their latency overlaps the shared-memory exchange.
+template <int LOGN>
+__device__ __forceinline__ void load_window_tw(const u32* __restrict__ tp, const u32* __restrict__ tsp, int w,
+                                               int jlo, int jhi, u32 high, u32 (&tw)[4][8], u32 (&tws)[4][8]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (j < jlo || j > jhi) continue;
+        const int b = w + j;
+        const u32 base = ((u32)(1 << LOGN) >> (b + 1)) + (high << (3 - j));
+        if (j == 3) load_tw<1>(tp, tsp, base, tw[j], tws[j]);
+        else if (j == 2) load_tw<2>(tp, tsp, base, tw[j], tws[j]);
+        else if (j == 1) load_tw<4>(tp, tsp, base, tw[j], tws[j]);
+        else load_tw<8>(tp, tsp, base, tw[j], tws[j]);
+    }
+}
+
 /// Forward NTT of NP polynomials (same prime) held in v (input mapping: window 0, i.e.
 /// x = r << (LOGN-4) | tid; output mapping: last window, x = tid << 4 | r).
 /// Values in [0, 4p) in and out (p < 2^30).  sm: NP * NttGeom<LOGN>::SMEM words.
@@ -68,6 +87,9 @@ __device__ __forceinline__ void ntt32_fwd_reg(u32 (&v)[NP][16], u32* sm, const u
     for (int k = 0; k < G::NW; ++k) {
         const int w = (LOGN - 4 - 4 * k) > 0 ? (LOGN - 4 - 4 * k) : 0;
         const int btop = LOGN - 1 - 4 * k;
+        const u32 high = tid >> w;
+        u32 tw[4][8], tws[4][8];
+        load_window_tw<LOGN>(rp, rps, w, 0, btop - w, high, tw, tws);
         if (k > 0) {
             const int wp = (LOGN - 4 - 4 * (k - 1)) > 0 ? (LOGN - 4 - 4 * (k - 1)) : 0;
             __syncthreads();
@@ -81,17 +103,9 @@ __device__ __forceinline__ void ntt32_fwd_reg(u32 (&v)[NP][16], u32* sm, const u
 #pragma unroll
                 for (int r = 0; r < 16; ++r) v[q][r] = sm[q * G::SMEM + pidx(win_index(tid, w, r))];
         }
-        const u32 high = tid >> w;
 #pragma unroll
         for (int b = btop; b >= w; --b) {
             const int j = b - w;  // register bit
-            const u32 m = (u32)G::N >> (b + 1);
-            u32 tw[8], tws[8];
-            const u32 base = m + (high << (3 - j));
-            if (j == 3) load_tw<1>(rp, rps, base, tw, tws);
-            else if (j == 2) load_tw<2>(rp, rps, base, tw, tws);
-            else if (j == 1) load_tw<4>(rp, rps, base, tw, tws);
-            else load_tw<8>(rp, rps, base, tw, tws);
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
                 if (r & (1 << j)) continue;
@@ -100,7 +114,7 @@ __device__ __forceinline__ void ntt32_fwd_reg(u32 (&v)[NP][16], u32* sm, const u
 #pragma unroll
                 for (int q = 0; q < NP; ++q) {  // Harvey: values in [0, 4p), p < 2^30
                     const u32 a = red32(v[q][r], 2 * p);
-                    const u32 t = shoup32(v[q][r2], tw[u], tws[u], p);
+                    const u32 t = shoup32(v[q][r2], tw[j][u], tws[j][u], p);
                     v[q][r] = a + t;
                     v[q][r2] = a - t + 2 * p;
                 }
@@ -121,6 +135,9 @@ __device__ __forceinline__ void ntt32_inv_reg(u32 (&v)[NP][16], u32* sm, const u
         const int w = (4 * k) < (LOGN - 4) ? (4 * k) : (LOGN - 4);
         const int bbot = 4 * k;
         const int btop = (4 * k + 3) < (LOGN - 1) ? (4 * k + 3) : (LOGN - 1);
+        const u32 high = tid >> w;
+        u32 tw[4][8], tws[4][8];
+        load_window_tw<LOGN>(irp, irps, w, bbot - w, btop - w, high, tw, tws);
         if (k > 0) {
             const int wp = (4 * (k - 1)) < (LOGN - 4) ? (4 * (k - 1)) : (LOGN - 4);
             __syncthreads();
@@ -134,17 +151,9 @@ __device__ __forceinline__ void ntt32_inv_reg(u32 (&v)[NP][16], u32* sm, const u
 #pragma unroll
                 for (int r = 0; r < 16; ++r) v[q][r] = sm[q * G::SMEM + pidx(win_index(tid, w, r))];
         }
-        const u32 high = tid >> w;
 #pragma unroll
         for (int b = bbot; b <= btop; ++b) {
             const int j = b - w;
-            const u32 h = (u32)G::N >> (b + 1);
-            u32 tw[8], tws[8];
-            const u32 base = h + (high << (3 - j));
-            if (j == 3) load_tw<1>(irp, irps, base, tw, tws);
-            else if (j == 2) load_tw<2>(irp, irps, base, tw, tws);
-            else if (j == 1) load_tw<4>(irp, irps, base, tw, tws);
-            else load_tw<8>(irp, irps, base, tw, tws);
 #pragma unroll
             for (int r = 0; r < 16; ++r) {
                 if (r & (1 << j)) continue;
@@ -154,7 +163,7 @@ __device__ __forceinline__ void ntt32_inv_reg(u32 (&v)[NP][16], u32* sm, const u
                 for (int q = 0; q < NP; ++q) {  // values in [0, 2p)
                     const u32 a = v[q][r], c = v[q][r2];
                     v[q][r] = red32(a + c, 2 * p);
-                    v[q][r2] = shoup32(a - c + 2 * p, tw[u], tws[u], p);
+                    v[q][r2] = shoup32(a - c + 2 * p, tw[j][u], tws[j][u], p);
                 }
             }
         }
@@ -297,9 +306,16 @@ struct RoundJ {
     u32 f0, f1;  // floor(frac(t (A/a_j) / q) * 2^64)
 };
 struct RoundK {
-    u32 a, gcoef, roff, c30;  // gcoef = (-I_A) mod a; roff = (-2^36) mod a; c30 = 2^30 mod a
+    // Montgomery forms (x 2^32 mod a): gcoef = -I_A, roff = -2^36, c0 = 1, c30 = 2^30
+    u32 a, pinv, gcoef, roff, c0, c30;
     u64 abar;
 };
+
+/// (acc + m a) / 2^32 with m = -acc a^-1 mod 2^32: acc 2^-32 mod a, in [0, 3a) for acc < 2^63 + 2^62.
+__device__ __forceinline__ u32 mont_red64(u64 acc, u32 a, u32 pinv) {
+    const u32 m = (u32)acc * pinv;
+    return (u32)((acc + (u64)m * a) >> 32);
+}
 
 /// Exact scale-and-round t*D/q (bfv.cpp:811-849) by HPS scaling:
 ///   D = sum_j w_j (A/a_j) - gamma A,  w_j = D_j (A/a_j)^-1 mod a_j,
@@ -330,7 +346,9 @@ __global__ void __launch_bounds__(256) k_round_mac_t(u32* __restrict__ D, u32 P,
         u32* Dp = D + pc * J * N + n;
         u32 d[JM];
 #pragma unroll
-        for (int j = 0; j < JM; ++j) d[j] = (j < (int)J) ? Dp[(size_t)j * N] : 0u;
+        for (int j = 0; j < JM; ++j) d[j] = Dp[(size_t)min(j, (int)J - 1) * N];  // padded j: any value (w_j = 0)
+#pragma unroll
+        for (int j = 0; j < JM; ++j) asm volatile("" : "+r"(d[j]));  // all plane loads in flight before any use
         u32 w[JM];
         u64 gs = 0;
         u32 s0 = 0, s1 = 0, s2 = 0, s3 = 0;
@@ -377,30 +395,26 @@ __global__ void __launch_bounds__(256) k_round_mac_t(u32* __restrict__ D, u32 P,
 #pragma unroll 2
             for (u32 k = 0; k < Mm; ++k) {
                 const RoundK ck = RK[k];
-                const uint4* Im = reinterpret_cast<const uint4*>(ImodT + k * JM);
-                u64 lo = 0;
-                u32 hi = 0;
+                const uint4* Im = reinterpret_cast<const uint4*>(ImodT + k * JM);  // Montgomery form
+                // groups of 8 products (< 2^63); the gamma / rho correction terms ride in group 0
+                u64 g0 = (u64)gamma * ck.gcoef + (u64)rlo * ck.c0 + (u64)rhi * ck.c30 + ck.roff;
+                u32 r = 0;
 #pragma unroll
-                for (int g0 = 0; g0 < JM; g0 += 16) {
-                    u64 g = 0;  // 16 products < 2^60 each: < 2^64
+                for (int gb = 0; gb < JM; gb += 8) {
+                    u64 g = gb == 0 ? g0 : 0;
 #pragma unroll
-                    for (int j0 = g0; j0 < g0 + 16 && j0 < JM; j0 += 4) {
+                    for (int j0 = gb; j0 < gb + 8; j0 += 4) {
                         const uint4 I = Im[j0 / 4];
                         g += (u64)w[j0] * I.x;
                         g += (u64)w[j0 + 1] * I.y;
                         g += (u64)w[j0 + 2] * I.z;
                         g += (u64)w[j0 + 3] * I.w;
                     }
-                    if (g0 == 0) {
-                        lo = g;
-                    } else {
-                        lo += g;
-                        hi += (lo < g);
-                    }
+                    u32 x = mont_red64(g, ck.a, ck.pinv);  // [0, 3a)
+                    x = red32(red32(x, 2 * ck.a), ck.a);
+                    r = red32(r + x, ck.a);
                 }
-                u64 t = (u64)bar64(lo, ck.a, ck.abar) + (u64)gamma * ck.gcoef + rlo + (u64)rhi * ck.c30 + ck.roff;
-                if (JM > 16) t += (u64)hi * bar64(0xffffffffffffffffull, ck.a, ck.abar) + hi;  // hi * 2^64
-                Dp[(size_t)k * N] = bar64(t, ck.a, ck.abar);
+                Dp[(size_t)k * N] = r;
             }
         } else {
             HpsState h;
@@ -420,4 +434,84 @@ __global__ void __launch_bounds__(256) k_round_mac_t(u32* __restrict__ D, u32 P,
     }
 }
 
+}  // namespace cwgpu
+
+namespace cwgpu {
+/// Payload multiply-accumulate (weighted_sum, bfv.cpp:944-986, in the NTT domain of the MAC
+/// basis): acc[sj][c][k][n] += sum_r Z[r][c][k][n] * DB[row0 + r][sj][k][n]  (mod a_k, lazily).
+/// Thread = 4 consecutive coefficients of one (sj, k) plane over a chunk of rows; 128-bit
+/// loads, 16-row u64 groups (products < 2^60), one 64-bit atomic add per output per chunk.
+/// Z: Z + ((r * nc + c) * zstride + k) * N.  DB: [rows][s][Mm][N].  acc: u64 sums of residues.
+template <int NC>
+__global__ void __launch_bounds__(256) k_mac2(const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB,
+                                              u32 R, u32 s, u32 chunk, DevTab T, unsigned long long* __restrict__ acc) {
+    const u32 N = T.N, Mm = T.Mm;
+    const u32 n4s = N >> 2;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const u32 nchunks = (R + chunk - 1) / chunk;
+    if (idx >= (size_t)s * Mm * n4s * nchunks) return;
+    // index order (slowest .. fastest): chunk, prime, 16-KB coefficient block, payload chunk sj,
+    // coefficient: the s slices that reuse the same selection values run back to back (L2 hits)
+    const u32 nb = (n4s + 255) / 256;
+    const u32 n4lo = (u32)(idx % 256);
+    size_t rest = idx / 256;
+    const u32 sj = (u32)(rest % s);
+    rest /= s;
+    const u32 blk = (u32)(rest % nb);
+    rest /= nb;
+    const u32 k = (u32)(rest % Mm);
+    const u32 ch = (u32)(rest / Mm);
+    const u32 n4 = blk * 256 + n4lo;
+    if (n4 >= n4s) return;
+    const u32 p = T.a[k];
+    const u64 pb = T.abar[k];
+    const u32 r0 = ch * chunk, r1 = min(R, r0 + chunk);
+    const size_t dbs = (size_t)s * Mm * N;
+    const uint4* dbp = reinterpret_cast<const uint4*>(DB + ((size_t)sj * Mm + k) * N) + n4;
+    const size_t zs = (size_t)NC * zstride * N;
+    const uint4* zp = reinterpret_cast<const uint4*>(Z + (size_t)k * N) + n4;
+    u32 accr[NC][4];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) accr[c][e] = 0;
+    for (u32 rg = r0; rg < r1; rg += 16) {
+        const u32 re = min(r1, rg + 16);
+        u64 g[NC][4];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) g[c][e] = 0;
+#pragma unroll 4
+        for (u32 r = rg; r < re; ++r) {
+            const uint4 d = __ldg(dbp + (size_t)r * (dbs >> 2));
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const uint4 z = __ldg(zp + ((size_t)r * zs + (size_t)c * zstride * N) / 4);
+                g[c][0] += (u64)z.x * d.x;
+                g[c][1] += (u64)z.y * d.y;
+                g[c][2] += (u64)z.z * d.z;
+                g[c][3] += (u64)z.w * d.w;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) accr[c][e] = red32(accr[c][e] + bar64(g[c][e], p, pb), p);
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        unsigned long long* o = acc + (((size_t)sj * 3 + c) * Mm + k) * N + 4 * n4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) atomicAdd(o + e, (unsigned long long)accr[c][e]);
+    }
+}
+
+/// acc (u64 sums of residues) -> partial[x] = acc mod a_k.
+__global__ void k_acc_mod(const unsigned long long* __restrict__ acc, size_t total, DevTab T, u64* __restrict__ partial) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    const u32 k = (u32)((idx >> T.logN) % T.Mm);
+    partial[idx] = bar64(acc[idx], T.a[k], T.abar[k]);
+}
 }  // namespace cwgpu

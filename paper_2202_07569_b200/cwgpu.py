@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = [
     "cwg_last_error", "cwg_create", "cwg_destroy", "cwg_get_info", "cwg_load_db", "cwg_set_keys",
     "cwg_answer", "cwg_partial_words", "cwg_answer_partial", "cwg_finish", "cwg_select", "cwg_ntt",
     "cwg_expand", "cwg_mul_lazy", "cwg_relinearize", "cwg_substitute", "cwg_kernel_launches",
-    "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats",
+    "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats", "cwg_bench_kernel",
     "cwg_client_last_error", "cwg_client_create", "cwg_client_destroy", "cwg_client_digits",
     "cwg_client_export_keys", "cwg_client_encrypt", "cwg_client_pack_query", "cwg_client_decrypt",
 ]
