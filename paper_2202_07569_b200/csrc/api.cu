@@ -72,6 +72,15 @@ struct Ctx {
     DevBuf tab, tab_self, round_tab;
     u32 JM = 16;  // aux-prime count padded to a multiple of 8 (rounding kernel template)
     int np_select = 3;  // register NTT polys per CTA (env CWGPU_NP)
+    bool tensor_split = false;  // one tensor component per CTA (env CWGPU_TENSOR_SPLIT)
+    bool old_mac = false;       // debugging: the first payload MAC kernel (env CWGPU_OLD_MAC)
+    // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
+    // the FMA-bound rounding of one tile overlaps the latency-bound NTTs of the next (env CWGPU_STREAMS)
+    int nstreams = 2;
+    cudaStream_t tst[2] = {nullptr, nullptr};
+    cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+    DevBuf Dbuf2;
+    DevBuf* dcur = nullptr;
     unsigned long long* d_fb = nullptr;
     // database
     bool db_loaded = false;
@@ -403,6 +412,7 @@ struct Reg32 {
         CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem(NP)));
         CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
+        CK(cudaFuncSetAttribute(k_tensor_intt_c<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
         CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
     }
     static void ntt(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale) {
@@ -422,7 +432,10 @@ struct Reg32 {
                          c.T, c.ab.J);
     }
     static void tensor(Ctx& c, const u32* pa, const u32* ia, const u32* pb, const u32* ib, u32 P, u32* D) {
-        if (NP == 3 && c.np_select == 3)
+        if (c.tensor_split)
+            launch_named(c, "k_tensor_intt", k_tensor_intt_c<LOGN>, (size_t)P * c.ab.J * 3, NttGeom<LOGN>::T, smem(1),
+                         pa, ia, pb, ib, P, c.T, D);
+        else if (NP == 3 && c.np_select == 3)
             launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN, NP>, (size_t)P * c.ab.J, NttGeom<LOGN>::T,
                          smem(NP), pa, ia, pb, ib, P, c.T, D);
         else
@@ -566,7 +579,7 @@ static void prepare(Ctx& c, const u64* src, size_t stride, const u32* sel, u32 c
 static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* prepB, const u32* idxB, u32 P,
                          bool to_mac, u64* chain_out) {
     const u32 N = c.cp.N, J = c.ab.J;
-    u32* D = c.Dbuf.get<u32>((size_t)P * 3 * J * N);
+    u32* D = c.dcur->get<u32>((size_t)P * 3 * J * N);
     if (reg32_ok(c.cp.logN)) {
         REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D));
     } else {
@@ -811,10 +824,25 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     const size_t accw = (size_t)c.s * 3 * Mm * N;
     auto* acc = reinterpret_cast<unsigned long long*>(c.acc_lo.get<u64>(accw));
     CK(cudaMemsetAsync(acc, 0, accw * 8, c.st));
+    if (c.old_mac) CK(cudaMemsetAsync(c.acc_hi.get<u64>(accw), 0, accw * 8, c.st));
     const u32 R = tile_rows(c);
     u32 nc_all = 2;
-    for (u64 r0 = 0; r0 < c.n_local; r0 += R) {
+    const bool piped = c.nstreams == 2 && op == CWG_OP_FOLKLORE && c.k <= 2 && c.n_local > R;
+    cudaStream_t main_st = c.st;
+    if (piped) {
+        // both D buffers exist before the streams diverge (allocation synchronises)
+        c.Dbuf2.ensure((size_t)R * 3 * J * N * 4);
+        c.Dbuf.ensure((size_t)R * 3 * J * N * 4);
+        CK(cudaEventRecord(c.tev[0], main_st));
+        for (int i = 0; i < 2; ++i) CK(cudaStreamWaitEvent(c.tst[i], c.tev[0], 0));
+    }
+    u64 tile = 0;
+    for (u64 r0 = 0; r0 < c.n_local; r0 += R, ++tile) {
         const u32 Rt = (u32)std::min<u64>(R, c.n_local - r0);
+        if (piped) {
+            c.st = c.tst[tile & 1];
+            c.dcur = (tile & 1) ? &c.Dbuf2 : &c.Dbuf;
+        }
         u32 nc = 0, zs = 0;
         u32* Z = select_tile(c, entries, prep, op, r0, Rt, nc, zs, nullptr);
         nc_all = std::max(nc_all, nc);
@@ -826,7 +854,10 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         chunks = (Rt + chunk - 1) / chunk;
         const u32* dbt = c.db.ptr<u32>() + (size_t)r0 * c.s * Mm * N;
         const size_t threads = (size_t)c.s * Mm * ((N / 4 + 255) / 256) * 256 * chunks;
-        if (nc == 3)
+        if (c.old_mac)
+            launch_named(c, "k_mac", k_mac, blocks((size_t)c.s * Mm * N, 128), 128, 0, (const u32*)Z, nc, zs, dbt, Rt,
+                         c.s, c.T, c.acc_lo.ptr<u64>(), c.acc_hi.ptr<u64>());
+        else if (nc == 3)
             launch_named(c, "k_mac", k_mac2<3>, blocks(threads, 256), 256, 0, (const u32*)Z, zs, dbt, Rt, c.s, chunk,
                          c.T, acc);
         else
@@ -834,7 +865,19 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
                          c.T, acc);
         tm.mark(TM_MAC);
     }
-    launch(c, k_acc_mod, blocks(accw, 256), 256, 0, (const unsigned long long*)acc, accw, c.T, dev_partial);
+    if (piped) {
+        c.st = main_st;
+        c.dcur = &c.Dbuf;
+        for (int i = 0; i < 2; ++i) {
+            CK(cudaEventRecord(c.tev[1 + i], c.tst[i]));
+            CK(cudaStreamWaitEvent(main_st, c.tev[1 + i], 0));
+        }
+    }
+    if (c.old_mac)
+        launch(c, k_acc_reduce, blocks(accw, 256), 256, 0, (const u64*)c.acc_lo.ptr<u64>(), (const u64*)c.acc_hi.ptr<u64>(),
+               accw, c.T, dev_partial);
+    else
+        launch(c, k_acc_mod, blocks(accw, 256), 256, 0, (const unsigned long long*)acc, accw, c.T, dev_partial);
     tm.mark(TM_MAC);
     return nc_all;
 }
@@ -982,6 +1025,12 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         CK(cudaMemset(c.d_fb, 0, 8));
         set_smem_limits(N);
         if (const char* e = std::getenv("CWGPU_NP")) c.np_select = std::atoi(e) == 1 ? 1 : 3;
+        if (const char* e = std::getenv("CWGPU_TENSOR_SPLIT")) c.tensor_split = std::atoi(e) != 0;
+        if (const char* e = std::getenv("CWGPU_STREAMS")) c.nstreams = std::atoi(e) >= 2 ? 2 : 1;
+        if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
+        c.dcur = &c.Dbuf;
+        for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));
+        for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c.tev[i], cudaEventDisableTiming));
         ensure_aux(c, 1);
         h = ctx.release();
     });
@@ -993,11 +1042,13 @@ void cwg_destroy(cwg_ctx* h) {
     Ctx& c = h->c;
     cudaSetDevice(c.device);
     cudaStreamSynchronize(c.st);
-    for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
+    for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.Dbuf2, &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
                       &c.digits, &c.dntt, &c.ks, &c.prep, &c.Dbuf, &c.chain3, &c.node2, &c.acc_lo, &c.acc_hi,
                       &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp})
         b->release();
     if (c.d_fb) cudaFree(c.d_fb);
+    for (int i = 0; i < 2; ++i) if (c.tst[i]) cudaStreamDestroy(c.tst[i]);
+    for (int i = 0; i < 3; ++i) if (c.tev[i]) cudaEventDestroy(c.tev[i]);
     if (c.st) cudaStreamDestroy(c.st);
     delete h;
 }

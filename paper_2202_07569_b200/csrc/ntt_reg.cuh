@@ -92,16 +92,19 @@ __device__ __forceinline__ void ntt32_fwd_reg(u32 (&v)[NP][16], u32* sm, const u
         load_window_tw<LOGN>(rp, rps, w, 0, btop - w, high, tw, tws);
         if (k > 0) {
             const int wp = (LOGN - 4 - 4 * (k - 1)) > 0 ? (LOGN - 4 - 4 * (k - 1)) : 0;
+            // pidx is GF(2)-linear and the thread / register fields of the index are disjoint:
+            // pidx(win_index(tid, w, r)) = pidx(win_index(tid, w, 0)) ^ pidx(r << w)
+            const u32 ps = pidx(win_index(tid, wp, 0)), pl = pidx(win_index(tid, w, 0));
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < NP; ++q)
 #pragma unroll
-                for (int r = 0; r < 16; ++r) sm[q * G::SMEM + pidx(win_index(tid, wp, r))] = v[q][r];
+                for (int r = 0; r < 16; ++r) sm[q * G::SMEM + (ps ^ pidx((u32)r << wp))] = v[q][r];
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < NP; ++q)
 #pragma unroll
-                for (int r = 0; r < 16; ++r) v[q][r] = sm[q * G::SMEM + pidx(win_index(tid, w, r))];
+                for (int r = 0; r < 16; ++r) v[q][r] = sm[q * G::SMEM + (pl ^ pidx((u32)r << w))];
         }
 #pragma unroll
         for (int b = btop; b >= w; --b) {
@@ -140,16 +143,19 @@ __device__ __forceinline__ void ntt32_inv_reg(u32 (&v)[NP][16], u32* sm, const u
         load_window_tw<LOGN>(irp, irps, w, bbot - w, btop - w, high, tw, tws);
         if (k > 0) {
             const int wp = (4 * (k - 1)) < (LOGN - 4) ? (4 * (k - 1)) : (LOGN - 4);
+            // pidx is GF(2)-linear and the thread / register fields of the index are disjoint:
+            // pidx(win_index(tid, w, r)) = pidx(win_index(tid, w, 0)) ^ pidx(r << w)
+            const u32 ps = pidx(win_index(tid, wp, 0)), pl = pidx(win_index(tid, w, 0));
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < NP; ++q)
 #pragma unroll
-                for (int r = 0; r < 16; ++r) sm[q * G::SMEM + pidx(win_index(tid, wp, r))] = v[q][r];
+                for (int r = 0; r < 16; ++r) sm[q * G::SMEM + (ps ^ pidx((u32)r << wp))] = v[q][r];
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < NP; ++q)
 #pragma unroll
-                for (int r = 0; r < 16; ++r) v[q][r] = sm[q * G::SMEM + pidx(win_index(tid, w, r))];
+                for (int r = 0; r < 16; ++r) v[q][r] = sm[q * G::SMEM + (pl ^ pidx((u32)r << w))];
         }
 #pragma unroll
         for (int b = bbot; b <= btop; ++b) {
@@ -325,7 +331,7 @@ __device__ __forceinline__ u32 mont_red64(u64 acc, u32 a, u32 pinv) {
 /// error band of a half-integer the exact multiword path (round_exact) decides.
 /// D planes: D[pc][j][N] for pc < P*3; writes r mod a_k (k < Mm) in place.
 template <int JM>
-__global__ void __launch_bounds__(256) k_round_mac_t(u32* __restrict__ D, u32 P, DevTab T,
+__global__ void __launch_bounds__(256, 4) k_round_mac_t(u32* __restrict__ D, u32 P, DevTab T,
                                                      const RoundJ* __restrict__ gRJ, const RoundK* __restrict__ gRK,
                                                      const u32* __restrict__ gImodT) {
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -443,13 +449,13 @@ namespace cwgpu {
 /// loads, 16-row u64 groups (products < 2^60), one 64-bit atomic add per output per chunk.
 /// Z: Z + ((r * nc + c) * zstride + k) * N.  DB: [rows][s][Mm][N].  acc: u64 sums of residues.
 template <int NC>
-__global__ void __launch_bounds__(256) k_mac2(const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB,
+__global__ void __launch_bounds__(256, 3) k_mac2(const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB,
                                               u32 R, u32 s, u32 chunk, DevTab T, unsigned long long* __restrict__ acc) {
     const u32 N = T.N, Mm = T.Mm;
     const u32 n4s = N >> 2;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     const u32 nchunks = (R + chunk - 1) / chunk;
-    if (idx >= (size_t)s * Mm * n4s * nchunks) return;
+    if (idx >= (size_t)s * Mm * ((n4s + 255) / 256) * 256 * nchunks) return;  // padded 256-wide blocks
     // index order (slowest .. fastest): chunk, prime, 16-KB coefficient block, payload chunk sj,
     // coefficient: the s slices that reuse the same selection values run back to back (L2 hits)
     const u32 nb = (n4s + 255) / 256;
@@ -482,7 +488,7 @@ __global__ void __launch_bounds__(256) k_mac2(const u32* __restrict__ Z, u32 zst
         for (int c = 0; c < NC; ++c)
 #pragma unroll
             for (int e = 0; e < 4; ++e) g[c][e] = 0;
-#pragma unroll 4
+#pragma unroll 2
         for (u32 r = rg; r < re; ++r) {
             const uint4 d = __ldg(dbp + (size_t)r * (dbs >> 2));
 #pragma unroll
@@ -513,5 +519,51 @@ __global__ void k_acc_mod(const unsigned long long* __restrict__ acc, size_t tot
     if (idx >= total) return;
     const u32 k = (u32)((idx >> T.logN) % T.Mm);
     partial[idx] = bar64(acc[idx], T.a[k], T.abar[k]);
+}
+}  // namespace cwgpu
+
+namespace cwgpu {
+/// Variant of k_tensor_intt_r with one tensor component per CTA (grid P * J * 3): 64 registers,
+/// two CTAs per SM whose barrier phases interleave.
+template <int LOGN>
+__global__ void __launch_bounds__(NttGeom<LOGN>::T, LOGN >= 14 ? 1 : 2) k_tensor_intt_c(
+    const u32* __restrict__ prepA, const u32* __restrict__ idxA, const u32* __restrict__ prepB,
+    const u32* __restrict__ idxB, u32 P, DevTab T, u32* __restrict__ D) {
+    using G = NttGeom<LOGN>;
+    extern __shared__ u32 smd[];
+    const u32 J = T.J;
+    const u32 tid = threadIdx.x;
+    const u32 comp = blockIdx.x % 3, pj = blockIdx.x / 3;
+    const u32 pr = pj / J, j = pj % J;
+    const u32 p = T.a[j], pinv = T.apinv[j];
+    const size_t per = (size_t)2 * J * G::N;
+    const u32* A = prepA + (size_t)(idxA ? idxA[pr] : pr) * per + (size_t)j * G::N + (tid << 4);
+    const u32* B = prepB + (size_t)(idxB ? idxB[pr] : pr) * per + (size_t)j * G::N + (tid << 4);
+    const size_t o1 = (size_t)J * G::N;
+    u32 v[1][16];
+#pragma unroll
+    for (int r = 0; r < 16; r += 4) {
+        if (comp == 0) {
+            const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(A + r)), y0 = __ldg(reinterpret_cast<const uint4*>(B + r));
+            v[0][r] = red32(mont32(x0.x, y0.x, p, pinv), p); v[0][r + 1] = red32(mont32(x0.y, y0.y, p, pinv), p);
+            v[0][r + 2] = red32(mont32(x0.z, y0.z, p, pinv), p); v[0][r + 3] = red32(mont32(x0.w, y0.w, p, pinv), p);
+        } else if (comp == 2) {
+            const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(A + o1 + r)), y1 = __ldg(reinterpret_cast<const uint4*>(B + o1 + r));
+            v[0][r] = red32(mont32(x1.x, y1.x, p, pinv), p); v[0][r + 1] = red32(mont32(x1.y, y1.y, p, pinv), p);
+            v[0][r + 2] = red32(mont32(x1.z, y1.z, p, pinv), p); v[0][r + 3] = red32(mont32(x1.w, y1.w, p, pinv), p);
+        } else {
+            const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(A + r)), y0 = __ldg(reinterpret_cast<const uint4*>(B + r));
+            const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(A + o1 + r)), y1 = __ldg(reinterpret_cast<const uint4*>(B + o1 + r));
+            v[0][r] = red32(mont32(x0.x, y1.x, p, pinv), p) + red32(mont32(x1.x, y0.x, p, pinv), p);
+            v[0][r + 1] = red32(mont32(x0.y, y1.y, p, pinv), p) + red32(mont32(x1.y, y0.y, p, pinv), p);
+            v[0][r + 2] = red32(mont32(x0.z, y1.z, p, pinv), p) + red32(mont32(x1.z, y0.z, p, pinv), p);
+            v[0][r + 3] = red32(mont32(x0.w, y1.w, p, pinv), p) + red32(mont32(x1.w, y0.w, p, pinv), p);
+        }
+    }
+    ntt32_inv_reg<LOGN, 1>(v, smd, T.airp + (size_t)j * G::N, T.airps + (size_t)j * G::N, p);
+    const u32 ni = T.ninvRA[j], nis = T.ninvRA_s[j];
+    u32* out = D + (((size_t)pr * 3 + comp) * J + j) * G::N;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) out[((u32)r << (LOGN - 4)) | tid] = red32(shoup32(v[0][r], ni, nis, p), p);
 }
 }  // namespace cwgpu

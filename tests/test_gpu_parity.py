@@ -289,3 +289,17 @@ def test_select_config2_style(gpu, reflib, k):
     for i in range(n):
         bit = int(np.array_equal(pos[i], pos[3]))
         assert be.decrypt(got[i][: comps[i]])[0] == bit
+
+
+@pytest.mark.parametrize("N,k", [(256, 1), (256, 2), (512, 2)])
+def test_answer_small_rings(gpu, reflib, N, k):
+    """Small rings exercise partially filled coefficient blocks in the payload MAC grid."""
+    from paper_2202_07569_b200 import configs
+
+    primes = configs.custom_chain(N, 2, 36)
+    n = 10
+    m = configs.min_code_length(n, k) if k > 1 else n
+    c = configs.default_compression(N, m)
+    got, want, be, payload = _answer_case(reflib, N, primes, 12289, n, k, m, c, s=2, op=0, seed=60 + N + k)
+    assert np.array_equal(got, want)
+    assert np.array_equal(be.decrypt(got[1]), payload[1])
