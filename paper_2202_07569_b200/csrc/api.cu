@@ -71,8 +71,6 @@ struct Ctx {
     DevTab T{};
     DevBuf tab, tab_self, round_tab;
     u32 JM = 16;  // aux-prime count padded to a multiple of 8 (rounding kernel template)
-    int np_select = 3;  // register NTT polys per CTA (env CWGPU_NP)
-    bool tensor_split = false;  // one tensor component per CTA (env CWGPU_TENSOR_SPLIT)
     bool old_mac = false;       // debugging: the first payload MAC kernel (env CWGPU_OLD_MAC)
     // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
     // the FMA-bound rounding of one tile overlaps the latency-bound NTTs of the next (env CWGPU_STREAMS)
@@ -403,44 +401,28 @@ static void ntt64(Ctx& c, u64* data, u32 npolys, bool inverse) {
 // radix-2 kernels remain for smaller rings.
 template <int LOGN>
 struct Reg32 {
-    static constexpr int NP = LOGN >= 14 ? 1 : 3;
-    static size_t smem(int np) { return (size_t)np * NttGeom<LOGN>::SMEM * 4; }
+    using R = RegNtt<LOGN>;
     static void limits() {
-        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
-        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
-        CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(NP)));
-        CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem(NP)));
-        CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
-        CK(cudaFuncSetAttribute(k_tensor_intt_c<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
-        CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem(1)));
+        const int sm = (int)R::SMEM;
+        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     }
     static void ntt(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale) {
         if (inverse)
-            launch_named(c, "k_ntt32r_inv", k_ntt32r<LOGN, true>, npolys, NttGeom<LOGN>::T, smem(1), base, c.T, gs,
-                         stride, off, scale);
+            launch_named(c, "k_ntt32r_inv", k_ntt32r<LOGN, true>, npolys, R::T, R::SMEM, base, c.T, gs, stride, off,
+                         scale);
         else
-            launch_named(c, "k_ntt32r_fwd", k_ntt32r<LOGN, false>, npolys, NttGeom<LOGN>::T, smem(1), base, c.T, gs,
-                         stride, off, scale);
+            launch_named(c, "k_ntt32r_fwd", k_ntt32r<LOGN, false>, npolys, R::T, R::SMEM, base, c.T, gs, stride, off,
+                         scale);
     }
     static void sel3(Ctx& c, u32* D, u32 P) {
-        if (NP == 3 && c.np_select == 3)
-            launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN, NP>, (size_t)P * c.ab.Mm, NttGeom<LOGN>::T, smem(NP),
-                         D, c.T, c.ab.J);
-        else
-            launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN, 1>, (size_t)P * c.ab.Mm, NttGeom<LOGN>::T, smem(1), D,
-                         c.T, c.ab.J);
+        launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN>, (size_t)P * 3 * c.ab.Mm, R::T, R::SMEM, D, c.T, c.ab.J);
     }
     static void tensor(Ctx& c, const u32* pa, const u32* ia, const u32* pb, const u32* ib, u32 P, u32* D) {
-        if (c.tensor_split)
-            launch_named(c, "k_tensor_intt", k_tensor_intt_c<LOGN>, (size_t)P * c.ab.J * 3, NttGeom<LOGN>::T, smem(1),
-                         pa, ia, pb, ib, P, c.T, D);
-        else if (NP == 3 && c.np_select == 3)
-            launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN, NP>, (size_t)P * c.ab.J, NttGeom<LOGN>::T,
-                         smem(NP), pa, ia, pb, ib, P, c.T, D);
-        else
-            launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN, 1>, (size_t)P * c.ab.J, NttGeom<LOGN>::T, smem(1),
-                         pa, ia, pb, ib, P, c.T, D);
+        launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN>, (size_t)P * c.ab.J * 3, R::T, R::SMEM, pa, ia, pb, ib,
+                     P, c.T, D);
     }
 };
 
@@ -1024,8 +1006,6 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         CK(cudaMalloc(&c.d_fb, 8));
         CK(cudaMemset(c.d_fb, 0, 8));
         set_smem_limits(N);
-        if (const char* e = std::getenv("CWGPU_NP")) c.np_select = std::atoi(e) == 1 ? 1 : 3;
-        if (const char* e = std::getenv("CWGPU_TENSOR_SPLIT")) c.tensor_split = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_STREAMS")) c.nstreams = std::atoi(e) >= 2 ? 2 : 1;
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
         c.dcur = &c.Dbuf;
@@ -1335,19 +1315,20 @@ int cwg_kernel_stats(const cwg_ctx* h, uint32_t idx, char* name, uint32_t name_l
 #include "ntt_bench.cuh"
 
 namespace {
-template <int NP, int MINB, bool INV>
-float bench_ntt_variant(cwgpu::Ctx& c, u32* buf, u32 npolys, int iters) {
+template <int WB, int NP, int MINB, bool INV, bool JSLOW = false>
+float bench_nttw_variant(cwgpu::Ctx& c, u32* buf, u32 npolys, int iters) {
     using namespace cwgpu;
     constexpr int LOGN = 13;
-    const size_t sm = (size_t)NP * NttGeom<LOGN>::SMEM * 4;
-    CK(cudaFuncSetAttribute(k_ntt_bench<LOGN, NP, MINB, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const size_t sm = (size_t)NP * (1 << LOGN) * 4;
+    auto kern = k_nttw_bench<LOGN, WB, NP, MINB, INV, JSLOW>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const u32 grid = npolys / NP;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    k_ntt_bench<LOGN, NP, MINB, INV><<<grid, NttGeom<LOGN>::T, sm, c.st>>>(buf, c.T);
+    kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T);
     CK(cudaEventRecord(e0, c.st));
-    for (int i = 0; i < iters; ++i) k_ntt_bench<LOGN, NP, MINB, INV><<<grid, NttGeom<LOGN>::T, sm, c.st>>>(buf, c.T);
+    for (int i = 0; i < iters; ++i) kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T);
     CK(cudaEventRecord(e1, c.st));
     CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
@@ -1370,15 +1351,16 @@ extern "C" int cwg_bench_kernel(cwg_ctx* h, int which, uint32_t npolys, int iter
         CK(cudaMemsetAsync(buf, 0x1a, (size_t)npolys * c.cp.N * 4, c.st));
         float ms = 0;
         switch (which) {
-            case 0: ms = bench_ntt_variant<1, 1, false>(c, buf, npolys, iters); break;
-            case 1: ms = bench_ntt_variant<1, 2, false>(c, buf, npolys, iters); break;
-            case 2: ms = bench_ntt_variant<1, 3, false>(c, buf, npolys, iters); break;
-            case 3: ms = bench_ntt_variant<3, 1, false>(c, buf, npolys, iters); break;
-            case 4: ms = bench_ntt_variant<2, 1, false>(c, buf, npolys, iters); break;
-            case 5: ms = bench_ntt_variant<3, 1, true>(c, buf, npolys, iters); break;
-            case 6: ms = bench_ntt_variant<1, 2, true>(c, buf, npolys, iters); break;
-            case 7: ms = bench_ntt_variant<1, 4, false>(c, buf, npolys, iters); break;
-            case 8: ms = bench_ntt_variant<2, 2, false>(c, buf, npolys, iters); break;
+            case 0: ms = bench_nttw_variant<5, 1, 3, false>(c, buf, npolys, iters); break;
+            case 1: ms = bench_nttw_variant<5, 1, 3, true>(c, buf, npolys, iters); break;
+            case 2: ms = bench_nttw_variant<5, 2, 2, false>(c, buf, npolys, iters); break;
+            case 3: ms = bench_nttw_variant<5, 2, 2, true>(c, buf, npolys, iters); break;
+            case 4: ms = bench_nttw_variant<4, 1, 3, false>(c, buf, npolys, iters); break;
+            case 5: ms = bench_nttw_variant<6, 2, 1, false>(c, buf, npolys, iters); break;
+            case 6: ms = bench_nttw_variant<5, 1, 3, false, true>(c, buf, npolys, iters); break;
+            case 7: ms = bench_nttw_variant<5, 1, 3, true, true>(c, buf, npolys, iters); break;
+            case 8: ms = bench_nttw_variant<5, 2, 2, false, true>(c, buf, npolys, iters); break;
+            case 9: ms = bench_nttw_variant<5, 1, 4, false, true>(c, buf, npolys, iters); break;
             default: throw std::invalid_argument("unknown benchmark variant");
         }
         *ms_per_launch = ms;

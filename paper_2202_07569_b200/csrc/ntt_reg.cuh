@@ -1,16 +1,18 @@
-// Register-resident negacyclic NTT for the 31-bit aux / MAC primes.
+// Register-resident negacyclic NTT for the 30-bit aux / MAC primes.
 //
 // Same transform as RingContext::ntt_forward / ntt_inverse (reference ring.cpp:78-144):
 // forward Cooley-Tukey, natural order in, bit-reversed out, twiddle root_pow[m + i]
 // for block i of stage m; inverse Gentleman-Sande back to natural order.
 //
-// A CTA of T = N/16 threads owns one polynomial; each thread keeps 16 coefficients in
-// registers.  The log2(N) stages are processed in 4-bit windows: within a window the
-// thread's 16 registers span the window's 4 index bits, so all of the window's
-// butterflies are register-local; between windows the polynomial is transposed through
-// shared memory (padded by one word per 16 to avoid bank conflicts).  Twiddles for a
-// window stage are contiguous in the bit-reversed tables and are fetched with vector
-// loads where 4 or more are needed.
+// A CTA of T = N/E threads owns one polynomial; each thread keeps E = 2^WB coefficients
+// in registers (WB = 5 for N >= 1024: 32 coefficients, 256 threads at N = 8192).  The
+// log2(N) stages are processed in WB-bit windows: inside a window the thread's registers
+// span the window's index bits, so all of its butterflies are register-local; between
+// windows the polynomial is transposed through shared memory (XOR-swizzled, unpadded,
+// bank-conflict free).  Twiddles are fetched per stage (at most 16 Shoup pairs live), and
+// the small CTAs let several polynomials per SM run out of barrier phase with each other:
+// measured 23-26 ns per 8192-point NTT on a B200 vs 52 ns for radix-16 / 512-thread CTAs
+// (scripts/bench_ntt.py).
 #pragma once
 #include "devtab.h"
 #include "modarith.cuh"
@@ -18,25 +20,10 @@
 namespace cwgpu {
 
 // XOR swizzle inside each 32-word row, y = x >> 5: bank(x) = x ^ (y ^ (y << 1)) mod 32 is conflict-free
-// for every transpose window of 2^8 <= N <= 2^14 (checked exhaustively) and needs no padding
+// for every transpose window (WB = 4 and 5) of 2^8 <= N <= 2^14 (checked exhaustively) and needs no padding
 __device__ __forceinline__ u32 pidx(u32 x) { const u32 y = x >> 5; return x ^ ((y ^ (y << 1)) & 31u); }
 
-template <int LOGN>
-struct NttGeom {
-    static constexpr int N = 1 << LOGN;
-    static constexpr int T = N / 16;
-    static constexpr int NW = (LOGN + 3) / 4;       // windows
-    static constexpr int SMEM = N;                  // u32 words per polynomial (swizzled, unpadded)
-};
-
-/// window w (low bit) mapping: x = (tid >> w) << (w + 4) | r << w | (tid & (2^w - 1))
-__device__ __forceinline__ u32 win_index(u32 tid, int w, int r) {
-    const u32 low = tid & ((1u << w) - 1u);
-    const u32 high = tid >> w;
-    return (high << (w + 4)) | ((u32)r << w) | low;
-}
-
-/// Load `cnt` consecutive twiddles (and Shoup companions) starting at base (cnt <= 8).
+/// Load `cnt` consecutive twiddles (and Shoup companions) starting at base (cnt a multiple of 4 or < 4).
 template <int CNT>
 __device__ __forceinline__ void load_tw(const u32* __restrict__ tp, const u32* __restrict__ tsp, u32 base, u32* w,
                                         u32* ws) {
@@ -57,67 +44,86 @@ __device__ __forceinline__ void load_tw(const u32* __restrict__ tp, const u32* _
     }
 }
 
-/// Twiddles of one 4-bit window: stage slot j (register bit) needs 2^(3-j) consecutive
-/// table entries starting at (N >> (b+1)) + (high << (3-j)), b = w + j.  Loaded for the whole
-/// window before its transpose so their latency overlaps the shared-memory exchange.
-template <int LOGN>
-__device__ __forceinline__ void load_window_tw(const u32* __restrict__ tp, const u32* __restrict__ tsp, int w,
-                                               int jlo, int jhi, u32 high, u32 (&tw)[4][8], u32 (&tws)[4][8]) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        if (j < jlo || j > jhi) continue;
-        const int b = w + j;
-        const u32 base = ((u32)(1 << LOGN) >> (b + 1)) + (high << (3 - j));
-        if (j == 3) load_tw<1>(tp, tsp, base, tw[j], tws[j]);
-        else if (j == 2) load_tw<2>(tp, tsp, base, tw[j], tws[j]);
-        else if (j == 1) load_tw<4>(tp, tsp, base, tw[j], tws[j]);
-        else load_tw<8>(tp, tsp, base, tw[j], tws[j]);
-    }
+template <int LOGN, int WB>
+struct NttW {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int E = 1 << WB;
+    static constexpr int T = N / E;
+    static constexpr int NW = (LOGN + WB - 1) / WB;
+};
+
+template <int WB>
+__device__ __forceinline__ u32 win_index_w(u32 tid, int w, int r) {
+    const u32 low = tid & ((1u << w) - 1u);
+    const u32 high = tid >> w;
+    return (high << (w + WB)) | ((u32)r << w) | low;
 }
 
-/// Forward NTT of NP polynomials (same prime) held in v (input mapping: window 0, i.e.
-/// x = r << (LOGN-4) | tid; output mapping: last window, x = tid << 4 | r).
-/// Values in [0, 4p) in and out (p < 2^30).  sm: NP * NttGeom<LOGN>::SMEM words.
-template <int LOGN, int NP>
-__device__ __forceinline__ void ntt32_fwd_reg(u32 (&v)[NP][16], u32* sm, const u32* __restrict__ rp,
-                                              const u32* __restrict__ rps, u32 p) {
-    using G = NttGeom<LOGN>;
+/// Twiddles of register bit j of a WB-bit window at low bit w: 2^(WB-1-j) consecutive
+/// entries from (N >> (w+j+1)) + (high << (WB-1-j)).
+template <int LOGN, int WB>
+__device__ __forceinline__ void load_stage_tw(const u32* __restrict__ tp, const u32* __restrict__ tsp, int w, int j,
+                                              u32 high, u32* tw, u32* tws) {
+    const u32 base = ((u32)(1 << LOGN) >> (w + j + 1)) + (high << (WB - 1 - j));
+    const int c = WB - 1 - j;
+    if (c == 0) load_tw<1>(tp, tsp, base, tw, tws);
+    else if (c == 1) load_tw<2>(tp, tsp, base, tw, tws);
+    else if (c == 2) load_tw<4>(tp, tsp, base, tw, tws);
+    else if (c == 3) load_tw<8>(tp, tsp, base, tw, tws);
+    else if constexpr (WB <= 5) load_tw<16>(tp, tsp, base, tw, tws);
+    else if (c == 4) load_tw<16>(tp, tsp, base, tw, tws);
+    else load_tw<32>(tp, tsp, base, tw, tws);
+}
+
+/// Move the E registers of each thread from window wp to window w through shared memory.
+template <int WB, int NP, int SMEM>
+__device__ __forceinline__ void nttw_transpose(u32 (&v)[NP][1 << WB], u32* sm, u32 tid, int wp, int w) {
+    constexpr int E = 1 << WB;
+    // pidx is GF(2)-linear and the thread / register fields of the index are disjoint
+    const u32 ps = pidx(win_index_w<WB>(tid, wp, 0)), pl = pidx(win_index_w<WB>(tid, w, 0));
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int r = 0; r < E; ++r) sm[q * SMEM + (ps ^ pidx((u32)r << wp))] = v[q][r];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int r = 0; r < E; ++r) v[q][r] = sm[q * SMEM + (pl ^ pidx((u32)r << w))];
+}
+
+/// Forward NTT; input mapping x = r << (LOGN-WB) | tid, output x = tid << WB | r.
+/// Values in [0, 4p) in and out (p < 2^30).  sm: NP * N words.
+template <int LOGN, int WB, int NP>
+__device__ __forceinline__ void nttw_fwd(u32 (&v)[NP][1 << WB], u32* sm, const u32* __restrict__ rp,
+                                         const u32* __restrict__ rps, u32 p) {
+    using G = NttW<LOGN, WB>;
+    constexpr int E = G::E;
     const u32 tid = threadIdx.x;
 #pragma unroll
     for (int k = 0; k < G::NW; ++k) {
-        const int w = (LOGN - 4 - 4 * k) > 0 ? (LOGN - 4 - 4 * k) : 0;
-        const int btop = LOGN - 1 - 4 * k;
+        const int w = (LOGN - WB - WB * k) > 0 ? (LOGN - WB - WB * k) : 0;
+        const int btop = LOGN - 1 - WB * k;
         const u32 high = tid >> w;
-        u32 tw[4][8], tws[4][8];
-        load_window_tw<LOGN>(rp, rps, w, 0, btop - w, high, tw, tws);
         if (k > 0) {
-            const int wp = (LOGN - 4 - 4 * (k - 1)) > 0 ? (LOGN - 4 - 4 * (k - 1)) : 0;
-            // pidx is GF(2)-linear and the thread / register fields of the index are disjoint:
-            // pidx(win_index(tid, w, r)) = pidx(win_index(tid, w, 0)) ^ pidx(r << w)
-            const u32 ps = pidx(win_index(tid, wp, 0)), pl = pidx(win_index(tid, w, 0));
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < NP; ++q)
-#pragma unroll
-                for (int r = 0; r < 16; ++r) sm[q * G::SMEM + (ps ^ pidx((u32)r << wp))] = v[q][r];
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < NP; ++q)
-#pragma unroll
-                for (int r = 0; r < 16; ++r) v[q][r] = sm[q * G::SMEM + (pl ^ pidx((u32)r << w))];
+            const int wp = (LOGN - WB - WB * (k - 1)) > 0 ? (LOGN - WB - WB * (k - 1)) : 0;
+            nttw_transpose<WB, NP, G::N>(v, sm, tid, wp, w);
         }
 #pragma unroll
         for (int b = btop; b >= w; --b) {
-            const int j = b - w;  // register bit
+            const int j = b - w;
+            u32 tw[E / 2], tws[E / 2];
+            load_stage_tw<LOGN, WB>(rp, rps, w, j, high, tw, tws);
 #pragma unroll
-            for (int r = 0; r < 16; ++r) {
+            for (int r = 0; r < E; ++r) {
                 if (r & (1 << j)) continue;
                 const int r2 = r | (1 << j);
                 const int u = r >> (j + 1);
 #pragma unroll
-                for (int q = 0; q < NP; ++q) {  // Harvey: values in [0, 4p), p < 2^30
+                for (int q = 0; q < NP; ++q) {
                     const u32 a = red32(v[q][r], 2 * p);
-                    const u32 t = shoup32(v[q][r2], tw[j][u], tws[j][u], p);
+                    const u32 t = shoup32(v[q][r2], tw[u], tws[u], p);
                     v[q][r] = a + t;
                     v[q][r2] = a - t + 2 * p;
                 }
@@ -126,179 +132,170 @@ __device__ __forceinline__ void ntt32_fwd_reg(u32 (&v)[NP][16], u32* sm, const u
     }
 }
 
-/// Inverse NTT of NP polynomials (input mapping: x = tid << 4 | r; output mapping:
-/// x = r << (LOGN-4) | tid).  Values in [0, 2p) in and out (no N^-1 scaling; p < 2^30).
-template <int LOGN, int NP>
-__device__ __forceinline__ void ntt32_inv_reg(u32 (&v)[NP][16], u32* sm, const u32* __restrict__ irp,
-                                              const u32* __restrict__ irps, u32 p) {
-    using G = NttGeom<LOGN>;
+/// Inverse NTT (no N^-1 scaling); input mapping x = tid << WB | r, output
+/// x = r << (LOGN-WB) | tid.  Values in [0, 2p) in and out.
+template <int LOGN, int WB, int NP>
+__device__ __forceinline__ void nttw_inv(u32 (&v)[NP][1 << WB], u32* sm, const u32* __restrict__ irp,
+                                         const u32* __restrict__ irps, u32 p) {
+    using G = NttW<LOGN, WB>;
+    constexpr int E = G::E;
     const u32 tid = threadIdx.x;
 #pragma unroll
     for (int k = 0; k < G::NW; ++k) {
-        const int w = (4 * k) < (LOGN - 4) ? (4 * k) : (LOGN - 4);
-        const int bbot = 4 * k;
-        const int btop = (4 * k + 3) < (LOGN - 1) ? (4 * k + 3) : (LOGN - 1);
+        const int w = (WB * k) < (LOGN - WB) ? (WB * k) : (LOGN - WB);
+        const int bbot = WB * k;
+        const int btop = (WB * k + WB - 1) < (LOGN - 1) ? (WB * k + WB - 1) : (LOGN - 1);
         const u32 high = tid >> w;
-        u32 tw[4][8], tws[4][8];
-        load_window_tw<LOGN>(irp, irps, w, bbot - w, btop - w, high, tw, tws);
         if (k > 0) {
-            const int wp = (4 * (k - 1)) < (LOGN - 4) ? (4 * (k - 1)) : (LOGN - 4);
-            // pidx is GF(2)-linear and the thread / register fields of the index are disjoint:
-            // pidx(win_index(tid, w, r)) = pidx(win_index(tid, w, 0)) ^ pidx(r << w)
-            const u32 ps = pidx(win_index(tid, wp, 0)), pl = pidx(win_index(tid, w, 0));
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < NP; ++q)
-#pragma unroll
-                for (int r = 0; r < 16; ++r) sm[q * G::SMEM + (ps ^ pidx((u32)r << wp))] = v[q][r];
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < NP; ++q)
-#pragma unroll
-                for (int r = 0; r < 16; ++r) v[q][r] = sm[q * G::SMEM + (pl ^ pidx((u32)r << w))];
+            const int wp = (WB * (k - 1)) < (LOGN - WB) ? (WB * (k - 1)) : (LOGN - WB);
+            nttw_transpose<WB, NP, G::N>(v, sm, tid, wp, w);
         }
 #pragma unroll
         for (int b = bbot; b <= btop; ++b) {
             const int j = b - w;
+            u32 tw[E / 2], tws[E / 2];
+            load_stage_tw<LOGN, WB>(irp, irps, w, j, high, tw, tws);
 #pragma unroll
-            for (int r = 0; r < 16; ++r) {
+            for (int r = 0; r < E; ++r) {
                 if (r & (1 << j)) continue;
                 const int r2 = r | (1 << j);
                 const int u = r >> (j + 1);
 #pragma unroll
-                for (int q = 0; q < NP; ++q) {  // values in [0, 2p)
+                for (int q = 0; q < NP; ++q) {
                     const u32 a = v[q][r], c = v[q][r2];
                     v[q][r] = red32(a + c, 2 * p);
-                    v[q][r2] = shoup32(a - c + 2 * p, tw[j][u], tws[j][u], p);
+                    v[q][r2] = shoup32(a - c + 2 * p, tw[u], tws[u], p);
                 }
             }
         }
     }
 }
 
-/// Batched forward / inverse NTT (register version of k_ntt32): poly p -> group g = p / gs,
-/// prime j = off + p % gs, address (g * stride + j) * N.  scale (inverse only):
-/// 0 = N^-1, 1 = (N 2^32)^-1.  Output canonical [0, p).
+
+/// Window width and occupancy of the production kernels for a degree 2^LOGN.
+template <int LOGN>
+struct RegNtt {
+    static constexpr int WB = LOGN >= 10 ? 5 : 4;
+    using G = NttW<LOGN, WB>;
+    static constexpr int T = G::T;
+    static constexpr int E = G::E;
+    // <= 85 registers at N = 8192 (3 CTAs / SM); 2 CTAs of 512 threads at N = 16384
+    static constexpr int MINB = LOGN >= 14 ? 2 : (768 / T > 16 ? 16 : 768 / T);
+    static constexpr size_t SMEM = (size_t)G::N * 4;
+};
+
+/// Batched forward / inverse NTT: poly p -> group g = p / gs, prime j = off + p % gs,
+/// address (g * stride + j) * N.  scale (inverse only): 0 = N^-1, 1 = (N 2^32)^-1.
+/// Output canonical [0, p).
 template <int LOGN, bool INV>
-__global__ void __launch_bounds__(NttGeom<LOGN>::T, LOGN >= 14 ? 1 : 2) k_ntt32r(u32* __restrict__ base, DevTab T, u32 gs, u32 stride,
-                                                            u32 off, int scale) {
-    using G = NttGeom<LOGN>;
+__global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_ntt32r(u32* __restrict__ base, DevTab T, u32 gs,
+                                                                               u32 stride, u32 off, int scale) {
+    using R = RegNtt<LOGN>;
+    constexpr int WB = R::WB, E = R::E, N = 1 << LOGN;
     extern __shared__ u32 sm[];
     const u32 tid = threadIdx.x;
     const u32 pi = blockIdx.x, g = pi / gs, j = off + pi % gs;
     const u32 pr = T.a[j];
-    u32* d = base + ((size_t)g * stride + j) * G::N;
-    u32 v[1][16];
+    u32* d = base + ((size_t)g * stride + j) * N;
+    u32 v[1][E];
     if (!INV) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) v[0][r] = d[((u32)r << (LOGN - 4)) | tid];
-        ntt32_fwd_reg<LOGN, 1>(v, sm, T.arp + (size_t)j * G::N, T.arps + (size_t)j * G::N, pr);
-        uint4* o = reinterpret_cast<uint4*>(d + (tid << 4));
+        for (int r = 0; r < E; ++r) v[0][r] = d[((u32)r << (LOGN - WB)) | tid];
+        nttw_fwd<LOGN, WB, 1>(v, sm, T.arp + (size_t)j * N, T.arps + (size_t)j * N, pr);
+        uint4* o = reinterpret_cast<uint4*>(d + (tid << WB));
 #pragma unroll
-        for (int r = 0; r < 16; ++r) v[0][r] = red32(red32(v[0][r], 2 * pr), pr);
+        for (int r = 0; r < E; ++r) v[0][r] = red32(red32(v[0][r], 2 * pr), pr);
 #pragma unroll
-        for (int r = 0; r < 16; r += 4) o[r / 4] = make_uint4(v[0][r], v[0][r + 1], v[0][r + 2], v[0][r + 3]);
+        for (int r = 0; r < E; r += 4) o[r / 4] = make_uint4(v[0][r], v[0][r + 1], v[0][r + 2], v[0][r + 3]);
     } else {
-        const uint4* in = reinterpret_cast<const uint4*>(d + (tid << 4));
+        const uint4* in = reinterpret_cast<const uint4*>(d + (tid << WB));
 #pragma unroll
-        for (int r = 0; r < 16; r += 4) {
+        for (int r = 0; r < E; r += 4) {
             const uint4 x = in[r / 4];
             v[0][r] = x.x; v[0][r + 1] = x.y; v[0][r + 2] = x.z; v[0][r + 3] = x.w;
         }
-        ntt32_inv_reg<LOGN, 1>(v, sm, T.airp + (size_t)j * G::N, T.airps + (size_t)j * G::N, pr);
+        nttw_inv<LOGN, WB, 1>(v, sm, T.airp + (size_t)j * N, T.airps + (size_t)j * N, pr);
         const u32 ni = scale ? T.ninvRA[j] : T.ninvA[j], nis = scale ? T.ninvRA_s[j] : T.ninvA_s[j];
 #pragma unroll
-        for (int r = 0; r < 16; ++r) d[((u32)r << (LOGN - 4)) | tid] = red32(shoup32(v[0][r], ni, nis, pr), pr);
+        for (int r = 0; r < E; ++r) d[((u32)r << (LOGN - WB)) | tid] = red32(shoup32(v[0][r], ni, nis, pr), pr);
     }
 }
 
-/// Forward NTT of the 3 selection components of one product for one MAC prime:
-/// polys at base + ((pr * 3 + comp) * stride_j + k) * N, k = blockIdx.x % Mm.
-template <int LOGN, int NP>
-__global__ void __launch_bounds__(NttGeom<LOGN>::T, (NP == 1 && LOGN < 14) ? 2 : 1) k_ntt32r_sel3(u32* __restrict__ base, DevTab T, u32 stride_j) {
-    using G = NttGeom<LOGN>;
+/// Forward NTT of the 3 selection components of P products for every MAC prime, one
+/// polynomial per CTA: block (pr * 3 + comp) * Mm + k transforms the plane at
+/// base + ((pr * 3 + comp) * stride_j + k) * N in place.
+template <int LOGN>
+__global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_ntt32r_sel3(u32* __restrict__ base, DevTab T,
+                                                                                    u32 stride_j) {
+    using R = RegNtt<LOGN>;
+    constexpr int WB = R::WB, E = R::E, N = 1 << LOGN;
     extern __shared__ u32 smd[];
     const u32 tid = threadIdx.x;
     const u32 Mm = T.Mm;
-    const u32 pr = blockIdx.x / Mm, k = blockIdx.x % Mm;
+    const u32 pc = blockIdx.x / Mm, k = blockIdx.x % Mm;
     const u32 p = T.a[k];
-#pragma unroll 1
-    for (int c0 = 0; c0 < 3; c0 += NP) {
-        u32 v[NP][16];
+    u32* d = base + ((size_t)pc * stride_j + k) * N;
+    u32 v[1][E];
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            const u32* d = base + (((size_t)pr * 3 + c0 + q) * stride_j + k) * G::N;
+    for (int r = 0; r < E; ++r) v[0][r] = d[((u32)r << (LOGN - WB)) | tid];
+    nttw_fwd<LOGN, WB, 1>(v, smd, T.arp + (size_t)k * N, T.arps + (size_t)k * N, p);
+    uint4* o = reinterpret_cast<uint4*>(d + (tid << WB));
 #pragma unroll
-            for (int r = 0; r < 16; ++r) v[q][r] = d[((u32)r << (LOGN - 4)) | tid];
-        }
-        ntt32_fwd_reg<LOGN, NP>(v, smd, T.arp + (size_t)k * G::N, T.arps + (size_t)k * G::N, p);
+    for (int r = 0; r < E; ++r) v[0][r] = red32(red32(v[0][r], 2 * p), p);
 #pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            uint4* o = reinterpret_cast<uint4*>(base + (((size_t)pr * 3 + c0 + q) * stride_j + k) * G::N + (tid << 4));
-#pragma unroll
-            for (int r = 0; r < 16; ++r) v[q][r] = red32(red32(v[q][r], 2 * p), p);
-#pragma unroll
-            for (int r = 0; r < 16; r += 4) o[r / 4] = make_uint4(v[q][r], v[q][r + 1], v[q][r + 2], v[q][r + 3]);
-        }
-        if (NP == 1) __syncthreads();
-    }
+    for (int r = 0; r < E; r += 4) o[r / 4] = make_uint4(v[0][r], v[0][r + 1], v[0][r + 2], v[0][r + 3]);
 }
 
-/// Tensor (mul_lazy_prepared, bfv.cpp:776-791) + INTT for P products, one aux prime per CTA.
-/// NP = 3: the three components are transformed together (shared twiddles, 3-way ILP);
-/// NP = 1: one component at a time (register budget of 1024-thread CTAs at N = 16384).
-/// Operands: Montgomery-form NTT residues [idx][2][J][N]; output D[p][comp][j][N] in normal
-/// form (the (N 2^32)^-1 scale undoes the Montgomery factor).
-template <int LOGN, int NP>
-__global__ void __launch_bounds__(NttGeom<LOGN>::T, (NP == 1 && LOGN < 14) ? 2 : 1) k_tensor_intt_r(const u32* __restrict__ prepA,
-                                                                   const u32* __restrict__ idxA,
-                                                                   const u32* __restrict__ prepB,
-                                                                   const u32* __restrict__ idxB, u32 P, DevTab T,
-                                                                   u32* __restrict__ D) {
-    using G = NttGeom<LOGN>;
+/// Tensor (mul_lazy_prepared, bfv.cpp:776-791) + INTT, one (product, aux prime, component)
+/// per CTA: block (pr * J + j) * 3 + comp (the three components of one product are adjacent,
+/// so their shared operand planes are L2 hits).  Operands: Montgomery-form NTT residues
+/// [idx][2][J][N]; output D[pr][comp][j][N] in normal form (the (N 2^32)^-1 scale undoes the
+/// Montgomery factor).
+template <int LOGN>
+__global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_tensor_intt_r(
+    const u32* __restrict__ prepA, const u32* __restrict__ idxA, const u32* __restrict__ prepB,
+    const u32* __restrict__ idxB, u32 P, DevTab T, u32* __restrict__ D) {
+    using R = RegNtt<LOGN>;
+    constexpr int WB = R::WB, E = R::E, N = 1 << LOGN;
     extern __shared__ u32 smd[];
     const u32 J = T.J;
     const u32 tid = threadIdx.x;
-    const u32 pr = blockIdx.x / J, j = blockIdx.x % J;
+    const u32 comp = blockIdx.x % 3, pj = blockIdx.x / 3;
+    const u32 pr = pj / J, j = pj % J;
     const u32 p = T.a[j], pinv = T.apinv[j];
-    const size_t per = (size_t)2 * J * G::N;
-    const u32* A = prepA + (size_t)(idxA ? idxA[pr] : pr) * per + (size_t)j * G::N + (tid << 4);
-    const u32* B = prepB + (size_t)(idxB ? idxB[pr] : pr) * per + (size_t)j * G::N + (tid << 4);
-    const size_t o1 = (size_t)J * G::N;
-    const u32 ni = T.ninvRA[j], nis = T.ninvRA_s[j];
-#pragma unroll 1
-    for (int c0 = 0; c0 < 3; c0 += NP) {
-        u32 v[NP][16];
+    const size_t per = (size_t)2 * J * N;
+    const u32* A = prepA + (size_t)(idxA ? idxA[pr] : pr) * per + (size_t)j * N + (tid << WB);
+    const u32* B = prepB + (size_t)(idxB ? idxB[pr] : pr) * per + (size_t)j * N + (tid << WB);
+    const size_t o1 = (size_t)J * N;
+    u32 v[1][E];
+    // comp 0: A0 B0, comp 2: A1 B1, comp 1: A0 B1 + A1 B0
+    const u32* X = A + (comp == 2 ? o1 : 0);
+    const u32* Y = B + (comp == 0 ? 0 : o1);
 #pragma unroll
-        for (int r = 0; r < 16; r += 4) {
-            const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(A + r));
-            const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(A + o1 + r));
-            const uint4 y0 = __ldg(reinterpret_cast<const uint4*>(B + r));
-            const uint4 y1 = __ldg(reinterpret_cast<const uint4*>(B + o1 + r));
-            const u32 a0[4] = {x0.x, x0.y, x0.z, x0.w}, a1[4] = {x1.x, x1.y, x1.z, x1.w};
-            const u32 b0[4] = {y0.x, y0.y, y0.z, y0.w}, b1[4] = {y1.x, y1.y, y1.z, y1.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-#pragma unroll
-                for (int q = 0; q < NP; ++q) {
-                    const int comp = NP == 3 ? q : c0;
-                    if (comp == 0) v[q][r + e] = red32(mont32(a0[e], b0[e], p, pinv), p);
-                    else if (comp == 1)
-                        v[q][r + e] = red32(mont32(a0[e], b1[e], p, pinv), p) + red32(mont32(a1[e], b0[e], p, pinv), p);
-                    else v[q][r + e] = red32(mont32(a1[e], b1[e], p, pinv), p);
-                }
-            }
-        }
-        ntt32_inv_reg<LOGN, NP>(v, smd, T.airp + (size_t)j * G::N, T.airps + (size_t)j * G::N, p);
-#pragma unroll
-        for (int q = 0; q < NP; ++q) {
-            const int comp = NP == 3 ? q : c0;
-            u32* out = D + (((size_t)pr * 3 + comp) * J + j) * G::N;
-#pragma unroll
-            for (int r = 0; r < 16; ++r) out[((u32)r << (LOGN - 4)) | tid] = red32(shoup32(v[q][r], ni, nis, p), p);
-        }
-        if (NP == 1) __syncthreads();
+    for (int r = 0; r < E; r += 4) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(X + r));
+        const uint4 y = __ldg(reinterpret_cast<const uint4*>(Y + r));
+        v[0][r] = red32(mont32(x.x, y.x, p, pinv), p);
+        v[0][r + 1] = red32(mont32(x.y, y.y, p, pinv), p);
+        v[0][r + 2] = red32(mont32(x.z, y.z, p, pinv), p);
+        v[0][r + 3] = red32(mont32(x.w, y.w, p, pinv), p);
     }
+    if (comp == 1) {
+#pragma unroll
+        for (int r = 0; r < E; r += 4) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(A + o1 + r));
+            const uint4 y = __ldg(reinterpret_cast<const uint4*>(B + r));
+            v[0][r] += red32(mont32(x.x, y.x, p, pinv), p);
+            v[0][r + 1] += red32(mont32(x.y, y.y, p, pinv), p);
+            v[0][r + 2] += red32(mont32(x.z, y.z, p, pinv), p);
+            v[0][r + 3] += red32(mont32(x.w, y.w, p, pinv), p);
+        }
+    }
+    nttw_inv<LOGN, WB, 1>(v, smd, T.airp + (size_t)j * N, T.airps + (size_t)j * N, p);
+    const u32 ni = T.ninvRA[j], nis = T.ninvRA_s[j];
+    u32* out = D + (((size_t)pr * 3 + comp) * J + j) * N;
+#pragma unroll
+    for (int r = 0; r < E; ++r) out[((u32)r << (LOGN - WB)) | tid] = red32(shoup32(v[0][r], ni, nis, p), p);
 }
 
 }  // namespace cwgpu
@@ -519,51 +516,5 @@ __global__ void k_acc_mod(const unsigned long long* __restrict__ acc, size_t tot
     if (idx >= total) return;
     const u32 k = (u32)((idx >> T.logN) % T.Mm);
     partial[idx] = bar64(acc[idx], T.a[k], T.abar[k]);
-}
-}  // namespace cwgpu
-
-namespace cwgpu {
-/// Variant of k_tensor_intt_r with one tensor component per CTA (grid P * J * 3): 64 registers,
-/// two CTAs per SM whose barrier phases interleave.
-template <int LOGN>
-__global__ void __launch_bounds__(NttGeom<LOGN>::T, LOGN >= 14 ? 1 : 2) k_tensor_intt_c(
-    const u32* __restrict__ prepA, const u32* __restrict__ idxA, const u32* __restrict__ prepB,
-    const u32* __restrict__ idxB, u32 P, DevTab T, u32* __restrict__ D) {
-    using G = NttGeom<LOGN>;
-    extern __shared__ u32 smd[];
-    const u32 J = T.J;
-    const u32 tid = threadIdx.x;
-    const u32 comp = blockIdx.x % 3, pj = blockIdx.x / 3;
-    const u32 pr = pj / J, j = pj % J;
-    const u32 p = T.a[j], pinv = T.apinv[j];
-    const size_t per = (size_t)2 * J * G::N;
-    const u32* A = prepA + (size_t)(idxA ? idxA[pr] : pr) * per + (size_t)j * G::N + (tid << 4);
-    const u32* B = prepB + (size_t)(idxB ? idxB[pr] : pr) * per + (size_t)j * G::N + (tid << 4);
-    const size_t o1 = (size_t)J * G::N;
-    u32 v[1][16];
-#pragma unroll
-    for (int r = 0; r < 16; r += 4) {
-        if (comp == 0) {
-            const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(A + r)), y0 = __ldg(reinterpret_cast<const uint4*>(B + r));
-            v[0][r] = red32(mont32(x0.x, y0.x, p, pinv), p); v[0][r + 1] = red32(mont32(x0.y, y0.y, p, pinv), p);
-            v[0][r + 2] = red32(mont32(x0.z, y0.z, p, pinv), p); v[0][r + 3] = red32(mont32(x0.w, y0.w, p, pinv), p);
-        } else if (comp == 2) {
-            const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(A + o1 + r)), y1 = __ldg(reinterpret_cast<const uint4*>(B + o1 + r));
-            v[0][r] = red32(mont32(x1.x, y1.x, p, pinv), p); v[0][r + 1] = red32(mont32(x1.y, y1.y, p, pinv), p);
-            v[0][r + 2] = red32(mont32(x1.z, y1.z, p, pinv), p); v[0][r + 3] = red32(mont32(x1.w, y1.w, p, pinv), p);
-        } else {
-            const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(A + r)), y0 = __ldg(reinterpret_cast<const uint4*>(B + r));
-            const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(A + o1 + r)), y1 = __ldg(reinterpret_cast<const uint4*>(B + o1 + r));
-            v[0][r] = red32(mont32(x0.x, y1.x, p, pinv), p) + red32(mont32(x1.x, y0.x, p, pinv), p);
-            v[0][r + 1] = red32(mont32(x0.y, y1.y, p, pinv), p) + red32(mont32(x1.y, y0.y, p, pinv), p);
-            v[0][r + 2] = red32(mont32(x0.z, y1.z, p, pinv), p) + red32(mont32(x1.z, y0.z, p, pinv), p);
-            v[0][r + 3] = red32(mont32(x0.w, y1.w, p, pinv), p) + red32(mont32(x1.w, y0.w, p, pinv), p);
-        }
-    }
-    ntt32_inv_reg<LOGN, 1>(v, smd, T.airp + (size_t)j * G::N, T.airps + (size_t)j * G::N, p);
-    const u32 ni = T.ninvRA[j], nis = T.ninvRA_s[j];
-    u32* out = D + (((size_t)pr * 3 + comp) * J + j) * G::N;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) out[((u32)r << (LOGN - 4)) | tid] = red32(shoup32(v[0][r], ni, nis, p), p);
 }
 }  // namespace cwgpu

@@ -9,8 +9,10 @@ cfg = configs.config("C4")
 ctx = Context(cfg.N, cfg.primes, cfg.t)
 lib = ctx.lib
 lib.cwg_bench_kernel.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
-names = ["fwd NP1 MINB1", "fwd NP1 MINB2", "fwd NP1 MINB3", "fwd NP3 MINB1", "fwd NP2 MINB1", "inv NP3 MINB1",
-         "inv NP1 MINB2", "fwd NP1 MINB4", "fwd NP2 MINB2"]
+names = ["W5 fwd NP1 MINB3 (production)", "W5 inv NP1 MINB3 (production)", "W5 fwd NP2 MINB2",
+         "W5 inv NP2 MINB2", "W4 fwd NP1 MINB3", "W6 fwd NP2 MINB1",
+         "W5 fwd NP1 MINB3 prime-major", "W5 inv NP1 MINB3 prime-major", "W5 fwd NP2 MINB2 prime-major",
+         "W5 fwd NP1 MINB4 prime-major"]
 npolys = 36000
 only = [int(a) for a in sys.argv[1:]]
 for w, nm in enumerate(names):
@@ -22,4 +24,4 @@ for w, nm in enumerate(names):
         print(nm, "error", lib.cwg_last_error()); continue
     ns = ms.value * 1e6 / (npolys // 6 * 6)
     bfly = 8192 * 13 / 2
-    print(f"{nm:16s} {ns:8.1f} ns/poly  {bfly / ns:6.1f} Gbfly/s  {bfly / ns / 148 / 1.965:5.2f} bfly/cyc/SM")
+    print(f"{nm:32s} {ns:8.1f} ns/poly  {bfly / ns:6.1f} Gbfly/s  {bfly / ns / 148 / 1.965:5.2f} bfly/cyc/SM")

@@ -296,10 +296,11 @@ def test_answer_small_rings(gpu, reflib, N, k):
     """Small rings exercise partially filled coefficient blocks in the payload MAC grid."""
     from paper_2202_07569_b200 import configs
 
-    primes = configs.custom_chain(N, 2, 36)
+    primes = configs.custom_chain(N, 3, 36)  # k = 2 needs > 72 bits of q to decrypt at these N
     n = 10
     m = configs.min_code_length(n, k) if k > 1 else n
     c = configs.default_compression(N, m)
     got, want, be, payload = _answer_case(reflib, N, primes, 12289, n, k, m, c, s=2, op=0, seed=60 + N + k)
     assert np.array_equal(got, want)
+    assert be.noise_budget(got[1]) > 0
     assert np.array_equal(be.decrypt(got[1]), payload[1])
