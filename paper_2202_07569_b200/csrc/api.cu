@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 #include "ntt_reg.cuh"
 #include "params.h"
+#include "round.cuh"
 
 namespace cwgpu {
 
@@ -71,10 +72,17 @@ struct Ctx {
     DevTab T{};
     DevBuf tab, tab_self, round_tab;
     u32 JM = 16;  // aux-prime count padded to a multiple of 8 (rounding kernel template)
+    std::vector<unsigned char> rpar;  // RoundPar<JM> (k_round_hyb kernel-parameter block), JM <= 32
+    std::vector<unsigned char> rtc;   // RoundTcPar<JM, NC> (k_round_tc kernel-parameter block)
+    DevBuf rtc_B;                     // k_round_tc B matrix (canonical UMMA K-major layout)
+    u32 rtc_nc = 0;                   // k_round_tc GEMM width (0: no instance for this JM / Mm)
+    int round_kind = 2;               // 2 tensor-core, 1 IMAD + DFMA, 0 IMAD only (env CWGPU_ROUND=tc|hyb|int)
     bool old_mac = false;       // debugging: the first payload MAC kernel (env CWGPU_OLD_MAC)
     // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
-    // the FMA-bound rounding of one tile overlaps the latency-bound NTTs of the next (env CWGPU_STREAMS)
-    int nstreams = 2;
+    // the rounding of one tile overlaps the NTTs of the next (env CWGPU_STREAMS).  Paid off with the
+    // FMA-bound integer rounding kernel (292 vs 317 ms); with the tensor-core rounding one stream is
+    // faster (272 vs 297 ms at C4), so 1 is the default.
+    int nstreams = 1;
     cudaStream_t tst[2] = {nullptr, nullptr};
     cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
     DevBuf Dbuf2;
@@ -169,6 +177,98 @@ static u32 inv32_neg(u32 a) {  // -a^-1 mod 2^32
 static u32 shoup32h(u32 w, u32 p) { return (u32)(((u64)w << 32) / p); }
 static u64 shoup64h(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
 
+/// RoundPar<JM> from the RoundJ / RoundK tables (Montgomery forms for the integer-pipe
+/// primes, plain residues split at 2^15 for the FP64-pipe primes).
+template <int JM>
+static void fill_round_par(std::vector<unsigned char>& out, const std::vector<RoundJ>& rj, const std::vector<RoundK>& rk,
+                           const std::vector<u32>& Imod, const std::vector<u32>& IAmod, const std::vector<u32>& a, u32 J,
+                           u32 Mm) {
+    using RP = RoundPar<JM>;
+    constexpr int MI = RP::MI;
+    out.assign(sizeof(RP), 0);
+    RP& P = *reinterpret_cast<RP*>(out.data());
+    for (int j = 0; j < JM; ++j) {
+        P.a[j] = rj[j].a; P.chat[j] = rj[j].chat; P.chat_s[j] = rj[j].chat_s;
+        P.f0[j] = rj[j].f0; P.f1[j] = rj[j].f1;
+        P.inva_j[j] = (u32)j < J ? 1.0 / (double)a[j] : 0.0;
+    }
+    for (int k = 0; k < RP::KP; ++k) {  // padding primes of the FP64 groups: a = 1, all-zero I
+        P.fa[k] = 1; P.ad[k] = 1.0; P.inva[k] = 1.0; P.off2a[k] = 4503599627370496.0 + 2.0;
+    }
+    auto mf = [](u64 x, u32 p) { return (u32)((((u128)(x % p)) << 32) % p); };  // Montgomery form
+    for (u32 k = 0; k < Mm && k < (u32)JM; ++k) {
+        const u32 p = a[k];
+        if ((int)k < MI) {
+            P.ka[k] = rk[k].a; P.kpinv[k] = rk[k].pinv; P.kgcoef[k] = rk[k].gcoef; P.kroff[k] = rk[k].roff;
+            P.kc0[k] = rk[k].c0; P.kc30[k] = rk[k].c30;
+            for (u32 j = 0; j < J; ++j) P.ImodT[k][j] = mf(Imod[(size_t)j * Mm + k], p);
+        }
+        P.fa[k] = p;
+        for (u32 j = 0; j < J; ++j) {
+            const u32 I = Imod[(size_t)j * Mm + k];
+            P.Ilo[k][j] = (double)(I & 0x7fffu);
+            P.Ihi[k][j] = (double)(I >> 15);
+        }
+        const u32 nIA = (p - IAmod[k] % p) % p;
+        P.nIAlo[k] = (double)(nIA & 0x7fffu);
+        P.nIAhi[k] = (double)(nIA >> 15);
+        P.roff[k] = (double)((p - (u32)(((u64)1 << 36) % p)) % p);
+        P.ad[k] = (double)p;
+        P.inva[k] = 1.0 / (double)p;
+        P.off2a[k] = 4503599627370496.0 + 2.0 * (double)p;
+    }
+}
+
+/// (JM, NC) pairs k_round_tc is instantiated for (TMEM: JM + NC <= 128 columns).
+static bool tc_instance(u32 JM, u32 nc) {
+    return (JM == 8 && (nc == 48 || nc == 64)) || (JM == 16 && (nc == 64 || nc == 80)) ||
+           (JM == 24 && (nc == 80 || nc == 96)) || (JM == 32 && nc == 96);
+}
+
+/// k_round_tc tables: the parameter block (integer epilogue constants, Montgomery forms) and the
+/// B matrix [NC][K = 4 JM] of u8, K-major in the canonical no-swizzle UMMA layout (8-row x 16-B
+/// core matrices; a row's 16-B K chunks 128 B apart, 8-row groups K/16 * 128 B apart).
+static void build_round_tc(u32 JM, u32 NC, const std::vector<RoundJ>& rj, const std::vector<RoundK>& rk,
+                           const std::vector<u32>& Imod, const std::vector<u32>& a, u32 J, u32 Mm,
+                           std::vector<unsigned char>& par, std::vector<unsigned char>& Bm) {
+    const u32 K = 4 * JM, F0 = NC - 17, G0 = NC - 6, MMAX = F0 / 4;
+    Bm.assign((size_t)NC * K, 0);
+    auto put = [&](u32 n, u32 kb, unsigned char v) {
+        Bm[(size_t)(n / 8) * (K / 16 * 128) + (kb / 16) * 128 + (n % 8) * 16 + kb % 16] = v;
+    };
+    auto mf = [](u64 x, u32 p) { return (u32)((((u128)(x % p)) << 32) % p); };  // Montgomery form
+    for (u32 k = 0; k < Mm; ++k)
+        for (u32 j = 0; j < J; ++j) {
+            const u32 p = a[k];
+            const u64 Im = mf(Imod[(size_t)j * Mm + k], p);
+            for (u32 aa = 0; aa < 4; ++aa) {
+                const u32 v = (u32)((Im << (8 * aa)) % p);  // (2^(8a) I_kj 2^32) mod a_k
+                for (u32 b = 0; b < 4; ++b) put(4 * k + b, 4 * j + aa, (unsigned char)(v >> (8 * b)));
+            }
+        }
+    for (u32 j = 0; j < J; ++j) {
+        const u64 F = ((u64)rj[j].f1 << 32) | rj[j].f0;
+        const u64 G = (1ull << 46) / a[j];
+        for (u32 aa = 0; aa < 4; ++aa) {
+            for (u32 sft = 0; sft < 11; ++sft)
+                if (sft >= aa && sft - aa < 8) put(F0 + sft, 4 * j + aa, (unsigned char)(F >> (8 * (sft - aa))));
+            for (u32 sft = 0; sft < 6; ++sft)
+                if (sft >= aa && sft - aa < 3) put(G0 + sft, 4 * j + aa, (unsigned char)(G >> (8 * (sft - aa))));
+        }
+    }
+    // parameter block: RoundTcPar<JM, NC> = 6 arrays of MMAX u32
+    par.assign((size_t)6 * MMAX * 4, 0);
+    u32* P = reinterpret_cast<u32*>(par.data());
+    for (u32 k = 0; k < Mm && k < MMAX; ++k) {
+        P[0 * MMAX + k] = rk[k].a;
+        P[1 * MMAX + k] = rk[k].pinv;
+        P[2 * MMAX + k] = rk[k].gcoef;
+        P[3 * MMAX + k] = rk[k].roff;
+        P[4 * MMAX + k] = rk[k].c0;
+        P[5 * MMAX + k] = rk[k].c30;
+    }
+}
+
 static void build_tables(Ctx& c) {
     const ChainParams& cp = c.cp;
     const AuxBasis& ab = c.ab;
@@ -227,7 +327,7 @@ static void build_tables(Ctx& c) {
     for (u32 k = 0; k < Mm; ++k) M = M.mul_u64(ab.a[k]);
     T.AW = (A.bits() + 31) / 32;
     if (T.AW > (u32)kAW) throw std::invalid_argument("cwgpu: aux basis too wide");
-    std::vector<u32> chat(J), chat_s(J), frac96(3 * J), Imod((size_t)J * Mm), Aov;
+    std::vector<u32> chat(J), chat_s(J), frac96(3 * J), Imod((size_t)J * Mm), Aov, ninvRAc(J), ninvRAc_s(J);
     std::vector<u64> ImodQ((size_t)J * L);
     std::vector<u32> liftV_m((size_t)L * J), liftV2_m((size_t)L * J), liftW_m(J), liftV_n((size_t)L * J),
         liftV2_n((size_t)L * J), liftW_n(J);
@@ -253,6 +353,8 @@ static void build_tables(Ctx& c) {
         Big Aj = A.div_u64(p);
         chat[j] = (u32)invmod64(Aj.mod_u64(p), p);
         chat_s[j] = shoup32h(chat[j], p);
+        ninvRAc[j] = (u32)mulmod64(ninvRA[j], chat[j], p);
+        ninvRAc_s[j] = shoup32h(ninvRAc[j], p);
         // t (A/a_j) = I_j q + R_j ; frac96 = floor(R_j 2^96 / q)
         Big tA = Aj.mul_u64(cp.t), I, R;
         Big::divmod(tA, Q, I, R);
@@ -309,7 +411,7 @@ static void build_tables(Ctx& c) {
     ADD(a); ADD(apinv); ADD(abar); ADD(a2_64); ADD(ninvA); ADD(ninvA_s); ADD(ninvRA); ADD(ninvRA_s);
     ADD(arp); ADD(arps); ADD(airp); ADD(airps);
     ADD(liftV_m); ADD(liftV2_m); ADD(liftW_m); ADD(liftV_n); ADD(liftV2_n); ADD(liftW_n);
-    ADD(chat); ADD(chat_s); ADD(aF); ADD(frac96); ADD(fracA); ADD(Imod); ADD(IAmod); ADD(ImodQ); ADD(IAmodQ);
+    ADD(chat); ADD(chat_s); ADD(ninvRAc); ADD(ninvRAc_s); ADD(aF); ADD(frac96); ADD(fracA); ADD(Imod); ADD(IAmod); ADD(ImodQ); ADD(IAmodQ);
     ADD(Aw); ADD(Aov); ADD(mhat); ADD(mhat_s); ADD(mF); ADD(Mconv); ADD(MnegQ);
 #undef ADD
     c.tab.ensure(blob.b.size());
@@ -324,7 +426,7 @@ static void build_tables(Ctx& c) {
     P32(ninvRA, ninvRA); P32(ninvRA_s, ninvRA_s); P32(arp, arp); P32(arps, arps); P32(airp, airp); P32(airps, airps);
     P32(liftV_m, liftV_m); P32(liftV2_m, liftV2_m); P32(liftW_m, liftW_m); P32(liftV_n, liftV_n);
     P32(liftV2_n, liftV2_n); P32(liftW_n, liftW_n);
-    P32(chat, chat); P32(chat_s, chat_s); P64(aF, aF); P32(frac96, frac96); P32(fracA, fracA); P32(Imod, Imod);
+    P32(chat, chat); P32(chat_s, chat_s); P32(ninvRAc, ninvRAc); P32(ninvRAc_s, ninvRAc_s); P64(aF, aF); P32(frac96, frac96); P32(fracA, fracA); P32(Imod, Imod);
     P32(IAmod, IAmod); P64(ImodQ, ImodQ); P64(IAmodQ, IAmodQ); P32(Aw, Aw); P32(Aov, Aov);
     P32(mhat, mhat); P32(mhat_s, mhat_s); P64(mF, mF); P64(Mconv, Mconv); P64(MnegQ, MnegQ);
 #undef P64
@@ -369,6 +471,30 @@ static void build_tables(Ctx& c) {
         std::memcpy(blob.data() + sizeof(RoundJ) * c.JM + sizeof(RoundK) * kMaxJ, imT.data(), imT.size() * 4);
         c.round_tab.ensure(bytes);
         CK(cudaMemcpy(c.round_tab.p, blob.data(), bytes, cudaMemcpyHostToDevice));
+        // kernel-parameter block of the hybrid IMAD / DFMA rounding kernel
+        c.rpar.clear();
+        switch (c.JM) {
+            case 8: fill_round_par<8>(c.rpar, rj, rk, Imod, IAmod, a, J, Mm); break;
+            case 16: fill_round_par<16>(c.rpar, rj, rk, Imod, IAmod, a, J, Mm); break;
+            case 24: fill_round_par<24>(c.rpar, rj, rk, Imod, IAmod, a, J, Mm); break;
+            case 32: fill_round_par<32>(c.rpar, rj, rk, Imod, IAmod, a, J, Mm); break;
+            default: break;  // JM = 40: the block would exceed the kernel-parameter limit
+        }
+        // tensor-core rounding: smallest instantiated GEMM width holding 4 Mm + 17 columns
+        c.rtc.clear();
+        c.rtc_nc = 0;
+        const u32 need = 4 * Mm + 17;
+        for (u32 nc : {48u, 64u, 80u, 96u, 112u}) {
+            if (nc < need || !tc_instance(c.JM, nc)) continue;
+            c.rtc_nc = nc;
+            break;
+        }
+        if (c.rtc_nc) {
+            std::vector<unsigned char> Bm;
+            build_round_tc(c.JM, c.rtc_nc, rj, rk, Imod, a, J, Mm, c.rtc, Bm);
+            c.rtc_B.ensure(Bm.size());
+            CK(cudaMemcpy(c.rtc_B.p, Bm.data(), Bm.size(), cudaMemcpyHostToDevice));
+        }
     }
     // device copy of the table itself (slow paths read it through T.self)
     c.tab_self.ensure(sizeof(DevTab));
@@ -420,9 +546,9 @@ struct Reg32 {
     static void sel3(Ctx& c, u32* D, u32 P) {
         launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN>, (size_t)P * 3 * c.ab.Mm, R::T, R::SMEM, D, c.T, c.ab.J);
     }
-    static void tensor(Ctx& c, const u32* pa, const u32* ia, const u32* pb, const u32* ib, u32 P, u32* D) {
+    static void tensor(Ctx& c, const u32* pa, const u32* ia, const u32* pb, const u32* ib, u32 P, u32* D, int fold) {
         launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN>, (size_t)P * c.ab.J * 3, R::T, R::SMEM, pa, ia, pb, ib,
-                     P, c.T, D);
+                     P, c.T, D, fold);
     }
 };
 
@@ -439,6 +565,9 @@ struct Reg32 {
     }
 
 static void set_smem_limits(u32 N) {
+#define RTC(JMv, NCv) CK(cudaFuncSetAttribute(k_round_tc<JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundTcSmem));
+    RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
+#undef RTC
     Reg32<8>::limits(); Reg32<9>::limits(); Reg32<10>::limits(); Reg32<11>::limits();
     Reg32<12>::limits(); Reg32<13>::limits(); Reg32<14>::limits();
     const int s64 = (int)(N * sizeof(u64)), s32 = (int)(N * sizeof(u32));
@@ -562,8 +691,9 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
                          bool to_mac, u64* chain_out) {
     const u32 N = c.cp.N, J = c.ab.J;
     u32* D = c.dcur->get<u32>((size_t)P * 3 * J * N);
+    const bool tc = to_mac && reg32_ok(c.cp.logN) && c.round_kind == 2 && c.rtc_nc != 0;
     if (reg32_ok(c.cp.logN)) {
-        REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D));
+        REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? 1 : 0));
     } else {
         launch(c, k_tensor_intt, (size_t)P * J, ntt_block(N), N * 4, prepA, idxA, prepB, idxB, P, c.T, D);
     }
@@ -574,7 +704,24 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         const RoundJ* rj = c.round_tab.ptr<RoundJ>();
         const RoundK* rk = reinterpret_cast<const RoundK*>(rj + c.JM);
         const u32* im = reinterpret_cast<const u32*>(rk + kMaxJ);
-        if (c.JM == 8) launch_named(c, "k_round_mac", k_round_mac_t<8>, grid, 256, sm, D, P, c.T, rj, rk, im);
+        if (tc) {
+            const u32 g3 = (u32)std::min<size_t>(items / 128, 148 * 4);
+            const uint4* Bm = c.rtc_B.ptr<uint4>();
+#define RTC(JMv, NCv)                                                                                             \
+    if (c.JM == JMv && c.rtc_nc == NCv)                                                                          \
+        launch_named(c, "k_round_mac", k_round_tc<JMv, NCv>, g3, 128, kRoundTcSmem, D, P, c.T,                    \
+                     *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk);
+            RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
+#undef RTC
+        } else if (!c.rpar.empty() && c.round_kind >= 1) {
+            const size_t g2 = std::min<size_t>(blocks(items, 256), 148 * 4);
+            switch (c.JM) {
+                case 8: launch_named(c, "k_round_mac", k_round_hyb<8>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<8>*>(c.rpar.data()), rk); break;
+                case 16: launch_named(c, "k_round_mac", k_round_hyb<16>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<16>*>(c.rpar.data()), rk); break;
+                case 24: launch_named(c, "k_round_mac", k_round_hyb<24>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<24>*>(c.rpar.data()), rk); break;
+                default: launch_named(c, "k_round_mac", k_round_hyb<32>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<32>*>(c.rpar.data()), rk); break;
+            }
+        } else if (c.JM == 8) launch_named(c, "k_round_mac", k_round_mac_t<8>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else if (c.JM == 16) launch_named(c, "k_round_mac", k_round_mac_t<16>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else if (c.JM == 24) launch_named(c, "k_round_mac", k_round_mac_t<24>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else if (c.JM == 32) launch_named(c, "k_round_mac", k_round_mac_t<32>, grid, 256, sm, D, P, c.T, rj, rk, im);
@@ -1007,6 +1154,8 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         CK(cudaMemset(c.d_fb, 0, 8));
         set_smem_limits(N);
         if (const char* e = std::getenv("CWGPU_STREAMS")) c.nstreams = std::atoi(e) >= 2 ? 2 : 1;
+        if (const char* e = std::getenv("CWGPU_ROUND"))
+            c.round_kind = std::string(e) == "int" ? 0 : std::string(e) == "hyb" ? 1 : 2;
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
         c.dcur = &c.Dbuf;
         for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));

@@ -40,6 +40,8 @@ struct DevTab {
     const std::uint32_t* ninvA_s;
     const std::uint32_t* ninvRA;   // (N * 2^32)^-1 mod a_j (+ Shoup): undoes the Montgomery factor
     const std::uint32_t* ninvRA_s;
+    const std::uint32_t* ninvRAc;  // ninvRA (A/a_j)^-1 mod a_j (+ Shoup): INTT output = HPS residue w_j
+    const std::uint32_t* ninvRAc_s;
     const std::uint32_t* arp;      // [J][N]
     const std::uint32_t* arps;
     const std::uint32_t* airp;

@@ -250,11 +250,12 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_ntt32r_
 /// per CTA: block (pr * J + j) * 3 + comp (the three components of one product are adjacent,
 /// so their shared operand planes are L2 hits).  Operands: Montgomery-form NTT residues
 /// [idx][2][J][N]; output D[pr][comp][j][N] in normal form (the (N 2^32)^-1 scale undoes the
-/// Montgomery factor).
+/// Montgomery factor).  fold: also multiply by (A/a_j)^-1, i.e. emit the HPS residues w_j
+/// that the tensor-core rounding kernel consumes directly.
 template <int LOGN>
 __global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_tensor_intt_r(
     const u32* __restrict__ prepA, const u32* __restrict__ idxA, const u32* __restrict__ prepB,
-    const u32* __restrict__ idxB, u32 P, DevTab T, u32* __restrict__ D) {
+    const u32* __restrict__ idxB, u32 P, DevTab T, u32* __restrict__ D, int fold) {
     using R = RegNtt<LOGN>;
     constexpr int WB = R::WB, E = R::E, N = 1 << LOGN;
     extern __shared__ u32 smd[];
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_tensor_
         }
     }
     nttw_inv<LOGN, WB, 1>(v, smd, T.airp + (size_t)j * N, T.airps + (size_t)j * N, p);
-    const u32 ni = T.ninvRA[j], nis = T.ninvRA_s[j];
+    const u32 ni = fold ? T.ninvRAc[j] : T.ninvRA[j], nis = fold ? T.ninvRAc_s[j] : T.ninvRA_s[j];
     u32* out = D + (((size_t)pr * 3 + comp) * J + j) * N;
 #pragma unroll
     for (int r = 0; r < E; ++r) out[((u32)r << (LOGN - WB)) | tid] = red32(shoup32(v[0][r], ni, nis, p), p);

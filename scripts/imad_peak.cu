@@ -8,8 +8,10 @@ template <int OP>
 __global__ void k(uint32_t* out, uint32_t iters, uint32_t seed) {
     uint32_t a[8], b = seed | 1, c = seed * 3 + 1;
     uint64_t w[8];
+    double d[8];
+    const double db = 1.0000001 + seed * 1e-9, dc = 0.5;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { a[i] = threadIdx.x * 7 + i; w[i] = a[i]; }
+    for (int i = 0; i < 8; ++i) { a[i] = threadIdx.x * 7 + i; w[i] = a[i]; d[i] = a[i]; }
     for (uint32_t it = 0; it < iters; ++it) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -19,11 +21,15 @@ __global__ void k(uint32_t* out, uint32_t iters, uint32_t seed) {
             if (OP == 3) a[i] = a[i] + b + c;                  // IADD3
             if (OP == 4) a[i] = min(a[i] - b, a[i]);           // VIADDMNMX
             if (OP == 5) a[i] = (a[i] ^ b) & c;                // LOP3
+            if (OP == 6) d[i] = fma(d[i], db, dc);             // DFMA
+            if (OP == 7) { a[i] = a[i] * b + c; d[i] = fma(d[i], db, dc); }  // IMAD || DFMA (1 each)
+            if (OP == 8) a[i] = (uint32_t)__double2uint_rz(d[i] + a[i]);    // DADD + F2I.U32.F64
+            if (OP == 9) d[i] = fma((double)a[i], db, d[i]);   // I2F.F64.U32 + DFMA
         }
     }
     uint32_t s = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) s += a[i] + (uint32_t)w[i] + (uint32_t)(w[i] >> 32);
+    for (int i = 0; i < 8; ++i) s += a[i] + (uint32_t)w[i] + (uint32_t)(w[i] >> 32) + (uint32_t)d[i];
     if (s == 0x12345678) out[0] = s;
 }
 
@@ -62,5 +68,9 @@ int main() {
     run<3>("IADD3", p.multiProcessorCount, ghz);
     run<4>("VIADDMNMX", p.multiProcessorCount, ghz);
     run<5>("LOP3", p.multiProcessorCount, ghz);
+    run<6>("DFMA", p.multiProcessorCount, ghz);
+    run<7>("IMAD+DFMA", p.multiProcessorCount, ghz);
+    run<8>("DADD+F2I", p.multiProcessorCount, ghz);
+    run<9>("I2F+DFMA", p.multiProcessorCount, ghz);
     return 0;
 }
