@@ -39,6 +39,9 @@ sys.path.insert(0, ROOT)
 HBM_FALLBACK = 6650.0
 
 
+IMAD_FALLBACK = 17999.2  # G IMAD lane-ops/s, profiles/r01_int_pipe_peaks.json
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -46,6 +49,68 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return HBM_FALLBACK, "fallback"
+
+
+def imad_peak():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_int_pipe_peaks.json")) as f:
+            return float(json.load(f)["imad_gops"]), "measured (scripts/imad_peak.cu)"
+    except Exception:
+        return IMAD_FALLBACK, "measured constant"
+
+
+# ncu --set full captures of the default C4 command (dram read + write bytes per launch) and the
+# algorithmic units of the same launch, so `traffic` can be scaled to any launch of the kernel
+def ncu_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic_C4.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def rooflines(kstats, cfg, info, hbm, hbm_kind):
+    """Per-kernel roofline from the profiled device times and the algorithmic work the
+    library counted (cwg_kernel_units):
+      NTT kernels (k_tensor_intt, k_ntt32r_sel3, ...): IMAD-bound; N/2 log2 N Shoup butterflies
+        per polynomial at 4 IMAD slots each (IMAD.HI = 2 slots) vs the measured IMAD rate;
+      k_round_tc / k_round_*: HBM; (J + Mm) 32-bit words per coefficient (read J residue planes,
+        write Mm MAC-basis planes);
+      k_mac: HBM; payload + selection words streamed."""
+    import math
+
+    ip, ip_kind = imad_peak()
+    tr = ncu_traffic()
+    out = {}
+    N = cfg.N
+    for name, (ms, cnt, units) in kstats.items():
+        if ms <= 0 or cnt == 0:
+            continue
+        per_launch_s = ms / cnt / 1e3
+        if name.startswith("k_ntt32r") or name == "k_tensor_intt":
+            bfly = units / cnt * (N // 2) * int(math.log2(N))
+            ach = bfly * 4 / per_launch_s / 1e9
+            r = {"bound": "imad", "achieved": ach, "peak": ip, "unit": "G IMAD-slots/s", "frac": ach / ip,
+                 "peak_kind": ip_kind, "work_per_launch": f"{units / cnt:.0f} polynomials x {N // 2 * int(math.log2(N))} "
+                 "butterflies x 4 IMAD slots"}
+        elif name.startswith("k_round"):
+            byt = units / cnt * (info.J + info.Mm) * 4
+            ach = byt / per_launch_s / 1e9
+            r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "peak_kind": hbm_kind,
+                 "work_per_launch": f"{units / cnt:.0f} coefficients x (J + Mm) x 4 B"}
+        elif name == "k_mac":
+            byt = units / cnt
+            ach = byt / per_launch_s / 1e9
+            r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "peak_kind": hbm_kind,
+                 "work_per_launch": f"{byt:.3e} B (payload + selection words)"}
+        else:
+            continue
+        t = tr.get(name)
+        r["traffic"] = t["dram_bytes_per_unit"] * units / cnt if t else None
+        r["launch_ms"] = ms / cnt
+        r["ms_per_answer"] = ms
+        out[name] = r
+    return out
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -319,7 +384,7 @@ def main():
         ctx.answer_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, dout.data_ptr(), timings=tm)
     else:
         ctx.answer_partial_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, partial.data_ptr(), timings=tm)
-    kstats = ctx.kernel_stats()
+    kstats = ctx.kernel_stats(units=True)
     ctx.set_profiling(False)
 
     if rank != 0:
@@ -331,14 +396,13 @@ def main():
     db_bytes = cfg.db_bytes()
     value = db_bytes / (ms / 1e3) / 1e9
     e2e = db_bytes / (ms_e2e / 1e3) / 1e9
-    # roofline of the payload MAC kernel (HBM-bound): algorithmic bytes = rows * s * L * N * 8 per
-    # launch (the NTT-form database words it streams), over the CUDA-event launch time.
-    mac_ms, mac_n = kstats.get("k_mac", (0.0, 0))
-    local_rows = hi - lo
-    bytes_per_launch = local_rows / max(mac_n, 1) * cfg.s * L * N * 8
-    mac_achieved = bytes_per_launch / (mac_ms / max(mac_n, 1) / 1e3) / 1e9 if mac_n else None
+    roof = rooflines(kstats, cfg, info, hbm, peak_kind)
     tot_prof = sum(v[0] for v in kstats.values())
-    dom = max(kstats.items(), key=lambda kv: kv[1][0]) if kstats else ("", (0, 0))
+    dom = max(kstats.items(), key=lambda kv: kv[1][0]) if kstats else ("", (0, 0, 0))
+    local_rows = hi - lo
+    top = dict(roof.get(dom[0], {}))
+    if top:
+        top = {"kernel": dom[0], **top, "share_of_step": dom[1][0] / tot_prof if tot_prof else None}
     line = {
         "metric": "db_GBps_scanned", "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -353,10 +417,8 @@ def main():
                 "d2h_bytes_per_step": int(resp_words * 8)},
         "gpu_launches": int(launches),
         "clocks": clocks,
-        "roofline": {"kernel": "k_mac", "bound": "hbm", "achieved": mac_achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": (mac_achieved / hbm) if mac_achieved else None, "traffic": None,
-                     "peak_kind": peak_kind, "bytes_per_launch": bytes_per_launch,
-                     "share_of_step": mac_ms / tot_prof if tot_prof else None},
+        "roofline": top or None,
+        "rooflines": roof,
         "kernels_ms_per_answer": {k: round(v[0], 3) for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
         "dominant_kernel": {"name": dom[0], "share_of_step": dom[1][0] / tot_prof if tot_prof else None},
         "stages_ms": {k: getattr(tm, k) for k in ("expand_ms", "select_ms", "mac_ms", "finish_ms")},

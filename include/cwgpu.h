@@ -130,6 +130,10 @@ void* cwg_stream(const cwg_ctx* ctx);
 int cwg_set_profiling(cwg_ctx* ctx, int on);
 int cwg_kernel_stats(const cwg_ctx* ctx, uint32_t idx, char* name, uint32_t name_len, double* total_ms,
                      uint64_t* count);
+/* Algorithmic work of kernel idx summed over its profiled launches: polynomials transformed
+ * (NTT kernels), coefficients rounded (k_round_*), bytes streamed (k_mac: payload + selection
+ * words).  Used for the roofline fractions in bench.py. */
+int cwg_kernel_units(const cwg_ctx* ctx, uint32_t idx, double* units);
 
 #ifdef __cplusplus
 }

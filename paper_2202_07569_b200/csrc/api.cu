@@ -107,8 +107,21 @@ struct Ctx {
     u64 launches = 0;
     // per-kernel profiling (CUDA events around every launch; off in timed runs)
     bool profiling = false;
-    std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
-    std::vector<std::pair<std::string, std::pair<double, u64>>> prof_stats;
+    struct ProfLaunch {
+        const char* name;
+        cudaEvent_t e0, e1;
+        double units;
+    };
+    struct ProfStat {
+        std::string name;
+        double ms = 0, units = 0;
+        u64 count = 0;
+    };
+    std::vector<ProfLaunch> prof_pending;
+    std::vector<ProfStat> prof_stats;
+    // algorithmic work of the next launch for the profile (0: the grid size, i.e. one unit per
+    // CTA -- polynomials for the NTT kernels); see cwg_kernel_units
+    double next_units = 0;
 };
 
 thread_local std::string g_err;
@@ -128,8 +141,9 @@ static void launch_named(Ctx& c, const char* name, K kern, size_t grid, unsigned
     ++c.launches;
     if (c.profiling) {
         CK(cudaEventRecord(e1, c.st));
-        c.prof_pending.push_back({name, {e0, e1}});
+        c.prof_pending.push_back({name, e0, e1, c.next_units > 0 ? c.next_units : (double)grid});
     }
+    c.next_units = 0;
 }
 #define launch(c, kern, ...) launch_named(c, #kern, kern, __VA_ARGS__)
 
@@ -137,17 +151,18 @@ static void launch_named(Ctx& c, const char* name, K kern, size_t grid, unsigned
 static void prof_collect(Ctx& c) {
     for (auto& p : c.prof_pending) {
         float f = 0;
-        CK(cudaEventElapsedTime(&f, p.second.first, p.second.second));
-        cudaEventDestroy(p.second.first);
-        cudaEventDestroy(p.second.second);
-        std::string name(p.first);
-        auto it = std::find_if(c.prof_stats.begin(), c.prof_stats.end(), [&](auto& x) { return x.first == name; });
+        CK(cudaEventElapsedTime(&f, p.e0, p.e1));
+        cudaEventDestroy(p.e0);
+        cudaEventDestroy(p.e1);
+        std::string name(p.name);
+        auto it = std::find_if(c.prof_stats.begin(), c.prof_stats.end(), [&](auto& x) { return x.name == name; });
         if (it == c.prof_stats.end()) {
-            c.prof_stats.push_back({name, {0.0, 0}});
+            c.prof_stats.push_back({name});
             it = c.prof_stats.end() - 1;
         }
-        it->second.first += f;
-        it->second.second += 1;
+        it->ms += f;
+        it->units += p.units;
+        it->count += 1;
     }
     c.prof_pending.clear();
 }
@@ -704,22 +719,23 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         const RoundJ* rj = c.round_tab.ptr<RoundJ>();
         const RoundK* rk = reinterpret_cast<const RoundK*>(rj + c.JM);
         const u32* im = reinterpret_cast<const u32*>(rk + kMaxJ);
+        c.next_units = (double)items;  // coefficients rounded
         if (tc) {
             const u32 g3 = (u32)std::min<size_t>(items / 128, 148 * 4);
             const uint4* Bm = c.rtc_B.ptr<uint4>();
 #define RTC(JMv, NCv)                                                                                             \
     if (c.JM == JMv && c.rtc_nc == NCv)                                                                          \
-        launch_named(c, "k_round_mac", k_round_tc<JMv, NCv>, g3, 128, kRoundTcSmem, D, P, c.T,                    \
+        launch_named(c, "k_round_tc", k_round_tc<JMv, NCv>, g3, 128, kRoundTcSmem, D, P, c.T,                    \
                      *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk);
             RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
 #undef RTC
         } else if (!c.rpar.empty() && c.round_kind >= 1) {
             const size_t g2 = std::min<size_t>(blocks(items, 256), 148 * 4);
             switch (c.JM) {
-                case 8: launch_named(c, "k_round_mac", k_round_hyb<8>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<8>*>(c.rpar.data()), rk); break;
-                case 16: launch_named(c, "k_round_mac", k_round_hyb<16>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<16>*>(c.rpar.data()), rk); break;
-                case 24: launch_named(c, "k_round_mac", k_round_hyb<24>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<24>*>(c.rpar.data()), rk); break;
-                default: launch_named(c, "k_round_mac", k_round_hyb<32>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<32>*>(c.rpar.data()), rk); break;
+                case 8: launch_named(c, "k_round_hyb", k_round_hyb<8>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<8>*>(c.rpar.data()), rk); break;
+                case 16: launch_named(c, "k_round_hyb", k_round_hyb<16>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<16>*>(c.rpar.data()), rk); break;
+                case 24: launch_named(c, "k_round_hyb", k_round_hyb<24>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<24>*>(c.rpar.data()), rk); break;
+                default: launch_named(c, "k_round_hyb", k_round_hyb<32>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<32>*>(c.rpar.data()), rk); break;
             }
         } else if (c.JM == 8) launch_named(c, "k_round_mac", k_round_mac_t<8>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else if (c.JM == 16) launch_named(c, "k_round_mac", k_round_mac_t<16>, grid, 256, sm, D, P, c.T, rj, rk, im);
@@ -983,6 +999,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         chunks = (Rt + chunk - 1) / chunk;
         const u32* dbt = c.db.ptr<u32>() + (size_t)r0 * c.s * Mm * N;
         const size_t threads = (size_t)c.s * Mm * ((N / 4 + 255) / 256) * 256 * chunks;
+        c.next_units = (double)Rt * (c.s + nc) * Mm * N * 4;  // DB + selection words streamed
         if (c.old_mac)
             launch_named(c, "k_mac", k_mac, blocks((size_t)c.s * Mm * N, 128), 128, 0, (const u32*)Z, nc, zs, dbt, Rt,
                          c.s, c.T, c.acc_lo.ptr<u64>(), c.acc_hi.ptr<u64>());
@@ -1452,9 +1469,16 @@ int cwg_kernel_stats(const cwg_ctx* h, uint32_t idx, char* name, uint32_t name_l
     const Ctx& c = h->c;
     if (idx >= c.prof_stats.size()) return CWG_EINVAL;
     const auto& e = c.prof_stats[idx];
-    std::snprintf(name, name_len, "%s", e.first.c_str());
-    *total_ms = e.second.first;
-    *count = e.second.second;
+    std::snprintf(name, name_len, "%s", e.name.c_str());
+    *total_ms = e.ms;
+    *count = e.count;
+    return CWG_OK;
+}
+
+int cwg_kernel_units(const cwg_ctx* h, uint32_t idx, double* units) {
+    const Ctx& c = h->c;
+    if (idx >= c.prof_stats.size()) return CWG_EINVAL;
+    *units = c.prof_stats[idx].units;
     return CWG_OK;
 }
 

@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = [
     "cwg_last_error", "cwg_create", "cwg_destroy", "cwg_get_info", "cwg_load_db", "cwg_set_keys",
     "cwg_answer", "cwg_partial_words", "cwg_answer_partial", "cwg_finish", "cwg_select", "cwg_ntt",
     "cwg_expand", "cwg_mul_lazy", "cwg_relinearize", "cwg_substitute", "cwg_kernel_launches",
-    "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats", "cwg_bench_kernel",
+    "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats", "cwg_kernel_units", "cwg_bench_kernel",
     "cwg_client_last_error", "cwg_client_create", "cwg_client_destroy", "cwg_client_digits",
     "cwg_client_export_keys", "cwg_client_encrypt", "cwg_client_pack_query", "cwg_client_decrypt",
 ]
@@ -110,6 +110,7 @@ def load_library(path: str = LIB_PATH):
     lib.cwg_set_profiling.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.cwg_kernel_stats.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_char_p, ctypes.c_uint32,
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
+    lib.cwg_kernel_units.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.POINTER(ctypes.c_double)]
     lib.cwg_client_last_error.restype = ctypes.c_char_p
     lib.cwg_client_create.restype = ctypes.c_void_p
     lib.cwg_client_create.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint64, ctypes.c_uint32,
@@ -328,13 +329,18 @@ class Context:
     def set_profiling(self, on: bool):
         _raise(self.lib, self.lib.cwg_set_profiling(self.h, int(on)))
 
-    def kernel_stats(self) -> dict:
-        """{kernel: (total_ms, launches)} collected while profiling was on."""
+    def kernel_stats(self, units: bool = False) -> dict:
+        """{kernel: (total_ms, launches)} collected while profiling was on; with units=True
+        {kernel: (total_ms, launches, algorithmic units)} (see cwg_kernel_units)."""
         out, i = {}, 0
         buf = ctypes.create_string_buffer(128)
-        tot, cnt = ctypes.c_double(), ctypes.c_uint64()
+        tot, cnt, u = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_double()
         while self.lib.cwg_kernel_stats(self.h, i, buf, 128, ctypes.byref(tot), ctypes.byref(cnt)) == CWG_OK:
-            out[buf.value.decode()] = (tot.value, cnt.value)
+            if units:
+                self.lib.cwg_kernel_units(self.h, i, ctypes.byref(u))
+                out[buf.value.decode()] = (tot.value, cnt.value, u.value)
+            else:
+                out[buf.value.decode()] = (tot.value, cnt.value)
             i += 1
         return out
 

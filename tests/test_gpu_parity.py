@@ -222,9 +222,11 @@ def test_errors_match_reference_messages(gpu):
         ctx.answer(q, 3, 6)
 
 
-def test_exact_fallback_paths_match(gpu, reflib):
+@pytest.mark.parametrize("kind", ["tc", "hyb", "int"])
+def test_exact_fallback_paths_match(gpu, reflib, kind):
     """Every rounding / centring decision forced through the exact multiword path
-    (round_exact, crt_round_exact) in a subprocess with CWGPU_FORCE_EXACT=1."""
+    (round_exact, crt_round_exact) in a subprocess with CWGPU_FORCE_EXACT=1, for each
+    rounding engine (tensor-core, IMAD + DFMA, IMAD only)."""
     import os
     import subprocess
     import sys
@@ -256,10 +258,28 @@ assert np.array_equal(got, want)
 assert tm["exact_fallbacks"] > 0
 print("ok", tm["exact_fallbacks"])
 ''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CWGPU_FORCE_EXACT="1")
+    env = dict(os.environ, CWGPU_FORCE_EXACT="1", CWGPU_ROUND=kind)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ok" in out.stdout
+
+
+@pytest.mark.parametrize("kind", ["tc", "hyb", "int"])
+@pytest.mark.parametrize("N,L,bits", [(2048, 4, 50), (4096, 3, 36), (1024, 8, 55)])
+def test_rounding_engines(gpu, reflib, monkeypatch, kind, N, L, bits):
+    """The three implementations of the tensor rounding (bfv.cpp:811-849) -- tcgen05 int8 GEMM
+    (k_round_tc), IMAD + DFMA (k_round_hyb), IMAD only (k_round_mac_t) -- against the reference
+    answer, across aux-basis widths (JM = 8, 16, 32)."""
+    from paper_2202_07569_b200 import configs
+
+    monkeypatch.setenv("CWGPU_ROUND", kind)
+    _, primes, t = small_params(N, L, bits, 65537)
+    n, k = 30, 2
+    m = configs.min_code_length(n, k)
+    c = configs.default_compression(N, m)
+    got, want, be, payload = _answer_case(reflib, N, primes, t, n, k, m, c, s=1, op=0, seed=70 + L)
+    assert np.array_equal(got, want)
+    assert np.array_equal(be.decrypt(got[0]), payload[0])
 
 
 @pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
