@@ -79,10 +79,9 @@ struct Ctx {
     int round_kind = 2;               // 2 tensor-core, 1 IMAD + DFMA, 0 IMAD only (env CWGPU_ROUND=tc|hyb|int)
     bool old_mac = false;       // debugging: the first payload MAC kernel (env CWGPU_OLD_MAC)
     // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
-    // the rounding of one tile overlaps the NTTs of the next (env CWGPU_STREAMS).  Paid off with the
-    // FMA-bound integer rounding kernel (292 vs 317 ms); with the tensor-core rounding one stream is
-    // faster (272 vs 297 ms at C4), so 1 is the default.
-    int nstreams = 1;
+    // the latency-bound kernels of one tile (NTTs, tensor-core rounding, MAC) co-reside with those
+    // of the next (env CWGPU_STREAMS; C4: 251 ms vs 272 ms on one stream)
+    int nstreams = 2;
     cudaStream_t tst[2] = {nullptr, nullptr};
     cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
     DevBuf Dbuf2;

@@ -214,8 +214,10 @@ struct RoundTcPar {
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 
-// dynamic shared memory requested per CTA only to cap residency at 4 CTAs / SM (4 x 128 TMEM columns)
-constexpr size_t kRoundTcSmem = 50 * 1024;
+// TMEM budget: <= 4 resident CTAs x 128 columns.  The register file already caps residency at 4
+// (>= 122 registers x 128 threads), so no shared-memory padding is requested (padding would keep
+// the NTT kernels of the other tile stream off the SM).
+constexpr size_t kRoundTcSmem = 0;
 
 template <int JM, int NC>
 __global__ void __launch_bounds__(128, 4) k_round_tc(u32* __restrict__ D, u32 P, DevTab T,
