@@ -82,9 +82,10 @@ struct Ctx {
     // the latency-bound kernels of one tile (NTTs, tensor-core rounding, MAC) co-reside with those
     // of the next (env CWGPU_STREAMS; C4: 251 ms vs 272 ms on one stream)
     int nstreams = 2;
-    cudaStream_t tst[2] = {nullptr, nullptr};
-    cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
-    DevBuf Dbuf2;
+    static constexpr int kMaxStreams = 4;
+    cudaStream_t tst[kMaxStreams] = {};
+    cudaEvent_t tev[kMaxStreams + 1] = {};
+    DevBuf Dmore[kMaxStreams - 1];  // D buffers of tile streams 1.. (stream 0 uses Dbuf)
     DevBuf* dcur = nullptr;
     unsigned long long* d_fb = nullptr;
     // database
@@ -971,21 +972,23 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     if (c.old_mac) CK(cudaMemsetAsync(c.acc_hi.get<u64>(accw), 0, accw * 8, c.st));
     const u32 R = tile_rows(c);
     u32 nc_all = 2;
-    const bool piped = c.nstreams == 2 && op == CWG_OP_FOLKLORE && c.k <= 2 && c.n_local > R;
+    const int ns = (int)std::min<u64>((u64)c.nstreams, (c.n_local + R - 1) / R);
+    const bool piped = ns >= 2 && op == CWG_OP_FOLKLORE && c.k <= 2;
     cudaStream_t main_st = c.st;
     if (piped) {
-        // both D buffers exist before the streams diverge (allocation synchronises)
-        c.Dbuf2.ensure((size_t)R * 3 * J * N * 4);
+        // all D buffers exist before the streams diverge (allocation synchronises)
         c.Dbuf.ensure((size_t)R * 3 * J * N * 4);
+        for (int i = 1; i < ns; ++i) c.Dmore[i - 1].ensure((size_t)R * 3 * J * N * 4);
         CK(cudaEventRecord(c.tev[0], main_st));
-        for (int i = 0; i < 2; ++i) CK(cudaStreamWaitEvent(c.tst[i], c.tev[0], 0));
+        for (int i = 0; i < ns; ++i) CK(cudaStreamWaitEvent(c.tst[i], c.tev[0], 0));
     }
     u64 tile = 0;
     for (u64 r0 = 0; r0 < c.n_local; r0 += R, ++tile) {
         const u32 Rt = (u32)std::min<u64>(R, c.n_local - r0);
         if (piped) {
-            c.st = c.tst[tile & 1];
-            c.dcur = (tile & 1) ? &c.Dbuf2 : &c.Dbuf;
+            const int i = (int)(tile % (u64)ns);
+            c.st = c.tst[i];
+            c.dcur = i ? &c.Dmore[i - 1] : &c.Dbuf;
         }
         u32 nc = 0, zs = 0;
         u32* Z = select_tile(c, entries, prep, op, r0, Rt, nc, zs, nullptr);
@@ -1013,7 +1016,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     if (piped) {
         c.st = main_st;
         c.dcur = &c.Dbuf;
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < ns; ++i) {
             CK(cudaEventRecord(c.tev[1 + i], c.tst[i]));
             CK(cudaStreamWaitEvent(main_st, c.tev[1 + i], 0));
         }
@@ -1169,13 +1172,14 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         CK(cudaMalloc(&c.d_fb, 8));
         CK(cudaMemset(c.d_fb, 0, 8));
         set_smem_limits(N);
-        if (const char* e = std::getenv("CWGPU_STREAMS")) c.nstreams = std::atoi(e) >= 2 ? 2 : 1;
+        if (const char* e = std::getenv("CWGPU_STREAMS"))
+            c.nstreams = std::max(1, std::min(Ctx::kMaxStreams, std::atoi(e)));
         if (const char* e = std::getenv("CWGPU_ROUND"))
             c.round_kind = std::string(e) == "int" ? 0 : std::string(e) == "hyb" ? 1 : 2;
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
         c.dcur = &c.Dbuf;
-        for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));
-        for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&c.tev[i], cudaEventDisableTiming));
+        for (int i = 0; i < Ctx::kMaxStreams; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));
+        for (int i = 0; i <= Ctx::kMaxStreams; ++i) CK(cudaEventCreateWithFlags(&c.tev[i], cudaEventDisableTiming));
         ensure_aux(c, 1);
         h = ctx.release();
     });
@@ -1187,13 +1191,13 @@ void cwg_destroy(cwg_ctx* h) {
     Ctx& c = h->c;
     cudaSetDevice(c.device);
     cudaStreamSynchronize(c.st);
-    for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.Dbuf2, &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
+    for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.Dmore[0], &c.Dmore[1], &c.Dmore[2], &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
                       &c.digits, &c.dntt, &c.ks, &c.prep, &c.Dbuf, &c.chain3, &c.node2, &c.acc_lo, &c.acc_hi,
                       &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp})
         b->release();
     if (c.d_fb) cudaFree(c.d_fb);
-    for (int i = 0; i < 2; ++i) if (c.tst[i]) cudaStreamDestroy(c.tst[i]);
-    for (int i = 0; i < 3; ++i) if (c.tev[i]) cudaEventDestroy(c.tev[i]);
+    for (int i = 0; i < Ctx::kMaxStreams; ++i) if (c.tst[i]) cudaStreamDestroy(c.tst[i]);
+    for (int i = 0; i <= Ctx::kMaxStreams; ++i) if (c.tev[i]) cudaEventDestroy(c.tev[i]);
     if (c.st) cudaStreamDestroy(c.st);
     delete h;
 }
