@@ -77,6 +77,7 @@ struct Ctx {
     DevBuf rtc_B;                     // k_round_tc B matrix (canonical UMMA K-major layout)
     u32 rtc_nc = 0;                   // k_round_tc GEMM width (0: no instance for this JM / Mm)
     int round_kind = 2;               // 2 tensor-core, 1 IMAD + DFMA, 0 IMAD only (env CWGPU_ROUND=tc|hyb|int)
+    int ntt_np = 1;                   // polynomials per CTA in the tensor / selection NTT kernels (env CWGPU_NTT_NP)
     bool old_mac = false;       // debugging: the first payload MAC kernel (env CWGPU_OLD_MAC)
     // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
     // the latency-bound kernels of one tile (NTTs, tensor-core rounding, MAC) co-reside with those
@@ -547,8 +548,10 @@ struct Reg32 {
         const int sm = (int)R::SMEM;
         CK(cudaFuncSetAttribute(k_ntt32r<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_ntt32r<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm));
+        CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm));
     }
     static void ntt(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale) {
         if (inverse)
@@ -559,11 +562,23 @@ struct Reg32 {
                          scale);
     }
     static void sel3(Ctx& c, u32* D, u32 P) {
-        launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN>, (size_t)P * 3 * c.ab.Mm, R::T, R::SMEM, D, c.T, c.ab.J);
+        const u32 npc = 3 * P;
+        c.next_units = (double)npc * c.ab.Mm;
+        if (c.ntt_np == 2)
+            launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN, 2>, (size_t)((npc + 1) / 2) * c.ab.Mm, R::T,
+                         2 * R::SMEM, D, c.T, c.ab.J, npc);
+        else
+            launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN, 1>, (size_t)npc * c.ab.Mm, R::T, R::SMEM, D, c.T,
+                         c.ab.J, npc);
     }
     static void tensor(Ctx& c, const u32* pa, const u32* ia, const u32* pb, const u32* ib, u32 P, u32* D, int fold) {
-        launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN>, (size_t)P * c.ab.J * 3, R::T, R::SMEM, pa, ia, pb, ib,
-                     P, c.T, D, fold);
+        c.next_units = (double)P * c.ab.J * 3;
+        if (c.ntt_np == 2)
+            launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN, 2>, (size_t)((P + 1) / 2) * c.ab.J * 3, R::T,
+                         2 * R::SMEM, pa, ia, pb, ib, P, c.T, D, fold);
+        else
+            launch_named(c, "k_tensor_intt", k_tensor_intt_r<LOGN, 1>, (size_t)P * c.ab.J * 3, R::T, R::SMEM, pa, ia,
+                         pb, ib, P, c.T, D, fold);
     }
 };
 
@@ -1174,6 +1189,7 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         set_smem_limits(N);
         if (const char* e = std::getenv("CWGPU_STREAMS"))
             c.nstreams = std::max(1, std::min(Ctx::kMaxStreams, std::atoi(e)));
+        if (const char* e = std::getenv("CWGPU_NTT_NP")) c.ntt_np = std::atoi(e) == 1 ? 1 : 2;
         if (const char* e = std::getenv("CWGPU_ROUND"))
             c.round_kind = std::string(e) == "int" ? 0 : std::string(e) == "hyb" ? 1 : 2;
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;

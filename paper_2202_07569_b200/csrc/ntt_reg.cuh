@@ -181,6 +181,8 @@ struct RegNtt {
     static constexpr int E = G::E;
     // <= 85 registers at N = 8192 (3 CTAs / SM); 2 CTAs of 512 threads at N = 16384
     static constexpr int MINB = LOGN >= 14 ? 2 : (768 / T > 16 ? 16 : 768 / T);
+    // two polynomials per CTA (shared twiddles, twice the ILP): <= 128 registers
+    static constexpr int MINB2 = 512 / T > 16 ? 16 : (512 / T < 1 ? 1 : 512 / T);
     static constexpr size_t SMEM = (size_t)G::N * 4;
 };
 
@@ -221,39 +223,48 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_ntt32r(
     }
 }
 
-/// Forward NTT of the 3 selection components of P products for every MAC prime, one
-/// polynomial per CTA: block (pr * 3 + comp) * Mm + k transforms the plane at
-/// base + ((pr * 3 + comp) * stride_j + k) * N in place.
-template <int LOGN>
-__global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_ntt32r_sel3(u32* __restrict__ base, DevTab T,
-                                                                                    u32 stride_j) {
+/// Forward NTT of the 3 selection components of P products for every MAC prime, NP planes
+/// of one prime per CTA: block (pc0 / NP) * Mm + k transforms the planes pc0 .. pc0 + NP - 1
+/// (pc = pr * 3 + comp < npc) at base + (pc * stride_j + k) * N in place.
+template <int LOGN, int NP>
+__global__ void __launch_bounds__(RegNtt<LOGN>::T, NP == 1 ? RegNtt<LOGN>::MINB : RegNtt<LOGN>::MINB2) k_ntt32r_sel3(
+    u32* __restrict__ base, DevTab T, u32 stride_j, u32 npc) {
     using R = RegNtt<LOGN>;
     constexpr int WB = R::WB, E = R::E, N = 1 << LOGN;
     extern __shared__ u32 smd[];
     const u32 tid = threadIdx.x;
     const u32 Mm = T.Mm;
-    const u32 pc = blockIdx.x / Mm, k = blockIdx.x % Mm;
+    const u32 pc0 = (blockIdx.x / Mm) * NP, k = blockIdx.x % Mm;
     const u32 p = T.a[k];
-    u32* d = base + ((size_t)pc * stride_j + k) * N;
-    u32 v[1][E];
+    u32* d[NP];
+    u32 v[NP][E];
 #pragma unroll
-    for (int r = 0; r < E; ++r) v[0][r] = d[((u32)r << (LOGN - WB)) | tid];
-    nttw_fwd<LOGN, WB, 1>(v, smd, T.arp + (size_t)k * N, T.arps + (size_t)k * N, p);
-    uint4* o = reinterpret_cast<uint4*>(d + (tid << WB));
+    for (int q = 0; q < NP; ++q) {
+        const u32 pc = min(pc0 + q, npc - 1);  // odd tail: the duplicate is transformed, not stored
+        d[q] = base + ((size_t)pc * stride_j + k) * N;
 #pragma unroll
-    for (int r = 0; r < E; ++r) v[0][r] = red32(red32(v[0][r], 2 * p), p);
+        for (int r = 0; r < E; ++r) v[q][r] = d[q][((u32)r << (LOGN - WB)) | tid];
+    }
+    nttw_fwd<LOGN, WB, NP>(v, smd, T.arp + (size_t)k * N, T.arps + (size_t)k * N, p);
 #pragma unroll
-    for (int r = 0; r < E; r += 4) o[r / 4] = make_uint4(v[0][r], v[0][r + 1], v[0][r + 2], v[0][r + 3]);
+    for (int q = 0; q < NP; ++q) {
+        if (pc0 + q >= npc) break;
+        uint4* o = reinterpret_cast<uint4*>(d[q] + (tid << WB));
+#pragma unroll
+        for (int r = 0; r < E; ++r) v[q][r] = red32(red32(v[q][r], 2 * p), p);
+#pragma unroll
+        for (int r = 0; r < E; r += 4) o[r / 4] = make_uint4(v[q][r], v[q][r + 1], v[q][r + 2], v[q][r + 3]);
+    }
 }
 
-/// Tensor (mul_lazy_prepared, bfv.cpp:776-791) + INTT, one (product, aux prime, component)
-/// per CTA: block (pr * J + j) * 3 + comp (the three components of one product are adjacent,
-/// so their shared operand planes are L2 hits).  Operands: Montgomery-form NTT residues
-/// [idx][2][J][N]; output D[pr][comp][j][N] in normal form (the (N 2^32)^-1 scale undoes the
-/// Montgomery factor).  fold: also multiply by (A/a_j)^-1, i.e. emit the HPS residues w_j
-/// that the tensor-core rounding kernel consumes directly.
-template <int LOGN>
-__global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_tensor_intt_r(
+/// Tensor (mul_lazy_prepared, bfv.cpp:776-791) + INTT of NP products per CTA for one (aux
+/// prime, component): block ((pr0 / NP) * J + j) * 3 + comp (the three components of the same
+/// products are adjacent, so their shared operand planes are L2 hits).  Operands:
+/// Montgomery-form NTT residues [idx][2][J][N]; output D[pr][comp][j][N] in normal form (the
+/// (N 2^32)^-1 scale undoes the Montgomery factor).  fold: also multiply by (A/a_j)^-1, i.e.
+/// emit the HPS residues w_j that the tensor-core rounding kernel consumes directly.
+template <int LOGN, int NP>
+__global__ void __launch_bounds__(RegNtt<LOGN>::T, NP == 1 ? RegNtt<LOGN>::MINB : RegNtt<LOGN>::MINB2) k_tensor_intt_r(
     const u32* __restrict__ prepA, const u32* __restrict__ idxA, const u32* __restrict__ prepB,
     const u32* __restrict__ idxB, u32 P, DevTab T, u32* __restrict__ D, int fold) {
     using R = RegNtt<LOGN>;
@@ -262,41 +273,49 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_tensor_
     const u32 J = T.J;
     const u32 tid = threadIdx.x;
     const u32 comp = blockIdx.x % 3, pj = blockIdx.x / 3;
-    const u32 pr = pj / J, j = pj % J;
+    const u32 pr0 = (pj / J) * NP, j = pj % J;
     const u32 p = T.a[j], pinv = T.apinv[j];
     const size_t per = (size_t)2 * J * N;
-    const u32* A = prepA + (size_t)(idxA ? idxA[pr] : pr) * per + (size_t)j * N + (tid << WB);
-    const u32* B = prepB + (size_t)(idxB ? idxB[pr] : pr) * per + (size_t)j * N + (tid << WB);
     const size_t o1 = (size_t)J * N;
-    u32 v[1][E];
-    // comp 0: A0 B0, comp 2: A1 B1, comp 1: A0 B1 + A1 B0
-    const u32* X = A + (comp == 2 ? o1 : 0);
-    const u32* Y = B + (comp == 0 ? 0 : o1);
+    u32 v[NP][E];
 #pragma unroll
-    for (int r = 0; r < E; r += 4) {
-        const uint4 x = __ldg(reinterpret_cast<const uint4*>(X + r));
-        const uint4 y = __ldg(reinterpret_cast<const uint4*>(Y + r));
-        v[0][r] = red32(mont32(x.x, y.x, p, pinv), p);
-        v[0][r + 1] = red32(mont32(x.y, y.y, p, pinv), p);
-        v[0][r + 2] = red32(mont32(x.z, y.z, p, pinv), p);
-        v[0][r + 3] = red32(mont32(x.w, y.w, p, pinv), p);
-    }
-    if (comp == 1) {
+    for (int q = 0; q < NP; ++q) {
+        const u32 pr = min(pr0 + q, P - 1);  // odd tail: the duplicate is transformed, not stored
+        const u32* A = prepA + (size_t)(idxA ? idxA[pr] : pr) * per + (size_t)j * N + (tid << WB);
+        const u32* B = prepB + (size_t)(idxB ? idxB[pr] : pr) * per + (size_t)j * N + (tid << WB);
+        // comp 0: A0 B0, comp 2: A1 B1, comp 1: A0 B1 + A1 B0
+        const u32* X = A + (comp == 2 ? o1 : 0);
+        const u32* Y = B + (comp == 0 ? 0 : o1);
 #pragma unroll
         for (int r = 0; r < E; r += 4) {
-            const uint4 x = __ldg(reinterpret_cast<const uint4*>(A + o1 + r));
-            const uint4 y = __ldg(reinterpret_cast<const uint4*>(B + r));
-            v[0][r] += red32(mont32(x.x, y.x, p, pinv), p);
-            v[0][r + 1] += red32(mont32(x.y, y.y, p, pinv), p);
-            v[0][r + 2] += red32(mont32(x.z, y.z, p, pinv), p);
-            v[0][r + 3] += red32(mont32(x.w, y.w, p, pinv), p);
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(X + r));
+            const uint4 y = __ldg(reinterpret_cast<const uint4*>(Y + r));
+            v[q][r] = red32(mont32(x.x, y.x, p, pinv), p);
+            v[q][r + 1] = red32(mont32(x.y, y.y, p, pinv), p);
+            v[q][r + 2] = red32(mont32(x.z, y.z, p, pinv), p);
+            v[q][r + 3] = red32(mont32(x.w, y.w, p, pinv), p);
+        }
+        if (comp == 1) {
+#pragma unroll
+            for (int r = 0; r < E; r += 4) {
+                const uint4 x = __ldg(reinterpret_cast<const uint4*>(A + o1 + r));
+                const uint4 y = __ldg(reinterpret_cast<const uint4*>(B + r));
+                v[q][r] += red32(mont32(x.x, y.x, p, pinv), p);
+                v[q][r + 1] += red32(mont32(x.y, y.y, p, pinv), p);
+                v[q][r + 2] += red32(mont32(x.z, y.z, p, pinv), p);
+                v[q][r + 3] += red32(mont32(x.w, y.w, p, pinv), p);
+            }
         }
     }
-    nttw_inv<LOGN, WB, 1>(v, smd, T.airp + (size_t)j * N, T.airps + (size_t)j * N, p);
+    nttw_inv<LOGN, WB, NP>(v, smd, T.airp + (size_t)j * N, T.airps + (size_t)j * N, p);
     const u32 ni = fold ? T.ninvRAc[j] : T.ninvRA[j], nis = fold ? T.ninvRAc_s[j] : T.ninvRA_s[j];
-    u32* out = D + (((size_t)pr * 3 + comp) * J + j) * N;
 #pragma unroll
-    for (int r = 0; r < E; ++r) out[((u32)r << (LOGN - WB)) | tid] = red32(shoup32(v[0][r], ni, nis, p), p);
+    for (int q = 0; q < NP; ++q) {
+        if (pr0 + q >= P) break;
+        u32* out = D + (((size_t)(pr0 + q) * 3 + comp) * J + j) * N;
+#pragma unroll
+        for (int r = 0; r < E; ++r) out[((u32)r << (LOGN - WB)) | tid] = red32(shoup32(v[q][r], ni, nis, p), p);
+    }
 }
 
 }  // namespace cwgpu
