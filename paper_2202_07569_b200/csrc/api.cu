@@ -77,6 +77,9 @@ struct Ctx {
     DevBuf rtc_B;                     // k_round_tc B matrix (canonical UMMA K-major layout)
     u32 rtc_nc = 0;                   // k_round_tc GEMM width (0: no instance for this JM / Mm)
     int round_kind = 2;               // 2 tensor-core, 1 IMAD + DFMA, 0 IMAD only (env CWGPU_ROUND=tc|hyb|int)
+    DevBuf prep_s;                    // A-side prepared operands with the INTT output scale folded in
+    bool prep_s_ok = false;           // prep_s valid for the current answer
+    bool prescale = true;             // env CWGPU_PRESCALE
     int ntt_np = 1;                   // polynomials per CTA in the tensor / selection NTT kernels (env CWGPU_NTT_NP)
     bool old_mac = false;       // debugging: the first payload MAC kernel (env CWGPU_OLD_MAC)
     // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
@@ -714,16 +717,29 @@ static void prepare(Ctx& c, const u64* src, size_t stride, const u32* sel, u32 c
     ntt32(c, out, count * 2 * J, J, J, 0, false, 0);
 }
 
+/// A-side copy of prepared operands with the INTT's output scale (N 2^32)^-1 (A/a_j)^-1 folded
+/// in: one pass per query instead of one Shoup product per tensor output coefficient.
+static u32* prepare_scaled(Ctx& c, const u32* prep, u32 count) {
+    const u32 N = c.cp.N, J = c.ab.J;
+    const size_t total = (size_t)count * 2 * J * N;
+    u32* out = c.prep_s.get<u32>(total);
+    launch(c, k_scale_planes, blocks(total, 256), 256, 0, prep, out, total, c.T.ninvRAc, c.T.ninvRAc_s, c.T);
+    return out;
+}
+
 /// Tensor + INTT + exact rounding for P products of prepared operands.
 /// to_mac: D planes k < Mm become the NTT-form MAC-basis selection values (in c.Dbuf);
 /// else the 3-comp chain products are written to chain_out [P][3][L][N].
+static bool round_tc_on(const Ctx& c) { return reg32_ok(c.cp.logN) && c.round_kind == 2 && c.rtc_nc != 0; }
+
+/// prepA_scaled: the A operands carry (N 2^32)^-1 (A/a_j)^-1 (see prepare_scaled; tc rounding only).
 static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* prepB, const u32* idxB, u32 P,
-                         bool to_mac, u64* chain_out) {
+                         bool to_mac, u64* chain_out, bool prepA_scaled = false) {
     const u32 N = c.cp.N, J = c.ab.J;
     u32* D = c.dcur->get<u32>((size_t)P * 3 * J * N);
-    const bool tc = to_mac && reg32_ok(c.cp.logN) && c.round_kind == 2 && c.rtc_nc != 0;
+    const bool tc = to_mac && round_tc_on(c);
     if (reg32_ok(c.cp.logN)) {
-        REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? 1 : 0));
+        REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? (prepA_scaled ? 2 : 1) : 0));
     } else {
         launch(c, k_tensor_intt, (size_t)P * J, ntt_block(N), N * 4, prepA, idxA, prepB, idxB, P, c.T, D);
     }
@@ -801,7 +817,8 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
             nc = 3;
             return nullptr;
         }
-        u32* D = mul_prepared(c, prep, col(0), prep, col(1), R, true, nullptr);
+        u32* D = c.prep_s_ok ? mul_prepared(c, c.prep_s.ptr<u32>(), col(0), prep, col(1), R, true, nullptr, true)
+                             : mul_prepared(c, prep, col(0), prep, col(1), R, true, nullptr);
         nc = 3;
         zstride = J;
         return D;
@@ -977,9 +994,14 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     u64* entries = expand(c, dq, h, comp, m);
     tm.mark(TM_EXPAND);
     u32* prep = nullptr;
+    c.prep_s_ok = false;
     if (op == CWG_OP_FOLKLORE && c.k >= 2) {
         prep = c.prep.get<u32>((size_t)m * 2 * J * N);
         prepare(c, entries, 2 * LN, nullptr, m, prep);
+        if (c.k == 2 && round_tc_on(c) && c.prescale) {
+            prepare_scaled(c, prep, m);
+            c.prep_s_ok = true;
+        }
     }
     const size_t accw = (size_t)c.s * 3 * Mm * N;
     auto* acc = reinterpret_cast<unsigned long long*>(c.acc_lo.get<u64>(accw));
@@ -1189,6 +1211,7 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         set_smem_limits(N);
         if (const char* e = std::getenv("CWGPU_STREAMS"))
             c.nstreams = std::max(1, std::min(Ctx::kMaxStreams, std::atoi(e)));
+        if (const char* e = std::getenv("CWGPU_PRESCALE")) c.prescale = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_NTT_NP")) c.ntt_np = std::atoi(e) == 1 ? 1 : 2;
         if (const char* e = std::getenv("CWGPU_ROUND"))
             c.round_kind = std::string(e) == "int" ? 0 : std::string(e) == "hyb" ? 1 : 2;
@@ -1207,7 +1230,7 @@ void cwg_destroy(cwg_ctx* h) {
     Ctx& c = h->c;
     cudaSetDevice(c.device);
     cudaStreamSynchronize(c.st);
-    for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.Dmore[0], &c.Dmore[1], &c.Dmore[2], &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
+    for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.prep_s, &c.Dmore[0], &c.Dmore[1], &c.Dmore[2], &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
                       &c.digits, &c.dntt, &c.ks, &c.prep, &c.Dbuf, &c.chain3, &c.node2, &c.acc_lo, &c.acc_hi,
                       &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp})
         b->release();
@@ -1330,6 +1353,7 @@ int cwg_select(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint6
         auto t0 = std::chrono::steady_clock::now();
         Timer tm(c, t != nullptr);
         tm.mark(TM_START);
+        c.prep_s_ok = false;  // the selection path uses the unscaled operands only
         if (relin) upload_keys(c, relin, n_galois, galois_g, galois);
         if (!c.have_keys) throw he_err("evaluation keys not set");
         const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J;

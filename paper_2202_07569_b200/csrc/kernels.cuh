@@ -849,6 +849,16 @@ __global__ void k_scale_const(u64* __restrict__ ct, u32 B, u64 c, DevTab T) {
     ct[idx] = reduce128(ph, pl, q, T.q_mu96[i]);
 }
 
+/// out = in * f_j mod a_j over planes [count][J][N] (Shoup constants per aux prime), canonical.
+__global__ void k_scale_planes(const u32* __restrict__ in, u32* __restrict__ out, size_t total,
+                               const u32* __restrict__ f, const u32* __restrict__ fs, DevTab T) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    const u32 j = (u32)((idx >> T.logN) % T.J);
+    const u32 p = T.a[j];
+    out[idx] = red32(red32(shoup32(in[idx], f[j], fs[j], p), 2 * p), p);
+}
+
 /// Gather 2-comp ciphertexts: out[x] = src[sel[x]] (each 2LN words).
 __global__ void k_gather_ct(const u64* __restrict__ src, const u32* __restrict__ sel, u32 count, size_t per,
                             u64* __restrict__ out) {

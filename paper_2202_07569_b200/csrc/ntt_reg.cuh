@@ -261,8 +261,10 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, NP == 1 ? RegNtt<LOGN>::MINB 
 /// prime, component): block ((pr0 / NP) * J + j) * 3 + comp (the three components of the same
 /// products are adjacent, so their shared operand planes are L2 hits).  Operands:
 /// Montgomery-form NTT residues [idx][2][J][N]; output D[pr][comp][j][N] in normal form (the
-/// (N 2^32)^-1 scale undoes the Montgomery factor).  fold: also multiply by (A/a_j)^-1, i.e.
-/// emit the HPS residues w_j that the tensor-core rounding kernel consumes directly.
+/// (N 2^32)^-1 scale undoes the Montgomery factor).  fold = 1: also multiply by (A/a_j)^-1, i.e.
+/// emit the HPS residues w_j that the tensor-core rounding kernel consumes directly; fold = 2:
+/// the A operands already carry (N 2^32)^-1 (A/a_j)^-1 (k_scale_planes, once per query), so the
+/// INTT output needs no scaling pass.
 template <int LOGN, int NP>
 __global__ void __launch_bounds__(RegNtt<LOGN>::T, NP == 1 ? RegNtt<LOGN>::MINB : RegNtt<LOGN>::MINB2) k_tensor_intt_r(
     const u32* __restrict__ prepA, const u32* __restrict__ idxA, const u32* __restrict__ prepB,
@@ -308,13 +310,18 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, NP == 1 ? RegNtt<LOGN>::MINB 
         }
     }
     nttw_inv<LOGN, WB, NP>(v, smd, T.airp + (size_t)j * N, T.airps + (size_t)j * N, p);
-    const u32 ni = fold ? T.ninvRAc[j] : T.ninvRA[j], nis = fold ? T.ninvRAc_s[j] : T.ninvRA_s[j];
+    const u32 ni = fold == 1 ? T.ninvRAc[j] : T.ninvRA[j], nis = fold == 1 ? T.ninvRAc_s[j] : T.ninvRA_s[j];
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         if (pr0 + q >= P) break;
         u32* out = D + (((size_t)(pr0 + q) * 3 + comp) * J + j) * N;
+        if (fold == 2) {  // scale already folded into the A operands
 #pragma unroll
-        for (int r = 0; r < E; ++r) out[((u32)r << (LOGN - WB)) | tid] = red32(shoup32(v[q][r], ni, nis, p), p);
+            for (int r = 0; r < E; ++r) out[((u32)r << (LOGN - WB)) | tid] = red32(v[q][r], p);
+        } else {
+#pragma unroll
+            for (int r = 0; r < E; ++r) out[((u32)r << (LOGN - WB)) | tid] = red32(shoup32(v[q][r], ni, nis, p), p);
+        }
     }
 }
 
