@@ -549,20 +549,28 @@ struct Reg32 {
     using R = RegNtt<LOGN>;
     static void limits() {
         const int sm = (int)R::SMEM;
-        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CK(cudaFuncSetAttribute(k_ntt32r<LOGN, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm));
         CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm));
     }
-    static void ntt(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale) {
-        if (inverse)
-            launch_named(c, "k_ntt32r_inv", k_ntt32r<LOGN, true>, npolys, R::T, R::SMEM, base, c.T, gs, stride, off,
-                         scale);
+    static void ntt(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale, bool perm) {
+        if (inverse && perm)
+            launch_named(c, "k_ntt32r_inv", k_ntt32r<LOGN, true, true>, npolys, R::T, R::SMEM, base, c.T, gs, stride,
+                         off, scale);
+        else if (perm)
+            launch_named(c, "k_ntt32r_fwd", k_ntt32r<LOGN, false, true>, npolys, R::T, R::SMEM, base, c.T, gs, stride,
+                         off, scale);
+        else if (inverse)
+            launch_named(c, "k_ntt32r_inv", k_ntt32r<LOGN, true, false>, npolys, R::T, R::SMEM, base, c.T, gs, stride,
+                         off, scale);
         else
-            launch_named(c, "k_ntt32r_fwd", k_ntt32r<LOGN, false>, npolys, R::T, R::SMEM, base, c.T, gs, stride, off,
-                         scale);
+            launch_named(c, "k_ntt32r_fwd", k_ntt32r<LOGN, false, false>, npolys, R::T, R::SMEM, base, c.T, gs, stride,
+                         off, scale);
     }
     static void sel3(Ctx& c, u32* D, u32 P) {
         const u32 npc = 3 * P;
@@ -614,10 +622,14 @@ static void set_smem_limits(u32 N) {
 
 static bool reg32_ok(u32 logN) { return logN >= 8 && logN <= 14; }
 
-static void ntt32(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale) {
+/// Aux / MAC-prime NTTs.  perm (default): the answer path's internal NTT-domain order (see
+/// k_ntt32r); false: the reference's order (cwg_ntt).  Rings below 2^8 use the shared-memory
+/// kernels in the reference's order throughout (their tensor kernel matches).
+static void ntt32(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale,
+                  bool perm = true) {
     const u32 N = c.cp.N;
     if (reg32_ok(c.cp.logN)) {
-        REG32_DISPATCH(c.cp.logN, ntt(c, base, npolys, gs, stride, off, inverse, scale));
+        REG32_DISPATCH(c.cp.logN, ntt(c, base, npolys, gs, stride, off, inverse, scale, perm));
         return;
     }
     if (inverse)
@@ -1410,7 +1422,7 @@ int cwg_ntt(cwg_ctx* h, int chain, uint32_t idx, uint64_t* data, uint32_t count,
             u32* d = c.lift_tmp.get<u32>(tmp.size());
             CK(cudaMemcpyAsync(d, tmp.data(), tmp.size() * 4, cudaMemcpyHostToDevice, c.st));
             // group size 1, stride 1, offset idx: poly p at (p + idx) * N uses prime idx
-            ntt32(c, d - (size_t)idx * N, count, 1, 1, idx, inverse != 0, 0);
+            ntt32(c, d - (size_t)idx * N, count, 1, 1, idx, inverse != 0, 0, false);
             CK(cudaMemcpyAsync(tmp.data(), d, tmp.size() * 4, cudaMemcpyDeviceToHost, c.st));
             CK(cudaStreamSynchronize(c.st));
             for (size_t x = 0; x < tmp.size(); ++x) data[x] = tmp[x];
@@ -1531,12 +1543,12 @@ int cwg_kernel_units(const cwg_ctx* h, uint32_t idx, double* units) {
 #include "ntt_bench.cuh"
 
 namespace {
-template <int WB, int NP, int MINB, bool INV, bool JSLOW = false>
+template <int WB, int NP, int MINB, bool INV, bool JSLOW = false, int FAKE = 0>
 float bench_nttw_variant(cwgpu::Ctx& c, u32* buf, u32 npolys, int iters) {
     using namespace cwgpu;
     constexpr int LOGN = 13;
     const size_t sm = (size_t)NP * (1 << LOGN) * 4;
-    auto kern = k_nttw_bench<LOGN, WB, NP, MINB, INV, JSLOW>;
+    auto kern = k_nttw_bench<LOGN, WB, NP, MINB, INV, JSLOW, FAKE>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     const u32 grid = npolys / NP;
     cudaEvent_t e0, e1;
@@ -1545,6 +1557,29 @@ float bench_nttw_variant(cwgpu::Ctx& c, u32* buf, u32 npolys, int iters) {
     kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T);
     CK(cudaEventRecord(e0, c.st));
     for (int i = 0; i < iters; ++i) kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T);
+    CK(cudaEventRecord(e1, c.st));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaGetLastError());
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms / iters;
+}
+template <int MINB>
+float bench_nttw_pf(cwgpu::Ctx& c, u32* buf, u32 npolys, int iters, u32 ctas_per_sm) {
+    using namespace cwgpu;
+    constexpr int LOGN = 13, WB = 5;
+    const size_t sm = (size_t)2 * (1 << LOGN) * 4;
+    auto kern = k_nttw_bench_pf<LOGN, WB, MINB>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    const u32 grid = 148 * ctas_per_sm;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T, npolys);
+    CK(cudaEventRecord(e0, c.st));
+    for (int i = 0; i < iters; ++i) kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T, npolys);
     CK(cudaEventRecord(e1, c.st));
     CK(cudaEventSynchronize(e1));
     CK(cudaGetLastError());
@@ -1577,6 +1612,15 @@ extern "C" int cwg_bench_kernel(cwg_ctx* h, int which, uint32_t npolys, int iter
             case 7: ms = bench_nttw_variant<5, 1, 3, true, true>(c, buf, npolys, iters); break;
             case 8: ms = bench_nttw_variant<5, 2, 2, false, true>(c, buf, npolys, iters); break;
             case 9: ms = bench_nttw_variant<5, 1, 4, false, true>(c, buf, npolys, iters); break;
+            case 10: ms = bench_nttw_variant<5, 1, 3, false, false, 1>(c, buf, npolys, iters); break;
+            case 11: ms = bench_nttw_variant<5, 2, 2, false, false, 1>(c, buf, npolys, iters); break;
+            case 12: ms = bench_nttw_variant<5, 1, 3, false, false, 2>(c, buf, npolys, iters); break;
+            case 13: ms = bench_nttw_variant<5, 1, 3, false, false, 4>(c, buf, npolys, iters); break;
+            case 14: ms = bench_nttw_variant<5, 1, 3, false, false, 7>(c, buf, npolys, iters); break;
+            case 15: ms = bench_nttw_variant<5, 2, 2, false, false, 7>(c, buf, npolys, iters); break;
+            case 16: ms = bench_nttw_pf<3>(c, buf, npolys, iters, 3); break;
+            case 18: ms = bench_nttw_variant<5, 1, 3, false, false, 8>(c, buf, npolys, iters); break;
+            case 17: ms = bench_nttw_pf<2>(c, buf, npolys, iters, 2); break;
             default: throw std::invalid_argument("unknown benchmark variant");
         }
         *ms_per_launch = ms;

@@ -61,9 +61,14 @@ __device__ __forceinline__ u32 win_index_w(u32 tid, int w, int r) {
 
 /// Twiddles of register bit j of a WB-bit window at low bit w: 2^(WB-1-j) consecutive
 /// entries from (N >> (w+j+1)) + (high << (WB-1-j)).
-template <int LOGN, int WB>
+template <int LOGN, int WB, int FAKE = 0>
 __device__ __forceinline__ void load_stage_tw(const u32* __restrict__ tp, const u32* __restrict__ tsp, int w, int j,
                                               u32 high, u32* tw, u32* tws) {
+    if constexpr ((FAKE & 1) != 0) {  // diagnostics only (microbenchmark): register twiddles, no loads
+#pragma unroll
+        for (int u = 0; u < (1 << (WB - 1)); ++u) { tw[u] = tp[u] + high; tws[u] = tsp[u] ^ high; }
+        return;
+    }
     const u32 base = ((u32)(1 << LOGN) >> (w + j + 1)) + (high << (WB - 1 - j));
     const int c = WB - 1 - j;
     if (c == 0) load_tw<1>(tp, tsp, base, tw, tws);
@@ -95,7 +100,7 @@ __device__ __forceinline__ void nttw_transpose(u32 (&v)[NP][1 << WB], u32* sm, u
 
 /// Forward NTT; input mapping x = r << (LOGN-WB) | tid, output x = tid << WB | r.
 /// Values in [0, 4p) in and out (p < 2^30).  sm: NP * N words.
-template <int LOGN, int WB, int NP>
+template <int LOGN, int WB, int NP, int FAKE = 0>
 __device__ __forceinline__ void nttw_fwd(u32 (&v)[NP][1 << WB], u32* sm, const u32* __restrict__ rp,
                                          const u32* __restrict__ rps, u32 p) {
     using G = NttW<LOGN, WB>;
@@ -108,13 +113,13 @@ __device__ __forceinline__ void nttw_fwd(u32 (&v)[NP][1 << WB], u32* sm, const u
         const u32 high = tid >> w;
         if (k > 0) {
             const int wp = (LOGN - WB - WB * (k - 1)) > 0 ? (LOGN - WB - WB * (k - 1)) : 0;
-            nttw_transpose<WB, NP, G::N>(v, sm, tid, wp, w);
+            if constexpr ((FAKE & 2) == 0) nttw_transpose<WB, NP, G::N>(v, sm, tid, wp, w);
         }
 #pragma unroll
         for (int b = btop; b >= w; --b) {
             const int j = b - w;
             u32 tw[E / 2], tws[E / 2];
-            load_stage_tw<LOGN, WB>(rp, rps, w, j, high, tw, tws);
+            load_stage_tw<LOGN, WB, FAKE>(rp, rps, w, j, high, tw, tws);
 #pragma unroll
             for (int r = 0; r < E; ++r) {
                 if (r & (1 << j)) continue;
@@ -188,8 +193,12 @@ struct RegNtt {
 
 /// Batched forward / inverse NTT: poly p -> group g = p / gs, prime j = off + p % gs,
 /// address (g * stride + j) * N.  scale (inverse only): 0 = N^-1, 1 = (N 2^32)^-1.
-/// Output canonical [0, p).
-template <int LOGN, bool INV>
+/// Output canonical [0, p).  PERM: the NTT-domain side is stored in the register-transposed
+/// order pos = r * (N / E) + tid (thread tid's r-th output), so both directions move it with
+/// coalesced scalar accesses; the answer path's aux / MAC-basis NTT-domain data (prepared
+/// operands, database, selection values, accumulators) all use this order and are only
+/// combined pointwise.  !PERM: the reference's bit-reversed order (cwg_ntt).
+template <int LOGN, bool INV, bool PERM = true>
 __global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_ntt32r(u32* __restrict__ base, DevTab T, u32 gs,
                                                                                u32 stride, u32 off, int scale) {
     using R = RegNtt<LOGN>;
@@ -204,17 +213,27 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, RegNtt<LOGN>::MINB) k_ntt32r(
 #pragma unroll
         for (int r = 0; r < E; ++r) v[0][r] = d[((u32)r << (LOGN - WB)) | tid];
         nttw_fwd<LOGN, WB, 1>(v, sm, T.arp + (size_t)j * N, T.arps + (size_t)j * N, pr);
-        uint4* o = reinterpret_cast<uint4*>(d + (tid << WB));
 #pragma unroll
         for (int r = 0; r < E; ++r) v[0][r] = red32(red32(v[0][r], 2 * pr), pr);
+        if (PERM) {
 #pragma unroll
-        for (int r = 0; r < E; r += 4) o[r / 4] = make_uint4(v[0][r], v[0][r + 1], v[0][r + 2], v[0][r + 3]);
+            for (int r = 0; r < E; ++r) d[((u32)r << (LOGN - WB)) | tid] = v[0][r];
+        } else {
+            uint4* o = reinterpret_cast<uint4*>(d + (tid << WB));
+#pragma unroll
+            for (int r = 0; r < E; r += 4) o[r / 4] = make_uint4(v[0][r], v[0][r + 1], v[0][r + 2], v[0][r + 3]);
+        }
     } else {
-        const uint4* in = reinterpret_cast<const uint4*>(d + (tid << WB));
+        if (PERM) {
 #pragma unroll
-        for (int r = 0; r < E; r += 4) {
-            const uint4 x = in[r / 4];
-            v[0][r] = x.x; v[0][r + 1] = x.y; v[0][r + 2] = x.z; v[0][r + 3] = x.w;
+            for (int r = 0; r < E; ++r) v[0][r] = d[((u32)r << (LOGN - WB)) | tid];
+        } else {
+            const uint4* in = reinterpret_cast<const uint4*>(d + (tid << WB));
+#pragma unroll
+            for (int r = 0; r < E; r += 4) {
+                const uint4 x = in[r / 4];
+                v[0][r] = x.x; v[0][r + 1] = x.y; v[0][r + 2] = x.z; v[0][r + 3] = x.w;
+            }
         }
         nttw_inv<LOGN, WB, 1>(v, sm, T.airp + (size_t)j * N, T.airps + (size_t)j * N, pr);
         const u32 ni = scale ? T.ninvRA[j] : T.ninvA[j], nis = scale ? T.ninvRA_s[j] : T.ninvA_s[j];
@@ -249,11 +268,8 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, NP == 1 ? RegNtt<LOGN>::MINB 
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         if (pc0 + q >= npc) break;
-        uint4* o = reinterpret_cast<uint4*>(d[q] + (tid << WB));
 #pragma unroll
-        for (int r = 0; r < E; ++r) v[q][r] = red32(red32(v[q][r], 2 * p), p);
-#pragma unroll
-        for (int r = 0; r < E; r += 4) o[r / 4] = make_uint4(v[q][r], v[q][r + 1], v[q][r + 2], v[q][r + 3]);
+        for (int r = 0; r < E; ++r) d[q][((u32)r << (LOGN - WB)) | tid] = red32(red32(v[q][r], 2 * p), p);  // PERM order
     }
 }
 
@@ -283,30 +299,28 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, NP == 1 ? RegNtt<LOGN>::MINB 
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         const u32 pr = min(pr0 + q, P - 1);  // odd tail: the duplicate is transformed, not stored
-        const u32* A = prepA + (size_t)(idxA ? idxA[pr] : pr) * per + (size_t)j * N + (tid << WB);
-        const u32* B = prepB + (size_t)(idxB ? idxB[pr] : pr) * per + (size_t)j * N + (tid << WB);
-        // comp 0: A0 B0, comp 2: A1 B1, comp 1: A0 B1 + A1 B0
+        const u32* A = prepA + (size_t)(idxA ? idxA[pr] : pr) * per + (size_t)j * N + tid;
+        const u32* B = prepB + (size_t)(idxB ? idxB[pr] : pr) * per + (size_t)j * N + tid;
+        // comp 0: A0 B0, comp 2: A1 B1, comp 1: A0 B1 + A1 B0; operands in the PERM order of
+        // k_ntt32r: thread tid's r-th value at r * (N / E) + tid (coalesced)
         const u32* X = A + (comp == 2 ? o1 : 0);
         const u32* Y = B + (comp == 0 ? 0 : o1);
+        u32 x[E], y[E];
 #pragma unroll
-        for (int r = 0; r < E; r += 4) {
-            const uint4 x = __ldg(reinterpret_cast<const uint4*>(X + r));
-            const uint4 y = __ldg(reinterpret_cast<const uint4*>(Y + r));
-            v[q][r] = red32(mont32(x.x, y.x, p, pinv), p);
-            v[q][r + 1] = red32(mont32(x.y, y.y, p, pinv), p);
-            v[q][r + 2] = red32(mont32(x.z, y.z, p, pinv), p);
-            v[q][r + 3] = red32(mont32(x.w, y.w, p, pinv), p);
+        for (int r = 0; r < E; ++r) {
+            x[r] = __ldg(X + ((u32)r << (LOGN - WB)));
+            y[r] = __ldg(Y + ((u32)r << (LOGN - WB)));
         }
+#pragma unroll
+        for (int r = 0; r < E; ++r) v[q][r] = red32(mont32(x[r], y[r], p, pinv), p);
         if (comp == 1) {
 #pragma unroll
-            for (int r = 0; r < E; r += 4) {
-                const uint4 x = __ldg(reinterpret_cast<const uint4*>(A + o1 + r));
-                const uint4 y = __ldg(reinterpret_cast<const uint4*>(B + r));
-                v[q][r] += red32(mont32(x.x, y.x, p, pinv), p);
-                v[q][r + 1] += red32(mont32(x.y, y.y, p, pinv), p);
-                v[q][r + 2] += red32(mont32(x.z, y.z, p, pinv), p);
-                v[q][r + 3] += red32(mont32(x.w, y.w, p, pinv), p);
+            for (int r = 0; r < E; ++r) {
+                x[r] = __ldg(A + o1 + ((u32)r << (LOGN - WB)));
+                y[r] = __ldg(B + ((u32)r << (LOGN - WB)));
             }
+#pragma unroll
+            for (int r = 0; r < E; ++r) v[q][r] += red32(mont32(x[r], y[r], p, pinv), p);
         }
     }
     nttw_inv<LOGN, WB, NP>(v, smd, T.airp + (size_t)j * N, T.airps + (size_t)j * N, p);

@@ -12,7 +12,11 @@ lib.cwg_bench_kernel.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32,
 names = ["W5 fwd NP1 MINB3 (production)", "W5 inv NP1 MINB3 (production)", "W5 fwd NP2 MINB2",
          "W5 inv NP2 MINB2", "W4 fwd NP1 MINB3", "W6 fwd NP2 MINB1",
          "W5 fwd NP1 MINB3 prime-major", "W5 inv NP1 MINB3 prime-major", "W5 fwd NP2 MINB2 prime-major",
-         "W5 fwd NP1 MINB4 prime-major"]
+         "W5 fwd NP1 MINB4 prime-major", "W5 fwd NP1 MINB3 register twiddles (diag)",
+         "W5 fwd NP2 MINB2 register twiddles (diag)", "W5 fwd NP1 MINB3 no transposes (diag)",
+         "W5 fwd NP1 MINB3 no global load/store (diag)", "W5 fwd NP1 MINB3 butterflies only (diag)",
+         "W5 fwd NP2 MINB2 butterflies only (diag)", "W5 fwd persistent cp.async prefetch 3/SM",
+         "W5 fwd persistent cp.async prefetch 2/SM", "W5 fwd NP1 MINB3 loads, no stores (diag)"]
 npolys = 36000
 only = [int(a) for a in sys.argv[1:]]
 for w, nm in enumerate(names):
