@@ -370,12 +370,15 @@ def main():
 
     # correctness of the benchmarked answer: the response decrypts to the selected row
     verified = None
+    verify_detail = None
     if rank == 0 and not args.no_verify:
         resp = dout.cpu().numpy().view(np.uint64).reshape(cfg.s, 2, L, N)
         trow = configs.db_payload(cfg, 1, target, target + 1)[0]
-        verified = all(np.array_equal(client.decrypt(resp[j]), trow[j]) for j in range(cfg.s))
+        dec_ok = all(np.array_equal(client.decrypt(resp[j]), trow[j]) for j in range(cfg.s))
         hresp = hout.numpy().view(np.uint64).reshape(cfg.s, 2, L, N)
-        verified = verified and np.array_equal(hresp, resp)
+        e2e_eq = bool(np.array_equal(hresp, resp))
+        verified = bool(dec_ok and e2e_eq)
+        verify_detail = {"decrypt_equals_row": bool(dec_ok), "e2e_response_equals_device_response": e2e_eq}
 
     # per-kernel device times (profiling pass, outside the timed region)
     ctx.set_profiling(True)
@@ -424,6 +427,7 @@ def main():
         "stages_ms": {k: getattr(tm, k) for k in ("expand_ms", "select_ms", "mac_ms", "finish_ms")},
         "exact_fallbacks": int(tm.exact_fallbacks),
         "verified_decrypt": verified,
+        "verify_detail": verify_detail,
         "db_load_s": t_load,
     }
     if world == 1 and not args.no_cpu_baseline:

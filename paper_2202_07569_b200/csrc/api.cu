@@ -24,6 +24,7 @@
 #include "ntt_reg.cuh"
 #include "params.h"
 #include "round.cuh"
+#include "mac.cuh"
 
 namespace cwgpu {
 
@@ -80,6 +81,8 @@ struct Ctx {
     DevBuf prep_s;                    // A-side prepared operands with the INTT output scale folded in
     bool prep_s_ok = false;           // prep_s valid for the current answer
     bool prescale = true;             // env CWGPU_PRESCALE
+    bool mac_tma = true;              // TMA-fed payload MAC (env CWGPU_MAC=v2 selects k_mac2)
+    int mac_waves = 2;                // k_mac_tma grid size in waves of 3 CTAs / SM (env CWGPU_MAC_WAVES)
     int ntt_np = 1;                   // polynomials per CTA in the tensor / selection NTT kernels (env CWGPU_NTT_NP)
     bool old_mac = false;       // debugging: the first payload MAC kernel (env CWGPU_OLD_MAC)
     // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
@@ -606,6 +609,8 @@ struct Reg32 {
     }
 
 static void set_smem_limits(u32 N) {
+    CK(cudaFuncSetAttribute(k_mac_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 4 * kMacBlock * 4));
+    CK(cudaFuncSetAttribute(k_mac_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 3 * kMacBlock * 4));
 #define RTC(JMv, NCv) CK(cudaFuncSetAttribute(k_round_tc<JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundTcSmem));
     RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
 #undef RTC
@@ -816,7 +821,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
             nc = 2;
             return nullptr;
         }
-        u32* Z = c.lift_tmp.get<u32>((size_t)R * 2 * Mm * N);
+        u32* Z = c.dcur->get<u32>((size_t)R * 2 * Mm * N);  // the tile stream's own buffer
         launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, entries, 2 * LN, col(0), R, Mm, 0, c.T, Z, Mm);
         ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
         nc = 2;
@@ -1051,7 +1056,23 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         const u32* dbt = c.db.ptr<u32>() + (size_t)r0 * c.s * Mm * N;
         const size_t threads = (size_t)c.s * Mm * ((N / 4 + 255) / 256) * 256 * chunks;
         c.next_units = (double)Rt * (c.s + nc) * Mm * N * 4;  // DB + selection words streamed
-        if (c.old_mac)
+        // TMA ring for multi-plaintext rows (C3: 37 vs 45 ms; the selection segments are reused
+        // across the s payload slices); the register stream is as fast for s = 1 (C4: 22.9 ms)
+        if (c.mac_tma && c.s >= 2 && N >= (u32)kMacBlock && !c.old_mac) {
+            // TMA-fed stream: whole waves of 3 CTAs / SM (no partial tail wave), >= 8 rows per chunk
+            const u32 per = Mm * (N / kMacBlock) * c.s;
+            const u32 slots = 148 * 3 * (c.mac_waves > 0 ? c.mac_waves : 2);
+            u32 ck = std::max<u32>(1, std::min<u32>((Rt + 7) / 8, slots / per));
+            const u32 crow = (Rt + ck - 1) / ck;
+            ck = (Rt + crow - 1) / crow;
+            const size_t smem = (size_t)kMacStages * (1 + nc) * kMacBlock * 4;
+            if (nc == 3)
+                launch_named(c, "k_mac", k_mac_tma<3>, (size_t)ck * per, 288, smem, (const u32*)Z, zs, dbt, Rt, c.s,
+                             crow, c.T, acc);
+            else
+                launch_named(c, "k_mac", k_mac_tma<2>, (size_t)ck * per, 288, smem, (const u32*)Z, zs, dbt, Rt, c.s,
+                             crow, c.T, acc);
+        } else if (c.old_mac)
             launch_named(c, "k_mac", k_mac, blocks((size_t)c.s * Mm * N, 128), 128, 0, (const u32*)Z, nc, zs, dbt, Rt,
                          c.s, c.T, c.acc_lo.ptr<u64>(), c.acc_hi.ptr<u64>());
         else if (nc == 3)
@@ -1223,6 +1244,8 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         set_smem_limits(N);
         if (const char* e = std::getenv("CWGPU_STREAMS"))
             c.nstreams = std::max(1, std::min(Ctx::kMaxStreams, std::atoi(e)));
+        if (const char* e = std::getenv("CWGPU_MAC")) c.mac_tma = std::string(e) != "v2";
+        if (const char* e = std::getenv("CWGPU_MAC_WAVES")) c.mac_waves = std::max(1, std::atoi(e));
         if (const char* e = std::getenv("CWGPU_PRESCALE")) c.prescale = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_NTT_NP")) c.ntt_np = std::atoi(e) == 1 ? 1 : 2;
         if (const char* e = std::getenv("CWGPU_ROUND"))

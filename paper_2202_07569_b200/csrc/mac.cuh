@@ -1,0 +1,147 @@
+// Payload multiply-accumulate (weighted_sum, reference bfv.cpp:944-986) as a TMA-fed stream.
+//
+// acc[sj][c][k][n] += sum_r Z[r][c][k][n] * DB[row0 + r][sj][k][n]   (NTT domain, MAC basis)
+//
+// One CTA owns a 1024-coefficient block of one (sj, k) plane over a chunk of rows.  A producer
+// warp streams, per row, the block's 4 KB payload segment and the NC 4 KB selection segments
+// into a 4-stage shared-memory ring with cp.async.bulk (1-D TMA: contiguous, no register
+// staging), signalling a `full` mbarrier by transaction bytes; 8 consumer warps (4 coefficients
+// per thread, 128-bit shared loads) accumulate 16-row groups of 60-bit products in u64 and
+// release the stage through an `empty` mbarrier (after a fence.proxy.async: the stage's next
+// writer is the async proxy).  Loads in flight are bounded by the ring, not
+// by registers, so the stream runs at HBM rate.
+#pragma once
+#include "devtab.h"
+#include "modarith.cuh"
+
+namespace cwgpu {
+
+constexpr int kMacStages = 4;
+constexpr int kMacBlock = 1024;  // coefficients per CTA (256 consumer threads x 4)
+
+__device__ __forceinline__ u32 mac_smem(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mac_smem(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, u32 phase) {
+    u32 done = 0;
+    while (!done)
+        asm volatile(
+            "{\n\t.reg .pred q;\n\tmbarrier.try_wait.parity.shared::cta.b64 q, [%1], %2;\n\tselp.u32 %0, 1, 0, q;\n\t}\n"
+            : "=r"(done)
+            : "r"(mac_smem(b)), "r"(phase)
+            : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mac_smem(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mac_smem(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, u32 bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     mac_smem(dst)),
+                 "l"(src), "r"(bytes), "r"(mac_smem(bar))
+                 : "memory");
+}
+
+/// Grid: chunks x Mm x (N / 1024) x s CTAs of 288 threads (8 consumer warps + 1 producer warp),
+/// block index (slowest .. fastest): chunk, prime k, coefficient block, payload slice sj.
+/// Z: Z + ((r * NC + c) * zstride + k) * N.  DB: [rows][s][Mm][N].  acc: u64 sums of residues.
+template <int NC>
+__global__ void __launch_bounds__(288, 3) k_mac_tma(const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB,
+                                                   u32 R, u32 s, u32 chunk, DevTab T, unsigned long long* __restrict__ acc) {
+    extern __shared__ __align__(128) uint4 ring[];  // [stage][1 + NC][kMacBlock / 4]
+    __shared__ __align__(8) unsigned long long full[kMacStages], empty[kMacStages];
+    const u32 N = T.N, Mm = T.Mm;
+    const u32 nblk = N / kMacBlock;
+    u32 b = blockIdx.x;
+    const u32 sj = b % s;
+    b /= s;
+    const u32 blk = b % nblk;
+    b /= nblk;
+    const u32 k = b % Mm;
+    const u32 ch = b / Mm;
+    const u32 r0 = ch * chunk, r1 = min(R, r0 + chunk);
+    const u32 rows = r1 > r0 ? r1 - r0 : 0;
+    const u32 tid = threadIdx.x, warp = tid >> 5;
+    constexpr u32 SEG = kMacBlock * 4;  // bytes per segment
+    constexpr u32 SEGV = kMacBlock / 4; // uint4 per segment
+    if (tid == 0) {
+        for (int i = 0; i < kMacStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {  // producer
+        if ((tid & 31) == 0) {
+            const size_t dbs = (size_t)s * Mm * N;
+            const u32* dbase = DB + ((size_t)sj * Mm + k) * N + (size_t)blk * kMacBlock;
+            const u32* zbase = Z + (size_t)k * N + (size_t)blk * kMacBlock;
+            const size_t zs = (size_t)NC * zstride * N;
+            for (u32 i = 0; i < rows; ++i) {
+                const u32 st = i % kMacStages;
+                if (i >= (u32)kMacStages) mbar_wait(&empty[st], ((i / kMacStages) - 1) & 1);
+                uint4* buf = ring + (size_t)st * (1 + NC) * SEGV;
+                mbar_expect_tx(&full[st], SEG * (1 + NC));
+                const size_t r = r0 + i;
+                tma_bulk_g2s(buf, dbase + r * dbs, SEG, &full[st]);
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    tma_bulk_g2s(buf + (1 + c) * SEGV, zbase + r * zs + (size_t)c * zstride * N, SEG, &full[st]);
+            }
+        }
+        return;
+    }
+    const u32 p = T.a[k];
+    const u64 pb = T.abar[k];
+    u32 accr[NC][4];
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) accr[c][e] = 0;
+    for (u32 g0 = 0; g0 < rows; g0 += 16) {
+        const u32 ge = min(rows, g0 + 16);
+        u64 g[NC][4];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) g[c][e] = 0;
+        for (u32 i = g0; i < ge; ++i) {
+            const u32 st = i % kMacStages;
+            mbar_wait(&full[st], (i / kMacStages) & 1);
+            const uint4* buf = ring + (size_t)st * (1 + NC) * SEGV;
+            const uint4 d = buf[tid];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const uint4 z = buf[(1 + c) * SEGV + tid];
+                g[c][0] += (u64)z.x * d.x;
+                g[c][1] += (u64)z.y * d.y;
+                g[c][2] += (u64)z.z * d.z;
+                g[c][3] += (u64)z.w * d.w;
+            }
+            // the stage is rewritten by TMA (async proxy): order this thread's generic-proxy reads
+            // of it before the release, then one arrival per warp
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) accr[c][e] = red32(accr[c][e] + bar64(g[c][e], p, pb), p);
+    }
+    if (rows == 0) return;
+    const u32 n = blk * kMacBlock + 4 * tid;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        unsigned long long* o = acc + (((size_t)sj * 3 + c) * Mm + k) * N + n;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) atomicAdd(o + e, (unsigned long long)accr[c][e]);
+    }
+}
+
+}  // namespace cwgpu

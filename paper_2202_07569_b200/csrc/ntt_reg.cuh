@@ -486,8 +486,8 @@ namespace cwgpu {
 /// Thread = 4 consecutive coefficients of one (sj, k) plane over a chunk of rows; 128-bit
 /// loads, 16-row u64 groups (products < 2^60), one 64-bit atomic add per output per chunk.
 /// Z: Z + ((r * nc + c) * zstride + k) * N.  DB: [rows][s][Mm][N].  acc: u64 sums of residues.
-template <int NC>
-__global__ void __launch_bounds__(256, 3) k_mac2(const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB,
+template <int NC, int RB = 4>
+__global__ void __launch_bounds__(256, 2) k_mac2(const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB,
                                               u32 R, u32 s, u32 chunk, DevTab T, unsigned long long* __restrict__ acc) {
     const u32 N = T.N, Mm = T.Mm;
     const u32 n4s = N >> 2;
@@ -526,16 +526,28 @@ __global__ void __launch_bounds__(256, 3) k_mac2(const u32* __restrict__ Z, u32 
         for (int c = 0; c < NC; ++c)
 #pragma unroll
             for (int e = 0; e < 4; ++e) g[c][e] = 0;
-#pragma unroll 2
-        for (u32 r = rg; r < re; ++r) {
-            const uint4 d = __ldg(dbp + (size_t)r * (dbs >> 2));
+        // RB rows per batch: all of a batch's loads are issued before its multiply-adds
+        // (memory-level parallelism for the latency-bound stream); tail rows clamp to re-1 and
+        // are masked by a zero DB word
+        for (u32 r = rg; r < re; r += RB) {
+            uint4 d[RB], z[RB][NC];
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const uint4 z = __ldg(zp + ((size_t)r * zs + (size_t)c * zstride * N) / 4);
-                g[c][0] += (u64)z.x * d.x;
-                g[c][1] += (u64)z.y * d.y;
-                g[c][2] += (u64)z.z * d.z;
-                g[c][3] += (u64)z.w * d.w;
+            for (int b = 0; b < RB; ++b) {
+                const u32 rr = min(r + b, re - 1);
+                d[b] = __ldg(dbp + (size_t)rr * (dbs >> 2));
+#pragma unroll
+                for (int c = 0; c < NC; ++c) z[b][c] = __ldg(zp + ((size_t)rr * zs + (size_t)c * zstride * N) / 4);
+            }
+#pragma unroll
+            for (int b = 0; b < RB; ++b) {
+                if (r + b >= re) d[b] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    g[c][0] += (u64)z[b][c].x * d[b].x;
+                    g[c][1] += (u64)z[b][c].y * d[b].y;
+                    g[c][2] += (u64)z[b][c].z * d[b].z;
+                    g[c][3] += (u64)z[b][c].w * d[b].w;
+                }
             }
         }
 #pragma unroll

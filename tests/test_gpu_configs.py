@@ -57,3 +57,34 @@ def test_config2_full_params_reduced_rows(gpu, reflib, k):
 
     cfg = configs.config(f"C2-k{k}")
     client, sel, pos, target = _run(reflib, cfg, 10, select_only=True)
+
+
+def test_payload_mac_kernels_agree_under_repetition(gpu, monkeypatch):
+    """The TMA-fed payload MAC (k_mac_tma: 4-stage shared-memory ring refilled by cp.async.bulk)
+    and the register-streaming MAC (k_mac2) produce the same partial accumulators, answer after
+    answer, at C4 parameters over several row tiles (a missing async-proxy fence once made the
+    ring race under load)."""
+    import torch
+
+    import bench
+    from paper_2202_07569_b200 import Context, configs
+
+    cfg = configs.config("C4")
+    cfg.n = 1536
+    _, keys, query, positions, _, _, _ = bench.make_inputs(cfg, 0, 1)
+    payload = configs.db_payload(cfg, 1, 0, cfg.n)
+    parts = {}
+    for mac in ("v2", "tma"):
+        monkeypatch.setenv("CWGPU_MAC", mac)
+        ctx = Context(cfg.N, cfg.primes, cfg.t)
+        ctx.load_db(positions, payload, n_total=cfg.n, m=cfg.m)
+        ctx.set_keys(keys)
+        runs = []
+        for _ in range(6 if mac == "tma" else 1):
+            dp = torch.zeros(ctx.partial_words(), dtype=torch.int64, device="cuda")
+            ctx.answer_partial(query, cfg.c, cfg.m, dp.data_ptr())
+            torch.cuda.synchronize()
+            runs.append(dp.cpu().numpy())
+        parts[mac] = runs
+    for r in parts["tma"]:
+        assert np.array_equal(r, parts["v2"][0])
