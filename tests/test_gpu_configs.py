@@ -62,15 +62,15 @@ def test_config2_full_params_reduced_rows(gpu, reflib, k):
 def test_payload_mac_kernels_agree_under_repetition(gpu, monkeypatch):
     """The TMA-fed payload MAC (k_mac_tma: 4-stage shared-memory ring refilled by cp.async.bulk)
     and the register-streaming MAC (k_mac2) produce the same partial accumulators, answer after
-    answer, at C4 parameters over several row tiles (a missing async-proxy fence once made the
-    ring race under load)."""
+    answer, at C3 parameters (15 plaintexts per row: the TMA path) over several row tiles (a
+    missing async-proxy fence once made the ring race under load)."""
     import torch
 
     import bench
     from paper_2202_07569_b200 import Context, configs
 
-    cfg = configs.config("C4")
-    cfg.n = 1536
+    cfg = configs.config("C3")
+    cfg.n = 1024
     _, keys, query, positions, _, _, _ = bench.make_inputs(cfg, 0, 1)
     payload = configs.db_payload(cfg, 1, 0, cfg.n)
     parts = {}
