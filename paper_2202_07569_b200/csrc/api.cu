@@ -250,7 +250,7 @@ static bool tc_instance(u32 JM, u32 nc) {
 /// k_round_tc tables: the parameter block (integer epilogue constants, Montgomery forms) and the
 /// B matrix [NC][K = 4 JM] of u8, K-major in the canonical no-swizzle UMMA layout (8-row x 16-B
 /// core matrices; a row's 16-B K chunks 128 B apart, 8-row groups K/16 * 128 B apart).
-static void build_round_tc(u32 JM, u32 NC, const std::vector<RoundJ>& rj, const std::vector<RoundK>& rk,
+static bool build_round_tc(u32 JM, u32 NC, const std::vector<RoundJ>& rj, const std::vector<RoundK>& rk,
                            const std::vector<u32>& Imod, const std::vector<u32>& a, u32 J, u32 Mm,
                            std::vector<unsigned char>& par, std::vector<unsigned char>& Bm) {
     const u32 K = 4 * JM, F0 = NC - 17, G0 = NC - 6, MMAX = F0 / 4;
@@ -278,17 +278,19 @@ static void build_round_tc(u32 JM, u32 NC, const std::vector<RoundJ>& rj, const 
                 if (sft >= aa && sft - aa < 3) put(G0 + sft, 4 * j + aa, (unsigned char)(G >> (8 * (sft - aa))));
         }
     }
-    // parameter block: RoundTcPar<JM, NC> = 6 arrays of MMAX u32
-    par.assign((size_t)6 * MMAX * 4, 0);
+    // parameter block: RoundTcPar<JM, NC> = uint4 kq[MMAX] + u32 krm[MMAX]
+    par.assign((size_t)MMAX * 16 + (size_t)MMAX * 4, 0);
     u32* P = reinterpret_cast<u32*>(par.data());
     for (u32 k = 0; k < Mm && k < MMAX; ++k) {
-        P[0 * MMAX + k] = rk[k].a;
-        P[1 * MMAX + k] = rk[k].pinv;
-        P[2 * MMAX + k] = rk[k].gcoef;
-        P[3 * MMAX + k] = rk[k].roff;
-        P[4 * MMAX + k] = rk[k].c0;
-        P[5 * MMAX + k] = rk[k].c30;
+        const u32 p = rk[k].a;
+        if (p >= (1u << 30) || (1u << 30) - p >= (1u << 24)) return false;  // epilogue needs 2^30 - a < 2^24
+        P[4 * k + 0] = p;
+        P[4 * k + 1] = rk[k].pinv;
+        P[4 * k + 2] = rk[k].gcoef;
+        P[4 * k + 3] = (1u << 30) - p;
+        P[4 * MMAX + k] = rk[k].roff;
     }
+    return true;
 }
 
 static void build_tables(Ctx& c) {
@@ -513,9 +515,12 @@ static void build_tables(Ctx& c) {
         }
         if (c.rtc_nc) {
             std::vector<unsigned char> Bm;
-            build_round_tc(c.JM, c.rtc_nc, rj, rk, Imod, a, J, Mm, c.rtc, Bm);
-            c.rtc_B.ensure(Bm.size());
-            CK(cudaMemcpy(c.rtc_B.p, Bm.data(), Bm.size(), cudaMemcpyHostToDevice));
+            if (build_round_tc(c.JM, c.rtc_nc, rj, rk, Imod, a, J, Mm, c.rtc, Bm)) {
+                c.rtc_B.ensure(Bm.size());
+                CK(cudaMemcpy(c.rtc_B.p, Bm.data(), Bm.size(), cudaMemcpyHostToDevice));
+            } else {
+                c.rtc_nc = 0;  // IMAD + DFMA rounding instead
+            }
         }
     }
     // device copy of the table itself (slow paths read it through T.self)

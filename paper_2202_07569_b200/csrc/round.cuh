@@ -209,7 +209,9 @@ struct RoundTcPar {
     static constexpr int F0 = NC - 17;      // fraction columns F0 .. F0+10
     static constexpr int G0 = NC - 6;       // gamma columns G0 .. G0+5
     static constexpr int MMAX = F0 / 4;     // residue column groups available
-    u32 ka[MMAX], kpinv[MMAX], kgcoef[MMAX], kroff[MMAX], kc0[MMAX], kc30[MMAX];
+    // per MAC prime: {a, -a^-1 mod 2^32, (-I_A) 2^32 mod a, 2^30 - a < 2^24}; (-2^36) 2^32 mod a
+    uint4 kq[MMAX];
+    u32 krm[MMAX];
 };
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
@@ -356,12 +358,16 @@ __global__ void __launch_bounds__(128, 4) k_round_tc(u32* __restrict__ D, u32 P,
 #pragma unroll
             for (int k = 0; k < RPT::MMAX; ++k) {
                 if (k < (int)Mm) {
-                    const u64 S = (u64)C[4 * k] + ((u64)C[4 * k + 1] << 8) + ((u64)C[4 * k + 2] << 16) +
-                                  ((u64)C[4 * k + 3] << 24);  // < 2^47
-                    const u64 g = S + (u64)gamma * RP.kgcoef[k] + (u64)rlo * RP.kc0[k] + (u64)rhi * RP.kc30[k] +
-                                  RP.kroff[k];  // < 2^63
-                    u32 x = mont_red64(g, RP.ka[k], RP.kpinv[k]);  // [0, 3a)
-                    Dp[(size_t)k * N] = red32(red32(x, 2 * RP.ka[k]), RP.ka[k]);
+                    const uint4 q = RP.kq[k];  // a, pinv, Montgomery(-I_A), 2^30 - a
+                    // S = sum_b C[4k+b] 2^(8b) < 2^47 from two 32-bit pair sums (column sums < 2^23)
+                    const u32 p01 = C[4 * k] + (C[4 * k + 1] << 8), p23 = C[4 * k + 2] + (C[4 * k + 3] << 8);
+                    const u64 S = (u64)p01 + ((u64)p23 << 16);
+                    // Montgomery part: (S + gamma (-I_A) 2^32 - 2^36 2^32) 2^-32 mod a
+                    const u64 X = (u64)gamma * q.z + S + RP.krm[k];
+                    const u32 x = red32(mont_red64(X, q.x, q.y), q.x);  // < 2a before the reduction
+                    // + (rho + 2^36) mod a, with 2^30 = a + (2^30 - a)
+                    const u32 y = red32(red32(rlo + rhi * q.w, 2 * q.x), q.x);  // < 2^30 + 2^31 < 4a
+                    Dp[(size_t)k * N] = red32(x + y, q.x);
                 }
             }
         } else {
