@@ -124,9 +124,10 @@ int cwg_bench_kernel(cwg_ctx* ctx, int which, uint32_t npolys, int iters, float*
 uint64_t cwg_kernel_launches(const cwg_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) so callers can record events on it. */
 void* cwg_stream(const cwg_ctx* ctx);
-/* Per-kernel CUDA-event timing of every launch (adds overhead; off by default).  Turning it
- * on or off clears the statistics; cwg_kernel_stats enumerates (idx = 0, 1, ...) name,
- * summed device time and launch count, returning CWG_EINVAL past the end. */
+/* Per-kernel CUDA-event timing of every launch (adds overhead; off by default; the row-tile
+ * pipeline runs on one stream meanwhile, so each kernel is timed alone).  Turning it on or off
+ * clears the statistics; cwg_kernel_stats enumerates (idx = 0, 1, ...) name, summed device time
+ * and launch count, returning CWG_EINVAL past the end. */
 int cwg_set_profiling(cwg_ctx* ctx, int on);
 int cwg_kernel_stats(const cwg_ctx* ctx, uint32_t idx, char* name, uint32_t name_len, double* total_ms,
                      uint64_t* count);

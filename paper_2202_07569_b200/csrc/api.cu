@@ -125,6 +125,7 @@ struct Ctx {
         u64 count = 0;
     };
     std::vector<ProfLaunch> prof_pending;
+    std::vector<cudaEvent_t> ev_pool;  // recycled profiling events
     std::vector<ProfStat> prof_stats;
     // algorithmic work of the next launch for the profile (0: the grid size, i.e. one unit per
     // CTA -- polynomials for the NTT kernels); see cwg_kernel_units
@@ -138,9 +139,15 @@ template <class K, class... A>
 static void launch_named(Ctx& c, const char* name, K kern, size_t grid, unsigned block, size_t smem, A... args) {
     if (grid == 0) return;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (c.profiling) {
-        CK(cudaEventCreate(&e0));
-        CK(cudaEventCreate(&e1));
+    if (c.profiling) {  // pooled events: creating them per launch would stall the host and open GPU gaps
+        for (cudaEvent_t* e : {&e0, &e1}) {
+            if (c.ev_pool.empty()) {
+                CK(cudaEventCreate(e));
+            } else {
+                *e = c.ev_pool.back();
+                c.ev_pool.pop_back();
+            }
+        }
         CK(cudaEventRecord(e0, c.st));
     }
     kern<<<(unsigned)grid, block, smem, c.st>>>(args...);
@@ -159,8 +166,8 @@ static void prof_collect(Ctx& c) {
     for (auto& p : c.prof_pending) {
         float f = 0;
         CK(cudaEventElapsedTime(&f, p.e0, p.e1));
-        cudaEventDestroy(p.e0);
-        cudaEventDestroy(p.e1);
+        c.ev_pool.push_back(p.e0);
+        c.ev_pool.push_back(p.e1);
         std::string name(p.name);
         auto it = std::find_if(c.prof_stats.begin(), c.prof_stats.end(), [&](auto& x) { return x.name == name; });
         if (it == c.prof_stats.end()) {
@@ -1031,7 +1038,9 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     if (c.old_mac) CK(cudaMemsetAsync(c.acc_hi.get<u64>(accw), 0, accw * 8, c.st));
     const u32 R = tile_rows(c);
     u32 nc_all = 2;
-    const int ns = (int)std::min<u64>((u64)c.nstreams, (c.n_local + R - 1) / R);
+    // profiling serialises the tile pipeline: per-kernel CUDA-event times then measure each kernel
+    // alone (as ncu's launch list does) instead of its overlap with the other stream's kernels
+    const int ns = c.profiling ? 1 : (int)std::min<u64>((u64)c.nstreams, (c.n_local + R - 1) / R);
     const bool piped = ns >= 2 && op == CWG_OP_FOLKLORE && c.k <= 2;
     cudaStream_t main_st = c.st;
     if (piped) {
@@ -1277,6 +1286,11 @@ void cwg_destroy(cwg_ctx* h) {
     if (c.d_fb) cudaFree(c.d_fb);
     for (int i = 0; i < Ctx::kMaxStreams; ++i) if (c.tst[i]) cudaStreamDestroy(c.tst[i]);
     for (int i = 0; i <= Ctx::kMaxStreams; ++i) if (c.tev[i]) cudaEventDestroy(c.tev[i]);
+    for (cudaEvent_t e : c.ev_pool) cudaEventDestroy(e);
+    for (auto& p : c.prof_pending) {
+        cudaEventDestroy(p.e0);
+        cudaEventDestroy(p.e1);
+    }
     if (c.st) cudaStreamDestroy(c.st);
     delete h;
 }

@@ -13,6 +13,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     > gpurun_out/${TAG}_launches.log 2>&1
 CMD="python bench.py --rows 4096 --steps 1 --warmup 3 --no-cpu-baseline --no-verify"
 $CMD > gpurun_out/${TAG}_full_plain.json 2>&1 || exit 1
-ncu --set full --clock-control none --import-source on -k regex:"k_tensor_intt|k_round_tc|k_ntt32r_sel3|k_mac2" \
+ncu --set full --clock-control none --import-source on -k regex:"k_tensor_intt|k_round_tc|k_ntt32r_sel3|k_mac2|k_mac_tma" \
     -s 8 -c 4 -o gpurun_out/${TAG}_full $CMD > gpurun_out/${TAG}_full_ncu.log 2>&1
 ls -la gpurun_out | grep ${TAG}
