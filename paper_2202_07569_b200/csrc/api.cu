@@ -25,6 +25,7 @@
 #include "params.h"
 #include "round.cuh"
 #include "mac.cuh"
+#include "ntt_mac.cuh"
 
 namespace cwgpu {
 
@@ -85,6 +86,11 @@ struct Ctx {
     int mac_waves = 2;                // k_mac_tma grid size in waves of 3 CTAs / SM (env CWGPU_MAC_WAVES)
     int ntt_np = 1;                   // polynomials per CTA in the tensor / selection NTT kernels (env CWGPU_NTT_NP)
     bool old_mac = false;       // debugging: the first payload MAC kernel (env CWGPU_OLD_MAC)
+    // fused selection NTT + payload MAC (k_ntt_mac) for s <= 2 (env CWGPU_FUSE_MAC=0 off,
+    // 2 = register accumulators for s = 1); fuse_now: the current answer uses it, so
+    // select_tile leaves the MAC-basis selection values in the coefficient domain
+    int fuse_mac = 1;
+    bool fuse_now = false;
     // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
     // the latency-bound kernels of one tile (NTTs, tensor-core rounding, MAC) co-reside with those
     // of the next (env CWGPU_STREAMS; C4: 251 ms vs 272 ms on one stream)
@@ -572,6 +578,32 @@ struct Reg32 {
         CK(cudaFuncSetAttribute(k_ntt32r_sel3<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm));
         CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm));
+#define NM(NC, S, A) CK(cudaFuncSetAttribute(k_ntt_mac<LOGN, NC, S, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NttMac<LOGN, S, A>::SMEM));
+        NM(2, 1, false) NM(3, 1, false) NM(2, 1, true) NM(3, 1, true) NM(2, 2, true) NM(3, 2, true)
+#undef NM
+    }
+    /// fused selection NTT + payload MAC over the R rows of a tile (Z: coefficient-domain
+    /// MAC-basis selection planes, Z + ((r * nc + comp) * zs + k) * N)
+    static void ntt_mac(Ctx& c, const u32* Z, u32 zs, u32 nc, const u32* dbt, u32 Rt, unsigned long long* acc) {
+        const u32 Mm = c.ab.Mm;
+        const u32 per = nc * Mm;  // CTAs per row chunk
+        // >= 2 waves of resident CTAs, >= 8 rows per chunk (fewer accumulator atomics)
+        const u32 slots = 148 * 3 * 2;
+        u32 ck = std::max<u32>(1, std::min<u32>((Rt + 7) / 8, (slots + per - 1) / per));
+        const u32 chunk = (Rt + ck - 1) / ck;
+        ck = (Rt + chunk - 1) / chunk;
+        c.next_units = (double)Rt * nc * Mm;  // polynomials transformed (+ payload words streamed)
+        const size_t grid = (size_t)ck * per;
+#define NMC(NC, S, A) launch_named(c, "k_ntt_mac", k_ntt_mac<LOGN, NC, S, A>, grid, R::T, NttMac<LOGN, S, A>::SMEM, Z, zs, dbt, Rt, chunk, c.T, acc)
+        const bool accr = c.fuse_mac == 2 && c.s == 1;
+        if (nc == 3) {
+            if (c.s == 1) { if (accr) NMC(3, 1, false); else NMC(3, 1, true); }
+            else NMC(3, 2, true);
+        } else {
+            if (c.s == 1) { if (accr) NMC(2, 1, false); else NMC(2, 1, true); }
+            else NMC(2, 2, true);
+        }
+#undef NMC
     }
     static void ntt(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bool inverse, int scale, bool perm) {
         if (inverse && perm)
@@ -802,7 +834,9 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         else if (c.JM == 24) launch_named(c, "k_round_mac", k_round_mac_t<24>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else if (c.JM == 32) launch_named(c, "k_round_mac", k_round_mac_t<32>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else launch_named(c, "k_round_mac", k_round_mac_t<40>, grid, 256, sm, D, P, c.T, rj, rk, im);
-        if (reg32_ok(c.cp.logN)) {
+        if (c.fuse_now) {
+            // forward NTT happens inside k_ntt_mac
+        } else if (reg32_ok(c.cp.logN)) {
             REG32_DISPATCH(c.cp.logN, sel3(c, D, P));
         } else {
             ntt32(c, D, P * 3 * c.ab.Mm, c.ab.Mm, J, 0, false, 0);
@@ -835,7 +869,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         }
         u32* Z = c.dcur->get<u32>((size_t)R * 2 * Mm * N);  // the tile stream's own buffer
         launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, entries, 2 * LN, col(0), R, Mm, 0, c.T, Z, Mm);
-        ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
+        if (!c.fuse_now) ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
         nc = 2;
         zstride = Mm;
         return Z;
@@ -951,7 +985,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
     u32* Z = c.Dbuf.get<u32>((size_t)R * 2 * Mm * N);
     launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, (const u64*)nodes, 2 * LN, (const u32*)nullptr, R, Mm,
            0, c.T, Z, Mm);
-    ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
+    if (!c.fuse_now) ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
     nc = 2;
     zstride = Mm;
     return Z;
@@ -1050,6 +1084,11 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         CK(cudaEventRecord(c.tev[0], main_st));
         for (int i = 0; i < ns; ++i) CK(cudaStreamWaitEvent(c.tst[i], c.tev[0], 0));
     }
+    c.fuse_now = c.fuse_mac != 0 && reg32_ok(c.cp.logN) && c.s <= 2 && !c.old_mac;
+    struct FuseReset {
+        Ctx& c;
+        ~FuseReset() { c.fuse_now = false; }
+    } fuse_reset{c};
     u64 tile = 0;
     for (u64 r0 = 0; r0 < c.n_local; r0 += R, ++tile) {
         const u32 Rt = (u32)std::min<u64>(R, c.n_local - r0);
@@ -1072,7 +1111,9 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         c.next_units = (double)Rt * (c.s + nc) * Mm * N * 4;  // DB + selection words streamed
         // TMA ring for multi-plaintext rows (C3: 37 vs 45 ms; the selection segments are reused
         // across the s payload slices); the register stream is as fast for s = 1 (C4: 22.9 ms)
-        if (c.mac_tma && c.s >= 2 && N >= (u32)kMacBlock && !c.old_mac) {
+        if (c.fuse_now) {
+            REG32_DISPATCH(c.cp.logN, ntt_mac(c, Z, zs, nc, dbt, Rt, acc));
+        } else if (c.mac_tma && c.s >= 2 && N >= (u32)kMacBlock && !c.old_mac) {
             // TMA-fed stream: whole waves of 3 CTAs / SM (no partial tail wave), >= 8 rows per chunk
             const u32 per = Mm * (N / kMacBlock) * c.s;
             const u32 slots = 148 * 3 * (c.mac_waves > 0 ? c.mac_waves : 2);
@@ -1265,6 +1306,7 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         if (const char* e = std::getenv("CWGPU_ROUND"))
             c.round_kind = std::string(e) == "int" ? 0 : std::string(e) == "hyb" ? 1 : 2;
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
+        if (const char* e = std::getenv("CWGPU_FUSE_MAC")) c.fuse_mac = std::atoi(e);
         c.dcur = &c.Dbuf;
         for (int i = 0; i < Ctx::kMaxStreams; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));
         for (int i = 0; i <= Ctx::kMaxStreams; ++i) CK(cudaEventCreateWithFlags(&c.tev[i], cudaEventDisableTiming));
