@@ -26,6 +26,7 @@
 #include "round.cuh"
 #include "mac.cuh"
 #include "ntt_mac.cuh"
+#include "tir.cuh"
 
 namespace cwgpu {
 
@@ -91,6 +92,12 @@ struct Ctx {
     // select_tile leaves the MAC-basis selection values in the coefficient domain
     int fuse_mac = 1;
     bool fuse_now = false;
+    // fused tensor + INTT + tensor-core rounding over a J-CTA cluster (k_tir; env CWGPU_FUSE_TIR=0
+    // off); -1 = not yet probed, 0 = unavailable for these parameters, 1 = on
+    int fuse_tir = -1;
+    bool round_tma = true;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
+    u32 zs_last = 0;        // MAC-basis plane stride of the last mul_prepared output (J or Mm)
+    unsigned next_cluster = 0;  // cluster size of the next launch (launch_named)
     // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
     // the latency-bound kernels of one tile (NTTs, tensor-core rounding, MAC) co-reside with those
     // of the next (env CWGPU_STREAMS; C4: 251 ms vs 272 ms on one stream)
@@ -156,7 +163,24 @@ static void launch_named(Ctx& c, const char* name, K kern, size_t grid, unsigned
         }
         CK(cudaEventRecord(e0, c.st));
     }
-    kern<<<(unsigned)grid, block, smem, c.st>>>(args...);
+    if (c.next_cluster > 1) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(block);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = c.st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = c.next_cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        c.next_cluster = 0;
+        CK(cudaLaunchKernelEx(&cfg, kern, args...));
+    } else {
+        kern<<<(unsigned)grid, block, smem, c.st>>>(args...);
+    }
     CK(cudaGetLastError());
     ++c.launches;
     if (c.profiling) {
@@ -619,15 +643,15 @@ struct Reg32 {
             launch_named(c, "k_ntt32r_fwd", k_ntt32r<LOGN, false, false>, npolys, R::T, R::SMEM, base, c.T, gs, stride,
                          off, scale);
     }
-    static void sel3(Ctx& c, u32* D, u32 P) {
+    static void sel3(Ctx& c, u32* D, u32 P, u32 stride) {
         const u32 npc = 3 * P;
         c.next_units = (double)npc * c.ab.Mm;
         if (c.ntt_np == 2)
             launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN, 2>, (size_t)((npc + 1) / 2) * c.ab.Mm, R::T,
-                         2 * R::SMEM, D, c.T, c.ab.J, npc);
+                         2 * R::SMEM, D, c.T, stride, npc);
         else
             launch_named(c, "k_ntt32r_sel3", k_ntt32r_sel3<LOGN, 1>, (size_t)npc * c.ab.Mm, R::T, R::SMEM, D, c.T,
-                         c.ab.J, npc);
+                         stride, npc);
     }
     static void tensor(Ctx& c, const u32* pa, const u32* ia, const u32* pb, const u32* ib, u32 P, u32* D, int fold) {
         c.next_units = (double)P * c.ab.J * 3;
@@ -656,6 +680,9 @@ static void set_smem_limits(u32 N) {
     CK(cudaFuncSetAttribute(k_mac_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 4 * kMacBlock * 4));
     CK(cudaFuncSetAttribute(k_mac_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 3 * kMacBlock * 4));
 #define RTC(JMv, NCv) CK(cudaFuncSetAttribute(k_round_tc<JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundTcSmem));
+    RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
+#undef RTC
+#define RTC(JMv, NCv) CK(cudaFuncSetAttribute(k_round_tma<JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>()));
     RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
 #undef RTC
     Reg32<8>::limits(); Reg32<9>::limits(); Reg32<10>::limits(); Reg32<11>::limits();
@@ -793,12 +820,74 @@ static u32* prepare_scaled(Ctx& c, const u32* prep, u32 count) {
 /// else the 3-comp chain products are written to chain_out [P][3][L][N].
 static bool round_tc_on(const Ctx& c) { return reg32_ok(c.cp.logN) && c.round_kind == 2 && c.rtc_nc != 0; }
 
+// k_tir instances: (log2 N, cluster = J aux primes, JM, rounding GEMM width)
+#define TIR_LIST(X) X(13, 16, 16, 64) X(13, 16, 16, 80) X(12, 8, 8, 48) X(12, 8, 8, 64) X(14, 16, 16, 64) X(14, 16, 16, 80)
+static bool tir_match(const Ctx& c, u32 L, u32 CL, u32 JM, u32 NC) {
+    return c.cp.logN == L && c.ab.J == CL && c.JM == JM && c.rtc_nc == NC;
+}
+/// k_tir usable for this context: an instance exists and a cluster of J CTAs fits on the GPU.
+static bool tir_on(Ctx& c) {
+    if (c.fuse_tir >= 0) return c.fuse_tir == 1;
+    c.fuse_tir = 0;
+    // measured slower than k_tensor_intt_r + k_round_tma at C4 (cluster barriers, DSMEM gather,
+    // lower residency): opt-in only (env CWGPU_FUSE_TIR=1)
+    const char* fe = std::getenv("CWGPU_FUSE_TIR");
+    if (!fe || std::atoi(fe) == 0) return false;
+    if (!round_tc_on(c)) return false;
+#define X(L, CL, JMv, NCv)                                                                                        \
+    if (tir_match(c, L, CL, JMv, NCv)) {                                                                          \
+        auto kf = k_tir<L, CL, JMv, NCv>;                                                                         \
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tir<L, CL>::SMEM));         \
+        if (CL > 8) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));              \
+        cudaLaunchConfig_t cfg = {};                                                                              \
+        cfg.gridDim = dim3(CL * 148);                                                                             \
+        cfg.blockDim = dim3(Tir<L, CL>::T);                                                                       \
+        cfg.dynamicSmemBytes = Tir<L, CL>::SMEM;                                                                  \
+        cudaLaunchAttribute at[1];                                                                                \
+        at[0].id = cudaLaunchAttributeClusterDimension;                                                           \
+        at[0].val.clusterDim.x = CL;                                                                              \
+        at[0].val.clusterDim.y = 1;                                                                               \
+        at[0].val.clusterDim.z = 1;                                                                               \
+        cfg.attrs = at;                                                                                           \
+        cfg.numAttrs = 1;                                                                                         \
+        int ncl = 0;                                                                                              \
+        if (cudaOccupancyMaxActiveClusters(&ncl, kf, &cfg) != cudaSuccess) {                                      \
+            cudaGetLastError();                                                                                   \
+            ncl = 0;                                                                                              \
+        }                                                                                                         \
+        c.fuse_tir = ncl > 0 ? 1 : 0;                                                                             \
+    }
+    TIR_LIST(X)
+#undef X
+    return c.fuse_tir == 1;
+}
+
 /// prepA_scaled: the A operands carry (N 2^32)^-1 (A/a_j)^-1 (see prepare_scaled; tc rounding only).
 static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* prepB, const u32* idxB, u32 P,
                          bool to_mac, u64* chain_out, bool prepA_scaled = false) {
     const u32 N = c.cp.N, J = c.ab.J;
     u32* D = c.dcur->get<u32>((size_t)P * 3 * J * N);
     const bool tc = to_mac && round_tc_on(c);
+    c.zs_last = J;
+    if (tc && tir_on(c)) {
+        // tensor + INTT + rounding in one cluster kernel: Z[P][3][Mm][N], coefficient domain
+        const RoundK* rk = reinterpret_cast<const RoundK*>(c.round_tab.ptr<RoundJ>() + c.JM);
+        const uint4* Bm = c.rtc_B.ptr<uint4>();
+        const int fold = prepA_scaled ? 2 : 1;
+        c.zs_last = c.ab.Mm;
+#define X(L, CL, JMv, NCv)                                                                                        \
+    if (tir_match(c, L, CL, JMv, NCv)) {                                                                          \
+        c.next_cluster = CL;                                                                                      \
+        c.next_units = (double)P * 3 * CL;                                                                        \
+        launch_named(c, "k_tir", k_tir<L, CL, JMv, NCv>, (size_t)P * 3 * CL, Tir<L, CL>::T, Tir<L, CL>::SMEM,      \
+                     prepA, idxA, prepB, idxB, P, c.T, fold,                                                      \
+                     *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk, D);                   \
+    }
+        TIR_LIST(X)
+#undef X
+        if (!c.fuse_now) REG32_DISPATCH(c.cp.logN, sel3(c, D, P, c.ab.Mm));
+        return D;
+    }
     if (reg32_ok(c.cp.logN)) {
         REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? (prepA_scaled ? 2 : 1) : 0));
     } else {
@@ -816,9 +905,15 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
             const u32 g3 = (u32)std::min<size_t>(items / 128, 148 * 4);
             const uint4* Bm = c.rtc_B.ptr<uint4>();
 #define RTC(JMv, NCv)                                                                                             \
-    if (c.JM == JMv && c.rtc_nc == NCv)                                                                          \
-        launch_named(c, "k_round_tc", k_round_tc<JMv, NCv>, g3, 128, kRoundTcSmem, D, P, c.T,                    \
-                     *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk);
+    if (c.JM == JMv && c.rtc_nc == NCv) {                                                                        \
+        if (c.round_tma)                                                                                          \
+            launch_named(c, "k_round_tc", k_round_tma<JMv, NCv>, std::min<size_t>(items / 128, 148 * 4), 160,    \
+                         round_tma_smem<JMv>(), D, P, c.T,                                                        \
+                         *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk);                   \
+        else                                                                                                      \
+            launch_named(c, "k_round_tc", k_round_tc<JMv, NCv>, g3, 128, kRoundTcSmem, D, P, c.T,                \
+                         *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk);                   \
+    }
             RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
 #undef RTC
         } else if (!c.rpar.empty() && c.round_kind >= 1) {
@@ -837,7 +932,7 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         if (c.fuse_now) {
             // forward NTT happens inside k_ntt_mac
         } else if (reg32_ok(c.cp.logN)) {
-            REG32_DISPATCH(c.cp.logN, sel3(c, D, P));
+            REG32_DISPATCH(c.cp.logN, sel3(c, D, P, J));
         } else {
             ntt32(c, D, P * 3 * c.ab.Mm, c.ab.Mm, J, 0, false, 0);
         }
@@ -883,7 +978,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         u32* D = c.prep_s_ok ? mul_prepared(c, c.prep_s.ptr<u32>(), col(0), prep, col(1), R, true, nullptr, true)
                              : mul_prepared(c, prep, col(0), prep, col(1), R, true, nullptr);
         nc = 3;
-        zstride = J;
+        zstride = c.zs_last;
         return D;
     }
     // ---- general product trees (k >= 3 folklore, arithmetic operator)
@@ -949,7 +1044,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
             }
             u32* D = mul_prepared(c, np_prep, di, np_prep, di + ia.size(), R, true, nullptr);
             nc = 3;
-            zstride = J;
+            zstride = c.zs_last;
             return D;
         }
         u64* c3 = c.chain3.get<u64>((size_t)R * np * 3 * LN);
@@ -1307,6 +1402,7 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
             c.round_kind = std::string(e) == "int" ? 0 : std::string(e) == "hyb" ? 1 : 2;
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_FUSE_MAC")) c.fuse_mac = std::atoi(e);
+        if (const char* e = std::getenv("CWGPU_ROUND_TMA")) c.round_tma = std::atoi(e) != 0;
         c.dcur = &c.Dbuf;
         for (int i = 0; i < Ctx::kMaxStreams; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));
         for (int i = 0; i <= Ctx::kMaxStreams; ++i) CK(cudaEventCreateWithFlags(&c.tev[i], cudaEventDisableTiming));
@@ -1705,6 +1801,8 @@ extern "C" int cwg_bench_kernel(cwg_ctx* h, int which, uint32_t npolys, int iter
             case 16: ms = bench_nttw_pf<3>(c, buf, npolys, iters, 3); break;
             case 18: ms = bench_nttw_variant<5, 1, 3, false, false, 8>(c, buf, npolys, iters); break;
             case 17: ms = bench_nttw_pf<2>(c, buf, npolys, iters, 2); break;
+            case 19: ms = bench_nttw_variant<5, 1, 3, false, false, 16>(c, buf, npolys, iters); break;
+            case 20: ms = bench_nttw_variant<5, 1, 3, true, false, 16>(c, buf, npolys, iters); break;
             default: throw std::invalid_argument("unknown benchmark variant");
         }
         *ms_per_launch = ms;

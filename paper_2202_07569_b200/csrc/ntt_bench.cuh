@@ -24,6 +24,10 @@ __global__ void __launch_bounds__(NttW<LOGN, WB>::T, MINB) k_nttw_bench(u32* __r
                                  : d[(size_t)q * G::N + (((u32)r << (LOGN - WB)) | tid)] & 0x3fffffffu;
     if (INV) nttw_inv<LOGN, WB, NP>(v, smb, T.airp + (size_t)j * G::N, T.airps + (size_t)j * G::N, p);
     else nttw_fwd<LOGN, WB, NP, FAKE>(v, smb, T.arp + (size_t)j * G::N, T.arps + (size_t)j * G::N, p);
+    if constexpr ((FAKE & 16) != 0 && NP == 1) {  // PERM-order output through smem + one bulk copy
+        bulk_store_poly<LOGN, WB>(d, smb, v[0]);
+        return;
+    }
     if ((FAKE & 4) || (FAKE & 8)) {  // keep the result live without storing it (4: no loads either)
         u32 x = 0;
 #pragma unroll

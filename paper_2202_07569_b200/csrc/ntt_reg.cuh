@@ -44,6 +44,29 @@ __device__ __forceinline__ void load_tw(const u32* __restrict__ tp, const u32* _
     }
 }
 
+/// Write one polynomial (thread tid's E registers at positions (r << (LOGN - WB)) | tid, the PERM
+/// order) to global memory through shared memory and one bulk copy.  Microbenchmark variant only
+/// (scripts/bench_ntt.py): 21.0 vs 25.9 ns per NTT against the strided uint4 stores of the
+/// benchmark's baseline, but no gain over the production kernels' coalesced PERM-order STG in
+/// situ (k_tensor_intt, persistent with deferred bulk-store waits: 96.6 vs 81.4 ms at C4).
+template <int LOGN, int WB>
+__device__ __forceinline__ void bulk_store_poly(u32* __restrict__ gdst, u32* sm, const u32 (&v)[1 << WB]) {
+    constexpr int E = 1 << WB, SH = LOGN - WB;
+    const u32 tid = threadIdx.x;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < E; ++r) sm[((u32)r << SH) | tid] = v[r];
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+                     "r"((u32)__cvta_generic_to_shared(sm)), "r"((u32)(4u << LOGN))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // smem stays valid until read
+    }
+}
+
 template <int LOGN, int WB>
 struct NttW {
     static constexpr int N = 1 << LOGN;

@@ -19,6 +19,7 @@
 #pragma once
 #include "kernels.cuh"
 #include "ntt_reg.cuh"
+#include "mac.cuh"
 
 namespace cwgpu {
 
@@ -389,6 +390,220 @@ __global__ void __launch_bounds__(128, 4) k_round_tc(u32* __restrict__ D, u32 P,
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(TCOLS));
+}
+
+}  // namespace cwgpu
+
+namespace cwgpu {
+
+// ---------------------------------------------------------------------------------------
+// TMA-fed variant of k_round_tc.  The plane loads of k_round_tc are issued by the same threads
+// that then wait for the MMA and run the epilogue, so at most one 128-coefficient tile per CTA
+// is in flight and the kernel is latency-bound (ncu: long-scoreboard stalls, ~45% of HBM).
+// Here a producer warp streams each tile's J plane segments (512 B each, contiguous) into a
+// kRtStages-deep shared-memory ring with cp.async.bulk, completing on a `full` mbarrier; the 4
+// consumer warps read their coefficient's J words from the ring (conflict-free), release the
+// stage, and run the tensor-core rounding and epilogue exactly as k_round_tc, writing the Mm
+// MAC-basis residues in place.  Persistent: CTA b handles tiles b, b + grid, ...
+// ---------------------------------------------------------------------------------------
+constexpr int kRtStages = 4;
+template <int JM>
+constexpr size_t round_tma_smem() { return (size_t)kRtStages * JM * 128 * 4; }
+
+template <int JM, int NC>
+__global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P, DevTab T,
+                                                     const __grid_constant__ RoundTcPar<JM, NC> RP,
+                                                     const uint4* __restrict__ Bglob, const RoundK* __restrict__ gRK) {
+    using RPT = RoundTcPar<JM, NC>;
+    constexpr int K = RPT::K, F0 = RPT::F0, G0 = RPT::G0;
+    constexpr int KSTEPS = K / 32;
+    __shared__ __align__(128) uint4 Bs[NC * K / 16];
+    extern __shared__ __align__(128) u32 ringd[];  // [kRtStages][JM][128]
+    auto ring = reinterpret_cast<u32(*)[JM][128]>(ringd);
+    __shared__ __align__(8) unsigned long long mbar, full[kRtStages], empty[kRtStages];
+    __shared__ u32 tmem_base_sh;
+    const u32 tid = threadIdx.x, warp = tid >> 5;
+    const u32 J = T.J, Mm = T.Mm, N = T.N, logN = T.logN;
+    const size_t total = (size_t)P * 3 * N;
+    const u32 ntiles = (u32)((total + 127) / 128);
+
+    for (u32 x = tid; x < NC * K / 16; x += blockDim.x) Bs[x] = Bglob[x];
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                     "n"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 32) {
+        mbar_init(&mbar, 1);
+        for (int i = 0; i < kRtStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // B visible to the tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+
+    if (warp == 4) {  // producer: J plane segments of each tile -> ring stage
+        if ((tid & 31) == 0) {
+            u32 i = 0;
+            for (u32 tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++i) {
+                const u32 st = i % kRtStages;
+                if (i >= (u32)kRtStages) mbar_wait(&empty[st], ((i / kRtStages) - 1) & 1);
+                const size_t base = (size_t)tl * 128;
+                const size_t pc = base >> logN;
+                const u32 n0 = (u32)(base & (N - 1));
+                mbar_expect_tx(&full[st], J * 512u);
+                const u32* src = D + pc * J * N + n0;
+                for (u32 j = 0; j < J; ++j) tma_bulk_g2s(&ring[st][j][0], src + (size_t)j * N, 512u, &full[st]);
+            }
+        }
+        return;
+    }
+
+    const u32 tbase = tmem_base_sh;
+    const u32 ta = tbase + ((warp * 32u) << 16);
+    const u32 td = ta + JM;
+    const u64 bdesc0 = ((u64)((smem_u32(Bs) >> 4) & 0x3fff)) | ((u64)(128 >> 4) << 16) |
+                       ((u64)((K / 16 * 128) >> 4) << 32) | (1ull << 46);
+    const u32 idesc = (2u << 4) | ((u32)(NC >> 3) << 17) | ((u32)(128 >> 4) << 24);
+    const u32 fA0 = T.fracA[1], fA1 = T.fracA[2];
+    u32 phase = 0, i = 0;
+#pragma unroll 1
+    for (u32 tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++i) {
+        const u32 st = i % kRtStages;
+        const size_t idx = (size_t)tl * 128 + tid;
+        const size_t pc = idx >> logN;
+        const u32 n = (u32)(idx & (N - 1));
+        u32* Dp = D + pc * J * N + n;
+        mbar_wait(&full[st], (i / kRtStages) & 1);
+        u32 w[JM];
+#pragma unroll
+        for (int j = 0; j < JM; ++j) w[j] = j < (int)J ? ring[st][j][tid] : 0u;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // next writer of the stage: TMA
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+#pragma unroll
+        for (int c = 0; c < JM; c += 8)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(ta + c),
+                         "r"(w[c]), "r"(w[c + 1]), "r"(w[c + 2]), "r"(w[c + 3]), "r"(w[c + 4]), "r"(w[c + 5]),
+                         "r"(w[c + 6]), "r"(w[c + 7])
+                         : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+            for (int s = 0; s < KSTEPS; ++s) {
+                const u64 bd = bdesc0 + (u64)((s * 2 * 128) >> 4);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tbase + JM),
+                    "r"(tbase + (u32)(s * 8)), "l"(bd), "r"(idesc), "r"(s)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                             smem_u32(&mbar))
+                         : "memory");
+        }
+        mbar_wait(&mbar, phase);
+        phase ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        u32 C[17];  // fraction / gamma columns F0 .. NC-1
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15}, [%16];\n"
+            : "=r"(C[1]), "=r"(C[2]), "=r"(C[3]), "=r"(C[4]), "=r"(C[5]), "=r"(C[6]), "=r"(C[7]), "=r"(C[8]),
+              "=r"(C[9]), "=r"(C[10]), "=r"(C[11]), "=r"(C[12]), "=r"(C[13]), "=r"(C[14]), "=r"(C[15]), "=r"(C[16])
+            : "r"(td + F0 + 1)
+            : "memory");
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];\n" : "=r"(C[0]) : "r"(td + F0) : "memory");
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        u64 gs = 0;
+#pragma unroll
+        for (int s = 0; s < 6; ++s) gs += (u64)C[G0 - F0 + s] << (8 * s);
+        const u32 gamma = (u32)((gs + (1ull << 45)) >> 46);
+        u64 plo = 0, phi = 0;
+#pragma unroll
+        for (int s = 0; s < 6; ++s) plo += (u64)C[s] << (8 * s);
+#pragma unroll
+        for (int s = 6; s < 11; ++s) phi += (u64)C[s] << (8 * (s - 6));
+        const u64 lo64 = plo + (phi << 48);
+        const u64 hi64 = (phi >> 16) + (lo64 < plo ? 1u : 0u);
+        u32 s0 = (u32)lo64, s1 = (u32)(lo64 >> 32), s2 = (u32)hi64, s3 = (u32)(hi64 >> 32);
+        {
+            const u64 p0 = (u64)gamma * fA0, p1 = (u64)gamma * fA1;
+            const u32 q0 = (u32)p0;
+            const u64 t1 = (p0 >> 32) + (u32)p1;
+            const u32 q1 = (u32)t1;
+            const u32 q2 = (u32)((t1 >> 32) + (p1 >> 32));
+            asm("sub.cc.u32  %0, %0, %4;\n\t"
+                "subc.cc.u32 %1, %1, %5;\n\t"
+                "subc.cc.u32 %2, %2, %6;\n\t"
+                "subc.u32    %3, %3, 0;\n\t"
+                "add.cc.u32  %1, %1, 0x80000000;\n\t"
+                "addc.cc.u32 %2, %2, 0;\n\t"
+                "addc.u32    %3, %3, 0;\n\t"
+                : "+r"(s0), "+r"(s1), "+r"(s2), "+r"(s3)
+                : "r"(q0), "r"(q1), "r"(q2));
+        }
+        const long long rho = (long long)(((u64)s3 << 32) | s2);
+        const bool bad = (s1 == 0u && s0 < 64u) || (s1 >= 0xfffffff0u) || T.force_exact;
+        {
+            const u64 rb = (u64)(rho + (1ll << 36));
+            const u32 rlo = (u32)(rb & ((1u << 30) - 1)), rhi = (u32)(rb >> 30);
+#pragma unroll
+            for (int k0 = 0; k0 < RPT::MMAX; k0 += 4) {  // 4 MAC primes per TMEM load (warp-uniform)
+                u32 Rc[16];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                    "%14, %15}, [%16];\n"
+                    : "=r"(Rc[0]), "=r"(Rc[1]), "=r"(Rc[2]), "=r"(Rc[3]), "=r"(Rc[4]), "=r"(Rc[5]), "=r"(Rc[6]),
+                      "=r"(Rc[7]), "=r"(Rc[8]), "=r"(Rc[9]), "=r"(Rc[10]), "=r"(Rc[11]), "=r"(Rc[12]), "=r"(Rc[13]),
+                      "=r"(Rc[14]), "=r"(Rc[15])
+                    : "r"(td + 4 * k0)
+                    : "memory");
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                if (!bad) {
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const int k = k0 + kk;
+                        if (k < RPT::MMAX && k < (int)Mm) {
+                            const uint4 q = RP.kq[k];
+                            const u32 p01 = Rc[4 * kk] + (Rc[4 * kk + 1] << 8), p23 = Rc[4 * kk + 2] + (Rc[4 * kk + 3] << 8);
+                            const u64 S = (u64)p01 + ((u64)p23 << 16);
+                            const u64 Xv = (u64)gamma * q.z + S + RP.krm[k];
+                            const u32 x = red32(mont_red64(Xv, q.x, q.y), q.x);
+                            const u32 y = red32(red32(rlo + rhi * q.w, 2 * q.x), q.x);
+                            Dp[(size_t)k * N] = red32(x + y, q.x);
+                        }
+                    }
+                }
+            }
+        }
+        if (bad) {  // exact multiword path (no tensor-memory instructions inside); D still holds w_j
+            HpsState h;
+            for (u32 j = 0; j < J; ++j) h.w[j] = Dp[(size_t)j * N];
+            h.gamma = gamma;
+            h.rho = rho;
+            u32 Rw[kAW + 2];
+            const bool neg = round_exact(h, *T.self, Rw);
+            for (u32 k = 0; k < Mm; ++k) {
+                const u32 a = gRK[k].a;
+                u32 r = mag_mod32(Rw, a, gRK[k].abar);
+                if (neg && r) r = a - r;
+                Dp[(size_t)k * N] = r;
+            }
+        }
+        __syncwarp();
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    }
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(128));
 }
 
 }  // namespace cwgpu

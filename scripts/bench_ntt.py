@@ -16,7 +16,8 @@ names = ["W5 fwd NP1 MINB3 (production)", "W5 inv NP1 MINB3 (production)", "W5 f
          "W5 fwd NP2 MINB2 register twiddles (diag)", "W5 fwd NP1 MINB3 no transposes (diag)",
          "W5 fwd NP1 MINB3 no global load/store (diag)", "W5 fwd NP1 MINB3 butterflies only (diag)",
          "W5 fwd NP2 MINB2 butterflies only (diag)", "W5 fwd persistent cp.async prefetch 3/SM",
-         "W5 fwd persistent cp.async prefetch 2/SM", "W5 fwd NP1 MINB3 loads, no stores (diag)"]
+         "W5 fwd persistent cp.async prefetch 2/SM", "W5 fwd NP1 MINB3 loads, no stores (diag)",
+         "W5 fwd NP1 MINB3 smem + bulk-copy store", "W5 inv NP1 MINB3 smem + bulk-copy store"]
 npolys = 36000
 only = [int(a) for a in sys.argv[1:]]
 for w, nm in enumerate(names):
