@@ -315,8 +315,8 @@ static bool build_round_tc(u32 JM, u32 NC, const std::vector<RoundJ>& rj, const 
                 if (sft >= aa && sft - aa < 3) put(G0 + sft, 4 * j + aa, (unsigned char)(G >> (8 * (sft - aa))));
         }
     }
-    // parameter block: RoundTcPar<JM, NC> = uint4 kq[MMAX] + u32 krm[MMAX]
-    par.assign((size_t)MMAX * 16 + (size_t)MMAX * 4, 0);
+    // parameter block: RoundTcPar<JM, NC> = uint4 kq[MMAX] + u32 krm[MMAX] + u32 kc0[MMAX] + u32 kc30[MMAX]
+    par.assign((size_t)MMAX * 16 + (size_t)MMAX * 12, 0);
     u32* P = reinterpret_cast<u32*>(par.data());
     for (u32 k = 0; k < Mm && k < MMAX; ++k) {
         const u32 p = rk[k].a;
@@ -326,6 +326,8 @@ static bool build_round_tc(u32 JM, u32 NC, const std::vector<RoundJ>& rj, const 
         P[4 * k + 2] = rk[k].gcoef;
         P[4 * k + 3] = (1u << 30) - p;
         P[4 * MMAX + k] = rk[k].roff;
+        P[5 * MMAX + k] = (u32)((1ull << 32) % p);
+        P[6 * MMAX + k] = (u32)(((u128)1 << 62) % p);
     }
     return true;
 }
@@ -682,7 +684,12 @@ static void set_smem_limits(u32 N) {
 #define RTC(JMv, NCv) CK(cudaFuncSetAttribute(k_round_tc<JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundTcSmem));
     RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
 #undef RTC
-#define RTC(JMv, NCv) CK(cudaFuncSetAttribute(k_round_tma<JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>()));
+#define RTC(JMv, NCv)                                                                                                \
+    CK(cudaFuncSetAttribute(k_round_tma<0, JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
+    {                                                                                                                \
+        constexpr int LN = JMv == 16 ? 13 : JMv == 8 ? 12 : JMv == 32 ? 14 : 0;                                     \
+        CK(cudaFuncSetAttribute(k_round_tma<LN, JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
+    }
     RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
 #undef RTC
     Reg32<8>::limits(); Reg32<9>::limits(); Reg32<10>::limits(); Reg32<11>::limits();
@@ -906,11 +913,17 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
             const uint4* Bm = c.rtc_B.ptr<uint4>();
 #define RTC(JMv, NCv)                                                                                             \
     if (c.JM == JMv && c.rtc_nc == NCv) {                                                                        \
-        if (c.round_tma)                                                                                          \
-            launch_named(c, "k_round_tc", k_round_tma<JMv, NCv>, std::min<size_t>(items / 128, 148 * 4), 160,    \
-                         round_tma_smem<JMv>(), D, P, c.T,                                                        \
-                         *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk);                   \
-        else                                                                                                      \
+        if (c.round_tma) {                                                                                        \
+            const size_t gr = std::min<size_t>(items / 128, 148 * 4);                                             \
+            const auto& rp = *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data());                        \
+            constexpr int LN = JMv == 16 ? 13 : JMv == 8 ? 12 : JMv == 32 ? 14 : 0;                              \
+            if (LN != 0 && c.cp.logN == (u32)LN)                                                                  \
+                launch_named(c, "k_round_tc", k_round_tma<LN, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T, \
+                             rp, Bm, rk);                                                                         \
+            else                                                                                                  \
+                launch_named(c, "k_round_tc", k_round_tma<0, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T,  \
+                             rp, Bm, rk);                                                                         \
+        } else                                                                                                      \
             launch_named(c, "k_round_tc", k_round_tc<JMv, NCv>, g3, 128, kRoundTcSmem, D, P, c.T,                \
                          *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk);                   \
     }

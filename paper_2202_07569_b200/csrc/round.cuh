@@ -213,6 +213,9 @@ struct RoundTcPar {
     // per MAC prime: {a, -a^-1 mod 2^32, (-I_A) 2^32 mod a, 2^30 - a < 2^24}; (-2^36) 2^32 mod a
     uint4 kq[MMAX];
     u32 krm[MMAX];
+    // k_round_tma epilogue: (rho + 2^36) mod a_k enters the Montgomery sum as rlo 2^32 + rhi 2^62
+    u32 kc0[MMAX];   // 2^32 mod a_k
+    u32 kc30[MMAX];  // 2^62 mod a_k
 };
 
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
@@ -410,7 +413,7 @@ constexpr int kRtStages = 4;
 template <int JM>
 constexpr size_t round_tma_smem() { return (size_t)kRtStages * JM * 128 * 4; }
 
-template <int JM, int NC>
+template <int LOGN, int JM, int NC>  // LOGN = 0: N at run time
 __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P, DevTab T,
                                                      const __grid_constant__ RoundTcPar<JM, NC> RP,
                                                      const uint4* __restrict__ Bglob, const RoundK* __restrict__ gRK) {
@@ -423,7 +426,8 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
     __shared__ __align__(8) unsigned long long mbar, full[kRtStages], empty[kRtStages];
     __shared__ u32 tmem_base_sh;
     const u32 tid = threadIdx.x, warp = tid >> 5;
-    const u32 J = T.J, Mm = T.Mm, N = T.N, logN = T.logN;
+    const u32 J = T.J, Mm = T.Mm;
+    const u32 N = LOGN ? (1u << LOGN) : T.N, logN = LOGN ? (u32)LOGN : T.logN;  // compile-time N: immediate plane offsets
     const size_t total = (size_t)P * 3 * N;
     const u32 ntiles = (u32)((total + 127) / 128);
 
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
             u32 i = 0;
             for (u32 tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++i) {
                 const u32 st = i % kRtStages;
-                if (i >= (u32)kRtStages) mbar_wait(&empty[st], ((i / kRtStages) - 1) & 1);
+                if (i >= (u32)kRtStages) mbar_wait_sleep(&empty[st], ((i / kRtStages) - 1) & 1);
                 const size_t base = (size_t)tl * 128;
                 const size_t pc = base >> logN;
                 const u32 n0 = (u32)(base & (N - 1));
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
         const size_t pc = idx >> logN;
         const u32 n = (u32)(idx & (N - 1));
         u32* Dp = D + pc * J * N + n;
-        mbar_wait(&full[st], (i / kRtStages) & 1);
+        mbar_wait_sleep(&full[st], (i / kRtStages) & 1);
         u32 w[JM];
 #pragma unroll
         for (int j = 0; j < JM; ++j) w[j] = j < (int)J ? ring[st][j][tid] : 0u;
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
                              smem_u32(&mbar))
                          : "memory");
         }
-        mbar_wait(&mbar, phase);
+        mbar_wait_sleep(&mbar, phase);
         phase ^= 1u;
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         u32 C[17];  // fraction / gamma columns F0 .. NC-1
@@ -572,13 +576,15 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
                     for (int kk = 0; kk < 4; ++kk) {
                         const int k = k0 + kk;
                         if (k < RPT::MMAX && k < (int)Mm) {
-                            const uint4 q = RP.kq[k];
+                            // S + gamma (-I_A) 2^32 + (rho + 2^36) 2^32 - 2^36 2^32 < 2^61, one Montgomery
+                            // reduction: < 2^29 + 2^30 < 2 a_k
+                            const u32 a = RP.kq[k].x;
                             const u32 p01 = Rc[4 * kk] + (Rc[4 * kk + 1] << 8), p23 = Rc[4 * kk + 2] + (Rc[4 * kk + 3] << 8);
-                            const u64 S = (u64)p01 + ((u64)p23 << 16);
-                            const u64 Xv = (u64)gamma * q.z + S + RP.krm[k];
-                            const u32 x = red32(mont_red64(Xv, q.x, q.y), q.x);
-                            const u32 y = red32(red32(rlo + rhi * q.w, 2 * q.x), q.x);
-                            Dp[(size_t)k * N] = red32(x + y, q.x);
+                            u64 X = (u64)p01 + ((u64)p23 << 16) + RP.krm[k];
+                            X += (u64)gamma * RP.kq[k].z;
+                            X += (u64)rlo * RP.kc0[k];
+                            X += (u64)rhi * RP.kc30[k];
+                            Dp[(size_t)k * N] = red32(mont_red64(X, a, RP.kq[k].y), a);
                         }
                     }
                 }
