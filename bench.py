@@ -93,6 +93,19 @@ def rooflines(kstats, cfg, info, hbm, hbm_kind):
             r = {"bound": "imad", "achieved": ach, "peak": ip, "unit": "G IMAD-slots/s", "frac": ach / ip,
                  "peak_kind": ip_kind, "work_per_launch": f"{units / cnt:.0f} polynomials x {N // 2 * int(math.log2(N))} "
                  "butterflies x 4 IMAD slots"}
+        elif name == "k_ntt_mac":
+            # fused forward NTT of the selection planes + payload MAC: IMAD-bound on the transform;
+            # the HBM view counts the selection + payload words it streams (Z and DB planes)
+            polys = units / cnt
+            bfly = polys * (N // 2) * int(math.log2(N))
+            ach = bfly * 4 / per_launch_s / 1e9
+            mac_bytes = polys * N * 4 * (1 + cfg.s)
+            r = {"bound": "imad", "achieved": ach, "peak": ip, "unit": "G IMAD-slots/s", "frac": ach / ip,
+                 "peak_kind": ip_kind, "work_per_launch": f"{polys:.0f} polynomials x {N // 2 * int(math.log2(N))} "
+                 "butterflies x 4 IMAD slots (+ pointwise MAC)",
+                 "hbm_view": {"achieved": mac_bytes / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s",
+                              "frac": mac_bytes / per_launch_s / 1e9 / hbm,
+                              "bytes_per_launch": mac_bytes, "what": "selection + payload words streamed"}}
         elif name.startswith("k_round"):
             byt = units / cnt * (info.J + info.Mm) * 4
             ach = byt / per_launch_s / 1e9

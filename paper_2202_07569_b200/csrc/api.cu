@@ -607,6 +607,8 @@ struct Reg32 {
 #define NM(NC, S, A) CK(cudaFuncSetAttribute(k_ntt_mac<LOGN, NC, S, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NttMac<LOGN, S, A>::SMEM));
         NM(2, 1, false) NM(3, 1, false) NM(2, 1, true) NM(3, 1, true) NM(2, 2, true) NM(3, 2, true)
 #undef NM
+        CK(cudaFuncSetAttribute(k_ntt_mac_tma<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * R::SMEM)));
+        CK(cudaFuncSetAttribute(k_ntt_mac_tma<LOGN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * R::SMEM)));
     }
     /// fused selection NTT + payload MAC over the R rows of a tile (Z: coefficient-domain
     /// MAC-basis selection planes, Z + ((r * nc + comp) * zs + k) * N)
@@ -621,6 +623,11 @@ struct Reg32 {
         c.next_units = (double)Rt * nc * Mm;  // polynomials transformed (+ payload words streamed)
         const size_t grid = (size_t)ck * per;
 #define NMC(NC, S, A) launch_named(c, "k_ntt_mac", k_ntt_mac<LOGN, NC, S, A>, grid, R::T, NttMac<LOGN, S, A>::SMEM, Z, zs, dbt, Rt, chunk, c.T, acc)
+        if (c.fuse_mac == 3 && c.s == 1) {
+            if (nc == 3) launch_named(c, "k_ntt_mac", k_ntt_mac_tma<LOGN, 3>, grid, R::T, 3 * R::SMEM, Z, zs, dbt, Rt, chunk, c.T, acc);
+            else launch_named(c, "k_ntt_mac", k_ntt_mac_tma<LOGN, 2>, grid, R::T, 3 * R::SMEM, Z, zs, dbt, Rt, chunk, c.T, acc);
+            return;
+        }
         const bool accr = c.fuse_mac == 2 && c.s == 1;
         if (nc == 3) {
             if (c.s == 1) { if (accr) NMC(3, 1, false); else NMC(3, 1, true); }

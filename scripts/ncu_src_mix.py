@@ -2,7 +2,8 @@
 export: executed warp instructions and stall samples per opcode.
 usage: python scripts/ncu_src_mix.py gpurun_out/src_<kernel>.csv.gz"""
 import csv, gzip, io, sys, collections
-rows = list(csv.reader(io.TextIOWrapper(gzip.open(sys.argv[1]))))
+fh = io.TextIOWrapper(gzip.open(sys.argv[1])) if sys.argv[1].endswith('.gz') else open(sys.argv[1])
+rows = list(csv.reader(fh))
 hdr = rows[1]
 data = []
 for r in rows[2:]:

@@ -46,9 +46,15 @@ for name, r in first.items():
     elif name == "k_ntt32r_sel3":
         key, units = name, grid
     elif name.startswith("k_round") and P:
-        key, units = name, P * 3 * cfg.N
+        key, units = "k_round_tc", P * 3 * cfg.N  # k_round_tma reports under the k_round_tc launch name
     elif name.startswith("k_mac2") and P:
         key, units = "k_mac", P * (cfg.s + 3) * Mm * cfg.N * 4
+    elif name.startswith("k_ntt_mac"):
+        # units = selection polynomials transformed (rows x components x MAC primes); the grid
+        # covers chunks of rows, so take the tile's P from the tensor launch
+        if not P:
+            continue
+        key, units = "k_ntt_mac", P * 3 * Mm
     else:
         continue
     res[key] = {"dram_bytes_per_launch": dram, "units_per_launch": units, "dram_bytes_per_unit": dram / units,
