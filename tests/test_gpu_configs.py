@@ -88,3 +88,25 @@ def test_payload_mac_kernels_agree_under_repetition(gpu, monkeypatch):
         parts[mac] = runs
     for r in parts["tma"]:
         assert np.array_equal(r, parts["v2"][0])
+
+
+@pytest.mark.parametrize("env", [
+    {"CWGPU_FUSE_MAC": "0", "CWGPU_ROUND_TMA": "0"},  # sel NTT + separate MAC kernels, k_round_tc
+    {},                                                # default: k_tensor_intt_r, k_round_tma, k_ntt_mac
+    {"CWGPU_FUSE_MAC": "2"},                           # k_ntt_mac with register accumulators
+    {"CWGPU_FUSE_MAC": "3"},                           # k_ntt_mac_tma (bulk-copied row planes)
+    {"CWGPU_FUSE_TIR": "1"},                           # k_tir: tensor + INTT + rounding over a J-CTA cluster
+    {"CWGPU_FUSE_TIR": "1", "CWGPU_FUSE_MAC": "0"},    # k_tir output through the unfused NTT + MAC
+    {"CWGPU_FORCE_EXACT": "1"},                        # every rounding through round_exact (k_round_tma)
+    {"CWGPU_FORCE_EXACT": "1", "CWGPU_FUSE_TIR": "1"},  # ... inside the cluster kernel
+], ids=["unfused", "default", "mac-regs", "mac-tma", "tir", "tir-unfused-mac", "exact", "exact-tir"])
+def test_answer_path_variants_match_reference(gpu, reflib, monkeypatch, env):
+    """Every kernel variant of the C4 answer path (tensor/rounding/NTT/MAC fusions, TMA feeds,
+    the exact multiword rounding inside each engine) against the reference at full C4 parameters,
+    over ragged 16-row tiles alternating between the two tile streams."""
+    from paper_2202_07569_b200 import configs
+
+    monkeypatch.setenv("CWGPU_TILE_ROWS", "16")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _run(reflib, configs.config("C4"), 40)
