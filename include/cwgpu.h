@@ -55,7 +55,7 @@ typedef struct cwg_timings {
     double finish_ms;  /* accumulator reduce, INTT, basis conversion, relinearisation */
     double d2h_ms;
     uint64_t kernel_launches;
-    uint64_t exact_fallbacks; /* coefficients decided by the multiword slow path */
+    uint64_t exact_fallbacks; /* coefficients decided by the multiword slow path (this answer) */
 } cwg_timings;
 
 const char* cwg_last_error(void);

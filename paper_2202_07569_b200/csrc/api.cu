@@ -1166,6 +1166,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     if (op == CWG_OP_ARITH && c.k < 2) throw std::invalid_argument("arithmetic operator needs k >= 2");
     const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J, Mm = c.ab.Mm;
     const size_t LN = (size_t)L * N;
+    CK(cudaMemsetAsync(c.d_fb, 0, 8, c.st));  // exact-path counter: per answer (cwg_timings.exact_fallbacks)
     u64* dq = c.query.get<u64>((size_t)h * 2 * LN);
     CK(cudaMemcpyAsync(dq, query, (size_t)h * 2 * LN * 8, cudaMemcpyDefault, c.st));  // host or device
     tm.mark(TM_H2D);
