@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -27,6 +28,7 @@
 #include "mac.cuh"
 #include "ntt_mac.cuh"
 #include "tir.cuh"
+#include "ks32.cuh"
 
 namespace cwgpu {
 
@@ -95,7 +97,12 @@ struct Ctx {
     // fused tensor + INTT + tensor-core rounding over a J-CTA cluster (k_tir; env CWGPU_FUSE_TIR=0
     // off); -1 = not yet probed, 0 = unavailable for these parameters, 1 = on
     int fuse_tir = -1;
-    bool round_tma = true;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
+    bool round_tma = true;
+    // key switching through the 30-bit aux primes (ks32.cuh; env CWGPU_KS32=0: 64-bit NTT path)
+    bool ks32 = true;
+    bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
+    KsCrt ksC_r{}, ksC_g{};            // K' = 0: this key type keeps the 64-bit path
+    DevBuf relinA, galoisA, ksdig, ksmac;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
     u32 zs_last = 0;        // MAC-basis plane stride of the last mul_prepared output (J or Mm)
     unsigned next_cluster = 0;  // cluster size of the next launch (launch_named)
     // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
@@ -578,6 +585,7 @@ static void ensure_aux(Ctx& c, u64 n_total) {
     if (same) return;
     c.ab = nb;
     build_tables(c);
+    c.ksA_ok = false;
 }
 
 // ------------------------------------------------------------------ NTT launchers
@@ -731,9 +739,100 @@ static void ntt32(Ctx& c, u32* base, u32 npolys, u32 gs, u32 stride, u32 off, bo
 // ------------------------------------------------------------------ key switching
 /// ks[b] (2 comps, coefficient form) = key_switch(poly_b) for B polys at polys + b*stride
 /// through automorphism ginv (0 = none) (bfv.cpp:343-372).
+/// Garner constants of the aux primes that hold sum_d digit_d * key_d exactly:
+/// |value| <= D N (2^bits - 1)(q_max - 1) (bits = 0: RNS digits < q_max), prod a_j > 2^2 |value|.
+static KsCrt make_ks_crt(const Ctx& c, u32 bits, u32 D) {
+    KsCrt C{};
+    double qb = 0;
+    for (u64 q : c.cp.q) qb = std::max(qb, std::log2((double)q));
+    const double need = std::log2((double)D) + c.cp.logN + (bits ? bits : qb) + qb + 2.0;
+    double have = 0;
+    u32 K = 0;
+    while (have < need) {
+        if (K >= (u32)kMaxKs || K >= c.ab.J) return KsCrt{};  // K = 0: keep the 64-bit path
+        C.a[K] = (u32)c.ab.a[K];
+        have += std::log2((double)C.a[K]);
+        ++K;
+    }
+    C.K = K;
+    for (u32 j = 0; j < K; ++j) {
+        C.half[j] = (C.a[j] - 1) / 2;
+        for (u32 k = 0; k < j; ++k) C.cinv[j][k] = (u32)invmod64(C.a[k] % C.a[j], C.a[j]);
+    }
+    for (u32 i = 0; i < c.cp.L; ++i) {
+        const u64 q = c.cp.q[i];
+        u64 p = 1 % q;
+        for (u32 j = 0; j < K; ++j) {
+            C.pmod[i][j] = p;
+            p = (u64)(((u128)p * C.a[j]) % q);
+        }
+        C.amod[i] = p;
+    }
+    return C;
+}
+
+/// Transform one key [D][2][L][N] (NTT form mod q_i, reference layout) into the key-switch aux
+/// basis: [D][2][L][K'][N] u32, NTT form mod a_j.
+static void key_to_aux(Ctx& c, const u64* key, u32 D, const KsCrt& C, u32* out) {
+    const u32 N = c.cp.N, L = c.cp.L;
+    const size_t np = (size_t)D * 2 * L;
+    u64* tmp = c.dntt.get<u64>(np * N);
+    CK(cudaMemcpyAsync(tmp, key, np * N * 8, cudaMemcpyDeviceToDevice, c.st));
+    ntt64(c, tmp, (u32)np, true);  // coefficient form in [0, q_i)
+    launch(c, k_to_ks_aux, blocks(np * N, 256), 256, 0, (const u64*)tmp, np, N, C, out);
+    ntt32(c, out, (u32)(np * C.K), C.K, C.K, 0, false, 0);
+}
+
+/// relinA / galoisA for the uploaded keys (once per key upload or aux-basis change).
+static bool ks32_ready(Ctx& c) {
+    if (!c.ks32 || !c.have_keys) return false;
+    if (c.ksA_ok) return true;
+    const u32 N = c.cp.N, L = c.cp.L;
+    c.ksC_r = make_ks_crt(c, c.cp.relin_bits, c.cp.Dr);
+    c.ksC_g = make_ks_crt(c, c.cp.galois_bits, c.cp.Dg);
+    if (c.ksC_r.K) {
+        const size_t w = (size_t)c.cp.Dr * 2 * L * c.ksC_r.K * N;
+        key_to_aux(c, c.relin.ptr<u64>(), c.cp.Dr, c.ksC_r, c.relinA.get<u32>(w));
+    }
+    if (c.ksC_g.K && !c.galois_g.empty()) {
+        const size_t w = (size_t)c.cp.Dg * 2 * L * c.ksC_g.K * N, gw = (size_t)c.cp.Dg * 2 * L * N;
+        u32* ga = c.galoisA.get<u32>(w * c.galois_g.size());
+        for (size_t a = 0; a < c.galois_g.size(); ++a)
+            key_to_aux(c, c.galois.ptr<u64>() + a * gw, c.cp.Dg, c.ksC_g, ga + a * w);
+    }
+    c.ksA_ok = true;
+    return true;
+}
+
 static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B, const u64* key, u32 bits,
                        u32 D, u64* ks) {
     const u32 N = c.cp.N, L = c.cp.L;
+    if (ks32_ready(c)) {
+        const bool rel = key == c.relin.ptr<u64>();
+        const KsCrt& C = rel ? c.ksC_r : c.ksC_g;
+        if (C.K) {
+            const u32 K = C.K;
+            const u32* kA = nullptr;
+            if (rel) {
+                kA = c.relinA.ptr<u32>();
+            } else {
+                const size_t gw = (size_t)D * 2 * L * N;
+                const size_t a = (size_t)(key - c.galois.ptr<u64>()) / gw;
+                kA = c.galoisA.ptr<u32>() + a * (size_t)D * 2 * L * K * N;
+            }
+            u64* dig = c.digits.get<u64>((size_t)B * D * N);
+            u32* dA = c.ksdig.get<u32>((size_t)B * D * K * N);
+            u32* mA = c.ksmac.get<u32>((size_t)B * 2 * L * K * N);
+            launch(c, k_decompose, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv, B, bits, D, c.T, dig);
+            launch(c, k_to_ks_aux, blocks((size_t)B * D * N, 256), 256, 0, (const u64*)dig, (size_t)B * D, N, C, dA);
+            ntt32(c, dA, B * D * K, K, K, 0, false, 0);
+            launch(c, k_ks_mac32, blocks((size_t)B * 2 * L * K * N, 256), 256, 0, (const u32*)dA, kA, B, D, L, N, C,
+                   (const u64*)c.T.abar, mA);
+            ntt32(c, mA, B * 2 * L * K, K, K, 0, true, 0);
+            launch(c, k_ks_crt, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u32*)mA, B, L, N, C, c.T, ks);
+            return;
+        }
+    }
     u64* dig = c.digits.get<u64>((size_t)B * D * N);
     u64* dn = c.dntt.get<u64>((size_t)B * D * L * N);
     launch(c, k_decompose, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv, B, bits, D, c.T, dig);
@@ -1153,6 +1252,7 @@ static void upload_keys(Ctx& c, const u64* relin, u32 n_galois, const u64* gg, c
         CK(cudaMemcpyAsync(c.galois.get<u64>(gw * n_galois), galois, gw * n_galois * 8, cudaMemcpyDefault, c.st));
     c.galois_g.assign(gg, gg + n_galois);
     c.have_keys = true;
+    c.ksA_ok = false;
 }
 
 /// expand + select + MAC; leaves the reduced partial accumulators [s][3][Mm][N] u64
@@ -1424,6 +1524,7 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_FUSE_MAC")) c.fuse_mac = std::atoi(e);
         if (const char* e = std::getenv("CWGPU_ROUND_TMA")) c.round_tma = std::atoi(e) != 0;
+        if (const char* e = std::getenv("CWGPU_KS32")) c.ks32 = std::atoi(e) != 0;
         c.dcur = &c.Dbuf;
         for (int i = 0; i < Ctx::kMaxStreams; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));
         for (int i = 0; i <= Ctx::kMaxStreams; ++i) CK(cudaEventCreateWithFlags(&c.tev[i], cudaEventDisableTiming));
@@ -1440,7 +1541,8 @@ void cwg_destroy(cwg_ctx* h) {
     cudaStreamSynchronize(c.st);
     for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.prep_s, &c.Dmore[0], &c.Dmore[1], &c.Dmore[2], &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
                       &c.digits, &c.dntt, &c.ks, &c.prep, &c.Dbuf, &c.chain3, &c.node2, &c.acc_lo, &c.acc_hi,
-                      &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp})
+                      &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp, &c.rtc_B, &c.relinA, &c.galoisA,
+                      &c.ksdig, &c.ksmac})
         b->release();
     if (c.d_fb) cudaFree(c.d_fb);
     for (int i = 0; i < Ctx::kMaxStreams; ++i) if (c.tst[i]) cudaStreamDestroy(c.tst[i]);

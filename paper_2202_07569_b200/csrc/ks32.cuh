@@ -1,0 +1,100 @@
+// Key switching through the 30-bit aux primes (bfv.cpp:343-372, key_switch).
+//
+// The reference multiplies the NTT of every decomposition digit with the key modulo each chain
+// prime q_i (64-bit NTTs: D L forward + 2 L inverse per switch).  The result is the ring element
+// sum_d digit_d * key_{d,c} mod q_i, i.e. the exact integer negacyclic convolution reduced mod
+// q_i; its integer value is bounded by D N 2^bits q_i (digits in [0, 2^bits), key coefficients in
+// [0, q_i)), so it is recovered exactly from K' aux primes with prod a_j > 2 D N 2^bits q_max and
+// reduced mod q_i afterwards.  Per switch that is D K' forward and 2 L K' inverse register NTTs on
+// 32-bit words (C4: 42 + 30, each ~4x cheaper than a 64-bit NTT), with the key transformed once
+// per key upload (INTT mod q_i, reduce mod a_j, NTT mod a_j).
+#pragma once
+#include "devtab.h"
+#include "modarith.cuh"
+
+namespace cwgpu {
+
+constexpr int kMaxKs = 5;  // aux primes for the key-switch convolution
+
+/// Garner / mixed-radix constants of the K' key-switch primes, and their images mod each q_i.
+struct KsCrt {
+    u32 K;
+    u32 a[kMaxKs];
+    u32 half[kMaxKs];             // (a_j - 1) / 2: mixed-radix digits of floor(A'/2)
+    u32 cinv[kMaxKs][kMaxKs];     // a_k^-1 mod a_j (k < j)
+    u64 pmod[kMaxL][kMaxKs];      // prod_{k<j} a_k mod q_i
+    u64 amod[kMaxL];              // A' mod q_i
+};
+
+/// u64 values (< 2^64) of npolys planes [npolys][N] -> u32 residues [npolys][K'][N] mod a_j.
+__global__ void k_to_ks_aux(const u64* __restrict__ src, size_t npolys, u32 N, const __grid_constant__ KsCrt C,
+                            u32* __restrict__ dst) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= npolys * N) return;
+    const size_t p = idx / N;
+    const u32 n = (u32)(idx % N);
+    const u64 v = src[idx];
+    for (u32 j = 0; j < C.K; ++j) dst[(p * C.K + j) * N + n] = (u32)(v % C.a[j]);
+}
+
+/// out[b][c][i][j][n] = sum_d dig[b][d][j][n] key[d][c][i][j][n] mod a_j (NTT domain, any order
+/// shared by both operands).  Products < 2^60; reduced every 8 terms.
+__global__ void k_ks_mac32(const u32* __restrict__ dig, const u32* __restrict__ key, u32 B, u32 D, u32 L, u32 N,
+                           const __grid_constant__ KsCrt C, const u64* __restrict__ abar, u32* __restrict__ out) {
+    const u32 K = C.K;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t per_b = (size_t)2 * L * K * N;
+    if (idx >= (size_t)B * per_b) return;
+    const u32 b = (u32)(idx / per_b);
+    const size_t r = idx % per_b;  // ((c L + i) K + j) N + n
+    const u32 n = (u32)(r % N);
+    const u32 j = (u32)((r / N) % K);
+    const size_t cij = r / N;      // (c L + i) K + j
+    const u32 a = C.a[j];
+    const u64 mu = abar[j];
+    const u32* dp = dig + ((size_t)b * D * K + j) * N + n;
+    const u32* kp = key + cij * N + n;
+    const size_t dstride = (size_t)K * N, kstride = (size_t)2 * L * K * N;
+    u64 acc = 0;
+    for (u32 d = 0; d < D; ++d) {
+        acc += (u64)dp[(size_t)d * dstride] * __ldg(kp + (size_t)d * kstride);
+        if ((d & 7) == 7) acc = bar64(acc, a, mu);
+    }
+    out[idx] = bar64(acc, a, mu);
+}
+
+/// ks[b][c][i][n] = (centred CRT of the K' residues x_j) mod q_i.  x: [B][2][L][K'][N] in [0, a_j).
+__global__ void k_ks_crt(const u32* __restrict__ x, u32 B, u32 L, u32 N, const __grid_constant__ KsCrt C, DevTab T,
+                         u64* __restrict__ ks) {
+    const u32 K = C.K;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)B * 2 * L * N) return;
+    const size_t bci = idx / N;  // (b 2 + c) L + i
+    const u32 n = (u32)(idx % N);
+    const u32 i = (u32)(bci % L);
+    const u32* xp = x + bci * K * N + n;
+    u32 y[kMaxKs];
+    // Garner: y_j = ((x_j - y_0) c_0j - y_1) c_1j ... mod a_j
+#pragma unroll
+    for (int jj = 0; jj < kMaxKs; ++jj) {
+        if (jj >= (int)K) break;
+        const u32 a = C.a[jj];
+        u64 t = xp[(size_t)jj * N];
+        for (int k = 0; k < jj; ++k) {
+            t = (t + a - (y[k] % a)) % a;
+            t = (t * C.cinv[jj][k]) % a;
+        }
+        y[jj] = (u32)t;
+    }
+    // centred: v > (A'-1)/2 <=> mixed-radix digits (top first) exceed the half digits
+    int cmp = 0;
+    for (int jj = (int)K - 1; jj >= 0 && cmp == 0; --jj) cmp = y[jj] > C.half[jj] ? 1 : (y[jj] < C.half[jj] ? -1 : 0);
+    const u64 q = T.q[i];
+    u64 hi = 0, lo = 0;
+    for (u32 jj = 0; jj < K; ++jj) mac128(hi, lo, (u64)y[jj], C.pmod[i][jj]);
+    u64 v = reduce128(hi, lo, q, T.q_mu96[i]);
+    if (cmp > 0) v = v >= C.amod[i] ? v - C.amod[i] : v + q - C.amod[i];
+    ks[idx] = v;
+}
+
+}  // namespace cwgpu
