@@ -757,7 +757,10 @@ static KsCrt make_ks_crt(const Ctx& c, u32 bits, u32 D) {
     C.K = K;
     for (u32 j = 0; j < K; ++j) {
         C.half[j] = (C.a[j] - 1) / 2;
-        for (u32 k = 0; k < j; ++k) C.cinv[j][k] = (u32)invmod64(C.a[k] % C.a[j], C.a[j]);
+        for (u32 k = 0; k < j; ++k) {
+            C.cinv[j][k] = (u32)invmod64(C.a[k] % C.a[j], C.a[j]);
+            C.cinv_s[j][k] = (u32)(((u64)C.cinv[j][k] << 32) / C.a[j]);
+        }
     }
     for (u32 i = 0; i < c.cp.L; ++i) {
         const u64 q = c.cp.q[i];
@@ -820,14 +823,19 @@ static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
                 const size_t a = (size_t)(key - c.galois.ptr<u64>()) / gw;
                 kA = c.galoisA.ptr<u32>() + a * (size_t)D * 2 * L * K * N;
             }
-            u64* dig = c.digits.get<u64>((size_t)B * D * N);
             u32* dA = c.ksdig.get<u32>((size_t)B * D * K * N);
             u32* mA = c.ksmac.get<u32>((size_t)B * 2 * L * K * N);
-            launch(c, k_decompose, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv, B, bits, D, c.T, dig);
-            launch(c, k_to_ks_aux, blocks((size_t)B * D * N, 256), 256, 0, (const u64*)dig, (size_t)B * D, N, C, dA);
+            launch_named(c, "k_decompose", k_decompose_t<true>, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv,
+                         B, bits, D, c.T, (u64*)nullptr, dA, K);
             ntt32(c, dA, B * D * K, K, K, 0, false, 0);
-            launch(c, k_ks_mac32, blocks((size_t)B * 2 * L * K * N, 256), 256, 0, (const u32*)dA, kA, B, D, L, N, C,
-                   (const u64*)c.T.abar, mA);
+            // shared-load variant once the level is wide enough to fill the GPU (B >= 64 rows of
+            // K N threads / 2); narrow levels keep one output per thread (latency-bound otherwise)
+            if (D <= (u32)kKsDmax && B >= 64)
+                launch_named(c, "k_ks_mac32", k_ks_mac32x, blocks((size_t)((B + 1) / 2) * K * N, 128), 128, 0,
+                             (const u32*)dA, kA, B, D, L, N, C, (const u64*)c.T.abar, mA);
+            else
+                launch(c, k_ks_mac32, blocks((size_t)B * 2 * L * K * N, 256), 256, 0, (const u32*)dA, kA, B, D, L, N, C,
+                       (const u64*)c.T.abar, mA);
             ntt32(c, mA, B * 2 * L * K, K, K, 0, true, 0);
             launch(c, k_ks_crt, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u32*)mA, B, L, N, C, c.T, ks);
             return;
@@ -835,7 +843,8 @@ static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
     }
     u64* dig = c.digits.get<u64>((size_t)B * D * N);
     u64* dn = c.dntt.get<u64>((size_t)B * D * L * N);
-    launch(c, k_decompose, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv, B, bits, D, c.T, dig);
+    launch_named(c, "k_decompose", k_decompose_t<false>, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv, B, bits,
+                 D, c.T, dig, (u32*)nullptr, 0u);
     launch_named(c, "k_ntt64_digits", k_ntt64<false, true>, (size_t)B * D * L, ntt_block(N), N * 8, dn, (const u64*)dig, c.T);
     launch(c, k_ks_mac, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u64*)dn, key, B, D, c.T, ks);
     ntt64(c, ks, B * 2 * L, true);

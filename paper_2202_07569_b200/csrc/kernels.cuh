@@ -266,8 +266,11 @@ __device__ __forceinline__ u32 crt_round(const u64* y, u32 ip, u64 frac, const D
 /// Digit decomposition (bfv.cpp:316-339) of B polys (each L x N at polys + b*stride),
 /// optionally through the automorphism with inverse exponent ginv (0 = identity).
 /// digits: [B][D][N].
-__global__ void k_decompose(const u64* __restrict__ polys, size_t stride, u64 ginv, u32 B, u32 bits,
-                            u32 D, DevTab T, u64* __restrict__ digits) {
+/// AUX (key switching through the aux primes, ks32.cuh): digit d is written as its residues
+/// mod the first K aux primes, u32 [B][D][K][N] at aux_out (digits < 2^29 need no reduction).
+template <bool AUX = false>
+__global__ void k_decompose_t(const u64* __restrict__ polys, size_t stride, u64 ginv, u32 B, u32 bits,
+                              u32 D, DevTab T, u64* __restrict__ digits, u32* __restrict__ aux_out, u32 K) {
     const u32 N = T.N;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)B * N) return;
@@ -287,8 +290,16 @@ __global__ void k_decompose(const u64* __restrict__ polys, size_t stride, u64 gi
         res[i] = v;
     }
     u64* out = digits + (size_t)b * D * N + n;
+    auto put = [&](u32 d, u64 v) {
+        if constexpr (AUX) {
+            u32* o = aux_out + ((size_t)b * D + d) * K * N + n;
+            for (u32 j = 0; j < K; ++j) o[(size_t)j * N] = (bits && bits <= 29) ? (u32)v : (u32)(v % T.a[j]);
+        } else {
+            out[(size_t)d * N] = v;
+        }
+    };
     if (bits == 0) {  // one RNS digit per chain prime (bfv.cpp:320-323)
-        for (u32 d = 0; d < D; ++d) out[(size_t)d * N] = res[d];
+        for (u32 d = 0; d < D; ++d) put(d, res[d]);
         return;
     }
     u64 y[kMaxL];
@@ -311,9 +322,10 @@ __global__ void k_decompose(const u64* __restrict__ polys, size_t stride, u64 gi
         const u64 lo64 = ((u64)l1 << 32) | l0;
         v = lo64 >> off;
         if (off) v |= ((u64)l2 << (64 - off));
-        out[(size_t)d * N] = v & mask;
+        put(d, v & mask);
     }
 }
+
 
 /// ks[b][k][i][n] = sum_d dntt[b][d][i][n] * key[d][k][i][n] mod q_i (key_switch MAC).
 __global__ void k_ks_mac(const u64* __restrict__ dntt, const u64* __restrict__ key, u32 B, u32 D, DevTab T,

@@ -22,6 +22,7 @@ struct KsCrt {
     u32 a[kMaxKs];
     u32 half[kMaxKs];             // (a_j - 1) / 2: mixed-radix digits of floor(A'/2)
     u32 cinv[kMaxKs][kMaxKs];     // a_k^-1 mod a_j (k < j)
+    u32 cinv_s[kMaxKs][kMaxKs];   // Shoup companions floor(cinv 2^32 / a_j)
     u64 pmod[kMaxL][kMaxKs];      // prod_{k<j} a_k mod q_i
     u64 amod[kMaxL];              // A' mod q_i
 };
@@ -63,6 +64,49 @@ __global__ void k_ks_mac32(const u32* __restrict__ dig, const u32* __restrict__ 
     out[idx] = bar64(acc, a, mu);
 }
 
+/// k_ks_mac32 with the loads shared: thread (b pair, j, n) keeps both rows' D digit residues in
+/// registers and loops over the 2 L (component, chain prime) outputs, each key word feeding two
+/// products (C4: 8.4 loads per output instead of 28).
+constexpr int kKsDmax = 16;
+__global__ void __launch_bounds__(128) k_ks_mac32x(const u32* __restrict__ dig, const u32* __restrict__ key, u32 B, u32 D,
+                                                   u32 L, u32 N, const __grid_constant__ KsCrt C, const u64* __restrict__ abar,
+                                                   u32* __restrict__ out) {
+    const u32 K = C.K;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t per = (size_t)K * N;
+    if (idx >= (size_t)((B + 1) / 2) * per) return;
+    const u32 b0 = (u32)(idx / per) * 2;
+    const u32 j = (u32)((idx / N) % K), n = (u32)(idx % N);
+    const bool two = b0 + 1 < B;
+    const u32 a = C.a[j];
+    const u64 mu = abar[j];
+    u32 d0[kKsDmax], d1[kKsDmax];
+    const u32* dp0 = dig + ((size_t)b0 * D * K + j) * N + n;
+#pragma unroll
+    for (int d = 0; d < kKsDmax; ++d) {
+        d0[d] = d < (int)D ? dp0[(size_t)d * K * N] : 0u;
+        d1[d] = (two && d < (int)D) ? dp0[((size_t)D + d) * K * N] : 0u;
+    }
+    const size_t kstride = (size_t)2 * L * K * N;
+    for (u32 ci = 0; ci < 2 * L; ++ci) {
+        const u32* kp = key + ((size_t)ci * K + j) * N + n;
+        u64 s0 = 0, s1 = 0;
+#pragma unroll
+        for (int d = 0; d < kKsDmax; ++d) {
+            if (d >= (int)D) break;
+            const u64 kv = __ldg(kp + (size_t)d * kstride);
+            s0 += (u64)d0[d] * kv;
+            s1 += (u64)d1[d] * kv;
+            if ((d & 7) == 7) {
+                s0 = bar64(s0, a, mu);
+                s1 = bar64(s1, a, mu);
+            }
+        }
+        out[(((size_t)b0 * 2 * L + ci) * K + j) * N + n] = bar64(s0, a, mu);
+        if (two) out[((((size_t)b0 + 1) * 2 * L + ci) * K + j) * N + n] = bar64(s1, a, mu);
+    }
+}
+
 /// ks[b][c][i][n] = (centred CRT of the K' residues x_j) mod q_i.  x: [B][2][L][K'][N] in [0, a_j).
 __global__ void k_ks_crt(const u32* __restrict__ x, u32 B, u32 L, u32 N, const __grid_constant__ KsCrt C, DevTab T,
                          u64* __restrict__ ks) {
@@ -79,12 +123,15 @@ __global__ void k_ks_crt(const u32* __restrict__ x, u32 B, u32 L, u32 N, const _
     for (int jj = 0; jj < kMaxKs; ++jj) {
         if (jj >= (int)K) break;
         const u32 a = C.a[jj];
-        u64 t = xp[(size_t)jj * N];
-        for (int k = 0; k < jj; ++k) {
-            t = (t + a - (y[k] % a)) % a;
-            t = (t * C.cinv[jj][k]) % a;
+        u32 t = xp[(size_t)jj * N];
+#pragma unroll
+        for (int k = 0; k < kMaxKs - 1; ++k) {
+            if (k >= jj) break;
+            const u32 yk = red32(y[k], a);                 // y_k < a_k < 2 a_j
+            t = red32(t + a - yk, a);                      // (t - y_k) mod a_j
+            t = red32(shoup32(t, C.cinv[jj][k], C.cinv_s[jj][k], a), a);
         }
-        y[jj] = (u32)t;
+        y[jj] = t;
     }
     // centred: v > (A'-1)/2 <=> mixed-radix digits (top first) exceed the half digits
     int cmp = 0;
