@@ -329,15 +329,38 @@ def main():
                 ctypes.cast(hgal.data_ptr(), u64p))
     h_q = query.shape[0]
     partial = None
+    # N > 1: the expansion is sharded too when the query is one ciphertext -- rank r expands the
+    # subtree of leaves r, r+W, ... (cwg_expand_shard) and an all-gather hands every rank all
+    # entries, so the per-query fixed cost shrinks with W instead of being replicated
+    shard = world > 1 and h_q == 1 and (world & (world - 1)) == 0 and world <= (1 << cfg.c) \
+        and os.environ.get("CWGPU_SHARD_EXPAND", "1") != "0"
     if world > 1:
         partial = torch.zeros(ctx.partial_words(), dtype=torch.int64, device="cuda")
+    if shard:
+        ent_words = 2 * L * N
+        shard_local = torch.zeros(ctx.shard_entries(cfg.c, world) * ent_words, dtype=torch.int64, device="cuda")
+        shards_all = torch.zeros(world * shard_local.numel(), dtype=torch.int64, device="cuda")
+
+    def after_collective():
+        # the library runs on its own stream: order it after the collective on torch's stream
+        ext.wait_stream(torch.cuda.current_stream())
+
+    def step_partial(q_ptr, kp):
+        if shard:
+            ctx.expand_shard_ptr(q_ptr, cfg.c, world, rank, shard_local.data_ptr(), keys_ptrs=kp)
+            dist.all_gather_into_tensor(shards_all, shard_local)
+            after_collective()
+            ctx.answer_partial_shards_ptr(shards_all.data_ptr(), world, cfg.c, cfg.m, cfg.op, partial.data_ptr())
+        else:
+            ctx.answer_partial_ptr(q_ptr, h_q, cfg.c, cfg.m, cfg.op, partial.data_ptr(), keys_ptrs=kp)
+        dist.reduce(partial, dst=0)
+        after_collective()
 
     def step_value():
         if world == 1:
             ctx.answer_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, dout.data_ptr())
         else:
-            ctx.answer_partial_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, partial.data_ptr())
-            dist.reduce(partial, dst=0)
+            step_partial(dq.data_ptr(), (None, 0, None, None))
             if rank == 0:
                 ctx.finish(partial.data_ptr(), cfg.op, out=dout.data_ptr())
 
@@ -345,8 +368,7 @@ def main():
         if world == 1:
             ctx.answer_ptr(hq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, hout.data_ptr(), keys_ptrs=key_ptrs)
         else:
-            ctx.answer_partial_ptr(hq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, partial.data_ptr(), keys_ptrs=key_ptrs)
-            dist.reduce(partial, dst=0)
+            step_partial(hq.data_ptr(), key_ptrs)
             if rank == 0:
                 ctx.finish(partial.data_ptr(), cfg.op, out=hout.data_ptr())
 
@@ -424,7 +446,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded rows/keys/query)",
         "config": {"workload": workload_desc(cfg), "db_bytes": db_bytes, "rows_per_gpu": local_rows,
-                   "parallelism": f"row-shard x{world}", "l2": "no flush: 21.5 GB DB >> 126 MB L2"
+                   "parallelism": f"row-shard x{world}" + (" + expansion-shard (all-gather)" if shard else ""), "l2": "no flush: 21.5 GB DB >> 126 MB L2"
                    if cfg.name == "C4" else "inputs larger than L2" if db_bytes > 2e8 else "small (L2-resident)",
                    "aux_primes": info.J, "mac_primes": info.Mm},
         "answer_ms": ms,

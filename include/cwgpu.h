@@ -99,6 +99,18 @@ int cwg_answer_partial(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, c
                        uint32_t op, uint64_t* dev_partial, cwg_timings* t);
 int cwg_finish(cwg_ctx* ctx, const uint64_t* dev_partial_sum, uint32_t op, uint64_t* out, cwg_timings* t);
 
+/* Sharded expansion for the row-sharded form (one query ciphertext, h = 1; W a power of two
+ * <= 2^c): rank r expands the subtree of level-log2(W) node r, i.e. the global leaves
+ * r, r + W, r + 2W, ... (2^c / W of them), into out (device, [2^c / W][2][L][N]).  Gathering
+ * the W outputs rank-major (e.g. an all-gather) and passing them to cwg_answer_partial_shards
+ * replaces each rank's full expand_query (expansion.cpp:67-83) -- same entries, 1/W of the
+ * key switches below level log2(W). */
+int cwg_expand_shard(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+                     const uint64_t* galois, uint32_t c, const uint64_t* query, uint32_t world, uint32_t rank,
+                     uint64_t* out);
+int cwg_answer_partial_shards(cwg_ctx* ctx, const uint64_t* shards, uint32_t world, uint32_t c, uint32_t m,
+                              uint32_t op, uint64_t* dev_partial, cwg_timings* t);
+
 /* compute_selection_vector (pir.cpp:277-312) without a payload (config 2): sel is
  * [n_local][3][L][N]; comps[r] receives 2 or 3 (a 2-component row leaves slot 2 zero). */
 int cwg_select(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,

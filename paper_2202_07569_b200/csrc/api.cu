@@ -883,23 +883,20 @@ static const u64* galois_key(Ctx& c, u64 g) {
     throw he_err("missing Galois key for requested exponent");
 }
 
-/// expand_query (expansion.cpp:67-83): query [h][2][L][N] on device -> entries [h * 2^c].
-/// Returns a pointer to the final level buffer (first m entries are the result).
-static u64* expand(Ctx& c, const u64* dquery, u32 h, u32 comp, u32 m) {
+/// Expansion levels a_from .. a_to - 1 (expansion.cpp:67-83) of h independent trees whose
+/// level-a_from nodes are at cur ([h][2^0 nodes] when a_from is the tree's local root level):
+/// node b of the local numbering at level a has children b and b + 2^(a - a_from); the Galois
+/// exponent and the monomial shift are those of the global level a.  Returns the buffer holding
+/// the level-a_to nodes ([h][2^(a_to - a_from)]).
+static u64* expand_levels(Ctx& c, u64* cur, u64* nxt, u32 h, u32 a_from, u32 a_to) {
     const u32 N = c.cp.N, L = c.cp.L;
     const size_t per = 2 * (size_t)L * N;
-    if ((u64(1) << comp) > N) throw std::invalid_argument("compression factor exceeds log2(N)");
-    if ((size_t)h << comp < m) throw std::invalid_argument("packed query too short for code length");
-    const size_t full = (size_t)h << comp;
-    u64* cur = c.exA.get<u64>(full * per);
-    u64* nxt = c.exB.get<u64>(full * per);
-    CK(cudaMemcpyAsync(cur, dquery, (size_t)h * per * 8, cudaMemcpyDeviceToDevice, c.st));
     const size_t chunk = ks_chunk(c, c.cp.Dg);
-    for (u32 a = 0; a < comp; ++a) {
+    for (u32 a = a_from; a < a_to; ++a) {
         const u64 g = N / (u64(1) << a) + 1;
         const u64 ginv = inv_mod_2n(g, 2 * (u64)N);
         const u64* key = galois_key(c, g);
-        const u32 Bq = 1u << a;  // entries per query at this level
+        const u32 Bq = 1u << (a - a_from);  // nodes per tree at this level
         for (u32 qi = 0; qi < h; ++qi) {
             const u64* in = cur + (size_t)qi * Bq * per;
             u64* out = nxt + (size_t)qi * 2 * Bq * per;
@@ -916,6 +913,45 @@ static u64* expand(Ctx& c, const u64* dquery, u32 h, u32 comp, u32 m) {
         std::swap(cur, nxt);
     }
     return cur;
+}
+
+static void check_expand(const Ctx& c, u32 h, u32 comp, u32 m) {
+    if ((u64(1) << comp) > c.cp.N) throw std::invalid_argument("compression factor exceeds log2(N)");
+    if ((size_t)h << comp < m) throw std::invalid_argument("packed query too short for code length");
+}
+
+/// expand_query (expansion.cpp:67-83): query [h][2][L][N] on device -> entries [h * 2^c].
+/// Returns a pointer to the final level buffer (first m entries are the result).
+static u64* expand(Ctx& c, const u64* dquery, u32 h, u32 comp, u32 m) {
+    check_expand(c, h, comp, m);
+    const size_t per = 2 * (size_t)c.cp.L * c.cp.N;
+    const size_t full = (size_t)h << comp;
+    u64* cur = c.exA.get<u64>(full * per);
+    u64* nxt = c.exB.get<u64>(full * per);
+    CK(cudaMemcpyAsync(cur, dquery, (size_t)h * per * 8, cudaMemcpyDeviceToDevice, c.st));
+    return expand_levels(c, cur, nxt, h, 0, comp);
+}
+
+/// Row-sharded expansion (one query ciphertext): the leaves with e = rank (mod W) all descend
+/// from node `rank` of level s = log2 W, so a rank runs levels 0 .. s-1 (2^s - 1 switches, the
+/// narrow latency-bound top of the tree) and then only its own subtree: 2^(comp - s) leaves,
+/// local leaf u = global leaf rank + W u, written to out (device, [2^(comp-s)][2][L][N]).
+/// Gathering the W shards rank-major gives every rank all entries (k_unshard reorders them).
+static void expand_shard(Ctx& c, const u64* dquery, u32 comp, u32 W, u32 rank, u64* out) {
+    u32 s = 0;
+    while ((1u << s) < W) ++s;
+    if ((1u << s) != W || s > comp) throw std::invalid_argument("shard count must be a power of two <= 2^c");
+    if (rank >= W) throw std::invalid_argument("shard rank out of range");
+    const size_t per = 2 * (size_t)c.cp.L * c.cp.N;
+    const size_t full = (size_t)1 << comp;
+    u64* A = c.exA.get<u64>(full * per);
+    u64* Bb = c.exB.get<u64>(full * per);
+    CK(cudaMemcpyAsync(A, dquery, per * 8, cudaMemcpyDeviceToDevice, c.st));
+    u64* top = expand_levels(c, A, Bb, 1, 0, s);
+    u64* other = top == A ? Bb : A;
+    CK(cudaMemcpyAsync(other, top + (size_t)rank * per, per * 8, cudaMemcpyDeviceToDevice, c.st));
+    u64* leaves = expand_levels(c, other, top, 1, s, comp);
+    CK(cudaMemcpyAsync(out, leaves, (full / W) * per * 8, cudaMemcpyDefault, c.st));
 }
 
 // ------------------------------------------------------------------ per-row selection
@@ -1266,7 +1302,8 @@ static void upload_keys(Ctx& c, const u64* relin, u32 n_galois, const u64* gg, c
 
 /// expand + select + MAC; leaves the reduced partial accumulators [s][3][Mm][N] u64
 /// in dev_partial; returns the response component count (2 or 3).
-static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 op, u64* dev_partial, Timer& tm) {
+static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 op, u64* dev_partial, Timer& tm,
+                          const u64* shards = nullptr, u32 W = 0) {
     if (!c.db_loaded) throw state_err("no database loaded");
     if (m != c.m) throw std::invalid_argument("query code length does not match the database");  // pir.cpp:339-341
     if (c.s == 0) throw state_err("database has no payload (selection-only); use cwg_select");
@@ -1276,11 +1313,22 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J, Mm = c.ab.Mm;
     const size_t LN = (size_t)L * N;
     CK(cudaMemsetAsync(c.d_fb, 0, 8, c.st));  // exact-path counter: per answer (cwg_timings.exact_fallbacks)
-    u64* dq = c.query.get<u64>((size_t)h * 2 * LN);
-    CK(cudaMemcpyAsync(dq, query, (size_t)h * 2 * LN * 8, cudaMemcpyDefault, c.st));  // host or device
-    tm.mark(TM_H2D);
-    u64* entries = expand(c, dq, h, comp, m);
-    tm.mark(TM_EXPAND);
+    u64* entries = nullptr;
+    if (shards) {  // entries expanded by W ranks (expand_shard) and gathered rank-major
+        check_expand(c, 1, comp, m);
+        tm.mark(TM_H2D);
+        const size_t full = (size_t)1 << comp;
+        entries = c.exA.get<u64>(full * 2 * LN);
+        launch(c, k_unshard, blocks((size_t)m * 2 * LN, 256), 256, 0, shards, (u32)m, W, (u32)(full / W), 2 * LN,
+               entries);
+        tm.mark(TM_EXPAND);
+    } else {
+        u64* dq = c.query.get<u64>((size_t)h * 2 * LN);
+        CK(cudaMemcpyAsync(dq, query, (size_t)h * 2 * LN * 8, cudaMemcpyDefault, c.st));  // host or device
+        tm.mark(TM_H2D);
+        entries = expand(c, dq, h, comp, m);
+        tm.mark(TM_EXPAND);
+    }
     u32* prep = nullptr;
     c.prep_s_ok = false;
     if (op == CWG_OP_FOLKLORE && c.k >= 2) {
@@ -1629,6 +1677,37 @@ int cwg_answer_partial(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, con
     });
 }
 
+int cwg_expand_shard(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+                     const uint64_t* galois, uint32_t comp, const uint64_t* query, uint32_t world, uint32_t rank,
+                     uint64_t* out) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        if (relin) upload_keys(c, relin, n_galois, galois_g, galois);
+        if (!c.have_keys) throw he_err("evaluation keys not set");
+        const size_t per = 2 * (size_t)c.cp.L * c.cp.N;
+        u64* dq = c.query.get<u64>(per);
+        CK(cudaMemcpyAsync(dq, query, per * 8, cudaMemcpyDefault, c.st));  // host or device
+        expand_shard(c, dq, comp, world, rank, out);
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+int cwg_answer_partial_shards(cwg_ctx* h, const uint64_t* shards, uint32_t world, uint32_t comp, uint32_t m,
+                              uint32_t op, uint64_t* dev_partial, cwg_timings* t) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        auto t0 = std::chrono::steady_clock::now();
+        Timer tm(c, t != nullptr);
+        tm.mark(TM_START);
+        answer_partial(c, 1, comp, m, nullptr, op, dev_partial, tm, shards, world);
+        CK(cudaStreamSynchronize(c.st));
+        fill_timings(c, tm, t,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    });
+}
 int cwg_finish(cwg_ctx* h, const uint64_t* dev_partial_sum, uint32_t op, uint64_t* out, cwg_timings* t) {
     return guarded([&] {
         Ctx& c = h->c;

@@ -344,6 +344,17 @@ __global__ void k_ks_mac(const u64* __restrict__ dntt, const u64* __restrict__ k
     ks[idx] = reduce128(hi, lo, T.q[i], T.q_mu96[i]);
 }
 
+/// Gathered expansion shards (rank-major: shard r holds global leaves r, r + W, r + 2W, ...,
+/// `per_shard` of them) -> entries in global order, the first m leaves.  Words per entry: wpe.
+__global__ void k_unshard(const u64* __restrict__ shards, u32 m, u32 W, u32 per_shard, size_t wpe,
+                          u64* __restrict__ entries) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)m * wpe) return;
+    const u32 e = (u32)(idx / wpe);
+    const size_t w = idx % wpe;
+    entries[idx] = shards[((size_t)(e % W) * per_shard + e / W) * wpe + w];
+}
+
 /// One expansion level node update for all B ciphertexts (expansion.cpp:55-59):
 ///   sub = (auto_g(c0) + ks0, ks1)
 ///   out[b]     = ct_b + sub

@@ -98,6 +98,11 @@ def load_library(path: str = LIB_PATH):
     lib.cwg_finish.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p,
                                ctypes.POINTER(CwgTimings)]
     lib.cwg_select.argtypes = [ctypes.c_void_p, *keyargs, *qargs, _u64p, _u32p, ctypes.POINTER(CwgTimings)]
+    lib.cwg_expand_shard.argtypes = [ctypes.c_void_p, *keyargs, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint32,
+                                     ctypes.c_uint32, ctypes.c_void_p]
+    lib.cwg_answer_partial_shards.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32,
+                                              ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                                              ctypes.POINTER(CwgTimings)]
     lib.cwg_ntt.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32, _u64p, ctypes.c_uint32, ctypes.c_int]
     lib.cwg_expand.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, _u64p, _u64p]
     lib.cwg_mul_lazy.argtypes = [ctypes.c_void_p, ctypes.c_uint32, _u64p, _u64p, _u64p]
@@ -256,6 +261,22 @@ class Context:
         ka, keep = self._key_args(keys)
         rc = self.lib.cwg_answer_partial(self.h, *ka, query.shape[0], c, m, query.ctypes.data, op, dev_partial_ptr,
                                          ctypes.byref(timings) if timings is not None else None)
+        _raise(self.lib, rc)
+
+    def shard_entries(self, c, world) -> int:
+        """Expanded entries one rank of `world` produces (cwg_expand_shard): 2^c / world."""
+        return (1 << c) // world
+
+    def expand_shard_ptr(self, query_ptr, c, world, rank, out_ptr, keys_ptrs=(None, 0, None, None)):
+        """cwg_expand_shard: this rank's subtree of expand_query (one query ciphertext) into the
+        device buffer out_ptr ([2^c / world][2][L][N] u64)."""
+        rc = self.lib.cwg_expand_shard(self.h, *keys_ptrs, c, query_ptr, world, rank, out_ptr)
+        _raise(self.lib, rc)
+
+    def answer_partial_shards_ptr(self, shards_ptr, world, c, m, op, dev_partial_ptr, timings=None):
+        """cwg_answer_partial_shards: the partial answer from the rank-major gathered shards."""
+        rc = self.lib.cwg_answer_partial_shards(self.h, shards_ptr, world, c, m, op, dev_partial_ptr,
+                                                ctypes.byref(timings) if timings is not None else None)
         _raise(self.lib, rc)
 
     def finish(self, dev_partial_ptr, op=OP_FOLKLORE, out=None, timings=None):

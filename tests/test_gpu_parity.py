@@ -208,6 +208,41 @@ def test_sharded_partials_equal_single(gpu, reflib):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_expansion_equals_full(gpu, reflib, world):
+    """Sharded expand_query (cwg_expand_shard): the W rank subtrees, gathered rank-major as an
+    all-gather would, give the full answer (cwg_answer_partial_shards + cwg_finish) and the
+    reference answer; each shard holds the global leaves r, r + W, ... of cwg_expand."""
+    import torch
+
+    from paper_2202_07569_b200 import configs
+
+    N, primes, t = small_params()
+    n, k, m, c, s = 40, 2, 10, 4, 1
+    be = _ref_backend(reflib, N, primes, t, seed=23, levels=c)
+    keys = _keys(be)
+    positions = configs.perfect_map(np.arange(n), m, k)
+    q = be.pack_query(configs.codeword_bits(positions[11], m), c)
+    db = np.random.default_rng(24).integers(0, t, (n, s, N), dtype=np.uint64)
+    want, _ = be.answer(q, c, m, positions, db)
+    ctx = _ctx(N, primes, t)
+    ctx.load_db(positions, db, n_total=n, m=m)
+    ctx.set_keys(keys)
+    L = len(primes)
+    per = ctx.shard_entries(c, world) * 2 * L * N
+    shards = torch.zeros(world * per, dtype=torch.int64, device="cuda")
+    for r in range(world):  # ranks run one after another on this device
+        ctx.expand_shard_ptr(q.ctypes.data, c, world, r, shards[r * per:].data_ptr())
+    full = ctx.expand(q, c, 1 << c)  # cwg_expand: all leaves in global order
+    sh = shards.cpu().numpy().view(np.uint64).reshape(world, (1 << c) // world, 2, L, N)
+    for e in range(1 << c):
+        assert np.array_equal(sh[e % world, e // world], full[e])
+    part = torch.zeros(ctx.partial_words(), dtype=torch.int64, device="cuda")
+    ctx.answer_partial_shards_ptr(shards.data_ptr(), world, c, m, 0, part.data_ptr())
+    got = ctx.finish(part.data_ptr())
+    assert np.array_equal(got, want)
+
+
 def test_errors_match_reference_messages(gpu):
     from paper_2202_07569_b200 import configs
 

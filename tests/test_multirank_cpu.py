@@ -68,3 +68,38 @@ def test_row_shards_sum_to_full_answer_gloo(tmp_path, reflib):
     ok = np.load(res)
     assert ok[0] == 1, "sharded answer differs from the single-process answer"
     assert ok[1] == 1, "sharded answer does not decrypt to the selected row"
+
+
+def _shard_worker(rank, world, port, result_path):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    c, wpe = 5, 3  # 2^c leaves, words per entry
+    P = (1 << c) // world
+    # rank r's cwg_expand_shard output: global leaves r, r + W, r + 2W, ... (each entry = wpe words)
+    local = torch.tensor([[(rank + world * u) * 10 + w for w in range(wpe)] for u in range(P)], dtype=torch.int64)
+    gathered = [torch.zeros_like(local) for _ in range(world)]
+    dist.all_gather(gathered, local)  # rank-major, as bench.py's all_gather_into_tensor on NCCL
+    shards = torch.cat(gathered).reshape(-1).numpy()
+    m = (1 << c) - 3
+    # k_unshard (kernels.cuh): entries[e][w] = shards[((e % W) * P + e / W) * wpe + w]
+    ent = np.array([[shards[((e % world) * P + e // world) * wpe + w] for w in range(wpe)] for e in range(m)])
+    ok = np.array_equal(ent, np.array([[e * 10 + w for w in range(wpe)] for e in range(m)]))
+    if rank == 0:
+        np.save(result_path, np.array([int(ok)]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_expansion_shards_gather_rank_major(tmp_path):
+    """bench.py's sharded expansion (N > 1): rank r holds global leaves r + W u; an all-gather
+    concatenates the shards rank-major and k_unshard's index map restores global order."""
+    import torch.multiprocessing as mp
+
+    world = 2
+    path = str(tmp_path / "shard.npy")
+    mp.spawn(_shard_worker, args=(world, _free_port(), path), nprocs=world, join=True)
+    assert np.load(path)[0] == 1
