@@ -33,7 +33,8 @@ OP_FOLKLORE, OP_ARITH = 0, 1
 # the symbols include/cwgpu.h and include/cwgpu_client.h declare
 EXPORTED_SYMBOLS = [
     "cwg_last_error", "cwg_create", "cwg_destroy", "cwg_get_info", "cwg_load_db", "cwg_set_keys",
-    "cwg_answer", "cwg_partial_words", "cwg_answer_partial", "cwg_finish", "cwg_select", "cwg_ntt",
+    "cwg_answer", "cwg_partial_words", "cwg_answer_partial", "cwg_finish", "cwg_expand_shard",
+    "cwg_answer_partial_shards", "cwg_select", "cwg_ntt",
     "cwg_expand", "cwg_mul_lazy", "cwg_relinearize", "cwg_substitute", "cwg_kernel_launches",
     "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats", "cwg_kernel_units", "cwg_bench_kernel",
     "cwg_client_last_error", "cwg_client_create", "cwg_client_destroy", "cwg_client_digits",
