@@ -413,7 +413,7 @@ constexpr int kRtStages = 4;
 template <int JM>
 constexpr size_t round_tma_smem() { return (size_t)kRtStages * JM * 128 * 4; }
 
-template <int LOGN, int JM, int NC>  // LOGN = 0: N at run time
+template <int LOGN, int JM, int NC, int MMT = 0>  // LOGN = 0: N at run time; MMT = 0: Mm at run time
 __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P, DevTab T,
                                                      const __grid_constant__ RoundTcPar<JM, NC> RP,
                                                      const uint4* __restrict__ Bglob, const RoundK* __restrict__ gRK) {
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
     __shared__ __align__(8) unsigned long long mbar, full[kRtStages], empty[kRtStages];
     __shared__ u32 tmem_base_sh;
     const u32 tid = threadIdx.x, warp = tid >> 5;
-    const u32 J = T.J, Mm = T.Mm;
+    const u32 J = T.J, Mm = MMT ? (u32)MMT : T.Mm;
     const u32 N = LOGN ? (1u << LOGN) : T.N, logN = LOGN ? (u32)LOGN : T.logN;  // compile-time N: immediate plane offsets
     const size_t total = (size_t)P * 3 * N;
     const u32 ntiles = (u32)((total + 127) / 128);
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
                         const int k = k0 + kk;
-                        if (k < RPT::MMAX && k < (int)Mm) {
+                        if (k < RPT::MMAX && (MMT ? k < MMT : k < (int)Mm)) {
                             // S + gamma (-I_A) 2^32 + (rho + 2^36) 2^32 - 2^36 2^32 < 2^61, one Montgomery
                             // reduction: < 2^29 + 2^30 < 2 a_k
                             const u32 a = RP.kq[k].x;
