@@ -97,7 +97,8 @@ struct Ctx {
     // fused tensor + INTT + tensor-core rounding over a J-CTA cluster (k_tir; env CWGPU_FUSE_TIR=0
     // off); -1 = not yet probed, 0 = unavailable for these parameters, 1 = on
     int fuse_tir = -1;
-    bool round_tma = true;
+    bool round_tma = true;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
+    u32 round_ctas = 4;     // k_round_tma grid: persistent CTAs per SM (env CWGPU_ROUND_CTAS)
     // key switching through the 30-bit aux primes (ks32.cuh; env CWGPU_KS32=0: 64-bit NTT path)
     bool ks32 = true;
     bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
@@ -1066,7 +1067,7 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
 #define RTC(JMv, NCv)                                                                                             \
     if (c.JM == JMv && c.rtc_nc == NCv) {                                                                        \
         if (c.round_tma) {                                                                                        \
-            const size_t gr = std::min<size_t>(items / 128, 148 * 4);                                             \
+            const size_t gr = std::min<size_t>(items / 128, (size_t)148 * c.round_ctas);                         \
             const auto& rp = *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data());                        \
             constexpr int LN = JMv == 16 ? 13 : JMv == 8 ? 12 : JMv == 32 ? 14 : 0;                              \
             if (LN == 13 && c.cp.logN == 13 && c.ab.Mm == 11)                                                    \
@@ -1585,6 +1586,7 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_FUSE_MAC")) c.fuse_mac = std::atoi(e);
         if (const char* e = std::getenv("CWGPU_ROUND_TMA")) c.round_tma = std::atoi(e) != 0;
+        if (const char* e = std::getenv("CWGPU_ROUND_CTAS")) c.round_ctas = (u32)std::max(1, std::min(4, std::atoi(e)));
         if (const char* e = std::getenv("CWGPU_KS32")) c.ks32 = std::atoi(e) != 0;
         c.dcur = &c.Dbuf;
         for (int i = 0; i < Ctx::kMaxStreams; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));
