@@ -75,6 +75,16 @@ int cwg_get_info(const cwg_ctx* ctx, cwg_info* out);
 int cwg_load_db(cwg_ctx* ctx, uint64_t n_total, uint64_t row_begin, uint64_t n_local, uint32_t s,
                 uint32_t k, uint32_t m, const uint32_t* positions, const uint64_t* payload);
 
+/* PirDatabase::setup + prepare_for from raw rows (pir.cpp:214-264), codewords and plaintexts
+ * built on the device: row r's codeword is perfect_map(id_r) (cw_code.cpp:80-102) with
+ * id_r = row_ids[r] (keyword mode: keyword_value of the key, pir.cpp:22-30) or, when row_ids is
+ * NULL, the global row index row_begin + r (index mode, map_index pir.cpp:149-153); payloads
+ * [n_local][payload_bytes] (host or device) are chunked into s = max(1, ceil(8 payload_bytes /
+ * (N floor(log2 t)))) plaintexts (chunk_payload, pir.cpp:169-193).  Errors as the reference:
+ * all-zero payloads, duplicate identifiers, ids outside the code capacity. */
+int cwg_load_db_bytes(cwg_ctx* ctx, uint64_t n_total, uint64_t row_begin, uint64_t n_local, uint32_t k, uint32_t m,
+                      uint64_t payload_bytes, const uint8_t* payloads, const uint64_t* row_ids);
+
 /* Evaluation keys (EvalKeySet, bfv.hpp:42-51).  Kept resident until replaced. */
 int cwg_set_keys(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
                  const uint64_t* galois);

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -29,6 +30,7 @@
 #include "ntt_mac.cuh"
 #include "tir.cuh"
 #include "ks32.cuh"
+#include "dbsetup.cuh"
 
 namespace cwgpu {
 
@@ -1475,14 +1477,16 @@ static void fill_timings(Ctx& c, Timer& tm, cwg_timings* t, double total_ms) {
 }
 
 // ------------------------------------------------------------------ database
-static void load_db(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s, u32 k, u32 m, const u32* positions,
-                    const u64* payload) {
+/// Common part of cwg_load_db / cwg_load_db_bytes: positions (host, [n_local][k]) checked and made
+/// resident; `fill(r0, R, stage)` writes rows [r0, r0+R)'s plaintext coefficients (< t) as u64
+/// [R][s][N] into the device staging buffer, which is lifted to the MAC basis and NTT'd.
+static void load_db_impl(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s, u32 k, u32 m, const u32* positions,
+                         const std::function<void(u64, u64, u64*)>& fill) {
     if (n_local == 0 || n_total == 0) throw std::invalid_argument("empty database");
     if (row_begin + n_local > n_total) throw std::invalid_argument("row range outside the database");
     if (k < 1) throw std::invalid_argument("hamming weight must be >= 1");
     if (k > 64) throw std::invalid_argument("cwgpu: hamming weight above 64 is not supported");
     if (c.cp.t <= k) throw std::invalid_argument("plaintext modulus must exceed the Hamming weight");
-    if (s > 0 && !payload) throw std::invalid_argument("payload missing");
     const u32 N = c.cp.N;
     for (u64 r = 0; r < n_local; ++r) {
         for (u32 p = 0; p < k; ++p) {
@@ -1508,14 +1512,12 @@ static void load_db(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s, u32 
     if (s > 0) {
         // prepare_plain (bfv.cpp:933-942) into the MAC basis: coefficients < t lifted unchanged,
         // NTT per MAC prime; staged in chunks of rows.
-        for (u64 i = 0; i < n_local * s * N; ++i)
-            if (payload[i] >= c.cp.t) throw std::invalid_argument("plain operand not reduced mod t");
         u32* dbp = c.db.get<u32>(n_local * s * Mm * N);
         const u64 chunk = std::max<u64>(1, (u64(256) << 20) / ((u64)s * N * 8));
         u64* stage = c.chain3.get<u64>(std::min(chunk, n_local) * s * N);
         for (u64 r0 = 0; r0 < n_local; r0 += chunk) {
             const u64 R = std::min(chunk, n_local - r0);
-            CK(cudaMemcpyAsync(stage, payload + r0 * s * N, R * s * N * 8, cudaMemcpyHostToDevice, c.st));
+            fill(r0, R, stage);
             u32* dst = dbp + r0 * s * Mm * N;
             launch(c, k_db_spread, blocks(R * s * Mm * N, 256), 256, 0, (const u64*)stage, R * s, c.T, dst);
             ntt32(c, dst, (u32)(R * s * Mm), Mm, Mm, 0, false, 0);
@@ -1523,6 +1525,79 @@ static void load_db(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s, u32 
         CK(cudaStreamSynchronize(c.st));
     }
     c.db_loaded = true;
+}
+
+static void load_db(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s, u32 k, u32 m, const u32* positions,
+                    const u64* payload) {
+    if (s > 0 && !payload) throw std::invalid_argument("payload missing");
+    const u32 N = c.cp.N;
+    if (s > 0)
+        for (u64 i = 0; i < n_local * s * N; ++i)
+            if (payload[i] >= c.cp.t) throw std::invalid_argument("plain operand not reduced mod t");
+    load_db_impl(c, n_total, row_begin, n_local, s, k, m, positions, [&](u64 r0, u64 R, u64* stage) {
+        CK(cudaMemcpyAsync(stage, payload + r0 * s * N, R * s * N * 8, cudaMemcpyHostToDevice, c.st));
+    });
+}
+
+/// PirDatabase::setup + prepare_for from raw rows (pir.cpp:214-264): codewords by perfect_map of
+/// the row ids on the device (index mode: the global row index, map_index pir.cpp:149-153;
+/// keyword mode: keyword_value of the row's key, pir.cpp:22-30 / 155-159, computed by the
+/// caller), payloads chunked on the device (chunk_payload, pir.cpp:169-193: s plaintexts of
+/// floor(log2 t)-bit coefficients, s = max(1, ceil(8 bytes / (N b))), pir.cpp:39-43).
+static void load_db_bytes(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 k, u32 m, u64 payload_bytes,
+                          const unsigned char* payloads, const u64* row_ids) {
+    if (n_local == 0 || n_total == 0) throw std::invalid_argument("empty database");
+    if (!payloads || payload_bytes == 0) throw std::invalid_argument("payload missing");
+    if (k < 1) throw std::invalid_argument("hamming weight must be >= 1");
+    if (k > 64) throw std::invalid_argument("cwgpu: hamming weight above 64 is not supported");
+    const u32 N = c.cp.N;
+    u32 b = 0;
+    while (b < 63 && (u64(1) << (b + 1)) <= c.cp.t) ++b;  // plain_bits_per_coeff (he.cpp:17-21)
+    const u64 cap_bits = (u64)N * b;
+    const u32 s = (u32)std::max<u64>(1, (payload_bytes * 8 + cap_bits - 1) / cap_bits);
+    // code capacity C(m, k) and the largest binomial the device unranking touches, C(m-1, j <= k)
+    auto binom = [](u32 n, u32 r) {  // C(n, r), saturating at 2^90 (products stay below 2^122)
+        if (r > n) return (u128)0;
+        u128 v = 1;
+        for (u32 j = 1; j <= r; ++j) {
+            if (v >> 90) return ((u128)1) << 90;
+            v = v * (n - r + j) / j;  // exact: C(n-r+j, j) = C(n-r+j-1, j-1) (n-r+j) / j
+        }
+        return v;
+    };
+    const u128 cap = binom(m, k);
+    u128 big = 0;
+    for (u32 j = 0; j <= k; ++j) big = std::max(big, binom(m - 1, j));
+    if (big >> 64) throw std::invalid_argument("cwgpu: code capacity above 2^64 is not supported");
+    std::vector<u64> ids(n_local);
+    for (u64 r = 0; r < n_local; ++r) {
+        ids[r] = row_ids ? row_ids[r] : row_begin + r;
+        if ((u128)ids[r] >= cap) throw std::invalid_argument("perfect_map: input out of range");
+    }
+    if (row_ids) {
+        std::vector<u64> srt(ids);
+        std::sort(srt.begin(), srt.end());
+        if (std::adjacent_find(srt.begin(), srt.end()) != srt.end()) throw std::invalid_argument("duplicate identifier");
+    }
+    for (u64 r = 0; r < n_local; ++r) {  // pir.cpp:231-235
+        const unsigned char* p = payloads + r * payload_bytes;
+        if (std::all_of(p, p + payload_bytes, [](unsigned char x) { return x == 0; }))
+            throw std::invalid_argument("all-zero payloads are reserved for the absent-keyword sentinel");
+    }
+    u64* dids = c.tmp_idx.get<u64>(n_local);
+    u32* dpos = c.digits.get<u32>(n_local * k);
+    CK(cudaMemcpyAsync(dids, ids.data(), n_local * 8, cudaMemcpyHostToDevice, c.st));
+    launch(c, k_perfect_map, blocks(n_local, 128), 128, 0, (const u64*)dids, n_local, m, k, dpos);
+    std::vector<u32> pos(n_local * k);
+    CK(cudaMemcpyAsync(pos.data(), dpos, pos.size() * 4, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    unsigned char* dbytes = nullptr;
+    load_db_impl(c, n_total, row_begin, n_local, s, k, m, pos.data(), [&](u64 r0, u64 R, u64* stage) {
+        dbytes = reinterpret_cast<unsigned char*>(c.lift_tmp.get<u32>((R * payload_bytes + 3) / 4));
+        CK(cudaMemcpyAsync(dbytes, payloads + r0 * payload_bytes, R * payload_bytes, cudaMemcpyDefault, c.st));
+        launch(c, k_chunk_payload, blocks(R * s * N, 256), 256, 0, (const unsigned char*)dbytes, R, payload_bytes, s,
+               N, b, stage);
+    });
 }
 
 }  // namespace cwgpu
@@ -1647,6 +1722,15 @@ int cwg_load_db(cwg_ctx* h, uint64_t n_total, uint64_t row_begin, uint64_t n_loc
         std::lock_guard<std::mutex> g(h->c.mu);
         CK(cudaSetDevice(h->c.device));
         load_db(h->c, n_total, row_begin, n_local, s, k, m, positions, payload);
+    });
+}
+
+int cwg_load_db_bytes(cwg_ctx* h, uint64_t n_total, uint64_t row_begin, uint64_t n_local, uint32_t k, uint32_t m,
+                      uint64_t payload_bytes, const uint8_t* payloads, const uint64_t* row_ids) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> g(h->c.mu);
+        CK(cudaSetDevice(h->c.device));
+        load_db_bytes(h->c, n_total, row_begin, n_local, k, m, payload_bytes, payloads, row_ids);
     });
 }
 

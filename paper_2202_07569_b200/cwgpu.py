@@ -32,7 +32,7 @@ OP_FOLKLORE, OP_ARITH = 0, 1
 
 # the symbols include/cwgpu.h and include/cwgpu_client.h declare
 EXPORTED_SYMBOLS = [
-    "cwg_last_error", "cwg_create", "cwg_destroy", "cwg_get_info", "cwg_load_db", "cwg_set_keys",
+    "cwg_last_error", "cwg_create", "cwg_destroy", "cwg_get_info", "cwg_load_db", "cwg_load_db_bytes", "cwg_set_keys",
     "cwg_answer", "cwg_partial_words", "cwg_answer_partial", "cwg_finish", "cwg_expand_shard",
     "cwg_answer_partial_shards", "cwg_select", "cwg_ntt",
     "cwg_expand", "cwg_mul_lazy", "cwg_relinearize", "cwg_substitute", "cwg_kernel_launches",
@@ -89,6 +89,8 @@ def load_library(path: str = LIB_PATH):
     lib.cwg_load_db.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                                 ctypes.c_uint32, ctypes.c_uint32, _u32p, _u64p]
     lib.cwg_set_keys.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, _u64p, _u64p]
+    lib.cwg_load_db_bytes.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                      ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
     keyargs = [_u64p, ctypes.c_uint32, _u64p, _u64p]
     qargs = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint32]
     lib.cwg_answer.argtypes = [ctypes.c_void_p, *keyargs, *qargs, ctypes.c_void_p, ctypes.POINTER(CwgTimings)]
@@ -216,6 +218,17 @@ class Context:
             assert payload.shape[0] == n_local and payload.shape[2] == self.N
             s, pp = payload.shape[1], _p64(payload)
         _raise(self.lib, self.lib.cwg_load_db(self.h, n_total, row_begin, n_local, s, k, m, _p32(positions), pp))
+
+    def load_db_bytes(self, payloads, k, m, n_total=None, row_begin=0, row_ids=None):
+        """cwg_load_db_bytes: PirDatabase::setup from raw rows on the device.  payloads:
+        [n_local][payload_bytes] uint8; row_ids: perfect_map inputs (keyword mode) or None
+        (index mode: the global row index)."""
+        payloads = np.ascontiguousarray(payloads, dtype=np.uint8)
+        n_local, nbytes = payloads.shape
+        n_total = n_local if n_total is None else n_total
+        ids = None if row_ids is None else np.ascontiguousarray(row_ids, dtype=np.uint64)
+        _raise(self.lib, self.lib.cwg_load_db_bytes(self.h, n_total, row_begin, n_local, k, m, nbytes,
+                                                    payloads.ctypes.data, None if ids is None else ids.ctypes.data))
 
     def set_keys(self, keys: Keys):
         relin, galois = _c64(keys.relin), _c64(keys.galois)

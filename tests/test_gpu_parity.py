@@ -359,3 +359,90 @@ def test_answer_small_rings(gpu, reflib, N, k):
     assert np.array_equal(got, want)
     assert be.noise_budget(got[1]) > 0
     assert np.array_equal(be.decrypt(got[1]), payload[1])
+
+
+@pytest.mark.parametrize("nbytes,s_rows", [(200, (0, 30)), (3000, (7, 23))])
+def test_load_db_bytes_matches_reference_setup(gpu, reflib, nbytes, s_rows):
+    """cwg_load_db_bytes (codewords by perfect_map and chunk_payload on the device) against the
+    reference's own process_query on a PirDatabase::setup database built from the same bytes
+    (pir.cpp:214-252): identical positions, plaintexts and response; also a row shard and a
+    payload spanning several plaintexts (3000 B > N floor(log2 t) / 8)."""
+    import torch
+
+    from paper_2202_07569_b200 import configs
+
+    N, primes, t = small_params()
+    n, k, c = 30, 2, 4
+    m = configs.min_code_length(n, k)
+    be = _ref_backend(reflib, N, primes, t, seed=41, levels=c)
+    keys = _keys(be)
+    r = np.random.default_rng(42)
+    payloads = r.integers(0, 256, (n, nbytes), dtype=np.uint8)
+    payloads[:, 0] |= 1  # no all-zero row (reserved by the reference)
+    q = be.pack_query(configs.codeword_bits(configs.perfect_map([13], m, k)[0], m), c)
+    want, chunks, pos = be.process_query_bytes(q, c, m, n, k, payloads)
+    lo, hi = s_rows
+    ctx = _ctx(N, primes, t)
+    if (lo, hi) == (0, n):
+        ctx.load_db_bytes(payloads, k, m)
+        got = ctx.answer(q, c, m, keys=keys)
+        assert np.array_equal(got, want)
+    else:  # shard [lo, hi) summed with the single-device partial of the rest
+        parts = []
+        for a, b_ in ((0, lo), (lo, hi), (hi, n)):
+            cx = _ctx(N, primes, t)
+            cx.load_db_bytes(payloads[a:b_], k, m, n_total=n, row_begin=a)
+            buf = torch.zeros(cx.partial_words(), dtype=torch.int64, device="cuda")
+            cx.answer_partial(q, c, m, buf.data_ptr(), keys=keys)
+            parts.append((cx, buf))
+        total = parts[0][1] + parts[1][1] + parts[2][1]
+        torch.cuda.synchronize()
+        assert np.array_equal(parts[0][0].finish(total.data_ptr()), want)
+    # the same database through cwg_load_db with the reference's own positions and plaintexts
+    ref_ctx = _ctx(N, primes, t)
+    ref_ctx.load_db(pos, chunks, m=m)
+    assert np.array_equal(ref_ctx.answer(q, c, m, keys=keys), want)
+
+
+def _chunk_payload(payloads, N, t):
+    """chunk_payload (pir.cpp:169-193) restated: floor(log2 t) bits per coefficient, LSB first."""
+    b = int(t).bit_length() - 1
+    nbytes = payloads.shape[1]
+    s = max(1, -(-(nbytes * 8) // (N * b)))
+    bits = np.unpackbits(payloads, axis=1, bitorder="little")
+    bits = np.pad(bits, ((0, 0), (0, s * N * b - bits.shape[1])))
+    w = (1 << np.arange(b, dtype=np.uint64)).astype(np.uint64)
+    return (bits.reshape(len(payloads), s, N, b).astype(np.uint64) * w).sum(axis=3).astype(np.uint64)
+
+
+def test_load_db_bytes_errors_and_keyword_ids(gpu, reflib):
+    """Keyword mode (row ids = keyword values, perfect_map on the device; config 5's CW(569, 4))
+    against the reference answer on its own perfect_map positions, and the reference errors of
+    PirDatabase::setup: all-zero payload, duplicate identifier, id outside the code."""
+    from paper_2202_07569_b200 import configs
+
+    N, primes, t = small_params(2048, 4, 50, 65537)
+    m, k, c = 569, 4, 10
+    n = 24
+    ids = np.random.default_rng(5).choice(1 << 32, n, replace=False).astype(np.uint64)
+    pl = np.random.default_rng(6).integers(1, 256, (n, 40), dtype=np.uint8)
+    pos_ref = np.stack([reflib.perfect_map(int(x), m, k) for x in ids])
+    chunks = _chunk_payload(pl, N, t)
+    be = _ref_backend(reflib, N, primes, t, seed=51, levels=c)
+    keys = _keys(be)
+    q = be.pack_query(configs.codeword_bits(pos_ref[7], m), c)
+    want, _ = be.answer(q, c, m, pos_ref, chunks)
+    ctx = _ctx(N, primes, t)
+    ctx.load_db_bytes(pl, k, m, row_ids=ids)
+    assert np.array_equal(ctx.answer(q, c, m, keys=keys), want)
+    assert np.array_equal(be.decrypt(want[0])[: chunks.shape[2]], chunks[7, 0])
+    with pytest.raises(ValueError, match="all-zero payloads"):
+        bad = pl.copy()
+        bad[5] = 0
+        ctx.load_db_bytes(bad, k, m, row_ids=ids)
+    with pytest.raises(ValueError, match="duplicate identifier"):
+        dup = ids.copy()
+        dup[3] = dup[9]
+        ctx.load_db_bytes(pl, k, m, row_ids=dup)
+    with pytest.raises(ValueError, match="perfect_map: input out of range"):
+        ctx.load_db_bytes(pl, 2, 8, row_ids=np.arange(n, dtype=np.uint64) + 20)
