@@ -108,10 +108,11 @@ struct Ctx {
     DevBuf relinA, galoisA, ksdig, ksmac;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
     u32 zs_last = 0;        // MAC-basis plane stride of the last mul_prepared output (J or Mm)
     unsigned next_cluster = 0;  // cluster size of the next launch (launch_named)
-    // row-tile pipeline on two streams (k <= 2 folklore): tiles alternate streams and D buffers so
-    // the latency-bound kernels of one tile (NTTs, tensor-core rounding, MAC) co-reside with those
-    // of the next (env CWGPU_STREAMS; C4: 251 ms vs 272 ms on one stream)
-    int nstreams = 2;
+    // row-tile pipeline on three streams (k <= 2 folklore): tiles rotate over streams and D buffers
+    // so the latency-bound kernels of one tile (NTTs, tensor-core rounding, MAC) co-reside with
+    // those of the next (env CWGPU_STREAMS; C4: 251 ms vs 272 ms on one stream when introduced;
+    // now 3 streams ~1 ms ahead of 2, profiles/r01_experiments.txt)
+    int nstreams = 3;
     static constexpr int kMaxStreams = 4;
     cudaStream_t tst[kMaxStreams] = {};
     cudaEvent_t tev[kMaxStreams + 1] = {};
