@@ -834,9 +834,10 @@ static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
                          B, bits, D, c.T, (u64*)nullptr, dA, K);
             ntt32(c, dA, B * D * K, K, K, 0, false, 0);
             // shared-load variant once the level is wide enough to fill the GPU (B >= 64 rows of
-            // K N threads / 2); narrow levels keep one output per thread (latency-bound otherwise)
+            // K N threads / 2); narrow levels and long digit chains keep one output per thread
+            // (latency-bound otherwise: C5's D = 25, L = 8 ran 917 vs 320 ms with it)
             if (D <= (u32)kKsDmax && B >= 64)
-                launch_named(c, "k_ks_mac32", k_ks_mac32x, blocks((size_t)((B + 1) / 2) * K * N, 128), 128, 0,
+                launch_named(c, "k_ks_mac32", k_ks_mac32x<kKsDmax>, blocks((size_t)((B + 1) / 2) * K * N, 128), 128, 0,
                              (const u32*)dA, kA, B, D, L, N, C, (const u64*)c.T.abar, mA);
             else
                 launch(c, k_ks_mac32, blocks((size_t)B * 2 * L * K * N, 256), 256, 0, (const u32*)dA, kA, B, D, L, N, C,

@@ -68,6 +68,7 @@ __global__ void k_ks_mac32(const u32* __restrict__ dig, const u32* __restrict__ 
 /// registers and loops over the 2 L (component, chain prime) outputs, each key word feeding two
 /// products (C4: 8.4 loads per output instead of 28).
 constexpr int kKsDmax = 16;
+template <int DMAX>
 __global__ void __launch_bounds__(128) k_ks_mac32x(const u32* __restrict__ dig, const u32* __restrict__ key, u32 B, u32 D,
                                                    u32 L, u32 N, const __grid_constant__ KsCrt C, const u64* __restrict__ abar,
                                                    u32* __restrict__ out) {
@@ -80,10 +81,10 @@ __global__ void __launch_bounds__(128) k_ks_mac32x(const u32* __restrict__ dig, 
     const bool two = b0 + 1 < B;
     const u32 a = C.a[j];
     const u64 mu = abar[j];
-    u32 d0[kKsDmax], d1[kKsDmax];
+    u32 d0[DMAX], d1[DMAX];
     const u32* dp0 = dig + ((size_t)b0 * D * K + j) * N + n;
 #pragma unroll
-    for (int d = 0; d < kKsDmax; ++d) {
+    for (int d = 0; d < DMAX; ++d) {
         d0[d] = d < (int)D ? dp0[(size_t)d * K * N] : 0u;
         d1[d] = (two && d < (int)D) ? dp0[((size_t)D + d) * K * N] : 0u;
     }
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(128) k_ks_mac32x(const u32* __restrict__ dig, 
         const u32* kp = key + ((size_t)ci * K + j) * N + n;
         u64 s0 = 0, s1 = 0;
 #pragma unroll
-        for (int d = 0; d < kKsDmax; ++d) {
+        for (int d = 0; d < DMAX; ++d) {
             if (d >= (int)D) break;
             const u64 kv = __ldg(kp + (size_t)d * kstride);
             s0 += (u64)d0[d] * kv;
