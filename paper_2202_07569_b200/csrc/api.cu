@@ -82,6 +82,7 @@ struct Ctx {
     std::vector<unsigned char> rpar;  // RoundPar<JM> (k_round_hyb kernel-parameter block), JM <= 32
     std::vector<unsigned char> rtc;   // RoundTcPar<JM, NC> (k_round_tc kernel-parameter block)
     DevBuf rtc_B;                     // k_round_tc B matrix (canonical UMMA K-major layout)
+    DevBuf rtc_B2;                    // k_round_tma second-GEMM B matrix (gamma / rho / offset terms)
     u32 rtc_nc = 0;                   // k_round_tc GEMM width (0: no instance for this JM / Mm)
     int round_kind = 2;               // 2 tensor-core, 1 IMAD + DFMA, 0 IMAD only (env CWGPU_ROUND=tc|hyb|int)
     DevBuf prep_s;                    // A-side prepared operands with the INTT output scale folded in
@@ -99,6 +100,8 @@ struct Ctx {
     // fused tensor + INTT + tensor-core rounding over a J-CTA cluster (k_tir; env CWGPU_FUSE_TIR=0
     // off); -1 = not yet probed, 0 = unavailable for these parameters, 1 = on
     int fuse_tir = -1;
+    int dbg_skip = 0;  // diagnostics (env CWGPU_DEBUG_SKIP: 1 rounding, 2 tensor, 3 NTT+MAC; wrong answers)
+    bool round_g2 = true;   // k_round_tma two-GEMM epilogue (env CWGPU_ROUND_G2=0: corrections on CUDA cores)
     bool round_tma = true;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
     u32 round_ctas = 4;     // k_round_tma grid: persistent CTAs per SM (env CWGPU_ROUND_CTAS)
     // key switching through the 30-bit aux primes (ks32.cuh; env CWGPU_KS32=0: 64-bit NTT path)
@@ -568,6 +571,28 @@ static void build_tables(Ctx& c) {
             if (build_round_tc(c.JM, c.rtc_nc, rj, rk, Imod, a, J, Mm, c.rtc, Bm)) {
                 c.rtc_B.ensure(Bm.size());
                 CK(cudaMemcpy(c.rtc_B.p, Bm.data(), Bm.size(), cudaMemcpyHostToDevice));
+                // second GEMM of k_round_tma (K = 32 bytes): A2 = [gamma, rb0..rb4, 1, 0...] per
+                // coefficient; column 4k+b collects byte b of gamma (-I_A 2^32), (2^(8i) 2^32) rb_i
+                // and (-2^36) 2^32, all mod a_k, so the residue columns end as S_k + the corrections
+                {
+                    const u32 NC = c.rtc_nc, K2 = 32;
+                    std::vector<unsigned char> B2((size_t)NC * K2, 0);
+                    auto put2 = [&](u32 n, u32 kb, unsigned char v) {
+                        B2[(size_t)(n / 8) * (K2 / 16 * 128) + (kb / 16) * 128 + (n % 8) * 16 + kb % 16] = v;
+                    };
+                    for (u32 k = 0; k < Mm && 4 * k + 3 < NC - 17; ++k) {
+                        const u64 p = rk[k].a;
+                        const u64 h32 = (1ull << 32) % p;
+                        u64 cst[7];
+                        cst[0] = rk[k].gcoef;  // (-I_A) 2^32 mod a_k
+                        for (u32 i = 0; i < 5; ++i) cst[1 + i] = (u64)(((u128)h32 << (8 * i)) % p);
+                        cst[6] = rk[k].roff;   // (-2^36) 2^32 mod a_k
+                        for (u32 kb = 0; kb < 7; ++kb)
+                            for (u32 b = 0; b < 4; ++b) put2(4 * k + b, kb, (unsigned char)(cst[kb] >> (8 * b)));
+                    }
+                    c.rtc_B2.ensure(B2.size());
+                    CK(cudaMemcpy(c.rtc_B2.p, B2.data(), B2.size(), cudaMemcpyHostToDevice));
+                }
             } else {
                 c.rtc_nc = 0;  // IMAD + DFMA rounding instead
             }
@@ -1053,7 +1078,7 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         return D;
     }
     if (reg32_ok(c.cp.logN)) {
-        REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? (prepA_scaled ? 2 : 1) : 0));
+        if (c.dbg_skip != 2) REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? (prepA_scaled ? 2 : 1) : 0));
     } else {
         launch(c, k_tensor_intt, (size_t)P * J, ntt_block(N), N * 4, prepA, idxA, prepB, idxB, P, c.T, D);
     }
@@ -1065,9 +1090,12 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         const RoundK* rk = reinterpret_cast<const RoundK*>(rj + c.JM);
         const u32* im = reinterpret_cast<const u32*>(rk + kMaxJ);
         c.next_units = (double)items;  // coefficients rounded
-        if (tc) {
+        if (tc && c.dbg_skip == 1) {
+            // diagnostics only (wrong answers): the pipelined cost of the rounding kernel
+        } else if (tc) {
             const u32 g3 = (u32)std::min<size_t>(items / 128, 148 * 4);
             const uint4* Bm = c.rtc_B.ptr<uint4>();
+            const uint4* B2m = c.round_g2 ? c.rtc_B2.ptr<uint4>() : nullptr;  // null: one-GEMM epilogue
 #define RTC(JMv, NCv)                                                                                             \
     if (c.JM == JMv && c.rtc_nc == NCv) {                                                                        \
         if (c.round_tma) {                                                                                        \
@@ -1076,13 +1104,13 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
             constexpr int LN = JMv == 16 ? 13 : JMv == 8 ? 12 : JMv == 32 ? 14 : 0;                              \
             if (LN == 13 && c.cp.logN == 13 && c.ab.Mm == 11)                                                    \
                 launch_named(c, "k_round_tc", k_round_tma<LN, JMv, NCv, 11>, gr, 160, round_tma_smem<JMv>(), D, P,  \
-                             c.T, rp, Bm, rk);                                                                    \
+                             c.T, rp, Bm, rk, B2m);                                                               \
             else if (LN != 0 && c.cp.logN == (u32)LN)                                                             \
                 launch_named(c, "k_round_tc", k_round_tma<LN, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T, \
-                             rp, Bm, rk);                                                                         \
+                             rp, Bm, rk, B2m);                                                                    \
             else                                                                                                  \
                 launch_named(c, "k_round_tc", k_round_tma<0, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T,  \
-                             rp, Bm, rk);                                                                         \
+                             rp, Bm, rk, B2m);                                                                    \
         } else                                                                                                      \
             launch_named(c, "k_round_tc", k_round_tc<JMv, NCv>, g3, 128, kRoundTcSmem, D, P, c.T,                \
                          *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk);                   \
@@ -1394,7 +1422,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         // TMA ring for multi-plaintext rows (C3: 37 vs 45 ms; the selection segments are reused
         // across the s payload slices); the register stream is as fast for s = 1 (C4: 22.9 ms)
         if (c.fuse_now) {
-            REG32_DISPATCH(c.cp.logN, ntt_mac(c, Z, zs, nc, dbt, Rt, acc));
+            if (c.dbg_skip != 3) REG32_DISPATCH(c.cp.logN, ntt_mac(c, Z, zs, nc, dbt, Rt, acc));
         } else if (c.mac_tma && c.s >= 2 && N >= (u32)kMacBlock && !c.old_mac) {
             // TMA-fed stream: whole waves of 3 CTAs / SM (no partial tail wave), >= 8 rows per chunk
             const u32 per = Mm * (N / kMacBlock) * c.s;
@@ -1663,6 +1691,8 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_FUSE_MAC")) c.fuse_mac = std::atoi(e);
         if (const char* e = std::getenv("CWGPU_ROUND_TMA")) c.round_tma = std::atoi(e) != 0;
+        if (const char* e = std::getenv("CWGPU_ROUND_G2")) c.round_g2 = std::atoi(e) != 0;
+        if (const char* e = std::getenv("CWGPU_DEBUG_SKIP")) c.dbg_skip = std::atoi(e);
         if (const char* e = std::getenv("CWGPU_ROUND_CTAS")) c.round_ctas = (u32)std::max(1, std::min(4, std::atoi(e)));
         if (const char* e = std::getenv("CWGPU_KS32")) c.ks32 = std::atoi(e) != 0;
         c.dcur = &c.Dbuf;
@@ -1681,7 +1711,7 @@ void cwg_destroy(cwg_ctx* h) {
     cudaStreamSynchronize(c.st);
     for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.prep_s, &c.Dmore[0], &c.Dmore[1], &c.Dmore[2], &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
                       &c.digits, &c.dntt, &c.ks, &c.prep, &c.Dbuf, &c.chain3, &c.node2, &c.acc_lo, &c.acc_hi,
-                      &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp, &c.rtc_B, &c.relinA, &c.galoisA,
+                      &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp, &c.rtc_B, &c.rtc_B2, &c.relinA, &c.galoisA,
                       &c.ksdig, &c.ksmac})
         b->release();
     if (c.d_fb) cudaFree(c.d_fb);

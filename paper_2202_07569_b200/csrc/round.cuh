@@ -416,11 +416,16 @@ constexpr size_t round_tma_smem() { return (size_t)kRtStages * JM * 128 * 4; }
 template <int LOGN, int JM, int NC, int MMT = 0>  // LOGN = 0: N at run time; MMT = 0: Mm at run time
 __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P, DevTab T,
                                                      const __grid_constant__ RoundTcPar<JM, NC> RP,
-                                                     const uint4* __restrict__ Bglob, const RoundK* __restrict__ gRK) {
+                                                     const uint4* __restrict__ Bglob, const RoundK* __restrict__ gRK,
+                                                     const uint4* __restrict__ B2glob) {
     using RPT = RoundTcPar<JM, NC>;
     constexpr int K = RPT::K, F0 = RPT::F0, G0 = RPT::G0;
     constexpr int KSTEPS = K / 32;
+    constexpr int A2 = JM + NC;  // TMEM columns of the second GEMM's A operand (8 x 32 bit = K 32 bytes)
+    constexpr bool G2OK = A2 + 8 <= 128;  // A, D and A2 fit the 128-column allocation
     __shared__ __align__(128) uint4 Bs[NC * K / 16];
+    __shared__ __align__(128) uint4 Bs2[G2OK ? NC * 32 / 16 : 1];
+    const bool g2 = G2OK && B2glob != nullptr;
     extern __shared__ __align__(128) u32 ringd[];  // [kRtStages][JM][128]
     auto ring = reinterpret_cast<u32(*)[JM][128]>(ringd);
     __shared__ __align__(8) unsigned long long mbar, full[kRtStages], empty[kRtStages];
@@ -432,6 +437,8 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
     const u32 ntiles = (u32)((total + 127) / 128);
 
     for (u32 x = tid; x < NC * K / 16; x += blockDim.x) Bs[x] = Bglob[x];
+    if (g2)
+        for (u32 x = tid; x < NC * 32 / 16; x += blockDim.x) Bs2[x] = B2glob[x];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
                      "n"(128));
@@ -473,6 +480,8 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
     const u64 bdesc0 = ((u64)((smem_u32(Bs) >> 4) & 0x3fff)) | ((u64)(128 >> 4) << 16) |
                        ((u64)((K / 16 * 128) >> 4) << 32) | (1ull << 46);
     const u32 idesc = (2u << 4) | ((u32)(NC >> 3) << 17) | ((u32)(128 >> 4) << 24);
+    const u64 bdesc2 = ((u64)((smem_u32(Bs2) >> 4) & 0x3fff)) | ((u64)(128 >> 4) << 16) |
+                       ((u64)((32 / 16 * 128) >> 4) << 32) | (1ull << 46);
     const u32 fA0 = T.fracA[1], fA1 = T.fracA[2];
     u32 phase = 0, i = 0;
 #pragma unroll 1
@@ -556,6 +565,60 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
         }
         const long long rho = (long long)(((u64)s3 << 32) | s2);
         const bool bad = (s1 == 0u && s0 < 64u) || (s1 >= 0xfffffff0u) || T.force_exact;
+        if (g2) {
+            // second GEMM: the gamma / rho / offset corrections enter the residue columns on the
+            // tensor core (K = 32 bytes: gamma < J, rb = rho + 2^36 < 2^37 in 5 bytes, a constant 1)
+            {
+                const u64 rb = (u64)(rho + (1ll << 36));
+                const u32 a0 = gamma | (u32)((rb & 0xffffffull) << 8);
+                const u32 a1 = (u32)((rb >> 24) & 0xffffull) | (1u << 16);
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %3, %3, %3, %3, %3};\n" ::"r"(ta + A2),
+                             "r"(a0), "r"(a1), "r"(0u)
+                             : "memory");
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                asm volatile("bar.sync 1, 128;\n" ::: "memory");
+                if (tid == 0) {
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tbase + JM),
+                        "r"(tbase + (u32)A2), "l"(bdesc2), "r"(idesc)
+                        : "memory");
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                     smem_u32(&mbar))
+                                 : "memory");
+                }
+                mbar_wait_sleep(&mbar, phase);
+                phase ^= 1u;
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            }
+#pragma unroll
+            for (int k0 = 0; k0 < RPT::MMAX; k0 += 4) {  // S'_k < 2^49: one Montgomery reduction, < a + 2^17
+                u32 Rc[16];
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                    "%14, %15}, [%16];\n"
+                    : "=r"(Rc[0]), "=r"(Rc[1]), "=r"(Rc[2]), "=r"(Rc[3]), "=r"(Rc[4]), "=r"(Rc[5]), "=r"(Rc[6]),
+                      "=r"(Rc[7]), "=r"(Rc[8]), "=r"(Rc[9]), "=r"(Rc[10]), "=r"(Rc[11]), "=r"(Rc[12]), "=r"(Rc[13]),
+                      "=r"(Rc[14]), "=r"(Rc[15])
+                    : "r"(td + 4 * k0)
+                    : "memory");
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                if (!bad) {
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const int k = k0 + kk;
+                        if (k < RPT::MMAX && (MMT ? k < MMT : k < (int)Mm)) {
+                            const u32 a = RP.kq[k].x;
+                            const u32 p01 = Rc[4 * kk] + (Rc[4 * kk + 1] << 8), p23 = Rc[4 * kk + 2] + (Rc[4 * kk + 3] << 8);
+                            const u64 X = (u64)p01 + ((u64)p23 << 16);
+                            Dp[(size_t)k * N] = red32(mont_red64(X, a, RP.kq[k].y), a);
+                        }
+                    }
+                }
+            }
+        } else {
         {
             const u64 rb = (u64)(rho + (1ll << 36));
             const u32 rlo = (u32)(rb & ((1u << 30) - 1)), rhi = (u32)(rb >> 30);
@@ -589,6 +652,7 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
                     }
                 }
             }
+        }
         }
         if (bad) {  // exact multiword path (no tensor-memory instructions inside); D still holds w_j
             HpsState h;
