@@ -102,6 +102,7 @@ struct Ctx {
     int fuse_tir = -1;
     int dbg_skip = 0;  // diagnostics (env CWGPU_DEBUG_SKIP: 1 rounding, 2 tensor, 3 NTT+MAC; wrong answers)
     bool round_g2 = true;   // k_round_tma two-GEMM epilogue (env CWGPU_ROUND_G2=0: corrections on CUDA cores)
+    u32 mac_ck = 0;         // k_ntt_mac row chunks per (component, prime) (env CWGPU_MAC_CK; 0 = auto)
     bool round_tma = true;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
     u32 round_ctas = 4;     // k_round_tma grid: persistent CTAs per SM (env CWGPU_ROUND_CTAS)
     // key switching through the 30-bit aux primes (ks32.cuh; env CWGPU_KS32=0: 64-bit NTT path)
@@ -652,11 +653,12 @@ struct Reg32 {
     static void ntt_mac(Ctx& c, const u32* Z, u32 zs, u32 nc, const u32* dbt, u32 Rt, unsigned long long* acc) {
         const u32 Mm = c.ab.Mm;
         const u32 per = nc * Mm;  // CTAs per row chunk
-        // >= 2 waves of resident CTAs, >= 8 rows per chunk (fewer accumulator atomics)
+        // row chunks per (component, prime), balanced to +-1 row: ~2 waves of resident CTAs, >= 8
+        // rows per chunk (fewer accumulator atomics); env CWGPU_MAC_CK overrides
         const u32 slots = 148 * 3 * 2;
         u32 ck = std::max<u32>(1, std::min<u32>((Rt + 7) / 8, (slots + per - 1) / per));
-        const u32 chunk = (Rt + ck - 1) / ck;
-        ck = (Rt + chunk - 1) / chunk;
+        if (c.mac_ck) ck = std::max<u32>(1, std::min<u32>(c.mac_ck, Rt));
+        const u32 chunk = ck;  // the kernels take the chunk count
         c.next_units = (double)Rt * nc * Mm;  // polynomials transformed (+ payload words streamed)
         const size_t grid = (size_t)ck * per;
 #define NMC(NC, S, A) launch_named(c, "k_ntt_mac", k_ntt_mac<LOGN, NC, S, A>, grid, R::T, NttMac<LOGN, S, A>::SMEM, Z, zs, dbt, Rt, chunk, c.T, acc)
@@ -1691,6 +1693,7 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_FUSE_MAC")) c.fuse_mac = std::atoi(e);
         if (const char* e = std::getenv("CWGPU_ROUND_TMA")) c.round_tma = std::atoi(e) != 0;
+        if (const char* e = std::getenv("CWGPU_MAC_CK")) c.mac_ck = (u32)std::max(0, std::atoi(e));
         if (const char* e = std::getenv("CWGPU_ROUND_G2")) c.round_g2 = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_DEBUG_SKIP")) c.dbg_skip = std::atoi(e);
         if (const char* e = std::getenv("CWGPU_ROUND_CTAS")) c.round_ctas = (u32)std::max(1, std::min(4, std::atoi(e)));

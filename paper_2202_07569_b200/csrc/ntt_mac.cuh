@@ -31,7 +31,7 @@ struct NttMac {
 
 template <int LOGN, int NC, int S, bool ACCS>
 __global__ void __launch_bounds__(NttMac<LOGN, S, ACCS>::T, NttMac<LOGN, S, ACCS>::MINB) k_ntt_mac(
-    const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB, u32 R, u32 chunk, DevTab T,
+    const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB, u32 R, u32 nchunks, DevTab T,
     unsigned long long* __restrict__ acc) {
     using G = NttMac<LOGN, S, ACCS>;
     constexpr int E = G::E, WB = G::WB, N = 1 << LOGN, SH = LOGN - WB;
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(NttMac<LOGN, S, ACCS>::T, NttMac<LOGN, S, ACCS
     const u32 Mm = T.Mm;
     const u32 c = blockIdx.x % NC, k = (blockIdx.x / NC) % Mm, ch = blockIdx.x / (NC * Mm);
     const u32 p = T.a[k], pinv = T.apinv[k], p2 = 2 * p;
-    const u32 r0 = ch * chunk, r1 = min(R, r0 + chunk);
+    const u32 r0 = (u32)(((u64)ch * R) / nchunks), r1 = (u32)(((u64)(ch + 1) * R) / nchunks);  // balanced
     u32 a[G::ACC_SMEM ? 1 : S][E];
     if constexpr (G::ACC_SMEM) {
 #pragma unroll
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(NttMac<LOGN, S, ACCS>::T, NttMac<LOGN, S, ACCS
 /// Shared memory: transposes N + selection slot N + payload slot N words (2 CTAs / SM at N = 8192).
 template <int LOGN, int NC>
 __global__ void __launch_bounds__(RegNtt<LOGN>::T, 2) k_ntt_mac_tma(
-    const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB, u32 R, u32 chunk, DevTab T,
+    const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB, u32 R, u32 nchunks, DevTab T,
     unsigned long long* __restrict__ acc) {
     using G = RegNtt<LOGN>;
     constexpr int E = G::E, WB = G::WB, N = 1 << LOGN, SH = LOGN - WB;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, 2) k_ntt_mac_tma(
     const u32 Mm = T.Mm;
     const u32 c = blockIdx.x % NC, k = (blockIdx.x / NC) % Mm, ch = blockIdx.x / (NC * Mm);
     const u32 p = T.a[k], pinv = T.apinv[k], p2 = 2 * p;
-    const u32 r0 = ch * chunk, r1 = min(R, r0 + chunk);
+    const u32 r0 = (u32)(((u64)ch * R) / nchunks), r1 = (u32)(((u64)(ch + 1) * R) / nchunks);  // balanced
     if (r0 >= r1) return;
     const size_t dbrow = (size_t)Mm * N;
     auto zsrc = [&](u32 i) { return Z + (((size_t)i * NC + c) * zstride + k) * N; };
