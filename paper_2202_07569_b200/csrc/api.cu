@@ -100,7 +100,6 @@ struct Ctx {
     // fused tensor + INTT + tensor-core rounding over a J-CTA cluster (k_tir; env CWGPU_FUSE_TIR=0
     // off); -1 = not yet probed, 0 = unavailable for these parameters, 1 = on
     int fuse_tir = -1;
-    int dbg_skip = 0;  // diagnostics (env CWGPU_DEBUG_SKIP: 1 rounding, 2 tensor, 3 NTT+MAC; wrong answers)
     bool round_g2 = true;   // k_round_tma two-GEMM epilogue (env CWGPU_ROUND_G2=0: corrections on CUDA cores)
     u32 mac_ck = 0;         // k_ntt_mac row chunks per (component, prime) (env CWGPU_MAC_CK; 0 = auto)
     bool round_tma = true;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
@@ -1080,7 +1079,7 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         return D;
     }
     if (reg32_ok(c.cp.logN)) {
-        if (c.dbg_skip != 2) REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? (prepA_scaled ? 2 : 1) : 0));
+        REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? (prepA_scaled ? 2 : 1) : 0));
     } else {
         launch(c, k_tensor_intt, (size_t)P * J, ntt_block(N), N * 4, prepA, idxA, prepB, idxB, P, c.T, D);
     }
@@ -1092,9 +1091,7 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         const RoundK* rk = reinterpret_cast<const RoundK*>(rj + c.JM);
         const u32* im = reinterpret_cast<const u32*>(rk + kMaxJ);
         c.next_units = (double)items;  // coefficients rounded
-        if (tc && c.dbg_skip == 1) {
-            // diagnostics only (wrong answers): the pipelined cost of the rounding kernel
-        } else if (tc) {
+        if (tc) {
             const u32 g3 = (u32)std::min<size_t>(items / 128, 148 * 4);
             const uint4* Bm = c.rtc_B.ptr<uint4>();
             const uint4* B2m = c.round_g2 ? c.rtc_B2.ptr<uint4>() : nullptr;  // null: one-GEMM epilogue
@@ -1424,7 +1421,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         // TMA ring for multi-plaintext rows (C3: 37 vs 45 ms; the selection segments are reused
         // across the s payload slices); the register stream is as fast for s = 1 (C4: 22.9 ms)
         if (c.fuse_now) {
-            if (c.dbg_skip != 3) REG32_DISPATCH(c.cp.logN, ntt_mac(c, Z, zs, nc, dbt, Rt, acc));
+            REG32_DISPATCH(c.cp.logN, ntt_mac(c, Z, zs, nc, dbt, Rt, acc));
         } else if (c.mac_tma && c.s >= 2 && N >= (u32)kMacBlock && !c.old_mac) {
             // TMA-fed stream: whole waves of 3 CTAs / SM (no partial tail wave), >= 8 rows per chunk
             const u32 per = Mm * (N / kMacBlock) * c.s;
@@ -1695,7 +1692,6 @@ cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint3
         if (const char* e = std::getenv("CWGPU_ROUND_TMA")) c.round_tma = std::atoi(e) != 0;
         if (const char* e = std::getenv("CWGPU_MAC_CK")) c.mac_ck = (u32)std::max(0, std::atoi(e));
         if (const char* e = std::getenv("CWGPU_ROUND_G2")) c.round_g2 = std::atoi(e) != 0;
-        if (const char* e = std::getenv("CWGPU_DEBUG_SKIP")) c.dbg_skip = std::atoi(e);
         if (const char* e = std::getenv("CWGPU_ROUND_CTAS")) c.round_ctas = (u32)std::max(1, std::min(4, std::atoi(e)));
         if (const char* e = std::getenv("CWGPU_KS32")) c.ks32 = std::atoi(e) != 0;
         c.dcur = &c.Dbuf;
