@@ -364,6 +364,8 @@ static void build_tables(Ctx& c) {
     T.t = cp.t;
     T.gbits = 6;
     T.force_exact = (std::getenv("CWGPU_FORCE_EXACT") && std::atoi(std::getenv("CWGPU_FORCE_EXACT"))) ? 1u : 0u;
+    // D-plane stride: J, or padded to a multiple of 8 (env CWGPU_DPAD=1; experiment)
+    T.DS = (std::getenv("CWGPU_DPAD") && std::atoi(std::getenv("CWGPU_DPAD"))) ? (c.ab.J + 7) / 8 * 8 : c.ab.J;
     const Big& Q = cp.Q;
     T.QW = (cp.q_bits + 31) / 32;
     if (T.QW > (u32)kQW) throw std::invalid_argument("cwgpu: modulus too wide");
@@ -1056,9 +1058,9 @@ static bool tir_on(Ctx& c) {
 static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* prepB, const u32* idxB, u32 P,
                          bool to_mac, u64* chain_out, bool prepA_scaled = false) {
     const u32 N = c.cp.N, J = c.ab.J;
-    u32* D = c.dcur->get<u32>((size_t)P * 3 * J * N);
+    u32* D = c.dcur->get<u32>((size_t)P * 3 * c.T.DS * N);
     const bool tc = to_mac && round_tc_on(c);
-    c.zs_last = J;
+    c.zs_last = c.T.DS;
     if (tc && tir_on(c)) {
         // tensor + INTT + rounding in one cluster kernel: Z[P][3][Mm][N], coefficient domain
         const RoundK* rk = reinterpret_cast<const RoundK*>(c.round_tab.ptr<RoundJ>() + c.JM);
@@ -1132,9 +1134,9 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         if (c.fuse_now) {
             // forward NTT happens inside k_ntt_mac
         } else if (reg32_ok(c.cp.logN)) {
-            REG32_DISPATCH(c.cp.logN, sel3(c, D, P, J));
+            REG32_DISPATCH(c.cp.logN, sel3(c, D, P, c.T.DS));
         } else {
-            ntt32(c, D, P * 3 * c.ab.Mm, c.ab.Mm, J, 0, false, 0);
+            ntt32(c, D, P * 3 * c.ab.Mm, c.ab.Mm, c.T.DS, 0, false, 0);
         }
     } else {
         launch(c, k_round_chain, blocks((size_t)P * 3 * N, 128), 128, 0, (const u32*)D, P, c.T, chain_out);
@@ -1287,8 +1289,8 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
 }
 
 static u32 tile_rows(const Ctx& c) {
-    // bound the per-tile aux buffer (P x 3 x J x N u32) to ~256 MB and tree scratch
-    const size_t per = (size_t)3 * c.ab.J * c.cp.N * 4 * std::max<u32>(1, c.k / 2);
+    // bound the per-tile aux buffer (P x 3 x DS x N u32) to ~256 MB and tree scratch
+    const size_t per = (size_t)3 * c.T.DS * c.cp.N * 4 * std::max<u32>(1, c.k / 2);
     size_t r = std::max<size_t>(4, (size_t(256) << 20) / per);
     if (c.k > 2) r = std::min<size_t>(r, 64);
     if (const char* e = std::getenv("CWGPU_TILE_ROWS")) r = std::max(1, std::atoi(e));
@@ -1388,8 +1390,8 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     cudaStream_t main_st = c.st;
     if (piped) {
         // all D buffers exist before the streams diverge (allocation synchronises)
-        c.Dbuf.ensure((size_t)R * 3 * J * N * 4);
-        for (int i = 1; i < ns; ++i) c.Dmore[i - 1].ensure((size_t)R * 3 * J * N * 4);
+        c.Dbuf.ensure((size_t)R * 3 * c.T.DS * N * 4);
+        for (int i = 1; i < ns; ++i) c.Dmore[i - 1].ensure((size_t)R * 3 * c.T.DS * N * 4);
         CK(cudaEventRecord(c.tev[0], main_st));
         for (int i = 0; i < ns; ++i) CK(cudaStreamWaitEvent(c.tst[i], c.tev[0], 0));
     }

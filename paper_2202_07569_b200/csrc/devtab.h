@@ -12,6 +12,7 @@ constexpr int kAW = 44;     // 32-bit limbs for A (<= 40 * 31 bits) + headroom
 
 struct DevTab {
     std::uint32_t N, logN, L, J, Mm, Dr, Dg, relin_bits, galois_bits, QW, AW, gbits;
+    std::uint32_t DS;           // planes per (product, component) in the tensor / rounding buffer D (>= J)
     std::uint32_t force_exact;  // test knob (env CWGPU_FORCE_EXACT): every rounding / centring decision
                                 // takes the exact multiword path
     std::uint64_t t;

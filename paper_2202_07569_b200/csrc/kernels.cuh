@@ -475,7 +475,7 @@ __global__ void k_tensor_intt(const u32* __restrict__ prepA, const u32* __restri
         __syncthreads();
         ntt32_inv_smem(sm32, N, T.logN, T.airp + (size_t)j * N, T.airps + (size_t)j * N, p);
         const u32 ni = T.ninvRA[j], nis = T.ninvRA_s[j];
-        u32* out = D + (((size_t)pr * 3 + comp) * J + j) * N;
+        u32* out = D + (((size_t)pr * 3 + comp) * T.DS + j) * N;
         for (u32 x = threadIdx.x; x < N; x += blockDim.x) out[x] = red32(shoup32(sm32[x], ni, nis, p), p);
         __syncthreads();
     }
@@ -656,7 +656,7 @@ __global__ void k_round_mac(u32* __restrict__ D, u32 P, DevTab T) {
     if (idx >= (size_t)P * 3 * N) return;
     const size_t pc = idx >> T.logN;
     const u32 n = (u32)(idx & (N - 1));
-    u32* Dp = D + pc * J * N + n;
+    u32* Dp = D + pc * T.DS * N + n;
     HpsState h;
     if (hps_prepare(Dp, N, T, h)) {
         for (u32 k = 0; k < T.Mm; ++k) {
@@ -700,7 +700,7 @@ __global__ void k_round_chain(const u32* __restrict__ D, u32 P, DevTab T, u64* _
     if (idx >= (size_t)P * 3 * N) return;
     const size_t pc = idx >> T.logN;
     const u32 n = (u32)(idx & (N - 1));
-    const u32* Dp = D + pc * J * N + n;
+    const u32* Dp = D + pc * T.DS * N + n;
     u64* o = out + pc * L * N + n;
     HpsState h;
     if (hps_prepare(Dp, N, T, h)) {

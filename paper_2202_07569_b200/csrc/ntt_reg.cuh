@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, NP == 1 ? RegNtt<LOGN>::MINB 
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
         if (pr0 + q >= P) break;
-        u32* out = D + (((size_t)(pr0 + q) * 3 + comp) * J + j) * N;
+        u32* out = D + (((size_t)(pr0 + q) * 3 + comp) * T.DS + j) * N;
         if (fold == 2) {  // scale already folded into the A operands
 #pragma unroll
             for (int r = 0; r < E; ++r) out[((u32)r << (LOGN - WB)) | tid] = red32(v[q][r], p);
@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(256, 4) k_round_mac_t(u32* __restrict__ D, u32
     for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
         const size_t pc = idx >> logN;
         const u32 n = (u32)(idx & (N - 1));
-        u32* Dp = D + pc * J * N + n;
+        u32* Dp = D + pc * T.DS * N + n;
         u32 d[JM];
 #pragma unroll
         for (int j = 0; j < JM; ++j) d[j] = Dp[(size_t)min(j, (int)J - 1) * N];  // padded j: any value (w_j = 0)

@@ -293,8 +293,16 @@ ChainParams make_chain(u32 N, u64 t, const std::vector<u64>& primes, unsigned re
 }
 
 AuxBasis choose_aux_basis(const ChainParams& cp, u64 n_rows_total) {
-    // A > 2^6 * N * q^2 (|D| <= N q^2 / 2 for the tensor of centred operands).
-    Big needA = (cp.Q * cp.Q).mul_u64(u64(cp.N) << 6);
+    // |D| <= N q^2 / 2 for the tensor of centred operands (comp 1 = a0 b1 + a1 b0), and the HPS
+    // rounding needs the integer gamma = round(sum_j w_j / a_j) with sum_j w_j / a_j = gamma + D / A:
+    // A > N q^2 (1 + 2^-8) keeps |D / A| <= 1/2 - 2^-10, far outside the J 2^-16 error of the
+    // 46-bit fixed-point gamma estimate (round.cuh), and A > 2 |D| for the centred representative.
+    const Big qq = cp.Q * cp.Q;
+#ifdef CWGPU_AUX_MARGIN6  // A/B builds only: the earlier, looser bound A > 2^6 N q^2 (C2-C4: J = 16)
+    Big needA = qq.mul_u64(u64(cp.N) << 6);
+#else
+    Big needA = qq.mul_u64(u64(cp.N)) + qq.mul_u64(u64(cp.N)).div_u64(256);
+#endif
     // |sel| <= t N q / 2 + 1 (rounded tensor) or q / 2 (a lifted ciphertext);
     // |MAC| <= |sel| (t-1) N n;  M > 2^6 * 2 * |MAC|.
     Big selb = cp.Q.mul_u64(cp.t).mul_u64(cp.N).div_u64(2) + Big(1);

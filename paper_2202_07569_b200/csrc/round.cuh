@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256, JM >= 32 ? 1 : 2) k_round_hyb(u32* __rest
     for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
         const size_t pc = idx >> logN;
         const u32 n = (u32)(idx & (N - 1));
-        u32* Dp = D + pc * J * N + n;
+        u32* Dp = D + pc * T.DS * N + n;
         u32 d[JM];
 #pragma unroll
         for (int j = 0; j < JM; ++j) d[j] = Dp[(size_t)min(j, (int)J - 1) * N];  // padded j: any value (w_j = 0)
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(128, 4) k_round_tc(u32* __restrict__ D, u32 P,
         const size_t idx = base + tid;
         const size_t pc = idx >> logN;
         const u32 n = (u32)(idx & (N - 1));
-        u32* Dp = D + pc * J * N + n;
+        u32* Dp = D + pc * T.DS * N + n;
         u32 w[JM];
 #pragma unroll
         for (int j = 0; j < JM; ++j) w[j] = j < (int)J ? Dp[(size_t)j * N] : 0u;
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
                 const size_t pc = base >> logN;
                 const u32 n0 = (u32)(base & (N - 1));
                 mbar_expect_tx(&full[st], J * 512u);
-                const u32* src = D + pc * J * N + n0;
+                const u32* src = D + pc * T.DS * N + n0;
                 for (u32 j = 0; j < J; ++j) tma_bulk_g2s(&ring[st][j][0], src + (size_t)j * N, 512u, &full[st]);
             }
         }
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
         const size_t idx = (size_t)tl * 128 + tid;
         const size_t pc = idx >> logN;
         const u32 n = (u32)(idx & (N - 1));
-        u32* Dp = D + pc * J * N + n;
+        u32* Dp = D + pc * T.DS * N + n;
         mbar_wait_sleep(&full[st], (i / kRtStages) & 1);
         u32 w[JM];
 #pragma unroll

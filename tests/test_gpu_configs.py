@@ -8,7 +8,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run(reflib, cfg, rows, seed=1, select_only=False):
+def _run(reflib, cfg, rows, seed=1, select_only=False, expect_kernel=None):
     from oracle import RefBackend
     from paper_2202_07569_b200 import Client, Context, configs
 
@@ -29,7 +29,11 @@ def _run(reflib, cfg, rows, seed=1, select_only=False):
     db = configs.db_payload(cfg, seed, 0, rows)
     want, _ = be.answer(q, cfg.c, cfg.m, pos, db, op=cfg.op)
     ctx.load_db(pos, db, n_total=rows, m=cfg.m)
+    if expect_kernel:
+        ctx.set_profiling(True)
     got = ctx.answer(q, cfg.c, cfg.m, op=cfg.op, keys=keys)
+    if expect_kernel:
+        assert expect_kernel in ctx.kernel_stats(), f"{expect_kernel} did not run"
     assert np.array_equal(got, want)
     for j in range(cfg.s):
         assert np.array_equal(client.decrypt(got[j]), db[target, j])
@@ -101,12 +105,17 @@ def test_payload_mac_kernels_agree_under_repetition(gpu, monkeypatch):
     {"CWGPU_FORCE_EXACT": "1", "CWGPU_FUSE_TIR": "1"},  # ... inside the cluster kernel
 ], ids=["unfused", "default", "mac-regs", "mac-tma", "tir", "tir-unfused-mac", "exact", "exact-tir"])
 def test_answer_path_variants_match_reference(gpu, reflib, monkeypatch, env):
-    """Every kernel variant of the C4 answer path (tensor/rounding/NTT/MAC fusions, TMA feeds,
-    the exact multiword rounding inside each engine) against the reference at full C4 parameters,
-    over ragged 16-row tiles alternating between the two tile streams."""
+    """Every kernel variant of the answer path (tensor/rounding/NTT/MAC fusions, TMA feeds, the
+    exact multiword rounding inside each engine) against the reference at full C4 parameters (the
+    cluster kernel at C1's), over ragged 16-row tiles rotating over the tile streams."""
     from paper_2202_07569_b200 import configs
 
     monkeypatch.setenv("CWGPU_TILE_ROWS", "16")
     for k, v in env.items():
         monkeypatch.setenv(k, v)
-    _run(reflib, configs.config("C4"), 40)
+    if env.get("CWGPU_FUSE_TIR") == "1":
+        # the cluster kernel needs one CTA per aux prime with N / J a multiple of 128: C1 (J = 8);
+        # C2-C4 use J = 15 aux primes
+        _run(reflib, configs.config("C1"), 40, expect_kernel="k_tir")
+    else:
+        _run(reflib, configs.config("C4"), 40, expect_kernel="k_round_tc")
