@@ -737,6 +737,7 @@ static void set_smem_limits(u32 N) {
         constexpr int LN = JMv == 16 ? 13 : JMv == 8 ? 12 : JMv == 32 ? 14 : 0;                                     \
         CK(cudaFuncSetAttribute(k_round_tma<LN, JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
         if (LN == 13) CK(cudaFuncSetAttribute(k_round_tma<LN, JMv, NCv, 11>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
+        if (LN == 13) CK(cudaFuncSetAttribute(k_round_tma<LN, JMv, NCv, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
     }
     RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
 #undef RTC
@@ -1105,6 +1106,9 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
             constexpr int LN = JMv == 16 ? 13 : JMv == 8 ? 12 : JMv == 32 ? 14 : 0;                              \
             if (LN == 13 && c.cp.logN == 13 && c.ab.Mm == 11)                                                    \
                 launch_named(c, "k_round_tc", k_round_tma<LN, JMv, NCv, 11>, gr, 160, round_tma_smem<JMv>(), D, P,  \
+                             c.T, rp, Bm, rk, B2m);                                                               \
+            else if (LN == 13 && c.cp.logN == 13 && c.ab.Mm == 10)                                               \
+                launch_named(c, "k_round_tc", k_round_tma<LN, JMv, NCv, 10>, gr, 160, round_tma_smem<JMv>(), D, P,  \
                              c.T, rp, Bm, rk, B2m);                                                               \
             else if (LN != 0 && c.cp.logN == (u32)LN)                                                             \
                 launch_named(c, "k_round_tc", k_round_tma<LN, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T, \

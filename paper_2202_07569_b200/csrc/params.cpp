@@ -304,9 +304,16 @@ AuxBasis choose_aux_basis(const ChainParams& cp, u64 n_rows_total) {
     Big needA = qq.mul_u64(u64(cp.N)) + qq.mul_u64(u64(cp.N)).div_u64(256);
 #endif
     // |sel| <= t N q / 2 + 1 (rounded tensor) or q / 2 (a lifted ciphertext);
-    // |MAC| <= |sel| (t-1) N n;  M > 2^6 * 2 * |MAC|.
+    // |MAC| <= |sel| (t-1) N n;  M > 2 |MAC| (1 + 2^-20): the centred value, and the MAC -> chain
+    // conversion's gamma = round(sum v_k / m_k) (58-bit fixed point, error < Mm 2^-28) stays exact
+    // with |MAC / M| < 1/2 - 2^-22.  (The first version asked M > 2^7 |MAC|: C3 / C4 Mm = 11, now 10.)
     Big selb = cp.Q.mul_u64(cp.t).mul_u64(cp.N).div_u64(2) + Big(1);
-    Big needM = selb.mul_u64(cp.t - 1).mul_u64(cp.N).mul_u64(std::max<u64>(n_rows_total, 1)).mul_u64(128);
+    Big mac2 = selb.mul_u64(cp.t - 1).mul_u64(cp.N).mul_u64(std::max<u64>(n_rows_total, 1)).mul_u64(2);
+#ifdef CWGPU_AUX_MARGIN6
+    Big needM = mac2.mul_u64(64);
+#else
+    Big needM = mac2 + mac2.div_u64(u64(1) << 20);
+#endif
     AuxBasis ab;
     // 30-bit NTT-friendly primes, descending below 2^30: 4p < 2^32 allows Harvey-style lazy
     // butterflies in 32-bit words and 16 residue products fit one u64 accumulator.
