@@ -1,6 +1,7 @@
-set -x
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/s_default.json 2> gpurun_out/s_default.err
-for R in 16 32 64; do for S in 2 4; do
-CWGPU_TILE_ROWS=$R CWGPU_STREAMS=$S python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-verify 2>>gpurun_out/sweep.err | python scripts/bench_brief.py R=$R S=$S >> gpurun_out/sweep.txt
+# tile rows x tile streams sweep of the C4 bench (pipelined ms per answer); results -> gpurun_out/sweep.txt
+mkdir -p gpurun_out
+rm -f gpurun_out/sweep.txt
+for R in 0 128 256 364; do for S in 2 3 4; do
+if [ "$R" = "0" ]; then unset CWGPU_TILE_ROWS; else export CWGPU_TILE_ROWS=$R; fi
+CWGPU_STREAMS=$S timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-verify 2>>gpurun_out/sweep.err | python scripts/bench_brief.py R=$R S=$S >> gpurun_out/sweep.txt
 done; done
-python bench.py --steps 3 --warmup 3 --no-cpu-baseline | python scripts/bench_brief.py default >> gpurun_out/sweep.txt
