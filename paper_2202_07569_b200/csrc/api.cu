@@ -617,6 +617,7 @@ static void ensure_aux(Ctx& c, u64 n_total) {
     c.ab = nb;
     build_tables(c);
     c.ksA_ok = false;
+    c.fuse_tir = -1;  // the cluster-kernel instance depends on J and the rounding width
 }
 
 // ------------------------------------------------------------------ NTT launchers
