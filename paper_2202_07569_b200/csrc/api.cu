@@ -1069,8 +1069,10 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         const uint4* Bm = c.rtc_B.ptr<uint4>();
         const int fold = prepA_scaled ? 2 : 1;
         c.zs_last = c.ab.Mm;
+        bool launched = false;
 #define X(L, CL, JMv, NCv)                                                                                        \
-    if (tir_match(c, L, CL, JMv, NCv)) {                                                                          \
+    if (!launched && tir_match(c, L, CL, JMv, NCv)) {                                                             \
+        launched = true;                                                                                          \
         c.next_cluster = CL;                                                                                      \
         c.next_units = (double)P * 3 * CL;                                                                        \
         launch_named(c, "k_tir", k_tir<L, CL, JMv, NCv>, (size_t)P * 3 * CL, Tir<L, CL>::T, Tir<L, CL>::SMEM,      \
@@ -1079,6 +1081,7 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
     }
         TIR_LIST(X)
 #undef X
+        if (!launched) throw std::logic_error("cluster kernel enabled without a matching instance");
         if (!c.fuse_now) REG32_DISPATCH(c.cp.logN, sel3(c, D, P, c.ab.Mm));
         return D;
     }
