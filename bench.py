@@ -106,6 +106,12 @@ def rooflines(kstats, cfg, info, hbm, hbm_kind):
                  "hbm_view": {"achieved": mac_bytes / per_launch_s / 1e9, "peak": hbm, "unit": "GB/s",
                               "frac": mac_bytes / per_launch_s / 1e9 / hbm,
                               "bytes_per_launch": mac_bytes, "what": "selection + payload words streamed"}}
+        elif name == "k_round_chain":
+            # exact rounding into the chain (selection output): J residue words read, L u64 written
+            byt = units / cnt * (info.J * 4 + cfg.L * 8)
+            ach = byt / per_launch_s / 1e9
+            r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "peak_kind": hbm_kind,
+                 "work_per_launch": f"{units / cnt:.0f} coefficients x (4 J + 8 L) B"}
         elif name.startswith("k_round"):
             byt = units / cnt * (info.J + info.Mm) * 4
             ach = byt / per_launch_s / 1e9
@@ -189,28 +195,50 @@ def make_inputs(cfg, rank, world, seed=1):
     return client, keys, query, positions, target, lo, hi
 
 
-def cpu_reference_sample(cfg, keys, query, positions, seed=1, sample_rows=None):
-    """The reference's own CPU path (oracle/_ref) on a bounded row sample, extrapolated.
-
-    Times expand_query + prepare_cipher (fixed per query), selection + inner product on
-    `sample_rows` rows (linear in rows), finalize; returns the extrapolated full answer."""
+def reference_inputs(cfg, seed=1):
+    """Keys and query for the reference arm from the REFERENCE itself (oracle/_ref: bfv_keygen with
+    Seed256::from_u64(seed), pack_query_bits from encryption index 1) -- the same words the repo's
+    client produces (pinned by tests/test_cpu_host.py), without mapping any repo library."""
     import oracle
     from paper_2202_07569_b200 import configs
 
     ref = oracle.RefLib()
     be = oracle.RefBackend(ref, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), relin_bits=cfg.relin_bits,
-                           galois_bits=cfg.galois_bits, keys=(keys.relin, keys.galois))
-    R = sample_rows or min(cfg.n, {"C1": 1024}.get(cfg.name, 512 if cfg.k <= 2 else 16))
+                           galois_bits=cfg.galois_bits, seed=seed, galois_levels=cfg.c)
+    positions = configs.db_positions(cfg, seed)
+    target = configs.query_row(cfg, seed)
+    query = be.pack_query(configs.codeword_bits(positions[target], cfg.m), cfg.c)
+    return ref, be, query, positions
+
+
+def cpu_reference_sample(cfg, be, ref, query, positions, seed=1, sample_rows=None):
+    """The reference's own CPU path (oracle/_ref: expand_query, prepare_cipher, the per-row
+    equality, weighted_sum, finalize -- pir.cpp:337-347's composition) on a bounded row sample.
+
+    The sample's plaintexts are prepared (NTT form, prepare_plain) outside the timed stages, as
+    the reference does offline (PirDatabase::prepare_for, pir.cpp:255-264).  The full answer is
+    extrapolated: fixed per-query stages (expansion, prepare_cipher, finalize) as measured, plus
+    the sample's per-row selection + inner-product time times n."""
+    from paper_2202_07569_b200 import configs
+
+    R = min(cfg.n, sample_rows or 4096)
     db = configs.db_payload(cfg, seed, 0, R)
     t0 = time.perf_counter()
     _, st = be.answer(query, cfg.c, cfg.m, positions[:R], db, op=cfg.op, tile_rows=R)
     wall = time.perf_counter() - t0
-    t_expand, t_select, t_inner, t_final, t_prep = [x / 1e3 for x in st]
+    t_expand, t_select, t_inner, t_final, t_prep, t_plain = [x / 1e3 for x in st]
     per_row = (t_select - t_prep + t_inner) / R
     full = t_expand + t_prep + per_row * cfg.n + t_final
     return {"seconds_full": full, "sample_rows": R, "sample_wall_s": wall, "threads": ref.worker_threads(),
-            "stages_s": {"expand": t_expand, "prepare": t_prep, "select_per_row": (t_select - t_prep) / R,
-                         "inner_per_row": t_inner / R, "finalize": t_final}}
+            "stages_s": {"expand": t_expand, "prepare_cipher": t_prep, "select_per_row": (t_select - t_prep) / R,
+                         "inner_per_row": t_inner / R, "finalize": t_final,
+                         "prepare_plain_untimed": t_plain}}
+
+
+def sample_rows_for(cfg, per_row_s, steps, budget_s=150.0):
+    """Rows per reference sample so that `steps` samples take about budget_s (>= 256 rows)."""
+    rows = int(budget_s / max(steps, 1) / max(per_row_s, 1e-6))
+    return int(min(cfg.n, max(256, min(rows, 8192))))
 
 
 def cpu_model():
@@ -231,36 +259,204 @@ def workload_desc(cfg):
 
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args, cfg):
+    """--impl reference: the reference's CPU implementation (oracle/_ref) on all host cores,
+    keys / query / rows generated by the reference itself (no repo library is loaded)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_2202_07569_b200 import Client, configs
-
-    positions = configs.db_positions(cfg, 1)
-    target = configs.query_row(cfg, 1)
-    client = Client(cfg.N, cfg.primes, cfg.t, seed=1, galois_levels=cfg.c)
-    keys = client.keys()
-    query = client.pack_query(configs.codeword_bits(positions[target], cfg.m), cfg.c, first_index=1)
-    for _ in range(args.warmup):
-        cpu_reference_sample(cfg, keys, query, positions, sample_rows=args.cpu_sample_rows or 64)
-    runs = [cpu_reference_sample(cfg, keys, query, positions, sample_rows=args.cpu_sample_rows)
-            for _ in range(args.steps)]
+    ref, be, query, positions = reference_inputs(cfg)
+    if cfg.s == 0:
+        return run_reference_select(args, cfg, ref, be, query, positions)
+    probe = cpu_reference_sample(cfg, be, ref, query, positions, sample_rows=min(cfg.n, 256))
+    per_row = probe["stages_s"]["select_per_row"] + probe["stages_s"]["inner_per_row"]
+    R = args.cpu_sample_rows or sample_rows_for(cfg, per_row, args.steps)
+    for _ in range(max(0, args.warmup - 1)):
+        cpu_reference_sample(cfg, be, ref, query, positions, sample_rows=min(R, 256))
+    runs, walls = [], []
+    for _ in range(args.steps):
+        runs.append(cpu_reference_sample(cfg, be, ref, query, positions, sample_rows=R))
+        walls.append(runs[-1]["sample_wall_s"])
     secs = statistics.median(r["seconds_full"] for r in runs)
     gbps = cfg.db_bytes() / secs / 1e9
+    sample = (f"each step: expand_query + prepare_cipher of the full query, then selection + weighted_sum on "
+              f"{R} of {cfg.n} rows (plaintexts prepared beforehand, as prepare_for does offline), finalize; "
+              f"full answer extrapolated linearly in rows ({secs:.1f} s); {runs[0]['threads']} threads, CPU {cpu_model()}")
     line = {
-        "impl": "reference", "metric": "db_GBps_scanned", "value": gbps, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded)",
-        "config": {"workload": workload_desc(cfg), "db_bytes": cfg.db_bytes()},
+        "impl": "reference", "metric": METRIC, "value": gbps, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(walls) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (seeded rows/keys/query)", "config": bench_config(cfg),
         "cpu_baseline": {"value": gbps, "unit": "GB/s", "cores": runs[0]["threads"], "kind": "reference",
-                         "sample": f"expand+prepare of the full query, selection+inner product on "
-                                   f"{runs[0]['sample_rows']} of {cfg.n} rows, extrapolated linearly in rows; "
-                                   f"CPU {cpu_model()}", "stages_s": runs[0]["stages_s"]},
+                         "sample": sample, "stages_s": runs[0]["stages_s"]},
         "e2e": {"value": gbps, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "answer_ms": secs * 1e3,
+        "note": "ms_per_step is the measured wall time of one sample step; value and answer_ms are the "
+                "full-database answer extrapolated from it",
     }
     print(json.dumps(line))
     return 0
+
+
+def reference_select_sample(cfg, be, ref, query, positions, rows):
+    """Config 2 on the reference: expand_query + prepare_cipher of the full query, then
+    compute_selection_vector's per-row equality on `rows` of the 16384 codewords; the full
+    selection time is extrapolated linearly in rows."""
+    R = min(cfg.n, rows)
+    t0 = time.perf_counter()
+    _, _, st = be.select(query, cfg.c, cfg.m, positions[:R], stages=True)
+    wall = time.perf_counter() - t0
+    t_expand, t_prep, t_sel = [x / 1e3 for x in st]
+    full = t_expand + t_prep + t_sel / R * cfg.n
+    return {"seconds_full": full, "sample_rows": R, "sample_wall_s": wall, "threads": ref.worker_threads(),
+            "stages_s": {"expand": t_expand, "prepare_cipher": t_prep, "select_per_row": t_sel / R}}
+
+
+def run_reference_select(args, cfg, ref, be, query, positions):
+    probe = reference_select_sample(cfg, be, ref, query, positions, 64)
+    R = args.cpu_sample_rows or sample_rows_for(cfg, probe["stages_s"]["select_per_row"], args.steps)
+    runs = [reference_select_sample(cfg, be, ref, query, positions, R) for _ in range(args.steps)]
+    secs = statistics.median(r["seconds_full"] for r in runs)
+    eqs = cfg.n / secs
+    line = {
+        "impl": "reference", "metric": SELECT_METRIC, "value": eqs, "unit": "equalities/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(r["sample_wall_s"] for r in runs) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded codewords/keys/query)",
+        "config": bench_config(cfg),
+        "cpu_baseline": {"value": eqs, "unit": "equalities/s", "cores": runs[0]["threads"], "kind": "reference",
+                         "sample": f"each step: expand_query + prepare_cipher of the full query, then the per-row "
+                                   f"equality on {R} of {cfg.n} codewords; extrapolated linearly in rows "
+                                   f"({secs:.1f} s for all); CPU {cpu_model()}", "stages_s": runs[0]["stages_s"]},
+        "e2e": {"value": eqs, "unit": "equalities/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "select_ms": secs * 1e3,
+        "note": "ms_per_step is the measured wall time of one sample step; value is the full 16384-codeword "
+                "selection extrapolated from it",
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_select_bench(args, cfg):
+    """Config 2 (equality-operator microbenchmark): compute_selection_vector over the 16384
+    seeded weight-k codewords, no payload.  value: equalities per second with the query and keys
+    resident and the selection written to device memory (expansion included: it is part of the
+    operator's cost, and at k = 1 it is all of it); e2e: the same through cwg_select with the
+    query and keys from pinned host memory and the whole selection (n x 3 x L x N words) read back."""
+    import ctypes
+
+    import torch
+
+    from paper_2202_07569_b200 import Context
+    from paper_2202_07569_b200.cwgpu import CwgTimings
+
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        raise SystemExit("the config-2 microbenchmark runs on one GPU")
+    client, keys, query, positions, target, lo, hi = make_inputs(cfg, 0, 1)
+    options = {kv.split("=", 1)[0]: int(kv.split("=", 1)[1]) for kv in args.opt}
+    ctx = Context(cfg.N, cfg.primes, cfg.t, relin_bits=cfg.relin_bits, galois_bits=cfg.galois_bits, options=options)
+    ctx.load_db(positions, None, m=cfg.m)
+    ctx.set_keys(keys)
+    info = ctx.info()
+    LN = cfg.L * cfg.N
+    sel = torch.empty(cfg.n * 3 * LN, dtype=torch.int64, device="cuda")
+    ext = torch.cuda.ExternalStream(ctx.stream())
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    hrelin = torch.from_numpy(keys.relin.view(np.int64).reshape(-1).copy()).pin_memory()
+    hgal = torch.from_numpy(keys.galois.view(np.int64).reshape(-1).copy()).pin_memory()
+    hg = np.ascontiguousarray(keys.exponents(cfg.N))
+    key_ptrs = (ctypes.cast(hrelin.data_ptr(), u64p), keys.galois.shape[0], hg.ctypes.data_as(u64p),
+                ctypes.cast(hgal.data_ptr(), u64p))
+    hq = np.ascontiguousarray(query)
+    hsel = np.empty(cfg.n * 3 * LN, np.uint64)
+
+    def timed(fn, steps):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        for _ in range(steps):
+            fn()
+        e1.record(ext)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    step = lambda: ctx.select_ptr(hq, cfg.c, cfg.m, sel.data_ptr())
+    for _ in range(args.warmup):
+        step()
+    l0 = ctx.kernel_launches()
+    clk = ClockSampler(0)
+    clk.start()
+    ms = timed(step, args.steps)
+    clocks = clk.stop()
+    launches = (ctx.kernel_launches() - l0) // args.steps
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        comps = ctx.select_ptr(hq, cfg.c, cfg.m, hsel.ctypes.data, keys_ptrs=key_ptrs)
+    ms_e2e = (time.perf_counter() - t0) / e2e_steps * 1e3
+    verified = None
+    if not args.no_verify:  # matching rows decrypt to 1, the others to 0 (constant coefficient)
+        dsel = sel.cpu().numpy().view(np.uint64).reshape(cfg.n, 3, cfg.L, cfg.N)
+        match = np.all(positions == positions[target], axis=1)
+        picks = list(np.flatnonzero(match)[:4]) + list(np.flatnonzero(~match)[:4])
+        verified = bool(all(client.decrypt(dsel[r, :comps[r]])[0] == int(match[r]) for r in picks)) and bool(
+            np.array_equal(hsel.reshape(dsel.shape), dsel))
+        del dsel
+    ctx.set_profiling(True)
+    tm = CwgTimings()
+    ctx.select_ptr(hq, cfg.c, cfg.m, sel.data_ptr(), timings=tm)
+    kstats = ctx.kernel_stats(units=True)
+    ctx.set_profiling(False)
+    hbm, peak_kind = peaks()
+    roof = rooflines(kstats, cfg, info, hbm, peak_kind)
+    tot = sum(v[0] for v in kstats.values())
+    dom = max(kstats.items(), key=lambda kv: kv[1][0]) if kstats else ("", (0, 0, 0))
+    top = dict(roof.get(dom[0], {}))
+    if top:
+        top = {"kernel": dom[0], **top, "share_of_step": dom[1][0] / tot if tot else None}
+    line = {
+        "metric": SELECT_METRIC, "value": cfg.n / (ms / 1e3), "unit": "equalities/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded codewords/keys/query)",
+        "config": bench_config(cfg),
+        "layout": {"rows_per_gpu": cfg.n, "l2": "selection output 16 GB >> L2", "aux_primes": info.J},
+        "select_ms": ms,
+        "e2e": {"value": cfg.n / (ms_e2e / 1e3), "unit": "equalities/s", "select_ms": ms_e2e,
+                "h2d_bytes_per_step": int(query.nbytes + keys.relin.nbytes + keys.galois.nbytes),
+                "d2h_bytes_per_step": int(hsel.nbytes + 4 * cfg.n), "timing": "host wall clock (synchronous call)"},
+        "gpu_launches": int(launches), "clocks": clocks, "roofline": top or None, "rooflines": roof,
+        "kernels_ms_per_step": {k: round(v[0], 3) for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
+        "stages_ms": {k: getattr(tm, k) for k in ("expand_ms", "select_ms")},
+        "exact_fallbacks": int(tm.exact_fallbacks), "verified_decrypt": verified,
+    }
+    if not args.no_cpu_baseline:
+        try:
+            import oracle
+
+            ref = oracle.RefLib()
+            be = oracle.RefBackend(ref, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), keys=(keys.relin, keys.galois))
+            probe = reference_select_sample(cfg, be, ref, query, positions, 64)
+            R = args.cpu_sample_rows or sample_rows_for(cfg, probe["stages_s"]["select_per_row"], 1, budget_s=20.0)
+            cb = reference_select_sample(cfg, be, ref, query, positions, R)
+            line["cpu_baseline"] = {
+                "value": cfg.n / cb["seconds_full"], "unit": "equalities/s", "cores": cb["threads"], "kind": "reference",
+                "sample": f"reference compute_selection_vector (oracle/_ref): expand_query + prepare_cipher of the "
+                          f"full query, per-row equality on {R} of {cfg.n} codewords, extrapolated linearly in rows "
+                          f"({cb['seconds_full']:.1f} s for all); CPU {cpu_model()}",
+                "select_s": cb["seconds_full"], "stages_s": cb["stages_s"]}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "unit": "equalities/s", "cores": os.cpu_count(),
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    print(json.dumps(line))
+    return 0
+
+
+SELECT_METRIC = "equalities_per_s"
+METRIC = "db_GBps_scanned"
+
+
+def bench_config(cfg):
+    """The `config` object, identical in both arms for the same workload."""
+    return {"workload": workload_desc(cfg), "db_bytes": cfg.db_bytes()}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -275,6 +471,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N > 1 collectives: nccl (one GPU per rank) or gloo (host-staged; ranks may share a GPU)")
+    ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
+                    help="library option (cwg_set_option), e.g. --opt tile_rows=256 --opt streams=2")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "cwgpu" else args.warmup
 
@@ -285,6 +485,8 @@ def main():
         cfg.n = args.rows
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if cfg.s == 0:
+        return run_select_bench(args, cfg)
 
     import torch
 
@@ -294,17 +496,25 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # --dist-backend gloo (harness only): ranks may share a GPU, collectives host-staged
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     client, keys, query, positions, target, lo, hi = make_inputs(cfg, rank, world)
     payload = configs.db_payload(cfg, 1, lo, hi)
-    ctx = Context(cfg.N, cfg.primes, cfg.t, relin_bits=cfg.relin_bits, galois_bits=cfg.galois_bits, device=local)
+    options = {kv.split("=", 1)[0]: int(kv.split("=", 1)[1]) for kv in args.opt}
+    ctx = Context(cfg.N, cfg.primes, cfg.t, relin_bits=cfg.relin_bits, galois_bits=cfg.galois_bits, device=local,
+                  options=options)
     t_load = time.perf_counter()
     ctx.load_db(positions[lo:hi], payload, n_total=cfg.n, row_begin=lo, m=cfg.m)
     t_load = time.perf_counter() - t_load
@@ -328,49 +538,24 @@ def main():
     key_ptrs = (ctypes.cast(hrelin.data_ptr(), u64p), keys.galois.shape[0], hg.ctypes.data_as(u64p),
                 ctypes.cast(hgal.data_ptr(), u64p))
     h_q = query.shape[0]
-    partial = None
-    # N > 1: the expansion is sharded too when the query is one ciphertext -- rank r expands the
-    # subtree of leaves r, r+W, ... (cwg_expand_shard) and an all-gather hands every rank all
-    # entries, so the per-query fixed cost shrinks with W instead of being replicated
-    shard = world > 1 and h_q == 1 and (world & (world - 1)) == 0 and world <= (1 << cfg.c) \
-        and os.environ.get("CWGPU_SHARD_EXPAND", "1") != "0"
+    rs = None
     if world > 1:
-        partial = torch.zeros(ctx.partial_words(), dtype=torch.int64, device="cuda")
-    if shard:
-        ent_words = 2 * L * N
-        shard_local = torch.zeros(ctx.shard_entries(cfg.c, world) * ent_words, dtype=torch.int64, device="cuda")
-        shards_all = torch.zeros(world * shard_local.numel(), dtype=torch.int64, device="cuda")
+        from paper_2202_07569_b200.rowshard import RowShardStep
 
-    def after_collective():
-        # the library runs on its own stream: order it after the collective on torch's stream
-        ext.wait_stream(torch.cuda.current_stream())
-
-    def step_partial(q_ptr, kp):
-        if shard:
-            ctx.expand_shard_ptr(q_ptr, cfg.c, world, rank, shard_local.data_ptr(), keys_ptrs=kp)
-            dist.all_gather_into_tensor(shards_all, shard_local)
-            after_collective()
-            ctx.answer_partial_shards_ptr(shards_all.data_ptr(), world, cfg.c, cfg.m, cfg.op, partial.data_ptr())
-        else:
-            ctx.answer_partial_ptr(q_ptr, h_q, cfg.c, cfg.m, cfg.op, partial.data_ptr(), keys_ptrs=kp)
-        dist.reduce(partial, dst=0)
-        after_collective()
+        rs = RowShardStep(ctx, cfg, rank, world, backend=args.dist_backend)
+    shard = rs is not None and rs.shard
 
     def step_value():
         if world == 1:
             ctx.answer_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, dout.data_ptr())
         else:
-            step_partial(dq.data_ptr(), (None, 0, None, None))
-            if rank == 0:
-                ctx.finish(partial.data_ptr(), cfg.op, out=dout.data_ptr())
+            rs.step(dq.data_ptr(), dout.data_ptr())
 
     def step_e2e():
         if world == 1:
             ctx.answer_ptr(hq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, hout.data_ptr(), keys_ptrs=key_ptrs)
         else:
-            step_partial(hq.data_ptr(), key_ptrs)
-            if rank == 0:
-                ctx.finish(partial.data_ptr(), cfg.op, out=hout.data_ptr())
+            rs.step(hq.data_ptr(), hout.data_ptr(), key_ptrs)
 
     def timed(fn, steps):
         if dist:
@@ -421,7 +606,7 @@ def main():
     if world == 1:
         ctx.answer_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, dout.data_ptr(), timings=tm)
     else:
-        ctx.answer_partial_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, partial.data_ptr(), timings=tm)
+        ctx.answer_partial_ptr(dq.data_ptr(), h_q, cfg.c, cfg.m, cfg.op, rs.partial.data_ptr(), timings=tm)
     kstats = ctx.kernel_stats(units=True)
     ctx.set_profiling(False)
 
@@ -442,13 +627,14 @@ def main():
     if top:
         top = {"kernel": dom[0], **top, "share_of_step": dom[1][0] / tot_prof if tot_prof else None}
     line = {
-        "metric": "db_GBps_scanned", "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded rows/keys/query)",
-        "config": {"workload": workload_desc(cfg), "db_bytes": db_bytes, "rows_per_gpu": local_rows,
-                   "parallelism": f"row-shard x{world}" + (" + expansion-shard (all-gather)" if shard else ""), "l2": "no flush: 21.5 GB DB >> 126 MB L2"
-                   if cfg.name == "C4" else "inputs larger than L2" if db_bytes > 2e8 else "small (L2-resident)",
-                   "aux_primes": info.J, "mac_primes": info.Mm},
+        "config": bench_config(cfg),
+        "layout": {"rows_per_gpu": local_rows,
+                   "parallelism": f"row-shard x{world}" + (" + expansion-shard (all-gather)" if shard else ""),
+                   "l2": "no flush: DB >> 126 MB L2" if db_bytes > 2e9 else "inputs larger than L2" if db_bytes > 2e8
+                   else "small (L2-resident)", "aux_primes": info.J, "mac_primes": info.Mm},
         "answer_ms": ms,
         "e2e": {"value": e2e, "unit": "GB/s", "answer_ms": ms_e2e,
                 "h2d_bytes_per_step": int(query.nbytes + keys.relin.nbytes + keys.galois.nbytes),
@@ -467,13 +653,22 @@ def main():
     }
     if world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_sample(cfg, keys, query, positions, sample_rows=args.cpu_sample_rows or None)
+            import oracle
+
+            ref = oracle.RefLib()
+            be = oracle.RefBackend(ref, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), relin_bits=cfg.relin_bits,
+                                   galois_bits=cfg.galois_bits, keys=(keys.relin, keys.galois))
+            probe = cpu_reference_sample(cfg, be, ref, query, positions, sample_rows=min(cfg.n, 256))
+            per_row = probe["stages_s"]["select_per_row"] + probe["stages_s"]["inner_per_row"]
+            R = args.cpu_sample_rows or sample_rows_for(cfg, per_row, 1, budget_s=20.0)
+            cb = cpu_reference_sample(cfg, be, ref, query, positions, sample_rows=R)
             line["cpu_baseline"] = {
                 "value": db_bytes / cb["seconds_full"] / 1e9, "unit": "GB/s", "cores": cb["threads"],
                 "kind": "reference",
-                "sample": f"reference process_query composition (oracle/_ref): expand+prepare of the query and "
-                          f"selection+inner product on {cb['sample_rows']} of {cfg.n} rows, extrapolated linearly "
-                          f"in rows ({cb['seconds_full']:.1f} s full answer); CPU {cpu_model()}",
+                "sample": f"reference process_query composition (oracle/_ref): expand_query + prepare_cipher of the "
+                          f"full query, selection + weighted_sum on {cb['sample_rows']} of {cfg.n} rows (plaintexts "
+                          f"prepared beforehand, as prepare_for does offline), finalize; extrapolated linearly in "
+                          f"rows ({cb['seconds_full']:.1f} s full answer); CPU {cpu_model()}",
                 "answer_s": cb["seconds_full"], "stages_s": cb["stages_s"]}
         except Exception as e:  # the baseline must not hide the GPU line
             line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",

@@ -56,15 +56,33 @@ typedef struct cwg_timings {
     double d2h_ms;
     uint64_t kernel_launches;
     uint64_t exact_fallbacks; /* coefficients decided by the multiword slow path (this answer) */
+    uint32_t keys_cached;     /* 1: the keys passed with this call equalled the resident set (device
+                                 key cache: upload compared on the device, aux-basis transform kept) */
+    uint32_t n_devices;       /* devices that worked on this call */
 } cwg_timings;
 
 const char* cwg_last_error(void);
+
+/* Number of CUDA devices visible to this process (0 without a driver / device). */
+int cwg_device_count(void);
 
 /* BfvContext equivalent (bfv.cpp:67-129) on one device.  q: L chain primes
  * (each 2^32 < q_i < 2^60, NTT-friendly), t: plaintext prime, digit widths as
  * HeParams::relin_digit_bits / galois_digit_bits (0 = one digit per prime). */
 cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint32_t relin_digit_bits,
                     uint32_t galois_digit_bits, int device);
+/* The same over several devices of this process (SURVEY 8b's device_ids / n_devices): the rows
+ * of cwg_load_db / cwg_load_db_bytes are split contiguously across device_ids (a device id may
+ * repeat: two contexts on one GPU); cwg_answer expands the query on every device (sharded by
+ * subtree and all-gathered by peer copies when the query is one ciphertext and n_devices is a
+ * power of two <= 2^c), runs each device's rows into partial accumulators, sums them on
+ * device_ids[0] (peer copies + one add kernel per device) and finishes there.  Bit-identical to
+ * one device.  cwg_select writes each device's rows to a host buffer; set_keys / set_option apply
+ * to all devices; the stage entry points (cwg_ntt ... cwg_substitute) and profiling use
+ * device_ids[0]; the per-process row-shard calls (cwg_answer_partial, cwg_finish, ...) need a
+ * single-device context. */
+cwg_ctx* cwg_create_multi(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint32_t relin_digit_bits,
+                          uint32_t galois_digit_bits, const int* device_ids, int n_devices);
 void cwg_destroy(cwg_ctx* ctx);
 int cwg_get_info(const cwg_ctx* ctx, cwg_info* out);
 
@@ -84,6 +102,12 @@ int cwg_load_db(cwg_ctx* ctx, uint64_t n_total, uint64_t row_begin, uint64_t n_l
  * all-zero payloads, duplicate identifiers, ids outside the code capacity. */
 int cwg_load_db_bytes(cwg_ctx* ctx, uint64_t n_total, uint64_t row_begin, uint64_t n_local, uint32_t k, uint32_t m,
                       uint64_t payload_bytes, const uint8_t* payloads, const uint64_t* row_ids);
+
+/* The reference's database file (CWDB v1, db_file.cpp:34-59: header + length-prefixed key /
+ * payload records; index or non-lossy keyword mode) parsed from memory and loaded as
+ * cwg_load_db_bytes does (codewords and plaintext chunks built on the device).  k, m: the
+ * PirConfig's Hamming weight and code length.  Errors as parse_db / PirDatabase::setup. */
+int cwg_load_db_file(cwg_ctx* ctx, const uint8_t* data, uint64_t size, uint32_t k, uint32_t m);
 
 /* Evaluation keys (EvalKeySet, bfv.hpp:42-51).  Kept resident until replaced. */
 int cwg_set_keys(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
@@ -122,7 +146,9 @@ int cwg_answer_partial_shards(cwg_ctx* ctx, const uint64_t* shards, uint32_t wor
                               uint32_t op, uint64_t* dev_partial, cwg_timings* t);
 
 /* compute_selection_vector (pir.cpp:277-312) without a payload (config 2): sel is
- * [n_local][3][L][N]; comps[r] receives 2 or 3 (a 2-component row leaves slot 2 zero). */
+ * [n_local][3][L][N] in host memory or (single-device context) device memory -- then the tiles
+ * are written in place with no copy back; comps (host) [r] receives 2 or 3 (a 2-component row
+ * leaves slot 2 zero). */
 int cwg_select(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
                const uint64_t* galois, uint32_t h, uint32_t c, uint32_t m, const uint64_t* query,
                uint32_t op, uint64_t* sel, uint32_t* comps, cwg_timings* t);
@@ -140,8 +166,14 @@ int cwg_relinearize(cwg_ctx* ctx, uint32_t count, const uint64_t* ct3, uint64_t*
 /* BfvBackend::substitute (bfv.cpp:694-712) with the resident Galois key for g. */
 int cwg_substitute(cwg_ctx* ctx, uint32_t count, const uint64_t* ct, uint64_t g, uint64_t* out);
 
-/* Microbenchmark of internal kernel variants (N = 8192 only); ms per launch over npolys. */
-int cwg_bench_kernel(cwg_ctx* ctx, int which, uint32_t npolys, int iters, float* ms_per_launch);
+/* Tuning / test options (defaults are the measured-fastest choices; no environment variables are
+ * read by the library).  key: "streams" (row-tile streams, 1-4), "tile_rows" (0 = auto),
+ * "fuse_mac" (0: separate selection NTT + MAC kernels), "mac" (0: k_mac2 instead of the TMA
+ * payload MAC for s >= 3), "round" (0: IMAD rounding instead of the tensor cores), "round_g2",
+ * "round_ctas", "mac_waves", "mac_ck", "ntt_np", "prescale", "ks32" (0: 64-bit key switching),
+ * "force_exact" (every rounding / lift decision through the exact multiword path; tests).
+ * Unknown keys return CWG_EINVAL. */
+int cwg_set_option(cwg_ctx* ctx, const char* key, int64_t value);
 /* Kernel launch counter (all launches by this library since cwg_create). */
 uint64_t cwg_kernel_launches(const cwg_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) so callers can record events on it. */

@@ -3,9 +3,24 @@
 //                                                 const PirDatabase&)   (pir.hpp:114-117)
 // Same signature in namespace cwgpu, implemented over include/cwgpu.h (libcwgpu.so).
 // Compiled and checked against the reference by oracle/build_ref.sh + tests/test_dropin.py.
+//
+// Devices: every visible GPU by default (rows split across them, cwg_create_multi), or the list
+// given to cwgpu::set_devices (a device may repeat).
+// Database residency: the NTT-form rows stay on the devices between calls.  The resident copy is
+// keyed on the database's CONTENTS -- shape (rows, chunks per row, code length, weight, params
+// fingerprint) plus a 64-bit digest of every codeword position and payload coefficient.  The
+// digest of the caller's database is recomputed on every call by host threads while the GPUs
+// answer from the resident copy; if it differs (a new database, possibly at the same address),
+// the rows are reloaded and the answer is recomputed, so a stale copy is never returned.
+// Evaluation keys travel with every call, as in the reference server (server.cpp:61-87); the
+// library keeps the resident set when the uploaded words are identical (device key cache).
+#include <algorithm>
+#include <cstring>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
+#include <thread>
 #include "cwpir/pir.hpp"
 #include "cwgpu.h"   // this repo's include/
 
@@ -19,14 +34,96 @@ namespace {
 }
 void check(int rc) { if (rc != CWG_OK) rethrow(rc); }
 
-struct Resident {                            // device-resident DB per (params, database)
+struct Shape {
+    std::uint64_t fp = 0, rows = 0, chunks = 0, m = 0, k = 0;
+    std::vector<int> devices;
+    bool operator==(const Shape& o) const {
+        return fp == o.fp && rows == o.rows && chunks == o.chunks && m == o.m && k == o.k && devices == o.devices;
+    }
+};
+
+struct Resident {                            // device-resident DB (one per process)
     cwg_ctx* ctx = nullptr;
-    const cwpir::PirDatabase* db = nullptr;
-    std::uint64_t fp = 0;
+    Shape shape;
+    std::uint64_t digest = 0;
+    std::vector<int> devices;                // empty: all visible
     std::mutex mu;
 };
 Resident& resident() { static Resident r; return r; }
+
+inline std::uint64_t mix64(std::uint64_t x) {  // splitmix64 finaliser
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+/// 64-bit digest of the database contents (codeword positions and payload coefficients of every
+/// row, position-sensitive), over host threads.
+std::uint64_t db_digest(const cwpir::PirDatabase& db) {
+    const std::size_t n = db.rows(), s = db.chunks_per_row();
+    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::uint64_t> part(T, 0);
+    auto work = [&](unsigned t) {
+        std::uint64_t acc = 0;
+        for (std::size_t i = n * t / T; i < n * (t + 1) / T; ++i) {
+            std::uint64_t a0 = i + 1, a1 = 0x9e3779b97f4a7c15ull, a2 = 0, a3 = 0;
+            for (auto p : db.codeword(i).positions()) a0 = (a0 + p) * 0xff51afd7ed558ccdull;
+            for (std::size_t j = 0; j < s; ++j) {
+                const auto& v = db.chunk(i, j).coeffs();
+                const std::uint64_t* w = v.data();
+                std::size_t x = 0, len = v.size();
+                for (; x + 4 <= len; x += 4) {
+                    a0 = (a0 + w[x]) * 0xc4ceb9fe1a85ec53ull;
+                    a1 = (a1 + w[x + 1]) * 0x9e3779b97f4a7c15ull;
+                    a2 = (a2 + w[x + 2]) * 0xbf58476d1ce4e5b9ull;
+                    a3 = (a3 + w[x + 3]) * 0x94d049bb133111ebull;
+                }
+                for (; x < len; ++x) a0 = (a0 + w[x]) * 0xc4ceb9fe1a85ec53ull;
+            }
+            acc += mix64(mix64(a0 ^ mix64(a1)) ^ mix64(a2 + mix64(a3)) ^ (i * 0x9e3779b97f4a7c15ull));
+        }
+        part[t] = acc;
+    };
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < T; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+    std::uint64_t d = 0;
+    for (auto x : part) d += x;
+    return d;
+}
+
+void load(Resident& R, const cwpir::HeParams& hp, const cwpir::PirDatabase& db, const Shape& shape) {
+    const std::size_t N = hp.degree, L = hp.coeff_primes.size();
+    if (!R.ctx || !(R.shape.fp == shape.fp && R.shape.devices == shape.devices)) {
+        if (R.ctx) cwg_destroy(R.ctx);
+        R.ctx = cwg_create_multi(N, L, hp.coeff_primes.data(), hp.plain_modulus, hp.relin_digit_bits,
+                                 hp.galois_digit_bits, shape.devices.data(), (int)shape.devices.size());
+        if (!R.ctx) rethrow(CWG_EINVAL);
+    }
+    const std::size_t n = db.rows(), s = db.chunks_per_row(), k = db.config().hamming_weight;
+    std::vector<std::uint32_t> pos(n * k);
+    std::vector<std::uint64_t> payload(n * s * N);
+    for (std::size_t i = 0; i < n; ++i) {
+        auto p = db.codeword(i).positions();
+        std::copy(p.begin(), p.end(), pos.begin() + i * k);
+        for (std::size_t j = 0; j < s; ++j)
+            std::copy(db.chunk(i, j).coeffs().begin(), db.chunk(i, j).coeffs().end(),
+                      payload.begin() + (i * s + j) * N);
+    }
+    R.shape = Shape{};  // invalid until the upload succeeded
+    check(cwg_load_db(R.ctx, n, 0, n, s, k, db.config().code_length, pos.data(), payload.data()));
+    R.shape = shape;
+}
 }  // namespace
+
+void set_devices(const std::vector<int>& device_ids) {
+    Resident& R = resident();
+    std::lock_guard<std::mutex> lk(R.mu);
+    R.devices = device_ids;
+}
 
 std::vector<cwpir::CipherValue> process_query(const cwpir::HeBackend& be, const cwpir::PackedQuery& query,
                                               const cwpir::PirDatabase& db) {
@@ -40,24 +137,20 @@ std::vector<cwpir::CipherValue> process_query(const cwpir::HeBackend& be, const 
 
     Resident& R = resident();
     std::lock_guard<std::mutex> lk(R.mu);
-    if (!R.ctx || R.db != &db || R.fp != hp.fingerprint()) {
-        if (R.ctx) cwg_destroy(R.ctx);
-        R.ctx = cwg_create(N, L, hp.coeff_primes.data(), hp.plain_modulus, hp.relin_digit_bits,
-                           hp.galois_digit_bits, /*device=*/0);
-        if (!R.ctx) rethrow(CWG_EINVAL);
-        const std::size_t n = db.rows(), s = db.chunks_per_row(), k = db.config().hamming_weight;
-        std::vector<std::uint32_t> pos(n * k);
-        std::vector<std::uint64_t> payload(n * s * N);
-        for (std::size_t i = 0; i < n; ++i) {
-            auto p = db.codeword(i).positions();
-            std::copy(p.begin(), p.end(), pos.begin() + i * k);
-            for (std::size_t j = 0; j < s; ++j)
-                std::copy(db.chunk(i, j).coeffs().begin(), db.chunk(i, j).coeffs().end(),
-                          payload.begin() + (i * s + j) * N);
-        }
-        check(cwg_load_db(R.ctx, n, 0, n, s, k, db.config().code_length, pos.data(), payload.data()));
-        R.db = &db;
-        R.fp = hp.fingerprint();
+    Shape shape{hp.fingerprint(), db.rows(), db.chunks_per_row(), db.config().code_length,
+                db.config().hamming_weight, R.devices};
+    if (shape.devices.empty()) {
+        const int nd = cwg_device_count();
+        if (nd < 1) throw he_error("cwgpu: no CUDA device");
+        for (int d = 0; d < nd; ++d) shape.devices.push_back(d);
+    }
+    // one device per row at most
+    if (shape.devices.size() > db.rows()) shape.devices.resize(db.rows());
+    bool fresh = false;
+    if (!R.ctx || !(R.shape == shape)) {
+        load(R, hp, db, shape);
+        R.digest = db_digest(db);
+        fresh = true;
     }
     // evaluation keys (reference layout: rows[d][k][i] in NTT form, bfv.cpp:394-402)
     const EvalKeySet& keys = bfv->eval_keys();
@@ -82,9 +175,27 @@ std::vector<cwpir::CipherValue> process_query(const cwpir::HeBackend& be, const 
             for (const auto& e : comp) q.insert(q.end(), e.coeffs().begin(), e.coeffs().end());
     const std::size_t s = db.chunks_per_row();
     std::vector<std::uint64_t> out(s * 2 * L * N);
-    check(cwg_answer(R.ctx, relin.data(), (uint32_t)gs.size(), gs.data(), galois.data(),
-                     (uint32_t)query.cts.size(), query.compression, query.code_length, q.data(),
-                     CWG_OP_FOLKLORE, out.data(), nullptr));
+    auto answer = [&] {
+        check(cwg_answer(R.ctx, relin.data(), (uint32_t)gs.size(), gs.data(), galois.data(),
+                         (uint32_t)query.cts.size(), query.compression, query.code_length, q.data(),
+                         CWG_OP_FOLKLORE, out.data(), nullptr));
+    };
+    if (fresh) {
+        answer();
+    } else {  // verify the resident rows against the caller's database while the GPUs answer
+        auto dig = std::async(std::launch::async, [&] { return db_digest(db); });
+        int rc = cwg_answer(R.ctx, relin.data(), (uint32_t)gs.size(), gs.data(), galois.data(),
+                            (uint32_t)query.cts.size(), query.compression, query.code_length, q.data(),
+                            CWG_OP_FOLKLORE, out.data(), nullptr);
+        const std::uint64_t d = dig.get();
+        if (d != R.digest) {  // different contents: reload and answer again
+            load(R, hp, db, shape);
+            R.digest = d;
+            answer();
+        } else {
+            check(rc);
+        }
+    }
     std::vector<CipherValue> resp(s);
     for (std::size_t j = 0; j < s; ++j) {
         resp[j].kind = BackendKind::bfv;

@@ -54,11 +54,16 @@ def build_ref(force: bool = False) -> str | None:
     """Compile the reference + harness when the reference sources are present."""
     if not os.path.isdir(REFERENCE_SRC):
         return REF_SO if os.path.exists(REF_SO) else None
-    harness = os.path.join(HERE, "ref_harness.cpp")
     script = os.path.join(HERE, "build_ref.sh")
-    if force or not os.path.exists(REF_SO) or os.path.getmtime(REF_SO) < max(
-        os.path.getmtime(harness), os.path.getmtime(script)
-    ):
+    inputs = [os.path.join(HERE, f) for f in ("ref_harness.cpp", "build_ref.sh", "dropin_test.cpp")]
+    inputs.append(os.path.join(os.path.dirname(HERE), "integration", "cwgpu_process_query.cpp"))
+    lib = os.path.join(os.path.dirname(HERE), "paper_2202_07569_b200", "libcwgpu.so")
+    dropin = os.path.join(HERE, "_ref", "libcwgpu_dropin.so")
+    newest = max(os.path.getmtime(f) for f in inputs)
+    stale = not os.path.exists(REF_SO) or os.path.getmtime(REF_SO) < newest
+    if os.path.exists(lib):  # the drop-in shim links the product library
+        stale = stale or not os.path.exists(dropin) or os.path.getmtime(dropin) < max(newest, os.path.getmtime(lib))
+    if force or stale:
         subprocess.check_call(["sh", script])
     return REF_SO
 
@@ -104,8 +109,11 @@ class RefLib:
                                    ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, _u32p,
                                    ctypes.c_uint32, _u64p, ctypes.c_uint32, ctypes.c_uint64, _u64p,
                                    ctypes.POINTER(ctypes.c_double)]
+        lib.ref_write_db_file.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64,
+                                          ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_void_p]
         lib.ref_select.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
-                                   ctypes.c_uint64, ctypes.c_uint32, _u32p, _u64p, _u32p]
+                                   ctypes.c_uint64, ctypes.c_uint32, _u32p, _u64p, _u32p,
+                                   ctypes.POINTER(ctypes.c_double)]
         lib.ref_answer_partial.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, ctypes.c_uint32,
                                            ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, _u32p,
                                            ctypes.c_uint32, _u64p, ctypes.c_uint32, _u64p]
@@ -137,6 +145,15 @@ class RefLib:
         out = np.zeros(k, np.uint32)
         self._check(self.lib.ref_perfect_map(x, m, k, _p32(out)))
         return out
+
+    def write_db_file(self, path, payloads, keys=None, keyword_bits=0):
+        """write_db_file (db_file.cpp): index mode when keys is None, else keyword mode."""
+        payloads = np.ascontiguousarray(payloads, dtype=np.uint8)
+        n, pb = payloads.shape
+        kk = None if keys is None else np.ascontiguousarray(keys, dtype=np.uint8)
+        self._check(self.lib.ref_write_db_file(path.encode(), 0 if kk is None else 1, keyword_bits, n,
+                                               0 if kk is None else kk.shape[1],
+                                               None if kk is None else kk.ctypes.data, pb, payloads.ctypes.data))
 
     def worker_threads(self) -> int:
         return int(self.lib.ref_worker_threads())
@@ -253,21 +270,23 @@ class RefBackend:
         n, k = positions.shape
         s = db.shape[1]
         out = np.zeros((s, 2, self.L, self.N), np.uint64)
-        st = (ctypes.c_double * 5)()
+        st = (ctypes.c_double * 6)()
         self.ref._check(self.ref.lib.ref_answer(self.h, _p64(query), query.shape[0], c, m, n, k,
                                                 _p32(positions), s, _p64(db), op, tile_rows, _p64(out), st))
         return out, list(st)
 
-    def select(self, query, c, m, positions):
-        """compute_selection_vector per row: ([n][3][L][N], comps[n])."""
+    def select(self, query, c, m, positions, stages=False):
+        """compute_selection_vector per row: ([n][3][L][N], comps[n]) (+ stage ms: expand,
+        prepare_cipher, selection, with stages=True)."""
         query = np.ascontiguousarray(query, dtype=np.uint64)
         positions = np.ascontiguousarray(positions, dtype=np.uint32)
         n, k = positions.shape
         sel = np.zeros((n, 3, self.L, self.N), np.uint64)
         comps = np.zeros(n, np.uint32)
+        st = (ctypes.c_double * 3)()
         self.ref._check(self.ref.lib.ref_select(self.h, _p64(query), query.shape[0], c, m, n, k, _p32(positions),
-                                                _p64(sel), _p32(comps)))
-        return sel, comps
+                                                _p64(sel), _p32(comps), st))
+        return (sel, comps, list(st)) if stages else (sel, comps)
 
     def answer_partial(self, query, c, m, positions, db, op=0):
         """Un-finalized inner product of a row shard: [s][3][L][N]."""

@@ -37,7 +37,7 @@ if grep -q 'u64 res\[4\]' "$OUT/src/bfv_patched.cpp"; then echo "patch failed: r
 CXX=${CXX:-g++}
 FLAGS="-std=c++20 -O2 -fPIC -ftrivial-auto-var-init=zero -I$REF/include -pthread"
 pids=""
-for f in bigint numeric prf ring cw_code he eq_circuits expansion pir parallel; do
+for f in bigint numeric prf ring cw_code he eq_circuits expansion pir parallel serialize db_file; do
     $CXX $FLAGS -c "$REF/src/$f.cpp" -o "$OUT/obj/$f.o" &
     pids="$pids $!"
 done
@@ -46,7 +46,9 @@ pids="$pids $!"
 $CXX $FLAGS -c "$HERE/ref_harness.cpp" -o "$OUT/obj/ref_harness.o" &
 pids="$pids $!"
 for p in $pids; do wait "$p"; done
-$CXX -shared -pthread -o "$OUT/libcwpir_ref.so" "$OUT"/obj/*.o
+# link to a temporary name and rename: a process that has the old library mapped keeps it
+$CXX -shared -pthread -o "$OUT/libcwpir_ref.so.tmp" "$OUT"/obj/*.o
+mv -f "$OUT/libcwpir_ref.so.tmp" "$OUT/libcwpir_ref.so"
 echo "built $OUT/libcwpir_ref.so"
 
 # Drop-in shim (integration/cwgpu_process_query.cpp) + its test harness, linked against the
@@ -55,7 +57,8 @@ LIBCWGPU="$HERE/../paper_2202_07569_b200/libcwgpu.so"
 if [ -f "$LIBCWGPU" ]; then
     $CXX $FLAGS -I"$HERE/../include" -c "$HERE/../integration/cwgpu_process_query.cpp" -o "$OUT/obj_dropin_shim.o"
     $CXX $FLAGS -c "$HERE/dropin_test.cpp" -o "$OUT/obj_dropin_test.o"
-    $CXX -shared -pthread -o "$OUT/libcwgpu_dropin.so" "$OUT/obj_dropin_shim.o" "$OUT/obj_dropin_test.o" \
+    $CXX -shared -pthread -o "$OUT/libcwgpu_dropin.so.tmp" "$OUT/obj_dropin_shim.o" "$OUT/obj_dropin_test.o" \
         "$OUT"/obj/*.o -L"$(dirname "$LIBCWGPU")" -lcwgpu -Wl,-rpath,'$ORIGIN/../../paper_2202_07569_b200'
+    mv -f "$OUT/libcwgpu_dropin.so.tmp" "$OUT/libcwgpu_dropin.so"
     echo "built $OUT/libcwgpu_dropin.so"
 fi

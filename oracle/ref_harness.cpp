@@ -26,6 +26,7 @@
 
 #include "cwpir/bfv.hpp"
 #include "cwpir/cw_code.hpp"
+#include "cwpir/db_file.hpp"
 #include "cwpir/eq_circuits.hpp"
 #include "cwpir/expansion.hpp"
 #include "cwpir/parallel.hpp"
@@ -360,7 +361,10 @@ int ref_weighted_sum(void* h, const std::uint64_t* cts, std::uint32_t comps, std
 ///        over row tiles of `tile_rows` and summed with be.add (bit-identical to the
 ///        untiled weighted_sum: INTT and mod-q addition are linear), then finalize
 ///        (pir.cpp:345).
-/// stage_ms (optional, 5 doubles): expand, select (incl. prepare), inner, finalize, prepare wall times.
+/// stage_ms (optional, 6 doubles): expand, select (incl. prepare_cipher), inner (weighted_sum + add),
+/// finalize, prepare_cipher, prepare_plain wall times.  prepare_plain (the database's NTT form) is
+/// timed apart from the inner product: the reference computes it offline (PirDatabase::prepare_for,
+/// pir.cpp:255-264), so a server answer does not pay it.
 int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint32_t c,
                std::uint32_t m, std::uint64_t n, std::uint32_t k, const std::uint32_t* positions,
                std::uint32_t s, const std::uint64_t* db, std::uint32_t op, std::uint64_t tile_rows,
@@ -379,7 +383,7 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
         for (std::uint32_t i = 0; i < nq; ++i) pq.cts.push_back(read_ct(be, query + i * per, 2));
         auto expanded = expand_query(be, pq);
         if (expanded.size() != m) throw std::invalid_argument("expanded query length must equal the code length");
-        double t_expand = ms_since(t0), t_select = 0, t_inner = 0;
+        double t_expand = ms_since(t0), t_select = 0, t_inner = 0, t_plain = 0;
 
         std::vector<BfvBackend::PreparedCipher> prepared;
         auto t1 = std::chrono::steady_clock::now();
@@ -432,7 +436,7 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
                 }
             });
             t_select += ms_since(ts);
-            auto ti = std::chrono::steady_clock::now();
+            auto tp = std::chrono::steady_clock::now();
             std::vector<std::vector<BfvBackend::PreparedPlain>> plains(
                 s, std::vector<BfvBackend::PreparedPlain>(r1 - r0));
             parallel_for(r1 - r0, [&](std::size_t ii) {
@@ -443,6 +447,8 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
                         be.plain_context(), std::vector<u64>(src, src + N)));
                 }
             });
+            t_plain += ms_since(tp);
+            auto ti = std::chrono::steady_clock::now();
             std::vector<CipherValue> part(s);
             parallel_for(s, [&](std::size_t j) { part[j] = be.weighted_sum(sel, plains[j]); });
             for (std::uint32_t j = 0; j < s; ++j) {
@@ -466,6 +472,7 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
             stage_ms[2] = t_inner;
             stage_ms[3] = ms_since(tf);
             stage_ms[4] = t_prepare;
+            stage_ms[5] = t_plain;
         }
     });
 }
@@ -473,9 +480,10 @@ int ref_answer(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
 /// compute_selection_vector's BFV branch (pir.cpp:287-302) for caller-given codewords
 /// (config 2 draws them at random, with duplicates, so PirDatabase::setup cannot be used).
 /// sel: [n][3][L][N] (2-component rows zero padded), comps[n].
+/// stage_ms (optional, 3 doubles): expand_query, prepare_cipher, per-row selection wall times.
 int ref_select(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint32_t c, std::uint32_t m,
                std::uint64_t n, std::uint32_t k, const std::uint32_t* positions, std::uint64_t* sel,
-               std::uint32_t* comps) {
+               std::uint32_t* comps, double* stage_ms) {
     return guarded([&] {
         auto* rb = static_cast<RefBackend*>(h);
         const BfvBackend& be = *rb->be;
@@ -485,12 +493,17 @@ int ref_select(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
         pq.compression = c;
         pq.code_length = m;
         for (std::uint32_t i = 0; i < nq; ++i) pq.cts.push_back(read_ct(be, query + i * per, 2));
+        auto t0 = std::chrono::steady_clock::now();
         auto expanded = expand_query(be, pq);
+        const double t_expand = ms_since(t0);
+        auto t1 = std::chrono::steady_clock::now();
         std::vector<BfvBackend::PreparedCipher> prepared;
         if (k >= 2) {
             prepared.resize(expanded.size());
             parallel_for(expanded.size(), [&](std::size_t j) { prepared[j] = be.prepare_cipher(expanded[j]); });
         }
+        const double t_prepare = ms_since(t1);
+        auto t2 = std::chrono::steady_clock::now();
         parallel_for(n, [&](std::size_t i) {
             std::vector<unsigned> pos(positions + i * k, positions + (i + 1) * k);
             CipherValue out;
@@ -511,6 +524,11 @@ int ref_select(void* h, const std::uint64_t* query, std::uint32_t nq, std::uint3
             write_ct(be, out, sel + i * 3 * L * N);
             comps[i] = static_cast<std::uint32_t>(out.comps.size());
         });
+        if (stage_ms) {
+            stage_ms[0] = t_expand;
+            stage_ms[1] = t_prepare;
+            stage_ms[2] = ms_since(t2);
+        }
     });
 }
 
@@ -560,6 +578,25 @@ int ref_process_query_bytes(void* h, const std::uint64_t* query, std::uint32_t n
             auto pos = db.codeword(i).positions();
             for (unsigned p = 0; p < k; ++p) positions_out[i * k + p] = pos[p];
         }
+    });
+}
+
+/// The reference's own database-file writer (db_file.cpp:13-31, write_db_file): mode 0 index,
+/// 1 keyword (keys: n x key_len bytes); payloads n x payload_bytes.
+int ref_write_db_file(const char* path, int mode, std::uint32_t keyword_bits, std::uint64_t n, std::uint32_t key_len,
+                      const std::uint8_t* keys, std::uint32_t payload_bytes, const std::uint8_t* payloads) {
+    return guarded([&] {
+        DbFileData db;
+        db.header.mode = mode ? PirMode::keyword : PirMode::index;
+        db.header.keyword_bits = keyword_bits;
+        db.header.row_count = n;
+        db.header.payload_bytes = payload_bytes;
+        db.rows.resize(n);
+        for (std::uint64_t i = 0; i < n; ++i) {
+            if (mode) db.rows[i].key.assign(keys + i * key_len, keys + (i + 1) * key_len);
+            db.rows[i].payload.assign(payloads + i * payload_bytes, payloads + (i + 1) * payload_bytes);
+        }
+        write_db_file(path, db);
     });
 }
 

@@ -7,7 +7,7 @@ host-side binding plus the seeded workload definitions.
 """
 from . import configs
 from .cwgpu import (OP_ARITH, OP_FOLKLORE, Client, Context, CudaError, HeError, Keys, StateError,
-                    load_library)
+                    load_client_library, load_library)
 
-__all__ = ["configs", "Context", "Client", "Keys", "HeError", "CudaError", "StateError", "load_library",
+__all__ = ["configs", "Context", "Client", "Keys", "HeError", "CudaError", "StateError", "load_library", "load_client_library",
            "OP_FOLKLORE", "OP_ARITH"]

@@ -17,6 +17,7 @@
 #include <functional>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -28,7 +29,6 @@
 #include "round.cuh"
 #include "mac.cuh"
 #include "ntt_mac.cuh"
-#include "tir.cuh"
 #include "ks32.cuh"
 #include "dbsetup.cuh"
 
@@ -44,9 +44,13 @@ struct state_err : std::runtime_error { using std::runtime_error::runtime_error;
         if (e_ != cudaSuccess) throw cuda_err(std::string(#x) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-struct DevBuf {
+struct DevBuf {  // owns one device allocation (freed on destruction; cudaFree finds the device)
     void* p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
     void ensure(size_t b) {
         if (b <= bytes && p) return;
         if (p) cudaFree(p);
@@ -79,41 +83,38 @@ struct Ctx {
     DevTab T{};
     DevBuf tab, tab_self, round_tab;
     u32 JM = 16;  // aux-prime count padded to a multiple of 8 (rounding kernel template)
-    std::vector<unsigned char> rpar;  // RoundPar<JM> (k_round_hyb kernel-parameter block), JM <= 32
-    std::vector<unsigned char> rtc;   // RoundTcPar<JM, NC> (k_round_tc kernel-parameter block)
-    DevBuf rtc_B;                     // k_round_tc B matrix (canonical UMMA K-major layout)
+    std::vector<unsigned char> rtc;   // RoundTcPar<JM, NC> (k_round_tma kernel-parameter block)
+    DevBuf rtc_B;                     // k_round_tma B matrix (canonical UMMA K-major layout)
     DevBuf rtc_B2;                    // k_round_tma second-GEMM B matrix (gamma / rho / offset terms)
-    u32 rtc_nc = 0;                   // k_round_tc GEMM width (0: no instance for this JM / Mm)
-    int round_kind = 2;               // 2 tensor-core, 1 IMAD + DFMA, 0 IMAD only (env CWGPU_ROUND=tc|hyb|int)
+    u32 rtc_nc = 0;                   // k_round_tma GEMM width (0: no instance for this JM / Mm)
+    int round_kind = 2;               // 2 tensor-core (k_round_tma), 0 IMAD only (k_round_mac_t); option "round"
     DevBuf prep_s;                    // A-side prepared operands with the INTT output scale folded in
     bool prep_s_ok = false;           // prep_s valid for the current answer
-    bool prescale = true;             // env CWGPU_PRESCALE
-    bool mac_tma = true;              // TMA-fed payload MAC (env CWGPU_MAC=v2 selects k_mac2)
-    int mac_waves = 2;                // k_mac_tma grid size in waves of 3 CTAs / SM (env CWGPU_MAC_WAVES)
-    int ntt_np = 1;                   // polynomials per CTA in the tensor / selection NTT kernels (env CWGPU_NTT_NP)
-    bool old_mac = false;       // debugging: the first payload MAC kernel (env CWGPU_OLD_MAC)
-    // fused selection NTT + payload MAC (k_ntt_mac) for s <= 2 (env CWGPU_FUSE_MAC=0 off,
-    // 2 = register accumulators for s = 1); fuse_now: the current answer uses it, so
-    // select_tile leaves the MAC-basis selection values in the coefficient domain
+    // tuning / test options (cwg_set_option; the defaults are the measured-fastest choices)
+    bool prescale = true;             // "prescale": fold the INTT output scale into the A operands
+    bool mac_tma = true;              // "mac": 1 TMA-fed payload MAC for s >= 3 (k_mac_tma), 0 k_mac2
+    int mac_waves = 2;                // "mac_waves": k_mac_tma grid size in waves of 3 CTAs / SM
+    int ntt_np = 1;                   // "ntt_np": polynomials per CTA in the tensor / selection NTT kernels
+    // fused selection NTT + payload MAC (k_ntt_mac) for s <= 2 ("fuse_mac" = 0 off); fuse_now: the
+    // current answer uses it, so select_tile leaves the MAC-basis selection values in the
+    // coefficient domain
     int fuse_mac = 1;
     bool fuse_now = false;
-    // fused tensor + INTT + tensor-core rounding over a J-CTA cluster (k_tir; env CWGPU_FUSE_TIR=0
-    // off); -1 = not yet probed, 0 = unavailable for these parameters, 1 = on
-    int fuse_tir = -1;
-    bool round_g2 = true;   // k_round_tma two-GEMM epilogue (env CWGPU_ROUND_G2=0: corrections on CUDA cores)
-    u32 mac_ck = 0;         // k_ntt_mac row chunks per (component, prime) (env CWGPU_MAC_CK; 0 = auto)
-    bool round_tma = true;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
-    u32 round_ctas = 4;     // k_round_tma grid: persistent CTAs per SM (env CWGPU_ROUND_CTAS)
-    // key switching through the 30-bit aux primes (ks32.cuh; env CWGPU_KS32=0: 64-bit NTT path)
+    bool round_g2 = true;   // "round_g2": k_round_tma two-GEMM epilogue (0: corrections on CUDA cores)
+    u32 mac_ck = 0;         // "mac_ck": k_ntt_mac row chunks per (component, prime) (0 = auto)
+    u32 round_ctas = 4;     // "round_ctas": k_round_tma grid, persistent CTAs per SM
+    u32 tile_rows_opt = 0;  // "tile_rows": rows per selection tile (0 = auto)
+    bool force_exact = false;  // "force_exact": every rounding / lift decision through the multiword path (tests)
+    // key switching through the 30-bit aux primes ("ks32" = 0: the 64-bit NTT path)
     bool ks32 = true;
     bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
     KsCrt ksC_r{}, ksC_g{};            // K' = 0: this key type keeps the 64-bit path
-    DevBuf relinA, galoisA, ksdig, ksmac;  // TMA-fed tensor-core rounding (k_round_tma; env CWGPU_ROUND_TMA=0: k_round_tc)
+    DevBuf relinA, galoisA, ksdig, ksmac;  // keys re-based into the aux primes, digit / MAC scratch
     u32 zs_last = 0;        // MAC-basis plane stride of the last mul_prepared output (J or Mm)
     unsigned next_cluster = 0;  // cluster size of the next launch (launch_named)
     // row-tile pipeline on three streams (k <= 2 folklore): tiles rotate over streams and D buffers
     // so the latency-bound kernels of one tile (NTTs, tensor-core rounding, MAC) co-reside with
-    // those of the next (env CWGPU_STREAMS; C4: 251 ms vs 272 ms on one stream when introduced;
+    // those of the next (option "streams"; C4: 251 ms vs 272 ms on one stream when introduced;
     // now 3 streams ~1 ms ahead of 2, profiles/r01_experiments.txt)
     int nstreams = 3;
     static constexpr int kMaxStreams = 4;
@@ -126,17 +127,18 @@ struct Ctx {
     bool db_loaded = false;
     u64 n_total = 0, row_begin = 0, n_local = 0;
     u32 s = 0, k = 0, m = 0;
-    std::vector<u32> h_pos;
     DevBuf pos_rows;  // [n_local][k]
     DevBuf pos_cols;  // [k][n_local]
     DevBuf db;        // [n_local][s][Mm][N] u32 NTT form (MAC basis)
     std::vector<u64> h_payload;  // kept to rebuild the NTT form if the basis changes
     // keys
     bool have_keys = false;
-    DevBuf relin, galois;
+    DevBuf relin, galois, key_stage, key_flag;
     std::vector<u64> galois_g;
+    bool keys_cached = false;  // the last call's keys equalled the resident set (cwg_timings.keys_cached)
     // scratch
-    DevBuf query, exA, exB, digits, dntt, ks, prep, Dbuf, chain3, node2, acc_lo, acc_hi, partial, X, resp3,
+    DevBuf shard_out, shard_all;  // multi-device context: this device's expansion shard, all shards
+    DevBuf query, exA, exB, digits, dntt, ks, prep, Dbuf, chain3, node2, acc_lo, partial, X, resp3,
         out2, tmp_idx, lift_tmp;
     u64 launches = 0;
     // per-kernel profiling (CUDA events around every launch; off in timed runs)
@@ -157,6 +159,26 @@ struct Ctx {
     // algorithmic work of the next launch for the profile (0: the grid size, i.e. one unit per
     // CTA -- polynomials for the NTT kernels); see cwg_kernel_units
     double next_units = 0;
+    Ctx() = default;
+    Ctx(const Ctx&) = delete;
+    Ctx& operator=(const Ctx&) = delete;
+    ~Ctx() {  // the DevBuf members free themselves afterwards
+        cudaSetDevice(device);
+        if (st) cudaStreamSynchronize(st);
+        for (cudaStream_t t : tst)
+            if (t) cudaStreamSynchronize(t);
+        if (d_fb) cudaFree(d_fb);
+        for (cudaStream_t t : tst)
+            if (t) cudaStreamDestroy(t);
+        for (cudaEvent_t e : tev)
+            if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+        for (auto& p : prof_pending) {
+            cudaEventDestroy(p.e0);
+            cudaEventDestroy(p.e1);
+        }
+        if (st) cudaStreamDestroy(st);
+    }
 };
 
 thread_local std::string g_err;
@@ -250,55 +272,13 @@ static u32 inv32_neg(u32 a) {  // -a^-1 mod 2^32
 static u32 shoup32h(u32 w, u32 p) { return (u32)(((u64)w << 32) / p); }
 static u64 shoup64h(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
 
-/// RoundPar<JM> from the RoundJ / RoundK tables (Montgomery forms for the integer-pipe
-/// primes, plain residues split at 2^15 for the FP64-pipe primes).
-template <int JM>
-static void fill_round_par(std::vector<unsigned char>& out, const std::vector<RoundJ>& rj, const std::vector<RoundK>& rk,
-                           const std::vector<u32>& Imod, const std::vector<u32>& IAmod, const std::vector<u32>& a, u32 J,
-                           u32 Mm) {
-    using RP = RoundPar<JM>;
-    constexpr int MI = RP::MI;
-    out.assign(sizeof(RP), 0);
-    RP& P = *reinterpret_cast<RP*>(out.data());
-    for (int j = 0; j < JM; ++j) {
-        P.a[j] = rj[j].a; P.chat[j] = rj[j].chat; P.chat_s[j] = rj[j].chat_s;
-        P.f0[j] = rj[j].f0; P.f1[j] = rj[j].f1;
-        P.inva_j[j] = (u32)j < J ? 1.0 / (double)a[j] : 0.0;
-    }
-    for (int k = 0; k < RP::KP; ++k) {  // padding primes of the FP64 groups: a = 1, all-zero I
-        P.fa[k] = 1; P.ad[k] = 1.0; P.inva[k] = 1.0; P.off2a[k] = 4503599627370496.0 + 2.0;
-    }
-    auto mf = [](u64 x, u32 p) { return (u32)((((u128)(x % p)) << 32) % p); };  // Montgomery form
-    for (u32 k = 0; k < Mm && k < (u32)JM; ++k) {
-        const u32 p = a[k];
-        if ((int)k < MI) {
-            P.ka[k] = rk[k].a; P.kpinv[k] = rk[k].pinv; P.kgcoef[k] = rk[k].gcoef; P.kroff[k] = rk[k].roff;
-            P.kc0[k] = rk[k].c0; P.kc30[k] = rk[k].c30;
-            for (u32 j = 0; j < J; ++j) P.ImodT[k][j] = mf(Imod[(size_t)j * Mm + k], p);
-        }
-        P.fa[k] = p;
-        for (u32 j = 0; j < J; ++j) {
-            const u32 I = Imod[(size_t)j * Mm + k];
-            P.Ilo[k][j] = (double)(I & 0x7fffu);
-            P.Ihi[k][j] = (double)(I >> 15);
-        }
-        const u32 nIA = (p - IAmod[k] % p) % p;
-        P.nIAlo[k] = (double)(nIA & 0x7fffu);
-        P.nIAhi[k] = (double)(nIA >> 15);
-        P.roff[k] = (double)((p - (u32)(((u64)1 << 36) % p)) % p);
-        P.ad[k] = (double)p;
-        P.inva[k] = 1.0 / (double)p;
-        P.off2a[k] = 4503599627370496.0 + 2.0 * (double)p;
-    }
-}
-
-/// (JM, NC) pairs k_round_tc is instantiated for (TMEM: JM + NC <= 128 columns).
+/// (JM, NC) pairs k_round_tma is instantiated for (TMEM: JM + NC <= 128 columns).
 static bool tc_instance(u32 JM, u32 nc) {
     return (JM == 8 && (nc == 48 || nc == 64)) || (JM == 16 && (nc == 64 || nc == 80)) ||
            (JM == 24 && (nc == 80 || nc == 96)) || (JM == 32 && nc == 96);
 }
 
-/// k_round_tc tables: the parameter block (integer epilogue constants, Montgomery forms) and the
+/// k_round_tma tables: the parameter block (integer epilogue constants, Montgomery forms) and the
 /// B matrix [NC][K = 4 JM] of u8, K-major in the canonical no-swizzle UMMA layout (8-row x 16-B
 /// core matrices; a row's 16-B K chunks 128 B apart, 8-row groups K/16 * 128 B apart).
 static bool build_round_tc(u32 JM, u32 NC, const std::vector<RoundJ>& rj, const std::vector<RoundK>& rk,
@@ -363,9 +343,8 @@ static void build_tables(Ctx& c) {
     T.galois_bits = cp.galois_bits;
     T.t = cp.t;
     T.gbits = 6;
-    T.force_exact = (std::getenv("CWGPU_FORCE_EXACT") && std::atoi(std::getenv("CWGPU_FORCE_EXACT"))) ? 1u : 0u;
-    // D-plane stride: J, or padded to a multiple of 8 (env CWGPU_DPAD=1; experiment)
-    T.DS = (std::getenv("CWGPU_DPAD") && std::atoi(std::getenv("CWGPU_DPAD"))) ? (c.ab.J + 7) / 8 * 8 : c.ab.J;
+    T.force_exact = c.force_exact ? 1u : 0u;
+    T.DS = c.ab.J;  // D-plane stride
     const Big& Q = cp.Q;
     T.QW = (cp.q_bits + 31) / 32;
     if (T.QW > (u32)kQW) throw std::invalid_argument("cwgpu: modulus too wide");
@@ -550,15 +529,6 @@ static void build_tables(Ctx& c) {
         std::memcpy(blob.data() + sizeof(RoundJ) * c.JM + sizeof(RoundK) * kMaxJ, imT.data(), imT.size() * 4);
         c.round_tab.ensure(bytes);
         CK(cudaMemcpy(c.round_tab.p, blob.data(), bytes, cudaMemcpyHostToDevice));
-        // kernel-parameter block of the hybrid IMAD / DFMA rounding kernel
-        c.rpar.clear();
-        switch (c.JM) {
-            case 8: fill_round_par<8>(c.rpar, rj, rk, Imod, IAmod, a, J, Mm); break;
-            case 16: fill_round_par<16>(c.rpar, rj, rk, Imod, IAmod, a, J, Mm); break;
-            case 24: fill_round_par<24>(c.rpar, rj, rk, Imod, IAmod, a, J, Mm); break;
-            case 32: fill_round_par<32>(c.rpar, rj, rk, Imod, IAmod, a, J, Mm); break;
-            default: break;  // JM = 40: the block would exceed the kernel-parameter limit
-        }
         // tensor-core rounding: smallest instantiated GEMM width holding 4 Mm + 17 columns
         c.rtc.clear();
         c.rtc_nc = 0;
@@ -596,7 +566,7 @@ static void build_tables(Ctx& c) {
                     CK(cudaMemcpy(c.rtc_B2.p, B2.data(), B2.size(), cudaMemcpyHostToDevice));
                 }
             } else {
-                c.rtc_nc = 0;  // IMAD + DFMA rounding instead
+                c.rtc_nc = 0;  // IMAD rounding (k_round_mac_t) instead
             }
         }
     }
@@ -617,7 +587,6 @@ static void ensure_aux(Ctx& c, u64 n_total) {
     c.ab = nb;
     build_tables(c);
     c.ksA_ok = false;
-    c.fuse_tir = -1;  // the cluster-kernel instance depends on J and the rounding width
 }
 
 // ------------------------------------------------------------------ NTT launchers
@@ -645,10 +614,8 @@ struct Reg32 {
         CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CK(cudaFuncSetAttribute(k_tensor_intt_r<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * sm));
 #define NM(NC, S, A) CK(cudaFuncSetAttribute(k_ntt_mac<LOGN, NC, S, A>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)NttMac<LOGN, S, A>::SMEM));
-        NM(2, 1, false) NM(3, 1, false) NM(2, 1, true) NM(3, 1, true) NM(2, 2, true) NM(3, 2, true)
+        NM(2, 1, true) NM(3, 1, true) NM(2, 2, true) NM(3, 2, true)
 #undef NM
-        CK(cudaFuncSetAttribute(k_ntt_mac_tma<LOGN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * R::SMEM)));
-        CK(cudaFuncSetAttribute(k_ntt_mac_tma<LOGN, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * R::SMEM)));
     }
     /// fused selection NTT + payload MAC over the R rows of a tile (Z: coefficient-domain
     /// MAC-basis selection planes, Z + ((r * nc + comp) * zs + k) * N)
@@ -664,17 +631,11 @@ struct Reg32 {
         c.next_units = (double)Rt * nc * Mm;  // polynomials transformed (+ payload words streamed)
         const size_t grid = (size_t)ck * per;
 #define NMC(NC, S, A) launch_named(c, "k_ntt_mac", k_ntt_mac<LOGN, NC, S, A>, grid, R::T, NttMac<LOGN, S, A>::SMEM, Z, zs, dbt, Rt, chunk, c.T, acc)
-        if (c.fuse_mac == 3 && c.s == 1) {
-            if (nc == 3) launch_named(c, "k_ntt_mac", k_ntt_mac_tma<LOGN, 3>, grid, R::T, 3 * R::SMEM, Z, zs, dbt, Rt, chunk, c.T, acc);
-            else launch_named(c, "k_ntt_mac", k_ntt_mac_tma<LOGN, 2>, grid, R::T, 3 * R::SMEM, Z, zs, dbt, Rt, chunk, c.T, acc);
-            return;
-        }
-        const bool accr = c.fuse_mac == 2 && c.s == 1;
         if (nc == 3) {
-            if (c.s == 1) { if (accr) NMC(3, 1, false); else NMC(3, 1, true); }
+            if (c.s == 1) NMC(3, 1, true);
             else NMC(3, 2, true);
         } else {
-            if (c.s == 1) { if (accr) NMC(2, 1, false); else NMC(2, 1, true); }
+            if (c.s == 1) NMC(2, 1, true);
             else NMC(2, 2, true);
         }
 #undef NMC
@@ -729,9 +690,6 @@ struct Reg32 {
 static void set_smem_limits(u32 N) {
     CK(cudaFuncSetAttribute(k_mac_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 4 * kMacBlock * 4));
     CK(cudaFuncSetAttribute(k_mac_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 3 * kMacBlock * 4));
-#define RTC(JMv, NCv) CK(cudaFuncSetAttribute(k_round_tc<JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRoundTcSmem));
-    RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
-#undef RTC
 #define RTC(JMv, NCv)                                                                                                \
     CK(cudaFuncSetAttribute(k_round_tma<0, JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
     {                                                                                                                \
@@ -1014,48 +972,6 @@ static u32* prepare_scaled(Ctx& c, const u32* prep, u32 count) {
 /// else the 3-comp chain products are written to chain_out [P][3][L][N].
 static bool round_tc_on(const Ctx& c) { return reg32_ok(c.cp.logN) && c.round_kind == 2 && c.rtc_nc != 0; }
 
-// k_tir instances: (log2 N, cluster = J aux primes, JM, rounding GEMM width)
-#define TIR_LIST(X) X(13, 16, 16, 64) X(13, 16, 16, 80) X(12, 8, 8, 48) X(12, 8, 8, 64) X(14, 16, 16, 64) X(14, 16, 16, 80)
-static bool tir_match(const Ctx& c, u32 L, u32 CL, u32 JM, u32 NC) {
-    return c.cp.logN == L && c.ab.J == CL && c.JM == JM && c.rtc_nc == NC;
-}
-/// k_tir usable for this context: an instance exists and a cluster of J CTAs fits on the GPU.
-static bool tir_on(Ctx& c) {
-    if (c.fuse_tir >= 0) return c.fuse_tir == 1;
-    c.fuse_tir = 0;
-    // measured slower than k_tensor_intt_r + k_round_tma at C4 (cluster barriers, DSMEM gather,
-    // lower residency): opt-in only (env CWGPU_FUSE_TIR=1)
-    const char* fe = std::getenv("CWGPU_FUSE_TIR");
-    if (!fe || std::atoi(fe) == 0) return false;
-    if (!round_tc_on(c)) return false;
-#define X(L, CL, JMv, NCv)                                                                                        \
-    if (tir_match(c, L, CL, JMv, NCv)) {                                                                          \
-        auto kf = k_tir<L, CL, JMv, NCv>;                                                                         \
-        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tir<L, CL>::SMEM));         \
-        if (CL > 8) CK(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));              \
-        cudaLaunchConfig_t cfg = {};                                                                              \
-        cfg.gridDim = dim3(CL * 148);                                                                             \
-        cfg.blockDim = dim3(Tir<L, CL>::T);                                                                       \
-        cfg.dynamicSmemBytes = Tir<L, CL>::SMEM;                                                                  \
-        cudaLaunchAttribute at[1];                                                                                \
-        at[0].id = cudaLaunchAttributeClusterDimension;                                                           \
-        at[0].val.clusterDim.x = CL;                                                                              \
-        at[0].val.clusterDim.y = 1;                                                                               \
-        at[0].val.clusterDim.z = 1;                                                                               \
-        cfg.attrs = at;                                                                                           \
-        cfg.numAttrs = 1;                                                                                         \
-        int ncl = 0;                                                                                              \
-        if (cudaOccupancyMaxActiveClusters(&ncl, kf, &cfg) != cudaSuccess) {                                      \
-            cudaGetLastError();                                                                                   \
-            ncl = 0;                                                                                              \
-        }                                                                                                         \
-        c.fuse_tir = ncl > 0 ? 1 : 0;                                                                             \
-    }
-    TIR_LIST(X)
-#undef X
-    return c.fuse_tir == 1;
-}
-
 /// prepA_scaled: the A operands carry (N 2^32)^-1 (A/a_j)^-1 (see prepare_scaled; tc rounding only).
 static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* prepB, const u32* idxB, u32 P,
                          bool to_mac, u64* chain_out, bool prepA_scaled = false) {
@@ -1063,28 +979,6 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
     u32* D = c.dcur->get<u32>((size_t)P * 3 * c.T.DS * N);
     const bool tc = to_mac && round_tc_on(c);
     c.zs_last = c.T.DS;
-    if (tc && tir_on(c)) {
-        // tensor + INTT + rounding in one cluster kernel: Z[P][3][Mm][N], coefficient domain
-        const RoundK* rk = reinterpret_cast<const RoundK*>(c.round_tab.ptr<RoundJ>() + c.JM);
-        const uint4* Bm = c.rtc_B.ptr<uint4>();
-        const int fold = prepA_scaled ? 2 : 1;
-        c.zs_last = c.ab.Mm;
-        bool launched = false;
-#define X(L, CL, JMv, NCv)                                                                                        \
-    if (!launched && tir_match(c, L, CL, JMv, NCv)) {                                                             \
-        launched = true;                                                                                          \
-        c.next_cluster = CL;                                                                                      \
-        c.next_units = (double)P * 3 * CL;                                                                        \
-        launch_named(c, "k_tir", k_tir<L, CL, JMv, NCv>, (size_t)P * 3 * CL, Tir<L, CL>::T, Tir<L, CL>::SMEM,      \
-                     prepA, idxA, prepB, idxB, P, c.T, fold,                                                      \
-                     *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk, D);                   \
-    }
-        TIR_LIST(X)
-#undef X
-        if (!launched) throw std::logic_error("cluster kernel enabled without a matching instance");
-        if (!c.fuse_now) REG32_DISPATCH(c.cp.logN, sel3(c, D, P, c.ab.Mm));
-        return D;
-    }
     if (reg32_ok(c.cp.logN)) {
         REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? (prepA_scaled ? 2 : 1) : 0));
     } else {
@@ -1099,41 +993,30 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         const u32* im = reinterpret_cast<const u32*>(rk + kMaxJ);
         c.next_units = (double)items;  // coefficients rounded
         if (tc) {
-            const u32 g3 = (u32)std::min<size_t>(items / 128, 148 * 4);
             const uint4* Bm = c.rtc_B.ptr<uint4>();
             const uint4* B2m = c.round_g2 ? c.rtc_B2.ptr<uint4>() : nullptr;  // null: one-GEMM epilogue
 #define RTC(JMv, NCv)                                                                                             \
     if (c.JM == JMv && c.rtc_nc == NCv) {                                                                        \
-        if (c.round_tma) {                                                                                        \
+        {                                                                                                         \
             const size_t gr = std::min<size_t>(items / 128, (size_t)148 * c.round_ctas);                         \
             const auto& rp = *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data());                        \
             constexpr int LN = JMv == 16 ? 13 : JMv == 8 ? 12 : JMv == 32 ? 14 : 0;                              \
             if (LN == 13 && c.cp.logN == 13 && c.ab.Mm == 11)                                                    \
-                launch_named(c, "k_round_tc", k_round_tma<LN, JMv, NCv, 11>, gr, 160, round_tma_smem<JMv>(), D, P,  \
+                launch_named(c, "k_round_tma", k_round_tma<LN, JMv, NCv, 11>, gr, 160, round_tma_smem<JMv>(), D, P,  \
                              c.T, rp, Bm, rk, B2m);                                                               \
             else if (LN == 13 && c.cp.logN == 13 && c.ab.Mm == 10)                                               \
-                launch_named(c, "k_round_tc", k_round_tma<LN, JMv, NCv, 10>, gr, 160, round_tma_smem<JMv>(), D, P,  \
+                launch_named(c, "k_round_tma", k_round_tma<LN, JMv, NCv, 10>, gr, 160, round_tma_smem<JMv>(), D, P,  \
                              c.T, rp, Bm, rk, B2m);                                                               \
             else if (LN != 0 && c.cp.logN == (u32)LN)                                                             \
-                launch_named(c, "k_round_tc", k_round_tma<LN, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T, \
+                launch_named(c, "k_round_tma", k_round_tma<LN, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T, \
                              rp, Bm, rk, B2m);                                                                    \
             else                                                                                                  \
-                launch_named(c, "k_round_tc", k_round_tma<0, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T,  \
+                launch_named(c, "k_round_tma", k_round_tma<0, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T,  \
                              rp, Bm, rk, B2m);                                                                    \
-        } else                                                                                                      \
-            launch_named(c, "k_round_tc", k_round_tc<JMv, NCv>, g3, 128, kRoundTcSmem, D, P, c.T,                \
-                         *reinterpret_cast<const RoundTcPar<JMv, NCv>*>(c.rtc.data()), Bm, rk);                   \
+        }                                                                                                         \
     }
             RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
 #undef RTC
-        } else if (!c.rpar.empty() && c.round_kind >= 1) {
-            const size_t g2 = std::min<size_t>(blocks(items, 256), 148 * 4);
-            switch (c.JM) {
-                case 8: launch_named(c, "k_round_hyb", k_round_hyb<8>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<8>*>(c.rpar.data()), rk); break;
-                case 16: launch_named(c, "k_round_hyb", k_round_hyb<16>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<16>*>(c.rpar.data()), rk); break;
-                case 24: launch_named(c, "k_round_hyb", k_round_hyb<24>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<24>*>(c.rpar.data()), rk); break;
-                default: launch_named(c, "k_round_hyb", k_round_hyb<32>, g2, 256, 0, D, P, c.T, *reinterpret_cast<const RoundPar<32>*>(c.rpar.data()), rk); break;
-            }
         } else if (c.JM == 8) launch_named(c, "k_round_mac", k_round_mac_t<8>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else if (c.JM == 16) launch_named(c, "k_round_mac", k_round_mac_t<16>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else if (c.JM == 24) launch_named(c, "k_round_mac", k_round_mac_t<24>, grid, 256, sm, D, P, c.T, rj, rk, im);
@@ -1147,6 +1030,7 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
             ntt32(c, D, P * 3 * c.ab.Mm, c.ab.Mm, c.T.DS, 0, false, 0);
         }
     } else {
+        c.next_units = (double)P * 3 * N;  // coefficients rounded
         launch(c, k_round_chain, blocks((size_t)P * 3 * N, 128), 128, 0, (const u32*)D, P, c.T, chain_out);
     }
     return D;
@@ -1163,12 +1047,9 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
     const u32* pcol = c.pos_cols.ptr<u32>();
     auto col = [&](u32 p) { return pcol + (size_t)p * c.n_local + r0; };
     if (op == CWG_OP_FOLKLORE && k == 1) {
-        if (chain_sel) {
-            u64* tmp = c.node2.get<u64>((size_t)R * 2 * LN);
-            launch(c, k_gather_ct, blocks((size_t)R * 2 * LN, 256), 256, 0, entries, col(0), R, 2 * LN, tmp);
-            for (u32 r = 0; r < R; ++r)
-                CK(cudaMemcpyAsync(chain_sel + (size_t)r * 3 * LN, tmp + (size_t)r * 2 * LN, 2 * LN * 8,
-                                   cudaMemcpyDeviceToDevice, c.st));
+        if (chain_sel) {  // the expanded entries themselves, 2-comp rows in 3-comp slots
+            launch(c, k_gather_strided, blocks((size_t)R * 2 * LN, 256), 256, 0, entries, 2 * LN, col(0), R, 2 * LN,
+                   chain_sel, 3 * LN);
             nc = 2;
             return nullptr;
         }
@@ -1191,43 +1072,37 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         zstride = c.zs_last;
         return D;
     }
-    // ---- general product trees (k >= 3 folklore, arithmetic operator)
-    // nodes: [R][cnt][2][L][N] 2-comp chain ciphertexts
+    // ---- general product trees (k >= 3 folklore, arithmetic operator); every index vector and
+    // node move is a device kernel (no host round trips inside the tile)
+    // nodes: [R][cnt][2][L][N] 2-comp chain ciphertexts, alternating between two buffers
+    const size_t per = 2 * LN;
     u32 cnt = 0;
     u64* nodes = nullptr;
+    DevBuf* nbuf[2] = {&c.node2, &c.out2};
+    int cur = 0;
+    const u32* prow = c.pos_rows.ptr<u32>();
     if (op == CWG_OP_FOLKLORE) {
         // leaves: pairs (pos[2p], pos[2p+1]) -> mul_lazy_prepared -> finalize (pir.cpp:294-300)
         const u32 np = k / 2;
         cnt = np + (k % 2);
-        nodes = c.node2.get<u64>((size_t)R * cnt * 2 * LN);
-        std::vector<u32> ia((size_t)R * np), ib((size_t)R * np);
-        for (u32 r = 0; r < R; ++r)
-            for (u32 p = 0; p < np; ++p) {
-                ia[(size_t)r * np + p] = c.h_pos[(r0 + r) * k + 2 * p];
-                ib[(size_t)r * np + p] = c.h_pos[(r0 + r) * k + 2 * p + 1];
-            }
-        u32* di = c.tmp_idx.get<u32>((size_t)2 * R * np + 2 * R);
-        CK(cudaMemcpyAsync(di, ia.data(), ia.size() * 4, cudaMemcpyHostToDevice, c.st));
-        CK(cudaMemcpyAsync(di + ia.size(), ib.data(), ib.size() * 4, cudaMemcpyHostToDevice, c.st));
+        u32* di = c.tmp_idx.get<u32>((size_t)2 * R * np);
+        launch(c, k_leaf_pairs, blocks((size_t)R * np, 256), 256, 0, prow, r0, R, k, di, di + (size_t)R * np);
         u64* c3 = c.chain3.get<u64>((size_t)R * np * 3 * LN);
-        mul_prepared(c, prep, di, prep, di + ia.size(), R * np, false, c3);
-        // relinearize into the node slots: node (r, p) = leaf r*np + p
-        u64* leaf2 = c.out2.get<u64>((size_t)R * np * 2 * LN);
-        relinearize(c, c3, R * np, leaf2);
-        for (u32 r = 0; r < R; ++r) {
-            CK(cudaMemcpyAsync(nodes + ((size_t)r * cnt) * 2 * LN, leaf2 + (size_t)r * np * 2 * LN,
-                               (size_t)np * 2 * LN * 8, cudaMemcpyDeviceToDevice, c.st));
-            if (k % 2) {
-                const u32 e = c.h_pos[(r0 + r) * k + k - 1];
-                CK(cudaMemcpyAsync(nodes + ((size_t)r * cnt + np) * 2 * LN, entries + (size_t)e * 2 * LN,
-                                   2 * LN * 8, cudaMemcpyDeviceToDevice, c.st));
-            }
+        mul_prepared(c, prep, di, prep, di + (size_t)R * np, R * np, false, c3);
+        nodes = nbuf[cur]->get<u64>((size_t)R * cnt * per);
+        if (k % 2 == 0) {
+            relinearize(c, c3, R * np, nodes);  // [R * np] == [R][cnt]
+        } else {
+            u64* leaf2 = c.resp3.get<u64>((size_t)R * np * per);
+            relinearize(c, c3, R * np, leaf2);
+            launch(c, k_tree_next, blocks((size_t)R * cnt * per, 256), 256, 0, (const u64*)leaf2, R, np, cnt, entries,
+                   (size_t)0, prow, r0, k, per, nodes);
         }
     } else {
         cnt = k;
-        nodes = c.node2.get<u64>((size_t)R * cnt * 2 * LN);
-        launch(c, k_arith_factors, blocks((size_t)R * 2 * LN, 256), 256, 0, entries,
-               c.pos_rows.ptr<u32>() + (size_t)r0 * k, R, k, c.T, nodes);
+        nodes = nbuf[cur]->get<u64>((size_t)R * cnt * per);
+        launch(c, k_arith_factors, blocks((size_t)R * 2 * LN, 256), 256, 0, entries, prow + (size_t)r0 * k, R, k, c.T,
+               nodes);
     }
     const bool lazy_root = (op == CWG_OP_FOLKLORE);
     // product_tree (eq_circuits.cpp:53-69)
@@ -1236,40 +1111,34 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         const u32 np = cnt / 2, ncnt = np + (cnt % 2);
         // prepare every node of every row (entries keep their own prepared buffer)
         u32* np_prep = c.lift_tmp.get<u32>((size_t)R * cnt * 2 * J * N);
-        prepare(c, nodes, 2 * LN, nullptr, R * cnt, np_prep);
-        std::vector<u32> ia((size_t)R * np), ib((size_t)R * np);
-        for (u32 r = 0; r < R; ++r)
-            for (u32 p = 0; p < np; ++p) {
-                ia[(size_t)r * np + p] = r * cnt + 2 * p;
-                ib[(size_t)r * np + p] = r * cnt + 2 * p + 1;
-            }
-        u32* di = c.tmp_idx.get<u32>((size_t)2 * R * np + 2);
-        CK(cudaMemcpyAsync(di, ia.data(), ia.size() * 4, cudaMemcpyHostToDevice, c.st));
-        CK(cudaMemcpyAsync(di + ia.size(), ib.data(), ib.size() * 4, cudaMemcpyHostToDevice, c.st));
+        prepare(c, nodes, per, nullptr, R * cnt, np_prep);
+        u32* di = c.tmp_idx.get<u32>((size_t)2 * R * np);
+        launch(c, k_level_pairs, blocks((size_t)R * np, 256), 256, 0, R, cnt, di, di + (size_t)R * np);
         if (last && lazy_root) {
             if (chain_sel) {
-                mul_prepared(c, np_prep, di, np_prep, di + ia.size(), R, false, chain_sel);
+                mul_prepared(c, np_prep, di, np_prep, di + (size_t)R * np, R, false, chain_sel);
                 nc = 3;
                 return nullptr;
             }
-            u32* D = mul_prepared(c, np_prep, di, np_prep, di + ia.size(), R, true, nullptr);
+            u32* D = mul_prepared(c, np_prep, di, np_prep, di + (size_t)R * np, R, true, nullptr);
             nc = 3;
             zstride = c.zs_last;
             return D;
         }
         u64* c3 = c.chain3.get<u64>((size_t)R * np * 3 * LN);
-        mul_prepared(c, np_prep, di, np_prep, di + ia.size(), R * np, false, c3);
-        u64* nn = c.out2.get<u64>((size_t)R * ncnt * 2 * LN);
-        u64* rl = c.resp3.get<u64>((size_t)R * np * 2 * LN);
-        relinearize(c, c3, R * np, rl);
-        for (u32 r = 0; r < R; ++r) {
-            CK(cudaMemcpyAsync(nn + (size_t)r * ncnt * 2 * LN, rl + (size_t)r * np * 2 * LN, (size_t)np * 2 * LN * 8,
-                               cudaMemcpyDeviceToDevice, c.st));
-            if (cnt % 2)
-                CK(cudaMemcpyAsync(nn + ((size_t)r * ncnt + np) * 2 * LN, nodes + ((size_t)r * cnt + cnt - 1) * 2 * LN,
-                                   2 * LN * 8, cudaMemcpyDeviceToDevice, c.st));
+        mul_prepared(c, np_prep, di, np_prep, di + (size_t)R * np, R * np, false, c3);
+        u64* nn = nbuf[cur ^ 1]->get<u64>((size_t)R * ncnt * per);
+        if (cnt % 2 == 0) {
+            relinearize(c, c3, R * np, nn);
+        } else {
+            u64* rl = c.resp3.get<u64>((size_t)R * np * per);
+            relinearize(c, c3, R * np, rl);
+            launch(c, k_tree_next, blocks((size_t)R * ncnt * per, 256), 256, 0, (const u64*)rl, R, np, ncnt,
+                   (const u64*)(nodes + (size_t)(cnt - 1) * per), (size_t)cnt * per, (const u32*)nullptr, (u64)0, 0u,
+                   per, nn);
         }
-        CK(cudaMemcpyAsync(nodes, nn, (size_t)R * ncnt * 2 * LN * 8, cudaMemcpyDeviceToDevice, c.st));
+        nodes = nn;
+        cur ^= 1;
         cnt = ncnt;
     }
     // root is a 2-comp ciphertext: arithmetic operator -> plain_mul((k!)^-1) (eq_circuits.cpp:126)
@@ -1281,13 +1150,12 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         launch(c, k_scale_const, blocks((size_t)R * 2 * LN, 256), 256, 0, nodes, R, kinv, c.T);
     }
     if (chain_sel) {
-        for (u32 r = 0; r < R; ++r)
-            CK(cudaMemcpyAsync(chain_sel + (size_t)r * 3 * LN, nodes + (size_t)r * 2 * LN, 2 * LN * 8,
-                               cudaMemcpyDeviceToDevice, c.st));
+        launch(c, k_gather_strided, blocks((size_t)R * per, 256), 256, 0, (const u64*)nodes, per, (const u32*)nullptr, R,
+               per, chain_sel, 3 * LN);
         nc = 2;
         return nullptr;
     }
-    u32* Z = c.Dbuf.get<u32>((size_t)R * 2 * Mm * N);
+    u32* Z = c.dcur->get<u32>((size_t)R * 2 * Mm * N);
     launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, (const u64*)nodes, 2 * LN, (const u32*)nullptr, R, Mm,
            0, c.T, Z, Mm);
     if (!c.fuse_now) ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
@@ -1298,10 +1166,11 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
 
 static u32 tile_rows(const Ctx& c) {
     // bound the per-tile aux buffer (P x 3 x DS x N u32) to ~256 MB and tree scratch
+    // (product trees, k > 2: ~2 GB for the leaf products' D planes; the node, chain-product and
+    // prepared-node buffers scale with it, ~12 GB in all at C5)
     const size_t per = (size_t)3 * c.T.DS * c.cp.N * 4 * std::max<u32>(1, c.k / 2);
-    size_t r = std::max<size_t>(4, (size_t(256) << 20) / per);
-    if (c.k > 2) r = std::min<size_t>(r, 64);
-    if (const char* e = std::getenv("CWGPU_TILE_ROWS")) r = std::max(1, std::atoi(e));
+    size_t r = std::max<size_t>(4, (size_t(c.k > 2 ? 2048 : 256) << 20) / per);
+    if (c.tile_rows_opt) r = c.tile_rows_opt;
     return (u32)std::min<size_t>(r, 512);
 }
 
@@ -1335,15 +1204,42 @@ struct Timer {
 };
 enum { TM_START = 0, TM_H2D, TM_EXPAND, TM_SELECT, TM_MAC, TM_FINISH, TM_D2H };
 
-static void upload_keys(Ctx& c, const u64* relin, u32 n_galois, const u64* gg, const u64* galois) {
+/// Evaluation keys for this call (EvalKeySet, bfv.hpp:42-51; the reference server receives them
+/// with every query, server.cpp:61-87).  Device key cache: when a key set of the same shape is
+/// resident, the upload goes to a staging buffer and is compared word for word on the device;
+/// identical keys keep the resident copy and its aux-basis transform (key_to_aux, ~2 ms at C4),
+/// different keys replace it.  Returns true when the resident keys were reused.
+static bool upload_keys(Ctx& c, const u64* relin, u32 n_galois, const u64* gg, const u64* galois) {
     const size_t LN = (size_t)c.cp.L * c.cp.N;
     const size_t rw = (size_t)c.cp.Dr * 2 * LN, gw = (size_t)c.cp.Dg * 2 * LN;
-    CK(cudaMemcpyAsync(c.relin.get<u64>(rw), relin, rw * 8, cudaMemcpyDefault, c.st));
+    const bool same_shape = c.have_keys && c.galois_g.size() == n_galois &&
+                            std::equal(c.galois_g.begin(), c.galois_g.end(), gg);
+    if (!same_shape) {
+        CK(cudaMemcpyAsync(c.relin.get<u64>(rw), relin, rw * 8, cudaMemcpyDefault, c.st));
+        if (n_galois)
+            CK(cudaMemcpyAsync(c.galois.get<u64>(gw * n_galois), galois, gw * n_galois * 8, cudaMemcpyDefault, c.st));
+        c.galois_g.assign(gg, gg + n_galois);
+        c.have_keys = true;
+        c.ksA_ok = false;
+        return false;
+    }
+    const size_t gall = gw * n_galois;
+    u64* stage = c.key_stage.get<u64>(rw + gall);
+    CK(cudaMemcpyAsync(stage, relin, rw * 8, cudaMemcpyDefault, c.st));
+    if (n_galois) CK(cudaMemcpyAsync(stage + rw, galois, gall * 8, cudaMemcpyDefault, c.st));
+    unsigned int* flag = c.key_flag.get<unsigned int>(1);
+    CK(cudaMemsetAsync(flag, 0, 4, c.st));
+    launch(c, k_words_differ, 148 * 8, 256, 0, (const u64*)stage, (const u64*)c.relin.ptr<u64>(), rw, flag);
     if (n_galois)
-        CK(cudaMemcpyAsync(c.galois.get<u64>(gw * n_galois), galois, gw * n_galois * 8, cudaMemcpyDefault, c.st));
-    c.galois_g.assign(gg, gg + n_galois);
-    c.have_keys = true;
+        launch(c, k_words_differ, 148 * 8, 256, 0, (const u64*)(stage + rw), (const u64*)c.galois.ptr<u64>(), gall, flag);
+    unsigned int differ = 1;
+    CK(cudaMemcpyAsync(&differ, flag, 4, cudaMemcpyDeviceToHost, c.st));
+    CK(cudaStreamSynchronize(c.st));
+    if (!differ) return true;
+    CK(cudaMemcpyAsync(c.relin.ptr<u64>(), stage, rw * 8, cudaMemcpyDeviceToDevice, c.st));
+    if (n_galois) CK(cudaMemcpyAsync(c.galois.ptr<u64>(), stage + rw, gall * 8, cudaMemcpyDeviceToDevice, c.st));
     c.ksA_ok = false;
+    return false;
 }
 
 /// expand + select + MAC; leaves the reduced partial accumulators [s][3][Mm][N] u64
@@ -1388,7 +1284,6 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     const size_t accw = (size_t)c.s * 3 * Mm * N;
     auto* acc = reinterpret_cast<unsigned long long*>(c.acc_lo.get<u64>(accw));
     CK(cudaMemsetAsync(acc, 0, accw * 8, c.st));
-    if (c.old_mac) CK(cudaMemsetAsync(c.acc_hi.get<u64>(accw), 0, accw * 8, c.st));
     const u32 R = tile_rows(c);
     u32 nc_all = 2;
     // profiling serialises the tile pipeline: per-kernel CUDA-event times then measure each kernel
@@ -1403,11 +1298,24 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         CK(cudaEventRecord(c.tev[0], main_st));
         for (int i = 0; i < ns; ++i) CK(cudaStreamWaitEvent(c.tst[i], c.tev[0], 0));
     }
-    c.fuse_now = c.fuse_mac != 0 && reg32_ok(c.cp.logN) && c.s <= 2 && !c.old_mac;
-    struct FuseReset {
+    c.fuse_now = c.fuse_mac != 0 && reg32_ok(c.cp.logN) && c.s <= 2;
+    // restores the context's stream / D buffer and the fuse flag on every exit, including an
+    // exception thrown inside the tile loop (the main stream then waits for the tile streams, so
+    // callers that captured cwg_stream() stay ordered after all of this answer's work)
+    struct PipeGuard {
         Ctx& c;
-        ~FuseReset() { c.fuse_now = false; }
-    } fuse_reset{c};
+        cudaStream_t main_st;
+        int ns;
+        bool piped;
+        ~PipeGuard() {
+            c.fuse_now = false;
+            if (!piped) return;
+            c.st = main_st;
+            c.dcur = &c.Dbuf;
+            for (int i = 0; i < ns; ++i)
+                if (cudaEventRecord(c.tev[1 + i], c.tst[i]) == cudaSuccess) cudaStreamWaitEvent(main_st, c.tev[1 + i], 0);
+        }
+    } pipe_guard{c, main_st, ns, piped};
     u64 tile = 0;
     for (u64 r0 = 0; r0 < c.n_local; r0 += R, ++tile) {
         const u32 Rt = (u32)std::min<u64>(R, c.n_local - r0);
@@ -1432,7 +1340,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         // across the s payload slices); the register stream is as fast for s = 1 (C4: 22.9 ms)
         if (c.fuse_now) {
             REG32_DISPATCH(c.cp.logN, ntt_mac(c, Z, zs, nc, dbt, Rt, acc));
-        } else if (c.mac_tma && c.s >= 2 && N >= (u32)kMacBlock && !c.old_mac) {
+        } else if (c.mac_tma && c.s >= 2 && N >= (u32)kMacBlock) {
             // TMA-fed stream: whole waves of 3 CTAs / SM (no partial tail wave), >= 8 rows per chunk
             const u32 per = Mm * (N / kMacBlock) * c.s;
             const u32 slots = 148 * 3 * (c.mac_waves > 0 ? c.mac_waves : 2);
@@ -1446,10 +1354,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
             else
                 launch_named(c, "k_mac", k_mac_tma<2>, (size_t)ck * per, 288, smem, (const u32*)Z, zs, dbt, Rt, c.s,
                              crow, c.T, acc);
-        } else if (c.old_mac)
-            launch_named(c, "k_mac", k_mac, blocks((size_t)c.s * Mm * N, 128), 128, 0, (const u32*)Z, nc, zs, dbt, Rt,
-                         c.s, c.T, c.acc_lo.ptr<u64>(), c.acc_hi.ptr<u64>());
-        else if (nc == 3)
+        } else if (nc == 3)
             launch_named(c, "k_mac", k_mac2<3>, blocks(threads, 256), 256, 0, (const u32*)Z, zs, dbt, Rt, c.s, chunk,
                          c.T, acc);
         else
@@ -1458,6 +1363,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         tm.mark(TM_MAC);
     }
     if (piped) {
+        pipe_guard.piped = false;
         c.st = main_st;
         c.dcur = &c.Dbuf;
         for (int i = 0; i < ns; ++i) {
@@ -1465,11 +1371,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
             CK(cudaStreamWaitEvent(main_st, c.tev[1 + i], 0));
         }
     }
-    if (c.old_mac)
-        launch(c, k_acc_reduce, blocks(accw, 256), 256, 0, (const u64*)c.acc_lo.ptr<u64>(), (const u64*)c.acc_hi.ptr<u64>(),
-               accw, c.T, dev_partial);
-    else
-        launch(c, k_acc_mod, blocks(accw, 256), 256, 0, (const unsigned long long*)acc, accw, c.T, dev_partial);
+    launch(c, k_acc_mod, blocks(accw, 256), 256, 0, (const unsigned long long*)acc, accw, c.T, dev_partial);
     tm.mark(TM_MAC);
     return nc_all;
 }
@@ -1513,6 +1415,8 @@ static void fill_timings(Ctx& c, Timer& tm, cwg_timings* t, double total_ms) {
     unsigned long long fb = 0;
     CK(cudaMemcpy(&fb, c.d_fb, 8, cudaMemcpyDeviceToHost));
     t->exact_fallbacks = fb;
+    t->keys_cached = c.keys_cached ? 1u : 0u;
+    t->n_devices = 1;
 }
 
 // ------------------------------------------------------------------ database
@@ -1534,6 +1438,7 @@ static void load_db_impl(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s,
             if (p && v <= positions[r * k + p - 1]) throw std::invalid_argument("codeword positions must ascend");
         }
     }
+    c.db_loaded = false;  // set again only after the upload and the stream sync succeed
     ensure_aux(c, n_total);
     const u32 Mm = c.ab.Mm;
     c.n_total = n_total;
@@ -1542,7 +1447,6 @@ static void load_db_impl(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s,
     c.s = s;
     c.k = k;
     c.m = m;
-    c.h_pos.assign(positions, positions + n_local * k);
     std::vector<u32> cols((size_t)k * n_local);
     for (u64 r = 0; r < n_local; ++r)
         for (u32 p = 0; p < k; ++p) cols[(size_t)p * n_local + r] = positions[r * k + p];
@@ -1561,8 +1465,8 @@ static void load_db_impl(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s,
             launch(c, k_db_spread, blocks(R * s * Mm * N, 256), 256, 0, (const u64*)stage, R * s, c.T, dst);
             ntt32(c, dst, (u32)(R * s * Mm), Mm, Mm, 0, false, 0);
         }
-        CK(cudaStreamSynchronize(c.st));
     }
+    CK(cudaStreamSynchronize(c.st));
     c.db_loaded = true;
 }
 
@@ -1639,13 +1543,74 @@ static void load_db_bytes(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 k
     });
 }
 
+/// compute_selection_vector (pir.cpp:277-312) for this context's rows into sel ([n_local][3][L][N],
+/// host or device memory) and comps (host).  Device output: tiles are written in place, no copies
+/// back and no per-tile synchronisation (the C2 equality microbenchmark times this).
+static void select_rows(Ctx& c, u32 nq, u32 comp, u32 m, const u64* query, u32 op, u64* sel, u32* comps, Timer& tm) {
+    if (!c.db_loaded) throw state_err("no database loaded");
+    if (m != c.m) throw std::invalid_argument("expanded query length must equal the code length");
+    if (!c.have_keys) throw he_err("evaluation keys not set");
+    if (op != CWG_OP_FOLKLORE && op != CWG_OP_ARITH) throw std::invalid_argument("unknown equality operator");
+    if (op == CWG_OP_ARITH && c.k < 2) throw std::invalid_argument("arithmetic operator needs k >= 2");
+    c.prep_s_ok = false;  // the selection path uses the unscaled operands only
+    cudaPointerAttributes pa{};
+    const bool dev_out = cudaPointerGetAttributes(&pa, sel) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J;
+    const size_t LN = (size_t)L * N;
+    u64* dq = c.query.get<u64>((size_t)nq * 2 * LN);
+    CK(cudaMemcpyAsync(dq, query, (size_t)nq * 2 * LN * 8, cudaMemcpyDefault, c.st));
+    tm.mark(TM_H2D);
+    u64* entries = expand(c, dq, nq, comp, m);
+    tm.mark(TM_EXPAND);
+    u32* prep = nullptr;
+    if (op == CWG_OP_FOLKLORE && c.k >= 2) {
+        prep = c.prep.get<u32>((size_t)m * 2 * J * N);
+        prepare(c, entries, 2 * LN, nullptr, m, prep);
+    }
+    const u32 R = tile_rows(c);
+    u64* dsel = dev_out ? nullptr : c.partial.get<u64>((size_t)R * 3 * LN);
+    u32 nc = 0;
+    for (u64 r0 = 0; r0 < c.n_local; r0 += R) {
+        const u32 Rt = (u32)std::min<u64>(R, c.n_local - r0);
+        u64* dst = dev_out ? sel + r0 * 3 * LN : dsel;
+        u32 zs = 0;
+        select_tile(c, entries, prep, op, r0, Rt, nc, zs, dst);
+        if (nc == 2)  // 2-component rows: slot 2 is zero
+            CK(cudaMemset2DAsync(dst + 2 * LN, 3 * LN * 8, 0, LN * 8, Rt, c.st));
+        tm.mark(TM_SELECT);
+        if (!dev_out) {
+            CK(cudaMemcpyAsync(sel + r0 * 3 * LN, dsel, (size_t)Rt * 3 * LN * 8, cudaMemcpyDeviceToHost, c.st));
+            CK(cudaStreamSynchronize(c.st));
+            tm.mark(TM_D2H);
+        }
+    }
+    CK(cudaStreamSynchronize(c.st));
+    for (u64 r = 0; r < c.n_local; ++r) comps[r] = nc;
+}
+
+
 }  // namespace cwgpu
+
 
 // ================================================================== C ABI
 using namespace cwgpu;
 
+/// One context = one device, or (cwg_create_multi) several: rows split contiguously across the
+/// devices, every device expands the query (sharded when possible) and runs its rows, the partial
+/// accumulators are summed on the root (device_ids[0]) by peer copies + k_add_u64, which finishes.
 struct cwg_ctx {
-    Ctx c;
+    Ctx c;                                   // device_ids[0]: reduction and finalize
+    std::vector<std::unique_ptr<Ctx>> more;  // device_ids[1..]
+    std::mutex mmu;                          // serialises calls on a multi-device context
+    DevBuf red;                              // root: a peer's partial accumulators in flight
+    std::vector<Ctx*> all() {
+        std::vector<Ctx*> v{&c};
+        for (auto& p : more) v.push_back(p.get());
+        return v;
+    }
+    bool multi() const { return !more.empty(); }
+    ~cwg_ctx() { cudaSetDevice(c.device); red.release(); }
 };
 
 template <class F>
@@ -1671,69 +1636,100 @@ static int guarded(F&& f) {
     }
 }
 
+/// f(ctx, index) on every device of h, one host thread per device (the first exception is
+/// rethrown on the calling thread after all have finished).
+template <class F>
+static void for_devices(cwg_ctx* h, F&& f) {
+    auto all = h->all();
+    if (all.size() == 1) {
+        CK(cudaSetDevice(all[0]->device));
+        f(*all[0], (size_t)0);
+        return;
+    }
+    std::vector<std::exception_ptr> err(all.size());
+    std::vector<std::thread> th;
+    for (size_t i = 0; i < all.size(); ++i)
+        th.emplace_back([&, i] {
+            try {
+                CK(cudaSetDevice(all[i]->device));
+                f(*all[i], i);
+            } catch (...) {
+                err[i] = std::current_exception();
+            }
+        });
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
+/// rows [lo, hi) of n of device i among W (contiguous split)
+static inline u64 split_lo(u64 n, size_t i, size_t W) { return n * i / W; }
+
+static void init_ctx(Ctx& c, uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint32_t relin_digit_bits,
+                     uint32_t galois_digit_bits, int device) {
+    c.cp = make_chain(N, t, std::vector<u64>(q, q + L), relin_digit_bits, galois_digit_bits);
+    if (N > 16384) throw std::invalid_argument("cwgpu: ring degree above 16384 is not supported");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw std::invalid_argument("cwgpu: device id out of range");
+    c.device = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+    CK(cudaMalloc(&c.d_fb, 8));
+    CK(cudaMemset(c.d_fb, 0, 8));
+    set_smem_limits(N);
+    c.dcur = &c.Dbuf;
+    for (int i = 0; i < Ctx::kMaxStreams; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));
+    for (int i = 0; i <= Ctx::kMaxStreams; ++i) CK(cudaEventCreateWithFlags(&c.tev[i], cudaEventDisableTiming));
+    ensure_aux(c, 1);
+}
+
 extern "C" {
 
 const char* cwg_last_error(void) { return g_err.c_str(); }
 
+int cwg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 cwg_ctx* cwg_create(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint32_t relin_digit_bits,
                     uint32_t galois_digit_bits, int device) {
+    return cwg_create_multi(N, L, q, t, relin_digit_bits, galois_digit_bits, &device, 1);
+}
+
+cwg_ctx* cwg_create_multi(uint32_t N, uint32_t L, const uint64_t* q, uint64_t t, uint32_t relin_digit_bits,
+                          uint32_t galois_digit_bits, const int* device_ids, int n_devices) {
     cwg_ctx* h = nullptr;
     int rc = guarded([&] {
+        if (n_devices < 1 || !device_ids) throw std::invalid_argument("cwgpu: no devices given");
         auto ctx = std::make_unique<cwg_ctx>();
-        Ctx& c = ctx->c;
-        c.cp = make_chain(N, t, std::vector<u64>(q, q + L), relin_digit_bits, galois_digit_bits);
-        if (N > 16384) throw std::invalid_argument("cwgpu: ring degree above 16384 is not supported");
-        c.device = device;
-        CK(cudaSetDevice(device));
-        CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
-        CK(cudaMalloc(&c.d_fb, 8));
-        CK(cudaMemset(c.d_fb, 0, 8));
-        set_smem_limits(N);
-        if (const char* e = std::getenv("CWGPU_STREAMS"))
-            c.nstreams = std::max(1, std::min(Ctx::kMaxStreams, std::atoi(e)));
-        if (const char* e = std::getenv("CWGPU_MAC")) c.mac_tma = std::string(e) != "v2";
-        if (const char* e = std::getenv("CWGPU_MAC_WAVES")) c.mac_waves = std::max(1, std::atoi(e));
-        if (const char* e = std::getenv("CWGPU_PRESCALE")) c.prescale = std::atoi(e) != 0;
-        if (const char* e = std::getenv("CWGPU_NTT_NP")) c.ntt_np = std::atoi(e) == 1 ? 1 : 2;
-        if (const char* e = std::getenv("CWGPU_ROUND"))
-            c.round_kind = std::string(e) == "int" ? 0 : std::string(e) == "hyb" ? 1 : 2;
-        if (const char* e = std::getenv("CWGPU_OLD_MAC")) c.old_mac = std::atoi(e) != 0;
-        if (const char* e = std::getenv("CWGPU_FUSE_MAC")) c.fuse_mac = std::atoi(e);
-        if (const char* e = std::getenv("CWGPU_ROUND_TMA")) c.round_tma = std::atoi(e) != 0;
-        if (const char* e = std::getenv("CWGPU_MAC_CK")) c.mac_ck = (u32)std::max(0, std::atoi(e));
-        if (const char* e = std::getenv("CWGPU_ROUND_G2")) c.round_g2 = std::atoi(e) != 0;
-        if (const char* e = std::getenv("CWGPU_ROUND_CTAS")) c.round_ctas = (u32)std::max(1, std::min(4, std::atoi(e)));
-        if (const char* e = std::getenv("CWGPU_KS32")) c.ks32 = std::atoi(e) != 0;
-        c.dcur = &c.Dbuf;
-        for (int i = 0; i < Ctx::kMaxStreams; ++i) CK(cudaStreamCreateWithFlags(&c.tst[i], cudaStreamNonBlocking));
-        for (int i = 0; i <= Ctx::kMaxStreams; ++i) CK(cudaEventCreateWithFlags(&c.tev[i], cudaEventDisableTiming));
-        ensure_aux(c, 1);
+        init_ctx(ctx->c, N, L, q, t, relin_digit_bits, galois_digit_bits, device_ids[0]);
+        for (int i = 1; i < n_devices; ++i) {
+            ctx->more.push_back(std::make_unique<Ctx>());
+            init_ctx(*ctx->more.back(), N, L, q, t, relin_digit_bits, galois_digit_bits, device_ids[i]);
+        }
+        // direct peer access where the topology allows it (NVLink / NVSwitch); cudaMemcpyPeerAsync
+        // stages through the host otherwise
+        for (int i = 0; i < n_devices; ++i)
+            for (int j = 0; j < n_devices; ++j) {
+                if (device_ids[i] == device_ids[j]) continue;
+                int ok = 0;
+                if (cudaDeviceCanAccessPeer(&ok, device_ids[i], device_ids[j]) == cudaSuccess && ok) {
+                    CK(cudaSetDevice(device_ids[i]));
+                    if (cudaDeviceEnablePeerAccess(device_ids[j], 0) != cudaSuccess) cudaGetLastError();
+                }
+            }
         h = ctx.release();
     });
     return rc == CWG_OK ? h : nullptr;
 }
 
-void cwg_destroy(cwg_ctx* h) {
-    if (!h) return;
-    Ctx& c = h->c;
-    cudaSetDevice(c.device);
-    cudaStreamSynchronize(c.st);
-    for (DevBuf* b : {&c.tab, &c.tab_self, &c.round_tab, &c.prep_s, &c.Dmore[0], &c.Dmore[1], &c.Dmore[2], &c.pos_rows, &c.pos_cols, &c.db, &c.relin, &c.galois, &c.query, &c.exA, &c.exB,
-                      &c.digits, &c.dntt, &c.ks, &c.prep, &c.Dbuf, &c.chain3, &c.node2, &c.acc_lo, &c.acc_hi,
-                      &c.partial, &c.X, &c.resp3, &c.out2, &c.tmp_idx, &c.lift_tmp, &c.rtc_B, &c.rtc_B2, &c.relinA, &c.galoisA,
-                      &c.ksdig, &c.ksmac})
-        b->release();
-    if (c.d_fb) cudaFree(c.d_fb);
-    for (int i = 0; i < Ctx::kMaxStreams; ++i) if (c.tst[i]) cudaStreamDestroy(c.tst[i]);
-    for (int i = 0; i <= Ctx::kMaxStreams; ++i) if (c.tev[i]) cudaEventDestroy(c.tev[i]);
-    for (cudaEvent_t e : c.ev_pool) cudaEventDestroy(e);
-    for (auto& p : c.prof_pending) {
-        cudaEventDestroy(p.e0);
-        cudaEventDestroy(p.e1);
-    }
-    if (c.st) cudaStreamDestroy(c.st);
-    delete h;
-}
+void cwg_destroy(cwg_ctx* h) { delete h; }
 
 int cwg_get_info(const cwg_ctx* h, cwg_info* out) {
     return guarded([&] {
@@ -1751,6 +1747,7 @@ int cwg_get_info(const cwg_ctx* h, cwg_info* out) {
         out->n_total = c.n_total;
         out->row_begin = c.row_begin;
         out->n_local = c.n_local;
+        for (const auto& p : h->more) out->n_local += p->n_local;  // multi-device: all rows held
         out->s = c.s;
         out->k = c.k;
         out->m = c.m;
@@ -1760,28 +1757,115 @@ int cwg_get_info(const cwg_ctx* h, cwg_info* out) {
 int cwg_load_db(cwg_ctx* h, uint64_t n_total, uint64_t row_begin, uint64_t n_local, uint32_t s, uint32_t k,
                 uint32_t m, const uint32_t* positions, const uint64_t* payload) {
     return guarded([&] {
-        std::lock_guard<std::mutex> g(h->c.mu);
-        CK(cudaSetDevice(h->c.device));
-        load_db(h->c, n_total, row_begin, n_local, s, k, m, positions, payload);
+        std::lock_guard<std::mutex> gm(h->mmu);
+        const size_t W = h->all().size();
+        if (n_local < W) throw std::invalid_argument("cwgpu: fewer rows than devices");
+        for_devices(h, [&](Ctx& c, size_t i) {
+            std::lock_guard<std::mutex> g(c.mu);
+            const u64 lo = split_lo(n_local, i, W), hi = split_lo(n_local, i + 1, W);
+            load_db(c, n_total, row_begin + lo, hi - lo, s, k, m, positions + lo * k,
+                    payload ? payload + lo * s * c.cp.N : nullptr);
+        });
     });
 }
 
 int cwg_load_db_bytes(cwg_ctx* h, uint64_t n_total, uint64_t row_begin, uint64_t n_local, uint32_t k, uint32_t m,
                       uint64_t payload_bytes, const uint8_t* payloads, const uint64_t* row_ids) {
     return guarded([&] {
-        std::lock_guard<std::mutex> g(h->c.mu);
-        CK(cudaSetDevice(h->c.device));
-        load_db_bytes(h->c, n_total, row_begin, n_local, k, m, payload_bytes, payloads, row_ids);
+        std::lock_guard<std::mutex> gm(h->mmu);
+        const size_t W = h->all().size();
+        if (n_local < W) throw std::invalid_argument("cwgpu: fewer rows than devices");
+        for_devices(h, [&](Ctx& c, size_t i) {
+            std::lock_guard<std::mutex> g(c.mu);
+            const u64 lo = split_lo(n_local, i, W), hi = split_lo(n_local, i + 1, W);
+            load_db_bytes(c, n_total, row_begin + lo, hi - lo, k, m, payload_bytes, payloads + lo * payload_bytes,
+                          row_ids ? row_ids + lo : nullptr);
+        });
     });
+}
+
+/// The reference's on-disk database (CWDB v1, db_file.cpp:34-59 / serialize.cpp: little-endian
+/// u8 / u16 / u32 / u64 fields, u16-length strings, 4 x u64 seed, then per row a u32-length key and
+/// a u32-length payload) straight into cwg_load_db_bytes: index mode -> codeword of the row index
+/// (map_index), non-lossy keyword mode -> codeword of keyword_value(key) (pir.cpp:22-30,155-159),
+/// payloads zero padded to the header's payload_bytes (chunk_payload pads the same way).
+int cwg_load_db_file(cwg_ctx* h, const uint8_t* data, uint64_t size, uint32_t k, uint32_t m) {
+    std::vector<uint8_t> payloads;
+    std::vector<uint64_t> ids;
+    uint64_t rows = 0, payload_bytes = 0, mode = 0;
+    const int rc = guarded([&] {
+        struct Rd {
+            const uint8_t* p;
+            uint64_t n, pos = 0;
+            void need(uint64_t x) {
+                if (x > n - pos) throw std::invalid_argument("truncated database file");
+            }
+            uint64_t le(int bytes) {
+                need(bytes);
+                uint64_t v = 0;
+                for (int i = 0; i < bytes; ++i) v |= (uint64_t)p[pos + i] << (8 * i);
+                pos += bytes;
+                return v;
+            }
+        } r{data, size};
+        if (!data) throw std::invalid_argument("database file missing");
+        if (r.le(4) != 0x42445743u) throw std::invalid_argument("not a database file");
+        if (r.le(1) != 1) throw std::invalid_argument("unsupported database version");
+        mode = r.le(1);
+        const uint64_t keyword_bits = r.le(2), lossy = r.le(1);
+        rows = r.le(8);
+        r.le(4);  // plaintexts_per_row (recomputed from payload_bytes, as PirConfig does)
+        payload_bytes = r.le(4);
+        const uint64_t slen = r.le(2);
+        r.need(slen);
+        r.pos += slen;  // preset name (the caller built the context for it)
+        for (int i = 0; i < 4; ++i) r.le(8);  // lossy seed
+        if (mode > 1) throw std::invalid_argument("unknown database mode");
+        if (lossy) throw std::invalid_argument("cwgpu: lossy keyword databases are not supported");
+        if (mode == 1 && (keyword_bits == 0 || keyword_bits > 64))
+            throw std::invalid_argument("keyword bit-length must be in [1, 64]");
+        if (rows == 0) throw std::invalid_argument("empty database");
+        payloads.assign(rows * payload_bytes, 0);
+        ids.assign(mode == 1 ? rows : 0, 0);
+        for (uint64_t i = 0; i < rows; ++i) {
+            const uint64_t klen = r.le(4);
+            r.need(klen);
+            if (mode == 1) {  // keyword_value (pir.cpp:22-30)
+                if (klen > 8) throw std::invalid_argument("numeric keyword longer than 8 bytes");
+                uint64_t v = 0;
+                for (uint64_t b = klen; b-- > 0;) v = (v << 8) | r.p[r.pos + b];
+                if (keyword_bits < 64 && v >= (uint64_t(1) << keyword_bits))
+                    throw std::invalid_argument("keyword outside the configured domain");
+                ids[i] = v;
+            }
+            r.pos += klen;
+            const uint64_t plen = r.le(4);
+            r.need(plen);
+            if (plen > payload_bytes) throw std::invalid_argument("payload exceeds the configured row size");
+            std::memcpy(payloads.data() + i * payload_bytes, r.p + r.pos, plen);
+            r.pos += plen;
+        }
+        if (r.pos != size) throw std::invalid_argument("trailing bytes in database file");
+        if (mode == 1) {  // parse_db's duplicate-key check, on the decoded keyword values
+            std::vector<uint64_t> srt(ids);
+            std::sort(srt.begin(), srt.end());
+            if (std::adjacent_find(srt.begin(), srt.end()) != srt.end())
+                throw std::invalid_argument("duplicate key in database file");
+        }
+    });
+    if (rc != CWG_OK) return rc;
+    return cwg_load_db_bytes(h, rows, 0, rows, k, m, payload_bytes, payloads.data(), mode == 1 ? ids.data() : nullptr);
 }
 
 int cwg_set_keys(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
                  const uint64_t* galois) {
     return guarded([&] {
-        std::lock_guard<std::mutex> g(h->c.mu);
-        CK(cudaSetDevice(h->c.device));
-        upload_keys(h->c, relin, n_galois, galois_g, galois);
-        CK(cudaStreamSynchronize(h->c.st));
+        std::lock_guard<std::mutex> gm(h->mmu);
+        for_devices(h, [&](Ctx& c, size_t) {
+            std::lock_guard<std::mutex> g(c.mu);
+            upload_keys(c, relin, n_galois, galois_g, galois);
+            CK(cudaStreamSynchronize(c.st));
+        });
     });
 }
 
@@ -1794,13 +1878,14 @@ int cwg_answer_partial(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, con
                        const uint64_t* galois, uint32_t nq, uint32_t comp, uint32_t m, const uint64_t* query,
                        uint32_t op, uint64_t* dev_partial, cwg_timings* t) {
     return guarded([&] {
+        if (h->multi()) throw state_err("cwgpu: row-shard entry points take a single-device context");
         Ctx& c = h->c;
         std::lock_guard<std::mutex> g(c.mu);
         CK(cudaSetDevice(c.device));
         auto t0 = std::chrono::steady_clock::now();
         Timer tm(c, t != nullptr);
         tm.mark(TM_START);
-        if (relin) upload_keys(c, relin, n_galois, galois_g, galois);
+        c.keys_cached = relin ? upload_keys(c, relin, n_galois, galois_g, galois) : false;
         answer_partial(c, nq, comp, m, query, op, dev_partial, tm);
         CK(cudaStreamSynchronize(c.st));
         fill_timings(c, tm, t,
@@ -1812,10 +1897,11 @@ int cwg_expand_shard(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const
                      const uint64_t* galois, uint32_t comp, const uint64_t* query, uint32_t world, uint32_t rank,
                      uint64_t* out) {
     return guarded([&] {
+        if (h->multi()) throw state_err("cwgpu: row-shard entry points take a single-device context");
         Ctx& c = h->c;
         std::lock_guard<std::mutex> g(c.mu);
         CK(cudaSetDevice(c.device));
-        if (relin) upload_keys(c, relin, n_galois, galois_g, galois);
+        c.keys_cached = relin ? upload_keys(c, relin, n_galois, galois_g, galois) : false;
         if (!c.have_keys) throw he_err("evaluation keys not set");
         const size_t per = 2 * (size_t)c.cp.L * c.cp.N;
         u64* dq = c.query.get<u64>(per);
@@ -1827,6 +1913,7 @@ int cwg_expand_shard(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const
 int cwg_answer_partial_shards(cwg_ctx* h, const uint64_t* shards, uint32_t world, uint32_t comp, uint32_t m,
                               uint32_t op, uint64_t* dev_partial, cwg_timings* t) {
     return guarded([&] {
+        if (h->multi()) throw state_err("cwgpu: row-shard entry points take a single-device context");
         Ctx& c = h->c;
         std::lock_guard<std::mutex> g(c.mu);
         CK(cudaSetDevice(c.device));
@@ -1841,6 +1928,7 @@ int cwg_answer_partial_shards(cwg_ctx* h, const uint64_t* shards, uint32_t world
 }
 int cwg_finish(cwg_ctx* h, const uint64_t* dev_partial_sum, uint32_t op, uint64_t* out, cwg_timings* t) {
     return guarded([&] {
+        if (h->multi()) throw state_err("cwgpu: row-shard entry points take a single-device context");
         Ctx& c = h->c;
         std::lock_guard<std::mutex> g(c.mu);
         CK(cudaSetDevice(c.device));
@@ -1856,17 +1944,84 @@ int cwg_finish(cwg_ctx* h, const uint64_t* dev_partial_sum, uint32_t op, uint64_
     });
 }
 
+/// cwg_answer on a multi-device context (see cwg_ctx).
+static void answer_multi(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+                         const uint64_t* galois, uint32_t nq, uint32_t comp, uint32_t m, const uint64_t* query,
+                         uint32_t op, uint64_t* out, cwg_timings* t) {
+    std::lock_guard<std::mutex> gm(h->mmu);
+    auto all = h->all();
+    const u32 W = (u32)all.size();
+    Ctx& root = h->c;
+    const auto t0 = std::chrono::steady_clock::now();
+    const size_t per = 2 * (size_t)root.cp.L * root.cp.N;
+    // sharded expansion when the query is one ciphertext and W | 2^c is a power of two: device i
+    // expands the leaves i, i + W, ... (cwg_expand_shard) and the shards are all-gathered by peer copies
+    const bool shard = nq == 1 && (W & (W - 1)) == 0 && W <= (1u << comp) && (1u << comp) <= root.cp.N;
+    const size_t shard_words = shard ? ((size_t)1 << comp) / W * per : 0;
+    std::vector<u32> ncs(W, 2);
+    for_devices(h, [&](Ctx& c, size_t i) {
+        std::lock_guard<std::mutex> g(c.mu);
+        c.keys_cached = relin ? upload_keys(c, relin, n_galois, galois_g, galois) : false;
+        if (!c.have_keys) throw he_err("evaluation keys not set");
+        if (shard) {
+            if (m != c.m) throw std::invalid_argument("query code length does not match the database");
+            u64* dq = c.query.get<u64>(per);
+            CK(cudaMemcpyAsync(dq, query, per * 8, cudaMemcpyDefault, c.st));
+            c.shard_all.get<u64>(shard_words * W);
+            expand_shard(c, dq, comp, W, (u32)i, c.shard_out.get<u64>(shard_words));
+        }
+        CK(cudaStreamSynchronize(c.st));
+    });
+    for_devices(h, [&](Ctx& c, size_t i) {
+        std::lock_guard<std::mutex> g(c.mu);
+        Timer tm(c, false);
+        u64* part = c.partial.get<u64>((size_t)c.s * 3 * c.ab.Mm * c.cp.N);
+        if (shard) {
+            u64* dst = c.shard_all.ptr<u64>();
+            for (u32 j = 0; j < W; ++j)
+                CK(cudaMemcpyPeerAsync(dst + j * shard_words, c.device, all[j]->shard_out.ptr<u64>(), all[j]->device,
+                                       shard_words * 8, c.st));
+            ncs[i] = answer_partial(c, 1, comp, m, nullptr, op, part, tm, dst, W);
+        } else {
+            ncs[i] = answer_partial(c, nq, comp, m, query, op, part, tm);
+        }
+        CK(cudaStreamSynchronize(c.st));
+    });
+    CK(cudaSetDevice(root.device));
+    std::lock_guard<std::mutex> g(root.mu);
+    Timer tm(root, t != nullptr);
+    tm.mark(TM_START);
+    const size_t words = (size_t)root.s * 3 * root.ab.Mm * root.cp.N;
+    u64* acc = root.partial.ptr<u64>();
+    u64* buf = h->red.get<u64>(words);
+    for (u32 j = 1; j < W; ++j) {  // row-shard reduction: u64 sums of residues < 2^31
+        CK(cudaMemcpyPeerAsync(buf, root.device, all[j]->partial.ptr<u64>(), all[j]->device, words * 8, root.st));
+        launch(root, k_add_u64, blocks(words, 256), 256, 0, acc, (const u64*)buf, words);
+    }
+    tm.mark(TM_MAC);
+    finish(root, acc, ncs[0], out, tm);
+    fill_timings(root, tm, t, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    if (t) {
+        t->n_devices = W;
+        for (Ctx* c : all) t->kernel_launches += c == &root ? 0 : c->launches;
+    }
+}
+
 int cwg_answer(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g, const uint64_t* galois,
                uint32_t nq, uint32_t comp, uint32_t m, const uint64_t* query, uint32_t op, uint64_t* out,
                cwg_timings* t) {
     return guarded([&] {
+        if (h->multi()) {
+            answer_multi(h, relin, n_galois, galois_g, galois, nq, comp, m, query, op, out, t);
+            return;
+        }
         Ctx& c = h->c;
         std::lock_guard<std::mutex> g(c.mu);
         CK(cudaSetDevice(c.device));
         auto t0 = std::chrono::steady_clock::now();
         Timer tm(c, t != nullptr);
         tm.mark(TM_START);
-        if (relin) upload_keys(c, relin, n_galois, galois_g, galois);
+        c.keys_cached = relin ? upload_keys(c, relin, n_galois, galois_g, galois) : false;
         u64* part = c.partial.get<u64>((size_t)c.s * 3 * c.ab.Mm * c.cp.N);
         const u32 nc = answer_partial(c, nq, comp, m, query, op, part, tm);
         finish(c, part, nc, out, tm);
@@ -1879,44 +2034,33 @@ int cwg_select(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint6
                uint32_t nq, uint32_t comp, uint32_t m, const uint64_t* query, uint32_t op, uint64_t* sel,
                uint32_t* comps, cwg_timings* t) {
     return guarded([&] {
-        Ctx& c = h->c;
-        std::lock_guard<std::mutex> g(c.mu);
-        CK(cudaSetDevice(c.device));
-        if (!c.db_loaded) throw state_err("no database loaded");
-        if (m != c.m) throw std::invalid_argument("expanded query length must equal the code length");
+        std::lock_guard<std::mutex> gm(h->mmu);
         auto t0 = std::chrono::steady_clock::now();
-        Timer tm(c, t != nullptr);
-        tm.mark(TM_START);
-        c.prep_s_ok = false;  // the selection path uses the unscaled operands only
-        if (relin) upload_keys(c, relin, n_galois, galois_g, galois);
-        if (!c.have_keys) throw he_err("evaluation keys not set");
-        const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J;
-        const size_t LN = (size_t)L * N;
-        u64* dq = c.query.get<u64>((size_t)nq * 2 * LN);
-        CK(cudaMemcpyAsync(dq, query, (size_t)nq * 2 * LN * 8, cudaMemcpyHostToDevice, c.st));
-        tm.mark(TM_H2D);
-        u64* entries = expand(c, dq, nq, comp, m);
-        tm.mark(TM_EXPAND);
-        u32* prep = nullptr;
-        if (op == CWG_OP_FOLKLORE && c.k >= 2) {
-            prep = c.prep.get<u32>((size_t)m * 2 * J * N);
-            prepare(c, entries, 2 * LN, nullptr, m, prep);
+        const size_t W = h->all().size();
+        u64 off = 0;
+        std::vector<u64> offs;
+        for (Ctx* c : h->all()) {
+            offs.push_back(off);
+            off += c->n_local;
         }
-        const u32 R = tile_rows(c);
-        u64* dsel = c.partial.get<u64>((size_t)R * 3 * LN);
-        for (u64 r0 = 0; r0 < c.n_local; r0 += R) {
-            const u32 Rt = (u32)std::min<u64>(R, c.n_local - r0);
-            CK(cudaMemsetAsync(dsel, 0, (size_t)Rt * 3 * LN * 8, c.st));
-            u32 nc = 0, zs = 0;
-            select_tile(c, entries, prep, op, r0, Rt, nc, zs, dsel);
-            tm.mark(TM_SELECT);
-            CK(cudaMemcpyAsync(sel + r0 * 3 * LN, dsel, (size_t)Rt * 3 * LN * 8, cudaMemcpyDeviceToHost, c.st));
-            CK(cudaStreamSynchronize(c.st));
-            for (u32 r = 0; r < Rt; ++r) comps[r0 + r] = nc;
-            tm.mark(TM_D2H);
+        if (W > 1) {
+            cudaPointerAttributes pa{};
+            if (cudaPointerGetAttributes(&pa, sel) == cudaSuccess && pa.type == cudaMemoryTypeDevice)
+                throw std::invalid_argument("cwgpu: a multi-device selection is written to host memory");
+            cudaGetLastError();
         }
-        fill_timings(c, tm, t,
-                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        for_devices(h, [&](Ctx& c, size_t i) {
+            std::lock_guard<std::mutex> g(c.mu);
+            Timer tm(c, t != nullptr && i == 0);
+            tm.mark(TM_START);
+            c.keys_cached = relin ? upload_keys(c, relin, n_galois, galois_g, galois) : false;
+            const size_t LN = (size_t)c.cp.L * c.cp.N;
+            select_rows(c, nq, comp, m, query, op, sel + offs[i] * 3 * LN, comps + offs[i], tm);
+            if (i == 0)
+                fill_timings(c, tm, t,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        });
+        if (t) t->n_devices = (uint32_t)W;
     });
 }
 
@@ -2026,11 +2170,45 @@ int cwg_substitute(cwg_ctx* h, uint32_t count, const uint64_t* ct, uint64_t g, u
     });
 }
 
-uint64_t cwg_kernel_launches(const cwg_ctx* h) { return h->c.launches; }
+int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
+    return guarded([&] {
+      for (Ctx* cp : h->all()) {
+        Ctx& c = *cp;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        const std::string k = key ? key : "";
+        const int v = (int)value;
+        if (k == "streams") c.nstreams = std::max(1, std::min(Ctx::kMaxStreams, v));
+        else if (k == "mac") c.mac_tma = v != 0;
+        else if (k == "mac_waves") c.mac_waves = std::max(1, v);
+        else if (k == "prescale") c.prescale = v != 0;
+        else if (k == "ntt_np") c.ntt_np = v == 2 ? 2 : 1;
+        else if (k == "round") c.round_kind = v == 0 ? 0 : 2;
+        else if (k == "fuse_mac") c.fuse_mac = v != 0;
+        else if (k == "mac_ck") c.mac_ck = (u32)std::max(0, v);
+        else if (k == "round_g2") c.round_g2 = v != 0;
+        else if (k == "round_ctas") c.round_ctas = (u32)std::max(1, std::min(4, v));
+        else if (k == "ks32") { c.ks32 = v != 0; c.ksA_ok = false; }
+        else if (k == "tile_rows") c.tile_rows_opt = (u32)std::max(0, v);
+        else if (k == "force_exact") {
+            c.force_exact = v != 0;
+            c.T.force_exact = c.force_exact ? 1u : 0u;
+            CK(cudaMemcpy(c.tab_self.p, &c.T, sizeof(DevTab), cudaMemcpyHostToDevice));
+        } else
+            throw std::invalid_argument("cwgpu: unknown option " + k);
+      }
+    });
+}
+
+uint64_t cwg_kernel_launches(const cwg_ctx* h) {
+    uint64_t n = h->c.launches;
+    for (const auto& p : h->more) n += p->launches;
+    return n;
+}
 
 void* cwg_stream(const cwg_ctx* h) { return (void*)h->c.st; }
 
-int cwg_set_profiling(cwg_ctx* h, int on) {
+int cwg_set_profiling(cwg_ctx* h, int on) {  // root device only on a multi-device context
     return guarded([&] {
         Ctx& c = h->c;
         std::lock_guard<std::mutex> g(c.mu);
@@ -2061,92 +2239,3 @@ int cwg_kernel_units(const cwg_ctx* h, uint32_t idx, double* units) {
 
 }  // extern "C"
 
-// ------------------------------------------------------------------ microbenchmarks
-#include "ntt_bench.cuh"
-
-namespace {
-template <int WB, int NP, int MINB, bool INV, bool JSLOW = false, int FAKE = 0>
-float bench_nttw_variant(cwgpu::Ctx& c, u32* buf, u32 npolys, int iters) {
-    using namespace cwgpu;
-    constexpr int LOGN = 13;
-    const size_t sm = (size_t)NP * (1 << LOGN) * 4;
-    auto kern = k_nttw_bench<LOGN, WB, NP, MINB, INV, JSLOW, FAKE>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const u32 grid = npolys / NP;
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T);
-    CK(cudaEventRecord(e0, c.st));
-    for (int i = 0; i < iters; ++i) kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T);
-    CK(cudaEventRecord(e1, c.st));
-    CK(cudaEventSynchronize(e1));
-    CK(cudaGetLastError());
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return ms / iters;
-}
-template <int MINB>
-float bench_nttw_pf(cwgpu::Ctx& c, u32* buf, u32 npolys, int iters, u32 ctas_per_sm) {
-    using namespace cwgpu;
-    constexpr int LOGN = 13, WB = 5;
-    const size_t sm = (size_t)2 * (1 << LOGN) * 4;
-    auto kern = k_nttw_bench_pf<LOGN, WB, MINB>;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    const u32 grid = 148 * ctas_per_sm;
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T, npolys);
-    CK(cudaEventRecord(e0, c.st));
-    for (int i = 0; i < iters; ++i) kern<<<grid, NttW<LOGN, WB>::T, sm, c.st>>>(buf, c.T, npolys);
-    CK(cudaEventRecord(e1, c.st));
-    CK(cudaEventSynchronize(e1));
-    CK(cudaGetLastError());
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return ms / iters;
-}
-}  // namespace
-
-extern "C" int cwg_bench_kernel(cwg_ctx* h, int which, uint32_t npolys, int iters, float* ms_per_launch) {
-    return guarded([&] {
-        Ctx& c = h->c;
-        std::lock_guard<std::mutex> g(c.mu);
-        CK(cudaSetDevice(c.device));
-        if (c.cp.logN != 13) throw std::invalid_argument("bench variants are compiled for N = 8192");
-        npolys = npolys / 6 * 6;
-        u32* buf = c.lift_tmp.get<u32>((size_t)npolys * c.cp.N);
-        CK(cudaMemsetAsync(buf, 0x1a, (size_t)npolys * c.cp.N * 4, c.st));
-        float ms = 0;
-        switch (which) {
-            case 0: ms = bench_nttw_variant<5, 1, 3, false>(c, buf, npolys, iters); break;
-            case 1: ms = bench_nttw_variant<5, 1, 3, true>(c, buf, npolys, iters); break;
-            case 2: ms = bench_nttw_variant<5, 2, 2, false>(c, buf, npolys, iters); break;
-            case 3: ms = bench_nttw_variant<5, 2, 2, true>(c, buf, npolys, iters); break;
-            case 4: ms = bench_nttw_variant<4, 1, 3, false>(c, buf, npolys, iters); break;
-            case 5: ms = bench_nttw_variant<6, 2, 1, false>(c, buf, npolys, iters); break;
-            case 6: ms = bench_nttw_variant<5, 1, 3, false, true>(c, buf, npolys, iters); break;
-            case 7: ms = bench_nttw_variant<5, 1, 3, true, true>(c, buf, npolys, iters); break;
-            case 8: ms = bench_nttw_variant<5, 2, 2, false, true>(c, buf, npolys, iters); break;
-            case 9: ms = bench_nttw_variant<5, 1, 4, false, true>(c, buf, npolys, iters); break;
-            case 10: ms = bench_nttw_variant<5, 1, 3, false, false, 1>(c, buf, npolys, iters); break;
-            case 11: ms = bench_nttw_variant<5, 2, 2, false, false, 1>(c, buf, npolys, iters); break;
-            case 12: ms = bench_nttw_variant<5, 1, 3, false, false, 2>(c, buf, npolys, iters); break;
-            case 13: ms = bench_nttw_variant<5, 1, 3, false, false, 4>(c, buf, npolys, iters); break;
-            case 14: ms = bench_nttw_variant<5, 1, 3, false, false, 7>(c, buf, npolys, iters); break;
-            case 15: ms = bench_nttw_variant<5, 2, 2, false, false, 7>(c, buf, npolys, iters); break;
-            case 16: ms = bench_nttw_pf<3>(c, buf, npolys, iters, 3); break;
-            case 18: ms = bench_nttw_variant<5, 1, 3, false, false, 8>(c, buf, npolys, iters); break;
-            case 17: ms = bench_nttw_pf<2>(c, buf, npolys, iters, 2); break;
-            case 19: ms = bench_nttw_variant<5, 1, 3, false, false, 16>(c, buf, npolys, iters); break;
-            case 20: ms = bench_nttw_variant<5, 1, 3, true, false, 16>(c, buf, npolys, iters); break;
-            default: throw std::invalid_argument("unknown benchmark variant");
-        }
-        *ms_per_launch = ms;
-    });
-}

@@ -9,8 +9,8 @@
 //                            automorphism / monomial_mul              ring.cpp:296-331
 //   k_lift                   to_aux_basis                             bfv.cpp:718-744
 //   k_tensor_intt            mul_lazy_prepared tensor + INTT          bfv.cpp:776-791
-//   k_round_mac/_chain       exact scale-and-round t/q                bfv.cpp:811-849
-//   k_mac                    weighted_sum                             bfv.cpp:944-986
+//   k_round_chain            exact scale-and-round t/q                bfv.cpp:811-849
+//   (payload MAC: k_ntt_mac in ntt_mac.cuh, k_mac2 in ntt_reg.cuh, k_mac_tma in mac.cuh: weighted_sum bfv.cpp:944-986)
 //   k_relin_add              relinearize                              bfv.cpp:859-869
 #pragma once
 #include "devtab.h"
@@ -648,51 +648,6 @@ __device__ __forceinline__ u64 mag_mod64(const u32* R, u64 q, u64 mu96) {
     return r;
 }
 
-/// Round t*D/q for P products x 3 comps x N coefficients; writes r mod a_k (k < Mm) in place
-/// into D[p][comp][k][n] (the lazy root's selection value in the MAC basis).
-__global__ void k_round_mac(u32* __restrict__ D, u32 P, DevTab T) {
-    const u32 N = T.N, J = T.J;
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)P * 3 * N) return;
-    const size_t pc = idx >> T.logN;
-    const u32 n = (u32)(idx & (N - 1));
-    u32* Dp = D + pc * T.DS * N + n;
-    HpsState h;
-    if (hps_prepare(Dp, N, T, h)) {
-        for (u32 k = 0; k < T.Mm; ++k) {
-            const u32 a = T.a[k];
-            const u64 ab = T.abar[k];
-            u64 lo = 0, hi = 0;
-            u32 j = 0;
-            for (; j + 4 <= J; j += 4) {  // 4 products < 2^64
-                u64 g = (u64)h.w[j] * T.Imod[(size_t)j * T.Mm + k];
-                g += (u64)h.w[j + 1] * T.Imod[(size_t)(j + 1) * T.Mm + k];
-                g += (u64)h.w[j + 2] * T.Imod[(size_t)(j + 2) * T.Mm + k];
-                g += (u64)h.w[j + 3] * T.Imod[(size_t)(j + 3) * T.Mm + k];
-                lo += g;
-                hi += (lo < g);
-            }
-            u64 g = 0;
-            for (; j < J; ++j) g += (u64)h.w[j] * T.Imod[(size_t)j * T.Mm + k];
-            lo += g;
-            hi += (lo < g);
-            u32 rm = h.rho >= 0 ? bar64((u64)h.rho, a, ab) : bar64((u64)(-h.rho), a, ab);
-            if (h.rho < 0 && rm) rm = a - rm;
-            const u64 tot = (u64)bar64(lo, a, ab) + hi * T.a2_64[k] + (u64)h.gamma * (a - T.IAmod[k]) + rm;
-            Dp[(size_t)k * N] = bar64(tot, a, ab);
-        }
-    } else {
-        u32 R[kAW + 2];
-        const bool neg = round_exact(h, *T.self, R);
-        for (u32 k = 0; k < T.Mm; ++k) {
-            const u32 a = T.a[k];
-            u32 r = mag_mod32(R, a, T.abar[k]);
-            if (neg && r) r = a - r;
-            Dp[(size_t)k * N] = r;
-        }
-    }
-}
-
 /// Round t*D/q into the chain: out[p][comp][i][n] = r mod q_i (mul_lazy_prepared output).
 __global__ void k_round_chain(const u32* __restrict__ D, u32 P, DevTab T, u64* __restrict__ out) {
     const u32 N = T.N, J = T.J, L = T.L;
@@ -733,65 +688,6 @@ __global__ void k_round_chain(const u32* __restrict__ D, u32 P, DevTab T, u64* _
 }
 
 // ============================================================== payload MAC
-/// acc[sj][comp][k][n] (lo, hi planes) += sum_{r < R} Z[r][comp][k][n] * DB[row0 + r][sj][k][n]
-/// Z layout: Z + ((r * nc + comp) * zstride + k) * N. DB: [rows][s][Mm][N] u32 (NTT form, mod a_k).
-__global__ void k_mac(const u32* __restrict__ Z, u32 nc, u32 zstride, const u32* __restrict__ DB, u32 R, u32 s,
-                      DevTab T, u64* __restrict__ acc_lo, u64* __restrict__ acc_hi) {
-    const u32 N = T.N, Mm = T.Mm;
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)s * Mm * N) return;
-    const u32 plane = (u32)(idx >> T.logN);
-    const u32 sj = plane / Mm, k = plane % Mm, n = (u32)(idx & (N - 1));
-    u64 lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
-    for (u32 c = 0; c < nc; ++c) {
-        const size_t o = (((size_t)sj * 3 + c) * Mm + k) * N + n;
-        lo[c] = acc_lo[o];
-        hi[c] = acc_hi[o];
-    }
-    const size_t dbs = (size_t)s * Mm * N;
-    const u32* dbp = DB + ((size_t)sj * Mm + k) * N + n;
-    u32 r = 0;
-    for (; r + 4 <= R; r += 4) {
-        const u32 d0 = __ldg(dbp + (size_t)r * dbs), d1 = __ldg(dbp + (size_t)(r + 1) * dbs);
-        const u32 d2 = __ldg(dbp + (size_t)(r + 2) * dbs), d3 = __ldg(dbp + (size_t)(r + 3) * dbs);
-        for (u32 c = 0; c < nc; ++c) {
-            const u32* zp = Z + ((size_t)c * zstride + k) * N + n;
-            const size_t zs = (size_t)nc * zstride * N;
-            u64 g = (u64)zp[(size_t)r * zs] * d0;
-            g += (u64)zp[(size_t)(r + 1) * zs] * d1;
-            g += (u64)zp[(size_t)(r + 2) * zs] * d2;
-            g += (u64)zp[(size_t)(r + 3) * zs] * d3;
-            lo[c] += g;
-            hi[c] += (lo[c] < g);
-        }
-    }
-    for (; r < R; ++r) {
-        const u32 d0 = __ldg(dbp + (size_t)r * dbs);
-        for (u32 c = 0; c < nc; ++c) {
-            const u64 g = (u64)Z[(((size_t)r * nc + c) * zstride + k) * N + n] * d0;
-            lo[c] += g;
-            hi[c] += (lo[c] < g);
-        }
-    }
-    for (u32 c = 0; c < nc; ++c) {
-        const size_t o = (((size_t)sj * 3 + c) * Mm + k) * N + n;
-        acc_lo[o] = lo[c];
-        acc_hi[o] = hi[c];
-    }
-}
-
-/// partial[x] = (hi 2^64 + lo) mod a_k (values < 2^31 stored as u64, summable across GPUs).
-__global__ void k_acc_reduce(const u64* __restrict__ acc_lo, const u64* __restrict__ acc_hi, size_t total,
-                             DevTab T, u64* __restrict__ partial) {
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= total) return;
-    const u32 k = (u32)((idx / T.N) % T.Mm);
-    const u32 a = T.a[k];
-    const u64 ab = T.abar[k];
-    const u64 v = (u64)bar64(acc_lo[idx], a, ab) + (u64)bar64(acc_hi[idx], a, ab) * T.a2_64[k];
-    partial[idx] = bar64(v, a, ab);
-}
-
 /// Summed partials -> u32 residues mod a_k (in place into a u32 plane array).
 __global__ void k_partial_mod(const u64* __restrict__ partial, size_t total, DevTab T, u32* __restrict__ X) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -889,6 +785,73 @@ __global__ void k_gather_ct(const u64* __restrict__ src, const u32* __restrict__
     if (idx >= (size_t)count * per) return;
     const size_t x = idx / per, o = idx % per;
     out[idx] = src[(size_t)sel[x] * per + o];
+}
+
+/// Strided ciphertext gather: out[x * out_stride + o] = src[(sel ? sel[x] : x) * src_stride + o] for
+/// o < per (per-row copies of the selection path as one launch).
+__global__ void k_gather_strided(const u64* __restrict__ src, size_t src_stride, const u32* __restrict__ sel,
+                                 u32 count, size_t per, u64* __restrict__ out, size_t out_stride) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)count * per) return;
+    const size_t x = idx / per, o = idx % per;
+    out[x * out_stride + o] = src[(size_t)(sel ? sel[x] : (u32)x) * src_stride + o];
+}
+
+/// Leaf pairs of the folklore product tree (pir.cpp:294-300, eq_circuits.cpp:53-69) for rows
+/// [r0, r0 + R): ia[r * np + p] = pos[r][2p], ib[...] = pos[r][2p + 1] (positions ascending).
+__global__ void k_leaf_pairs(const u32* __restrict__ pos_rows, u64 r0, u32 R, u32 k, u32* __restrict__ ia,
+                             u32* __restrict__ ib) {
+    const u32 np = k / 2;
+    const size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= (size_t)R * np) return;
+    const size_t r = x / np, p = x % np;
+    const u32* pr = pos_rows + (r0 + r) * k;
+    ia[x] = pr[2 * p];
+    ib[x] = pr[2 * p + 1];
+}
+
+/// Node pairs of one product-tree level: ia[r * np + p] = r * cnt + 2p, ib = ia + 1.
+__global__ void k_level_pairs(u32 R, u32 cnt, u32* __restrict__ ia, u32* __restrict__ ib) {
+    const u32 np = cnt / 2;
+    const size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= (size_t)R * np) return;
+    const u32 r = (u32)(x / np), p = (u32)(x % np);
+    ia[x] = r * cnt + 2 * p;
+    ib[x] = r * cnt + 2 * p + 1;
+}
+
+/// Next product-tree level [R][ncnt] from the np products per row (prod [R * np], 2-comp) and, when
+/// cnt is odd, the carried last node of each row (carry + r * carry_stride, or the expanded entry
+/// pos[r][k-1] when carry_pos != nullptr) (eq_circuits.cpp:53-69: an odd leftover moves up unchanged).
+__global__ void k_tree_next(const u64* __restrict__ prod, u32 R, u32 np, u32 ncnt, const u64* __restrict__ carry,
+                            size_t carry_stride, const u32* __restrict__ carry_pos, u64 r0, u32 k, size_t per,
+                            u64* __restrict__ out) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)R * ncnt * per) return;
+    const size_t o = idx % per, slot = (idx / per) % ncnt, r = idx / (per * ncnt);
+    u64 v;
+    if (slot < np)
+        v = prod[(r * np + slot) * per + o];
+    else if (carry_pos)
+        v = carry[(size_t)carry_pos[(r0 + r) * k + k - 1] * per + o];
+    else
+        v = carry[r * carry_stride + o];
+    out[idx] = v;
+}
+
+/// flag |= (a != b) over n words (evaluation-key cache: is the uploaded key set the resident one?)
+__global__ void k_words_differ(const u64* __restrict__ a, const u64* __restrict__ b, size_t n,
+                               unsigned int* __restrict__ flag) {
+    bool d = false;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        d |= a[i] != b[i];
+    if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(flag, 1u);
+}
+
+/// dst[x] += src[x] (row-shard partial accumulators: each word < 2^31, any device count < 2^32 sums)
+__global__ void k_add_u64(u64* __restrict__ dst, const u64* __restrict__ src, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] += src[i];
 }
 
 }  // namespace cwgpu

@@ -90,71 +90,4 @@ __global__ void __launch_bounds__(NttMac<LOGN, S, ACCS>::T, NttMac<LOGN, S, ACCS
     }
 }
 
-/// k_ntt_mac with the row planes streamed by the copy engine (s = 1, accumulators in registers):
-/// one thread bulk-copies the next row's selection plane into a shared-memory slot as soon as
-/// the current one is in registers, and the next payload plane as soon as the current MAC has
-/// read its slot, so neither global latency is exposed in the row loop (k_ntt_mac: long
-/// scoreboard stalls on the Z loads at each row start and the DB loads after the transform).
-/// Shared memory: transposes N + selection slot N + payload slot N words (2 CTAs / SM at N = 8192).
-template <int LOGN, int NC>
-__global__ void __launch_bounds__(RegNtt<LOGN>::T, 2) k_ntt_mac_tma(
-    const u32* __restrict__ Z, u32 zstride, const u32* __restrict__ DB, u32 R, u32 nchunks, DevTab T,
-    unsigned long long* __restrict__ acc) {
-    using G = RegNtt<LOGN>;
-    constexpr int E = G::E, WB = G::WB, N = 1 << LOGN, SH = LOGN - WB;
-    extern __shared__ __align__(128) u32 smd[];
-    u32* zs = smd + N;      // selection slot
-    u32* ds = smd + 2 * N;  // payload slot
-    __shared__ __align__(8) unsigned long long zfull, dfull;
-    const u32 tid = threadIdx.x;
-    const u32 Mm = T.Mm;
-    const u32 c = blockIdx.x % NC, k = (blockIdx.x / NC) % Mm, ch = blockIdx.x / (NC * Mm);
-    const u32 p = T.a[k], pinv = T.apinv[k], p2 = 2 * p;
-    const u32 r0 = (u32)(((u64)ch * R) / nchunks), r1 = (u32)(((u64)(ch + 1) * R) / nchunks);  // balanced
-    if (r0 >= r1) return;
-    const size_t dbrow = (size_t)Mm * N;
-    auto zsrc = [&](u32 i) { return Z + (((size_t)i * NC + c) * zstride + k) * N; };
-    auto dsrc = [&](u32 i) { return DB + (size_t)i * dbrow + (size_t)k * N; };
-    if (tid == 0) {
-        mbar_init(&zfull, 1);
-        mbar_init(&dfull, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(&zfull, 4u << LOGN);
-        tma_bulk_g2s(zs, zsrc(r0), 4u << LOGN, &zfull);
-        mbar_expect_tx(&dfull, 4u << LOGN);
-        tma_bulk_g2s(ds, dsrc(r0), 4u << LOGN, &dfull);
-    }
-    __syncthreads();
-    u32 a[E];
-#pragma unroll
-    for (int r = 0; r < E; ++r) a[r] = 0;
-    u32 ph = 0;
-    for (u32 i = r0; i < r1; ++i, ph ^= 1u) {
-        u32 v[1][E];
-        mbar_wait_sleep(&zfull, ph);
-#pragma unroll
-        for (int r = 0; r < E; ++r) v[0][r] = zs[((u32)r << SH) | tid];
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();  // every thread's selection words are in registers
-        if (tid == 0 && i + 1 < r1) {
-            mbar_expect_tx(&zfull, 4u << LOGN);
-            tma_bulk_g2s(zs, zsrc(i + 1), 4u << LOGN, &zfull);
-        }
-        nttw_fwd<LOGN, WB, 1>(v, smd, T.arp + (size_t)k * N, T.arps + (size_t)k * N, p);  // [0, 4p)
-        mbar_wait_sleep(&dfull, ph);
-#pragma unroll
-        for (int r = 0; r < E; ++r) a[r] = red32(a[r] + mont32(v[0][r], ds[((u32)r << SH) | tid], p, pinv), p2);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();  // every thread's payload reads done
-        if (tid == 0 && i + 1 < r1) {
-            mbar_expect_tx(&dfull, 4u << LOGN);
-            tma_bulk_g2s(ds, dsrc(i + 1), 4u << LOGN, &dfull);
-        }
-    }
-    const u32 r64 = T.a2_64[k];
-    unsigned long long* o = acc + ((size_t)c * Mm + k) * N + tid;
-#pragma unroll
-    for (int r = 0; r < E; ++r) atomicAdd(o + ((u32)r << SH), (unsigned long long)red32(mont32(a[r], r64, p, pinv), p));
-}
-
 }  // namespace cwgpu

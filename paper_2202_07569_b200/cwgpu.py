@@ -6,7 +6,8 @@ Mirrors the reference's server-side interface for the answer path:
   (``bfv.hpp:68-136``, ``pir.hpp:64-100``); ``Context.answer`` is
   ``process_query`` (``pir.cpp:337-347``), ``Context.select`` is
   ``compute_selection_vector`` (``pir.cpp:277-312``).
-* ``Client``   ~ the reference client (keygen / ``pack_query_bits`` / decrypt).
+* ``Client``   ~ the reference client (keygen / ``pack_query_bits`` / decrypt), CPU code in its
+  own library ``libcwgpu_client.so`` (no CUDA).
 
 Errors raise the reference's exception types: ``ValueError`` for
 ``std::invalid_argument``, ``HeError`` for ``he_error``.  There is no CPU fallback:
@@ -22,6 +23,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libcwgpu.so")
+CLIENT_LIB_PATH = os.path.join(HERE, "libcwgpu_client.so")
 
 _u64p = ctypes.POINTER(ctypes.c_uint64)
 _u32p = ctypes.POINTER(ctypes.c_uint32)
@@ -30,13 +32,16 @@ _u8p = ctypes.POINTER(ctypes.c_uint8)
 CWG_OK, CWG_EINVAL, CWG_EHE, CWG_ECUDA, CWG_ESTATE = 0, -1, -2, -3, -4
 OP_FOLKLORE, OP_ARITH = 0, 1
 
-# the symbols include/cwgpu.h and include/cwgpu_client.h declare
+# the symbols include/cwgpu.h (libcwgpu.so) and include/cwgpu_client.h (libcwgpu_client.so) declare
 EXPORTED_SYMBOLS = [
     "cwg_last_error", "cwg_create", "cwg_destroy", "cwg_get_info", "cwg_load_db", "cwg_load_db_bytes", "cwg_set_keys",
     "cwg_answer", "cwg_partial_words", "cwg_answer_partial", "cwg_finish", "cwg_expand_shard",
     "cwg_answer_partial_shards", "cwg_select", "cwg_ntt",
     "cwg_expand", "cwg_mul_lazy", "cwg_relinearize", "cwg_substitute", "cwg_kernel_launches",
-    "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats", "cwg_kernel_units", "cwg_bench_kernel",
+    "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats", "cwg_kernel_units", "cwg_set_option",
+    "cwg_create_multi", "cwg_device_count", "cwg_load_db_file",
+]
+CLIENT_SYMBOLS = [
     "cwg_client_last_error", "cwg_client_create", "cwg_client_destroy", "cwg_client_digits",
     "cwg_client_export_keys", "cwg_client_encrypt", "cwg_client_pack_query", "cwg_client_decrypt",
 ]
@@ -63,7 +68,8 @@ class CwgInfo(ctypes.Structure):
 class CwgTimings(ctypes.Structure):
     _fields_ = [(n, ctypes.c_double) for n in ("total_ms", "h2d_ms", "expand_ms", "select_ms", "mac_ms",
                                                "finish_ms", "d2h_ms")] + [
-        ("kernel_launches", ctypes.c_uint64), ("exact_fallbacks", ctypes.c_uint64)]
+        ("kernel_launches", ctypes.c_uint64), ("exact_fallbacks", ctypes.c_uint64), ("keys_cached", ctypes.c_uint32),
+        ("n_devices", ctypes.c_uint32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -84,10 +90,16 @@ def load_library(path: str = LIB_PATH):
     lib.cwg_create.restype = ctypes.c_void_p
     lib.cwg_create.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint64, ctypes.c_uint32,
                                ctypes.c_uint32, ctypes.c_int]
+    lib.cwg_create_multi.restype = ctypes.c_void_p
+    lib.cwg_create_multi.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint64, ctypes.c_uint32,
+                                     ctypes.c_uint32, ctypes.POINTER(ctypes.c_int), ctypes.c_int]
+    lib.cwg_device_count.restype = ctypes.c_int
     lib.cwg_destroy.argtypes = [ctypes.c_void_p]
     lib.cwg_get_info.argtypes = [ctypes.c_void_p, ctypes.POINTER(CwgInfo)]
     lib.cwg_load_db.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
                                 ctypes.c_uint32, ctypes.c_uint32, _u32p, _u64p]
+    lib.cwg_load_db_file.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32,
+                                     ctypes.c_uint32]
     lib.cwg_set_keys.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, _u64p, _u64p]
     lib.cwg_load_db_bytes.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                       ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
@@ -119,6 +131,22 @@ def load_library(path: str = LIB_PATH):
     lib.cwg_kernel_stats.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_char_p, ctypes.c_uint32,
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)]
     lib.cwg_kernel_units.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.POINTER(ctypes.c_double)]
+    lib.cwg_set_option.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int64]
+    _LIB = lib
+    return lib
+
+
+_CLIENT_LIB = None
+
+
+def load_client_library(path: str = CLIENT_LIB_PATH):
+    """Load libcwgpu_client.so (CPU only; built in-tree by paper_2202_07569_b200.build)."""
+    global _CLIENT_LIB
+    if _CLIENT_LIB is not None:
+        return _CLIENT_LIB
+    if not os.path.exists(path):
+        raise RuntimeError(f"libcwgpu_client.so not built ({path}); run python -m paper_2202_07569_b200.build")
+    lib = ctypes.CDLL(path)
     lib.cwg_client_last_error.restype = ctypes.c_char_p
     lib.cwg_client_create.restype = ctypes.c_void_p
     lib.cwg_client_create.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint64, ctypes.c_uint32,
@@ -131,7 +159,7 @@ def load_library(path: str = LIB_PATH):
     lib.cwg_client_pack_query.argtypes = [ctypes.c_void_p, _u8p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
                                           _u64p]
     lib.cwg_client_decrypt.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, _u64p]
-    _LIB = lib
+    _CLIENT_LIB = lib
     return lib
 
 
@@ -177,20 +205,32 @@ class Keys:
 
 
 class Context:
-    """The B200 server for one parameter set on one device."""
+    """The B200 server for one parameter set on one device, or -- device=[ids] -- on several
+    devices of this process (cwg_create_multi: rows split across them, one reduction)."""
 
-    def __init__(self, N, primes, t, relin_bits=16, galois_bits=16, device=0):
+    def __init__(self, N, primes, t, relin_bits=16, galois_bits=16, device=0, options=None):
         self.lib = lib = load_library()
         self.N, self.t = int(N), int(t)
         self.primes = _c64(primes)
         self.L = len(self.primes)
-        h = lib.cwg_create(self.N, self.L, _p64(self.primes), self.t, relin_bits, galois_bits, device)
+        if isinstance(device, (list, tuple)):
+            ids = (ctypes.c_int * len(device))(*device)
+            h = lib.cwg_create_multi(self.N, self.L, _p64(self.primes), self.t, relin_bits, galois_bits, ids,
+                                     len(device))
+        else:
+            h = lib.cwg_create(self.N, self.L, _p64(self.primes), self.t, relin_bits, galois_bits, device)
         if not h:
             msg = lib.cwg_last_error().decode()
             if "CUDA" in msg or "cuda" in msg:
                 raise CudaError(msg)
             raise ValueError(msg)
         self.h = h
+        for key, value in (options or {}).items():
+            self.set_option(key, value)
+
+    def set_option(self, key: str, value: int):
+        """cwg_set_option: tuning / test switches (see include/cwgpu.h)."""
+        _raise(self.lib, self.lib.cwg_set_option(self.h, key.encode(), int(value)))
 
     def close(self):
         if getattr(self, "h", None):
@@ -229,6 +269,15 @@ class Context:
         ids = None if row_ids is None else np.ascontiguousarray(row_ids, dtype=np.uint64)
         _raise(self.lib, self.lib.cwg_load_db_bytes(self.h, n_total, row_begin, n_local, k, m, nbytes,
                                                     payloads.ctypes.data, None if ids is None else ids.ctypes.data))
+
+    def load_db_file(self, path_or_bytes, k, m):
+        """cwg_load_db_file: the reference's CWDB database file (db_file.cpp) into the device."""
+        data = path_or_bytes
+        if isinstance(path_or_bytes, str):
+            with open(path_or_bytes, "rb") as f:
+                data = f.read()
+        buf = np.frombuffer(data, dtype=np.uint8)
+        _raise(self.lib, self.lib.cwg_load_db_file(self.h, buf.ctypes.data, buf.size, k, m))
 
     def set_keys(self, keys: Keys):
         relin, galois = _c64(keys.relin), _c64(keys.galois)
@@ -303,6 +352,16 @@ class Context:
                                  ctypes.byref(timings) if timings is not None else None)
         _raise(self.lib, rc)
         return out
+
+    def select_ptr(self, query, c, m, sel_ptr, op=OP_FOLKLORE, keys_ptrs=(None, 0, None, None), timings=None):
+        """cwg_select into a raw (device or host) buffer of n_local x 3 x L x N words; returns comps."""
+        query = _c64(query)
+        comps = np.zeros(self.info().n_local, np.uint32)
+        rc = self.lib.cwg_select(self.h, *keys_ptrs, query.shape[0], c, m, query.ctypes.data, op,
+                                 ctypes.cast(sel_ptr, _u64p), _p32(comps),
+                                 ctypes.byref(timings) if timings is not None else None)
+        _raise(self.lib, rc)
+        return comps
 
     def select(self, query, c, m, op=OP_FOLKLORE, keys=None, timings=False):
         """compute_selection_vector (pir.cpp:277-312): ([n][3][L][N], comps[n])."""
@@ -384,7 +443,7 @@ class Client:
     """Client side (keygen / query / decrypt) on the CPU; reproduces the reference's seeded keys."""
 
     def __init__(self, N, primes, t, seed, galois_levels, relin_bits=16, galois_bits=16):
-        self.lib = lib = load_library()
+        self.lib = lib = load_client_library()
         self.N, self.t = int(N), int(t)
         self.primes = _c64(primes)
         self.L = len(self.primes)

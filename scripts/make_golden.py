@@ -90,10 +90,59 @@ def full(names):
         print(name, gold[name], flush=True)
 
 
+C2_TILE = 1024  # rows per tile hash (GPU tests may check the selection tile by tile)
+
+
+def c2(names):
+    """Config 2 (equality microbenchmark): the reference's compute_selection_vector BFV branch
+    (pir.cpp:287-302, via ref_select) over all 16384 seeded codewords for each k, hashed as
+    SHA-256 of the [n][3][L][N] selection array (2-component rows zero padded) in C2_TILE-row
+    tiles plus the whole array, and of comps[n]."""
+    import oracle
+    from paper_2202_07569_b200 import Client, configs
+
+    ref = oracle.RefLib()
+    path = os.path.join(GOLD, "answers.json")
+    gold = json.load(open(path)) if os.path.exists(path) else {}
+    for name in names:
+        cfg = configs.config(name)
+        t0 = time.time()
+        client = Client(cfg.N, cfg.primes, cfg.t, seed=1, galois_levels=cfg.c)
+        keys = client.keys()
+        pos = configs.db_positions(cfg, 1)
+        target = configs.query_row(cfg, 1)
+        q = client.pack_query(configs.codeword_bits(pos[target], cfg.m), cfg.c, first_index=1)
+        be = oracle.RefBackend(ref, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), keys=(keys.relin, keys.galois))
+        sel, comps = be.select(q, cfg.c, cfg.m, pos)
+        secs = time.time() - t0
+        whole = hashlib.sha256()
+        tiles = []
+        for r0 in range(0, cfg.n, C2_TILE):
+            b = sel[r0:r0 + C2_TILE].tobytes()
+            whole.update(b)
+            tiles.append(hashlib.sha256(b).hexdigest())
+        # decrypt spot check: matching rows decrypt to the constant 1, others to 0 (coefficient 0)
+        match = np.all(pos == pos[target], axis=1)
+        rows = [int(np.flatnonzero(match)[0]), int(np.flatnonzero(~match)[0])]
+        dec = [int(client.decrypt(sel[r, :comps[r]])[0]) for r in rows]
+        gold[name] = {"sha256": whole.hexdigest(), "tile_rows": C2_TILE, "tile_sha256": tiles,
+                      "comps_sha256": hashlib.sha256(comps.astype(np.uint32).tobytes()).hexdigest(),
+                      "comps": int(comps[0]), "seed": 1, "target": int(target), "shape": list(sel.shape),
+                      "matches": int(match.sum()), "decrypt_match_nonmatch": dec,
+                      "reference_seconds": round(secs, 1), "reference_threads": ref.worker_threads()}
+        del sel
+        json.dump(gold, open(path, "w"), indent=1, sort_keys=True)
+        print(name, {k: v for k, v in gold[name].items() if k != "tile_sha256"}, flush=True)
+
+
 if __name__ == "__main__":
     args = sys.argv[1:] or ["small"]
     if "small" in args:
         small()
         args = [a for a in args if a != "small"]
+    c2_names = [a for a in args if a.startswith("C2")]
+    if c2_names:
+        c2(c2_names)
+    args = [a for a in args if not a.startswith("C2")]
     if args:
         full(args)

@@ -11,24 +11,35 @@ import pytest
 from conftest import ROOT, small_params
 
 
-def _declared_symbols():
-    names = []
-    for h in ("cwgpu.h", "cwgpu_client.h"):
-        src = open(os.path.join(ROOT, "include", h)).read()
-        names += re.findall(r"\b(cwg_[a-z_]+)\s*\(", src)
-    return sorted(set(names))
+def _declared_symbols(header):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    return sorted(set(re.findall(r"\b(cwg_[a-z_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
     from paper_2202_07569_b200 import build
-    from paper_2202_07569_b200.cwgpu import EXPORTED_SYMBOLS
+    from paper_2202_07569_b200.cwgpu import CLIENT_SYMBOLS, EXPORTED_SYMBOLS
 
-    lib = ctypes.CDLL(build.build())
-    declared = _declared_symbols()
-    assert declared, "no declarations parsed"
-    for name in declared:
-        assert hasattr(lib, name), name
-    assert sorted(EXPORTED_SYMBOLS) == declared
+    build.build()
+    for path, header, listed in ((build.LIB, "cwgpu.h", EXPORTED_SYMBOLS),
+                                 (build.CLIENT_LIB, "cwgpu_client.h", CLIENT_SYMBOLS)):
+        lib = ctypes.CDLL(path)
+        declared = _declared_symbols(header)
+        assert declared, "no declarations parsed"
+        for name in declared:
+            assert hasattr(lib, name), name
+        assert sorted(listed) == declared
+
+
+def test_client_library_has_no_cuda_dependency():
+    """The seeded client is CPU code in its own library: harness code that only needs keys and
+    queries (the reference arm of bench.py, the golden-vector script) never maps libcwgpu.so."""
+    import subprocess
+
+    from paper_2202_07569_b200 import build
+
+    out = subprocess.run(["ldd", build.build_client()], capture_output=True, text=True).stdout
+    assert "cuda" not in out.lower() and "libcwgpu.so" not in out
 
 
 def test_create_without_gpu_fails_loudly():

@@ -8,7 +8,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run(reflib, cfg, rows, seed=1, select_only=False, expect_kernel=None):
+def _run(reflib, cfg, rows, seed=1, select_only=False, expect_kernel=None, options=None):
     from oracle import RefBackend
     from paper_2202_07569_b200 import Client, Context, configs
 
@@ -18,7 +18,7 @@ def _run(reflib, cfg, rows, seed=1, select_only=False, expect_kernel=None):
     target = rows // 3
     q = client.pack_query(configs.codeword_bits(pos[target], cfg.m), cfg.c, first_index=1)
     be = RefBackend(reflib, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), keys=(keys.relin, keys.galois))
-    ctx = Context(cfg.N, cfg.primes, cfg.t)
+    ctx = Context(cfg.N, cfg.primes, cfg.t, options=options)
     if select_only:
         want, wc = be.select(q, cfg.c, cfg.m, pos)
         ctx.load_db(pos, None, m=cfg.m)
@@ -63,7 +63,7 @@ def test_config2_full_params_reduced_rows(gpu, reflib, k):
     client, sel, pos, target = _run(reflib, cfg, 10, select_only=True)
 
 
-def test_payload_mac_kernels_agree_under_repetition(gpu, monkeypatch):
+def test_payload_mac_kernels_agree_under_repetition(gpu):
     """The TMA-fed payload MAC (k_mac_tma: 4-stage shared-memory ring refilled by cp.async.bulk)
     and the register-streaming MAC (k_mac2) produce the same partial accumulators, answer after
     answer, at C3 parameters (15 plaintexts per row: the TMA path) over several row tiles (a
@@ -79,8 +79,7 @@ def test_payload_mac_kernels_agree_under_repetition(gpu, monkeypatch):
     payload = configs.db_payload(cfg, 1, 0, cfg.n)
     parts = {}
     for mac in ("v2", "tma"):
-        monkeypatch.setenv("CWGPU_MAC", mac)
-        ctx = Context(cfg.N, cfg.primes, cfg.t)
+        ctx = Context(cfg.N, cfg.primes, cfg.t, options={"mac": int(mac == "tma")})
         ctx.load_db(positions, payload, n_total=cfg.n, m=cfg.m)
         ctx.set_keys(keys)
         runs = []
@@ -94,28 +93,20 @@ def test_payload_mac_kernels_agree_under_repetition(gpu, monkeypatch):
         assert np.array_equal(r, parts["v2"][0])
 
 
-@pytest.mark.parametrize("env", [
-    {"CWGPU_FUSE_MAC": "0", "CWGPU_ROUND_TMA": "0"},  # sel NTT + separate MAC kernels, k_round_tc
-    {},                                                # default: k_tensor_intt_r, k_round_tma, k_ntt_mac
-    {"CWGPU_FUSE_MAC": "2"},                           # k_ntt_mac with register accumulators
-    {"CWGPU_FUSE_MAC": "3"},                           # k_ntt_mac_tma (bulk-copied row planes)
-    {"CWGPU_FUSE_TIR": "1"},                           # k_tir: tensor + INTT + rounding over a J-CTA cluster
-    {"CWGPU_FUSE_TIR": "1", "CWGPU_FUSE_MAC": "0"},    # k_tir output through the unfused NTT + MAC
-    {"CWGPU_FORCE_EXACT": "1"},                        # every rounding through round_exact (k_round_tma)
-    {"CWGPU_FORCE_EXACT": "1", "CWGPU_FUSE_TIR": "1"},  # ... inside the cluster kernel
-], ids=["unfused", "default", "mac-regs", "mac-tma", "tir", "tir-unfused-mac", "exact", "exact-tir"])
-def test_answer_path_variants_match_reference(gpu, reflib, monkeypatch, env):
+@pytest.mark.parametrize("opts,kernel", [
+    ({"fuse_mac": 0}, "k_round_tma"),                   # selection NTT + separate payload MAC kernels
+    ({}, "k_round_tma"),                                # default: k_tensor_intt_r, k_round_tma, k_ntt_mac
+    ({"streams": 1}, "k_round_tma"),                    # one tile stream
+    ({"round_g2": 0}, "k_round_tma"),                   # one-GEMM rounding epilogue
+    ({"round": 0}, "k_round_mac"),                      # IMAD-only rounding
+    ({"ks32": 0}, "k_round_tma"),                       # 64-bit key switching in the expansion
+    ({"force_exact": 1}, "k_round_tma"),                # every rounding through round_exact
+    ({"force_exact": 1, "fuse_mac": 0}, "k_round_tma"),
+], ids=["unfused", "default", "one-stream", "one-gemm", "imad-round", "ks64", "exact", "exact-unfused"])
+def test_answer_path_variants_match_reference(gpu, reflib, opts, kernel):
     """Every kernel variant of the answer path (tensor/rounding/NTT/MAC fusions, TMA feeds, the
-    exact multiword rounding inside each engine) against the reference at full C4 parameters (the
-    cluster kernel at C1's), over ragged 16-row tiles rotating over the tile streams."""
+    exact multiword rounding) against the reference at full C4 parameters, over ragged 16-row
+    tiles rotating over the tile streams."""
     from paper_2202_07569_b200 import configs
 
-    monkeypatch.setenv("CWGPU_TILE_ROWS", "16")
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    if env.get("CWGPU_FUSE_TIR") == "1":
-        # the cluster kernel needs one CTA per aux prime with N / J a multiple of 128: C1 (J = 8);
-        # C2-C4 use J = 15 aux primes
-        _run(reflib, configs.config("C1"), 40, expect_kernel="k_tir")
-    else:
-        _run(reflib, configs.config("C4"), 40, expect_kernel="k_round_tc")
+    _run(reflib, configs.config("C4"), 40, expect_kernel=kernel, options={"tile_rows": 16, **opts})

@@ -120,7 +120,7 @@ def test_relinearize(gpu, reflib):
     assert np.array_equal(ctx.relinearize(ct3), be.finalize(ct3))
 
 
-def _answer_case(reflib, N, primes, t, n, k, m, c, s, op, seed, positions=None, target=None, tile=0):
+def _answer_case(reflib, N, primes, t, n, k, m, c, s, op, seed, positions=None, target=None, tile=0, options=None):
     from paper_2202_07569_b200 import configs
 
     be = _ref_backend(reflib, N, primes, t, seed=seed, levels=c)
@@ -132,7 +132,7 @@ def _answer_case(reflib, N, primes, t, n, k, m, c, s, op, seed, positions=None, 
     q = be.pack_query(configs.codeword_bits(positions[target], m), c)
     db = r.integers(0, t, (n, s, N), dtype=np.uint64)
     want, _ = be.answer(q, c, m, positions, db, op=op, tile_rows=tile)
-    ctx = _ctx(N, primes, t)
+    ctx = _ctx(N, primes, t, options=options)
     ctx.load_db(positions, db, m=m)
     got = ctx.answer(q, c, m, op=op, keys=keys)
     return got, want, be, db[target]
@@ -257,62 +257,48 @@ def test_errors_match_reference_messages(gpu):
         ctx.answer(q, 3, 6)
 
 
-@pytest.mark.parametrize("kind", ["tc", "hyb", "int"])
+@pytest.mark.parametrize("kind", ["tc", "int"])
 def test_exact_fallback_paths_match(gpu, reflib, kind):
     """Every rounding / centring decision forced through the exact multiword path
-    (round_exact, crt_round_exact) in a subprocess with CWGPU_FORCE_EXACT=1, for each
-    rounding engine (tensor-core, IMAD + DFMA, IMAD only)."""
-    import os
-    import subprocess
-    import sys
+    (round_exact, crt_round_exact; option force_exact) for each rounding engine (tensor-core
+    k_round_tma, IMAD-only k_round_mac_t)."""
+    from paper_2202_07569_b200 import Context, configs
 
-    code = r'''
-import numpy as np, sys
-sys.path.insert(0, %r)
-sys.path.insert(0, %r)
-from conftest import small_params
-from oracle import RefLib, RefBackend
-from paper_2202_07569_b200 import Context, configs, Keys
-ref = RefLib()
-N, primes, t = small_params(1024, 3, 36, 12289)
-be = RefBackend(ref, N, t, np.array(primes, np.uint64), seed=31, galois_levels=4)
-r = np.random.default_rng(5)
-a = np.stack([np.stack([r.integers(0, p, N, dtype=np.uint64) for p in primes]) for _ in range(2)])
-b = np.stack([np.stack([r.integers(0, p, N, dtype=np.uint64) for p in primes]) for _ in range(2)])
-ctx = Context(N, primes, t)
-assert np.array_equal(ctx.mul_lazy(a, b), be.mul_lazy(a, b))
-n, k, m, c = 20, 2, 7, 3
-pos = configs.perfect_map(np.arange(n), m, k)
-q = be.pack_query(configs.codeword_bits(pos[4], m), c)
-db = r.integers(0, t, (n, 1, N), dtype=np.uint64)
-want, _ = be.answer(q, c, m, pos, db)
-rk, gk = be.export_keys()
-ctx.load_db(pos, db, m=m)
-got, tm = ctx.answer(q, c, m, keys=Keys(rk, gk), timings=True)
-assert np.array_equal(got, want)
-assert tm["exact_fallbacks"] > 0
-print("ok", tm["exact_fallbacks"])
-''' % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CWGPU_FORCE_EXACT="1", CWGPU_ROUND=kind)
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0, out.stdout + out.stderr
-    assert "ok" in out.stdout
+    N, primes, t = small_params(1024, 3, 36, 12289)
+    be = _ref_backend(reflib, N, primes, t, seed=31, levels=4)
+    r = np.random.default_rng(5)
+    a = np.stack([np.stack([r.integers(0, p, N, dtype=np.uint64) for p in primes]) for _ in range(2)])
+    b = np.stack([np.stack([r.integers(0, p, N, dtype=np.uint64) for p in primes]) for _ in range(2)])
+    opts = {"force_exact": 1, "round": 2 if kind == "tc" else 0}
+    ctx = Context(N, primes, t, options=opts)
+    assert np.array_equal(ctx.mul_lazy(a, b), be.mul_lazy(a, b))
+    n, k, m, c = 20, 2, 7, 3
+    pos = configs.perfect_map(np.arange(n), m, k)
+    q = be.pack_query(configs.codeword_bits(pos[4], m), c)
+    db = r.integers(0, t, (n, 1, N), dtype=np.uint64)
+    want, _ = be.answer(q, c, m, pos, db)
+    ctx.load_db(pos, db, m=m)
+    ctx.set_profiling(True)
+    got, tm = ctx.answer(q, c, m, keys=_keys(be), timings=True)
+    assert np.array_equal(got, want)
+    assert tm["exact_fallbacks"] > 0
+    assert ("k_round_tma" if kind == "tc" else "k_round_mac") in ctx.kernel_stats()
 
 
-@pytest.mark.parametrize("kind", ["tc", "hyb", "int"])
+@pytest.mark.parametrize("kind", ["tc", "int"])
 @pytest.mark.parametrize("N,L,bits", [(2048, 4, 50), (4096, 3, 36), (1024, 8, 55)])
-def test_rounding_engines(gpu, reflib, monkeypatch, kind, N, L, bits):
-    """The three implementations of the tensor rounding (bfv.cpp:811-849) -- tcgen05 int8 GEMM
-    (k_round_tc), IMAD + DFMA (k_round_hyb), IMAD only (k_round_mac_t) -- against the reference
-    answer, across aux-basis widths (JM = 8, 16, 32)."""
+def test_rounding_engines(gpu, reflib, kind, N, L, bits):
+    """The two implementations of the tensor rounding (bfv.cpp:811-849) -- tcgen05 int8 GEMM
+    (k_round_tma) and IMAD only (k_round_mac_t) -- against the reference answer, across
+    aux-basis widths (JM = 8, 16, 32)."""
     from paper_2202_07569_b200 import configs
 
-    monkeypatch.setenv("CWGPU_ROUND", kind)
     _, primes, t = small_params(N, L, bits, 65537)
     n, k = 30, 2
     m = configs.min_code_length(n, k)
     c = configs.default_compression(N, m)
-    got, want, be, payload = _answer_case(reflib, N, primes, t, n, k, m, c, s=1, op=0, seed=70 + L)
+    got, want, be, payload = _answer_case(reflib, N, primes, t, n, k, m, c, s=1, op=0, seed=70 + L,
+                                          options={"round": 2 if kind == "tc" else 0})
     assert np.array_equal(got, want)
     assert np.array_equal(be.decrypt(got[0]), payload[0])
 
@@ -446,3 +432,95 @@ def test_load_db_bytes_errors_and_keyword_ids(gpu, reflib):
         ctx.load_db_bytes(pl, k, m, row_ids=dup)
     with pytest.raises(ValueError, match="perfect_map: input out of range"):
         ctx.load_db_bytes(pl, 2, 8, row_ids=np.arange(n, dtype=np.uint64) + 20)
+
+
+@pytest.mark.parametrize("ndev", [1, 2])
+def test_load_db_file_matches_reference(gpu, reflib, tmp_path, ndev):
+    """The reference's own CWDB file (write_db_file, db_file.cpp:13-31) loaded by cwg_load_db_file
+    (index mode, ragged payloads zero padded as chunk_payload does) answers exactly as the
+    reference's process_query on PirDatabase::setup of the same rows; keyword mode equals the
+    device setup from the decoded keyword values; the parse_db / setup errors come back as the
+    reference's messages.  ndev = 2: two contexts on one GPU (cwg_create_multi, rows split)."""
+    from paper_2202_07569_b200 import configs
+
+    N, primes, t = small_params()
+    n, k, c, pb = 30, 2, 4, 300
+    m = configs.min_code_length(n, k)
+    be = _ref_backend(reflib, N, primes, t, seed=61, levels=c)
+    keys = _keys(be)
+    r = np.random.default_rng(62)
+    payloads = r.integers(0, 256, (n, pb), dtype=np.uint8)
+    payloads[:, 0] |= 1
+    path = str(tmp_path / "db.cwdb")
+    reflib.write_db_file(path, payloads)
+    q = be.pack_query(configs.codeword_bits(configs.perfect_map([17], m, k)[0], m), c)
+    want, _, _ = be.process_query_bytes(q, c, m, n, k, payloads)
+    ctx = _ctx(N, primes, t, device=[0] * ndev)
+    ctx.load_db_file(path, k, m)
+    assert np.array_equal(ctx.answer(q, c, m, keys=keys), want)
+    # keyword mode: 4-byte little-endian keys -> keyword_value
+    mk, kk = 569, 4
+    ids = r.choice(1 << 32, n, replace=False).astype(np.uint64)
+    kbytes = ids.astype("<u4").view(np.uint8).reshape(n, 4)
+    kpath = str(tmp_path / "kw.cwdb")
+    reflib.write_db_file(kpath, payloads, keys=kbytes, keyword_bits=32)
+    ctx.load_db_file(kpath, kk, mk)
+    be10 = _ref_backend(reflib, N, primes, t, seed=61, levels=10)
+    k10 = _keys(be10)
+    qk = be10.pack_query(configs.codeword_bits(configs.perfect_map([int(ids[5])], mk, kk)[0], mk), 10)
+    got = ctx.answer(qk, 10, mk, keys=k10)
+    ref_ctx = _ctx(N, primes, t)
+    ref_ctx.load_db_bytes(payloads, kk, mk, row_ids=ids)
+    assert np.array_equal(got, ref_ctx.answer(qk, 10, mk, keys=k10))
+    # errors (parse_db / setup wording)
+    data = open(path, "rb").read()
+    with pytest.raises(ValueError, match="not a database file"):
+        ctx.load_db_file(b"XXXX" + data[4:], k, m)
+    with pytest.raises(ValueError, match="trailing bytes in database file"):
+        ctx.load_db_file(data + b"\0", k, m)
+    with pytest.raises(ValueError, match="truncated database file"):
+        ctx.load_db_file(data[:-1], k, m)
+    dup = kbytes.copy()
+    dup[3] = dup[8]
+    reflib.write_db_file(kpath, payloads, keys=dup, keyword_bits=32)
+    with pytest.raises(ValueError, match="duplicate key in database file"):
+        ctx.load_db_file(kpath, kk, mk)
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
+def test_multi_device_context_matches_single(gpu, reflib, devices):
+    """cwg_create_multi (SURVEY 8b device_ids): rows split across contexts (here several on one
+    GPU), sharded expansion all-gathered by peer copies (power-of-two counts) or replicated, partials
+    summed on the root -- bit-identical to the reference answer; selection rows land in place; the
+    per-process row-shard entry points refuse a multi-device context."""
+    import torch
+
+    from paper_2202_07569_b200 import StateError, configs
+
+    N, primes, t = small_params(2048, 4, 50, 65537)
+    for k, op, s in ((2, 0, 1), (4, 1, 2)):
+        n = 41
+        m = configs.min_code_length(n, k)
+        c = configs.default_compression(N, m)
+        be = _ref_backend(reflib, N, primes, t, seed=90 + k, levels=c)
+        keys = _keys(be)
+        r = np.random.default_rng(k)
+        pos = configs.perfect_map(np.arange(n), m, k)
+        target = 29
+        q = be.pack_query(configs.codeword_bits(pos[target], m), c)
+        db = r.integers(0, t, (n, s, N), dtype=np.uint64)
+        want, _ = be.answer(q, c, m, pos, db, op=op)
+        ctx = _ctx(N, primes, t, device=devices)
+        ctx.load_db(pos, db, m=m)
+        assert ctx.info().n_local == n
+        got, tm = ctx.answer(q, c, m, op=op, keys=keys, timings=True)
+        assert np.array_equal(got, want)
+        assert tm["n_devices"] == len(devices)
+        got2, tm2 = ctx.answer(q, c, m, op=op, keys=keys, timings=True)  # same keys again: device key cache
+        assert np.array_equal(got2, want) and tm2["keys_cached"] == 1
+        if op == 0:
+            sel_want, comps_want = be.select(q, c, m, pos)
+            sel, comps = ctx.select(q, c, m, keys=keys)
+            assert np.array_equal(sel, sel_want) and np.array_equal(comps, comps_want)
+        with pytest.raises(StateError):
+            ctx.answer_partial(q, c, m, torch.zeros(8, dtype=torch.int64, device="cuda").data_ptr())
