@@ -22,6 +22,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/cwgpu.h"
 #include "kernels.cuh"
 #include "ntt_reg.cuh"
@@ -107,6 +109,7 @@ struct Ctx {
     bool force_exact = false;  // "force_exact": every rounding / lift decision through the multiword path (tests)
     // key switching through the 30-bit aux primes ("ks32" = 0: the 64-bit NTT path)
     bool ks32 = true;
+    bool ks_wide = true;  // "ks_wide": shared-load key-switch MAC also for 16 < D <= 32 digits
     bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
     KsCrt ksC_r{}, ksC_g{};            // K' = 0: this key type keeps the 64-bit path
     DevBuf relinA, galoisA, ksdig, ksmac;  // keys re-based into the aux primes, digit / MAC scratch
@@ -183,6 +186,15 @@ struct Ctx {
 
 thread_local std::string g_err;
 
+/// NVTX range for the host-side stages (expand / select / MAC / finish / load / keys): visible in
+/// Nsight timelines, free when no tool is attached.
+struct Nvtx {
+    explicit Nvtx(const char* s) { nvtxRangePushA(s); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
+
 // ------------------------------------------------------------------ launches
 template <class K, class... A>
 static void launch_named(Ctx& c, const char* name, K kern, size_t grid, unsigned block, size_t smem, A... args) {
@@ -226,6 +238,32 @@ static void launch_named(Ctx& c, const char* name, K kern, size_t grid, unsigned
     c.next_units = 0;
 }
 #define launch(c, kern, ...) launch_named(c, #kern, kern, __VA_ARGS__)
+
+/// launch_named for an explicit (multi-dimensional) launch configuration (cfg.stream is replaced by
+/// the context's stream); the same profiling / counting.
+template <class K, class... A>
+static void launch_grid(Ctx& c, const char* name, K kern, cudaLaunchConfig_t cfg, A... args) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c.profiling) {
+        for (cudaEvent_t* e : {&e0, &e1}) {
+            if (c.ev_pool.empty()) {
+                CK(cudaEventCreate(e));
+            } else {
+                *e = c.ev_pool.back();
+                c.ev_pool.pop_back();
+            }
+        }
+        CK(cudaEventRecord(e0, c.st));
+    }
+    cfg.stream = c.st;
+    CK(cudaLaunchKernelEx(&cfg, kern, args...));
+    ++c.launches;
+    if (c.profiling) {
+        CK(cudaEventRecord(e1, c.st));
+        c.prof_pending.push_back({name, e0, e1, c.next_units > 0 ? c.next_units : (double)cfg.gridDim.x});
+    }
+    c.next_units = 0;
+}
 
 /// fold finished launch events into per-kernel totals (call after a stream sync)
 static void prof_collect(Ctx& c) {
@@ -824,7 +862,22 @@ static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
             // shared-load variant once the level is wide enough to fill the GPU (B >= 64 rows of
             // K N threads / 2); narrow levels and long digit chains keep one output per thread
             // (latency-bound otherwise: C5's D = 25, L = 8 ran 917 vs 320 ms with it)
-            if (D <= (u32)kKsDmax && B >= 64)
+            // slot-major MAC (key block in registers, rows streamed) for the digit counts of the
+            // 16-bit decompositions of the configured chains (7: 108-bit q, 14: 218-bit, 25: 400-bit)
+            const u32 gx = (u32)blocks((size_t)K * N, 128);
+            const u32 gy = std::max<u32>(1, std::min<u32>(B, (148 * 6 + gx - 1) / gx));
+            auto ks_s = [&](auto kern) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(gx, gy);
+                cfg.blockDim = dim3(128);
+                cfg.stream = c.st;
+                c.next_units = (double)B * 2 * L * K;  // output planes
+                launch_grid(c, "k_ks_mac32", kern, cfg, (const u32*)dA, kA, B, L, N, C, (const u64*)c.T.abar, mA);
+            };
+            if (c.ks_wide && D == 7) ks_s(k_ks_mac32s<7, 6, 8, 3>);
+            else if (c.ks_wide && D == 14) ks_s(k_ks_mac32s<14, 5, 8, 2>);
+            else if (c.ks_wide && D == 25) ks_s(k_ks_mac32s<25, 4, 8, 2>);
+            else if (D <= (u32)kKsDmax && B >= 64)
                 launch_named(c, "k_ks_mac32", k_ks_mac32x<kKsDmax>, blocks((size_t)((B + 1) / 2) * K * N, 128), 128, 0,
                              (const u32*)dA, kA, B, D, L, N, C, (const u64*)c.T.abar, mA);
             else
@@ -977,14 +1030,18 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
                          bool to_mac, u64* chain_out, bool prepA_scaled = false) {
     const u32 N = c.cp.N, J = c.ab.J;
     u32* D = c.dcur->get<u32>((size_t)P * 3 * c.T.DS * N);
-    const bool tc = to_mac && round_tc_on(c);
+    // tensor-core rounding for both outputs: MAC-basis selection values (to_mac) or, for chain
+    // outputs (product-tree nodes, selection ciphertexts), r mod a_k converted to r mod q_i by the
+    // exact centred base conversion (the MAC basis M > 2 |r|: choose_aux_basis sizes it for
+    // |MAC| >= (t - 1) N |r|), which replaces the per-coefficient multiword k_round_chain
+    const bool tc = round_tc_on(c);
     c.zs_last = c.T.DS;
     if (reg32_ok(c.cp.logN)) {
         REG32_DISPATCH(c.cp.logN, tensor(c, prepA, idxA, prepB, idxB, P, D, tc ? (prepA_scaled ? 2 : 1) : 0));
     } else {
         launch(c, k_tensor_intt, (size_t)P * J, ntt_block(N), N * 4, prepA, idxA, prepB, idxB, P, c.T, D);
     }
-    if (to_mac) {
+    if (to_mac || tc) {
         const size_t items = (size_t)P * 3 * N;
         const size_t grid = std::min<size_t>(blocks(items, 256), 148 * 8);
         const size_t sm = sizeof(RoundJ) * c.JM + sizeof(RoundK) * kMaxJ + (size_t)c.ab.Mm * c.JM * 4;
@@ -1022,7 +1079,9 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         else if (c.JM == 24) launch_named(c, "k_round_mac", k_round_mac_t<24>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else if (c.JM == 32) launch_named(c, "k_round_mac", k_round_mac_t<32>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else launch_named(c, "k_round_mac", k_round_mac_t<40>, grid, 256, sm, D, P, c.T, rj, rk, im);
-        if (c.fuse_now) {
+        if (!to_mac) {
+            launch(c, k_mac_to_chain, blocks(items, 128), 128, 0, (const u32*)D, c.T.DS, P * 3, c.T, chain_out);
+        } else if (c.fuse_now) {
             // forward NTT happens inside k_ntt_mac
         } else if (reg32_ok(c.cp.logN)) {
             REG32_DISPATCH(c.cp.logN, sel3(c, D, P, c.T.DS));
@@ -1210,6 +1269,7 @@ enum { TM_START = 0, TM_H2D, TM_EXPAND, TM_SELECT, TM_MAC, TM_FINISH, TM_D2H };
 /// identical keys keep the resident copy and its aux-basis transform (key_to_aux, ~2 ms at C4),
 /// different keys replace it.  Returns true when the resident keys were reused.
 static bool upload_keys(Ctx& c, const u64* relin, u32 n_galois, const u64* gg, const u64* galois) {
+    Nvtx nv("cwgpu keys");
     const size_t LN = (size_t)c.cp.L * c.cp.N;
     const size_t rw = (size_t)c.cp.Dr * 2 * LN, gw = (size_t)c.cp.Dg * 2 * LN;
     const bool same_shape = c.have_keys && c.galois_g.size() == n_galois &&
@@ -1268,7 +1328,10 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         u64* dq = c.query.get<u64>((size_t)h * 2 * LN);
         CK(cudaMemcpyAsync(dq, query, (size_t)h * 2 * LN * 8, cudaMemcpyDefault, c.st));  // host or device
         tm.mark(TM_H2D);
-        entries = expand(c, dq, h, comp, m);
+        {
+            Nvtx nv("cwgpu expand_query");
+            entries = expand(c, dq, h, comp, m);
+        }
         tm.mark(TM_EXPAND);
     }
     u32* prep = nullptr;
@@ -1325,6 +1388,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
             c.dcur = i ? &c.Dmore[i - 1] : &c.Dbuf;
         }
         u32 nc = 0, zs = 0;
+        Nvtx nv("cwgpu row tile");
         u32* Z = select_tile(c, entries, prep, op, r0, Rt, nc, zs, nullptr);
         nc_all = std::max(nc_all, nc);
         tm.mark(TM_SELECT);
@@ -1378,6 +1442,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
 
 /// summed partials -> responses: mod a_k, INTT, M -> chain, finalize (pir.cpp:345).
 static void finish(Ctx& c, const u64* dev_partial, u32 nc, u64* out_host, Timer& tm) {
+    Nvtx nv("cwgpu finalize");
     const u32 N = c.cp.N, L = c.cp.L, Mm = c.ab.Mm;
     const size_t LN = (size_t)L * N;
     const size_t accw = (size_t)c.s * 3 * Mm * N;
@@ -1385,7 +1450,7 @@ static void finish(Ctx& c, const u64* dev_partial, u32 nc, u64* out_host, Timer&
     launch(c, k_partial_mod, blocks(accw, 256), 256, 0, dev_partial, accw, c.T, X);
     ntt32(c, X, c.s * 3 * Mm, Mm, Mm, 0, true, 0);
     u64* r3 = c.resp3.get<u64>((size_t)c.s * 3 * LN);
-    launch(c, k_mac_to_chain, blocks((size_t)c.s * 3 * N, 128), 128, 0, (const u32*)X, c.s * 3, c.T, r3);
+    launch(c, k_mac_to_chain, blocks((size_t)c.s * 3 * N, 128), 128, 0, (const u32*)X, Mm, c.s * 3, c.T, r3);
     u64* o2 = c.out2.get<u64>((size_t)c.s * 2 * LN);
     if (nc == 3) {
         relinearize(c, r3, c.s, o2);
@@ -1425,6 +1490,7 @@ static void fill_timings(Ctx& c, Timer& tm, cwg_timings* t, double total_ms) {
 /// [R][s][N] into the device staging buffer, which is lifted to the MAC basis and NTT'd.
 static void load_db_impl(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 s, u32 k, u32 m, const u32* positions,
                          const std::function<void(u64, u64, u64*)>& fill) {
+    Nvtx nv("cwgpu load_db");
     if (n_local == 0 || n_total == 0) throw std::invalid_argument("empty database");
     if (row_begin + n_local > n_total) throw std::invalid_argument("row range outside the database");
     if (k < 1) throw std::invalid_argument("hamming weight must be >= 1");
@@ -1547,6 +1613,7 @@ static void load_db_bytes(Ctx& c, u64 n_total, u64 row_begin, u64 n_local, u32 k
 /// host or device memory) and comps (host).  Device output: tiles are written in place, no copies
 /// back and no per-tile synchronisation (the C2 equality microbenchmark times this).
 static void select_rows(Ctx& c, u32 nq, u32 comp, u32 m, const u64* query, u32 op, u64* sel, u32* comps, Timer& tm) {
+    Nvtx nv("cwgpu select");
     if (!c.db_loaded) throw state_err("no database loaded");
     if (m != c.m) throw std::invalid_argument("expanded query length must equal the code length");
     if (!c.have_keys) throw he_err("evaluation keys not set");
@@ -2190,6 +2257,7 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "round_ctas") c.round_ctas = (u32)std::max(1, std::min(4, v));
         else if (k == "ks32") { c.ks32 = v != 0; c.ksA_ok = false; }
         else if (k == "tile_rows") c.tile_rows_opt = (u32)std::max(0, v);
+        else if (k == "ks_wide") c.ks_wide = v != 0;
         else if (k == "force_exact") {
             c.force_exact = v != 0;
             c.T.force_exact = c.force_exact ? 1u : 0u;

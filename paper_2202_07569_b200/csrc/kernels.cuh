@@ -418,9 +418,30 @@ __global__ void k_relin_add(const u64* __restrict__ ct3, size_t ct_stride, const
 /// Centred lift of chain ciphertexts into aux residues (to_aux_basis, bfv.cpp:718-744):
 /// for count ciphertexts (2 comps each, ct c at src + sel(c) * src_stride),
 /// out[c][k][j][n] for j < nj, constants mont (x 2^32, tensor operands) or plain.
-__global__ void k_lift(const u64* __restrict__ src, size_t src_stride, const u32* __restrict__ sel, u32 count,
-                       u32 nj, int mont, DevTab T, u32* __restrict__ out, u32 out_stride_j) {
+__global__ void __launch_bounds__(256) k_lift(const u64* __restrict__ src, size_t src_stride, const u32* __restrict__ sel,
+                                             u32 count, u32 nj, int mont, DevTab T, u32* __restrict__ out,
+                                             u32 out_stride_j) {
+    // per-prime lift constants staged in shared memory once per CTA (they were L1 loads inside the
+    // L x nj loop: 2 L nj loads per coefficient)
+    __shared__ u32 sV[kMaxL * kMaxJ], sV2[kMaxL * kMaxJ], sW[kMaxJ], sA[kMaxJ];
+    __shared__ u64 sAb[kMaxJ];
     const u32 N = T.N, L = T.L;
+    {
+        const u32* V = mont ? T.liftV_m : T.liftV_n;
+        const u32* V2 = mont ? T.liftV2_m : T.liftV2_n;
+        const u32* W = mont ? T.liftW_m : T.liftW_n;
+        for (u32 x = threadIdx.x; x < L * nj; x += blockDim.x) {
+            const u32 i = x / nj, j = x % nj;
+            sV[x] = V[i * T.J + j];
+            sV2[x] = V2[i * T.J + j];
+        }
+        for (u32 j = threadIdx.x; j < nj; j += blockDim.x) {
+            sW[j] = W[j];
+            sA[j] = T.a[j];
+            sAb[j] = T.abar[j];
+        }
+        __syncthreads();
+    }
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)count * 2 * N) return;
     const u32 c = (u32)(idx / (2 * N)), k = (u32)((idx / N) % 2), n = (u32)(idx % N);
@@ -430,18 +451,20 @@ __global__ void k_lift(const u64* __restrict__ src, size_t src_stride, const u32
     u32 ip;
     const u64 fr = crt_prepare(res, T, y, &ip);
     const u32 rho = crt_round(y, ip, fr, T);
-    const u32* V = mont ? T.liftV_m : T.liftV_n;
-    const u32* V2 = mont ? T.liftV2_m : T.liftV2_n;
-    const u32* W = mont ? T.liftW_m : T.liftW_n;
+    u32 ylo[kMaxL], yhi[kMaxL];
+    for (u32 i = 0; i < L; ++i) {
+        ylo[i] = (u32)(y[i] & ((1u << 30) - 1));
+        yhi[i] = (u32)(y[i] >> 30);
+    }
     u32* o = out + ((size_t)c * 2 + k) * out_stride_j * N + n;
     for (u32 j = 0; j < nj; ++j) {
-        const u32 a = T.a[j];
-        u64 accA = 0, accB = (u64)rho * (a - W[j]);
+        const u32 a = sA[j];
+        u64 accA = 0, accB = (u64)rho * (a - sW[j]);
         for (u32 i = 0; i < L; ++i) {
-            accA += (u64)(u32)(y[i] & ((1u << 30) - 1)) * V[i * T.J + j];
-            accB += (u64)(u32)(y[i] >> 30) * V2[i * T.J + j];
+            accA += (u64)ylo[i] * sV[i * nj + j];
+            accB += (u64)yhi[i] * sV2[i * nj + j];
         }
-        const u64 ab = T.abar[j];
+        const u64 ab = sAb[j];
         o[(size_t)j * N] = red32(bar64(accA, a, ab) + bar64(accB, a, ab), a);
     }
 }
@@ -697,8 +720,8 @@ __global__ void k_partial_mod(const u64* __restrict__ partial, size_t total, Dev
 }
 
 /// MAC basis -> chain: X (coefficient form, centred |X| < M/2) -> out[g][i][n] mod q_i.
-/// X layout [G][Mm][N]; out layout [G][L][N].
-__global__ void k_mac_to_chain(const u32* __restrict__ X, u32 G, DevTab T, u64* __restrict__ out) {
+/// X layout [G][xs][N] (the first Mm planes of each group of xs); out layout [G][L][N].
+__global__ void k_mac_to_chain(const u32* __restrict__ X, u32 xs, u32 G, DevTab T, u64* __restrict__ out) {
     const u32 N = T.N, Mm = T.Mm, L = T.L;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)G * N) return;
@@ -708,7 +731,7 @@ __global__ void k_mac_to_chain(const u32* __restrict__ X, u32 G, DevTab T, u64* 
     u64 gs = 0;
     for (u32 k = 0; k < Mm; ++k) {
         const u32 a = T.a[k];
-        v[k] = red32(shoup32(X[(g * Mm + k) * N + n], T.mhat[k], T.mhat_s[k], a), a);
+        v[k] = red32(shoup32(X[(g * xs + k) * N + n], T.mhat[k], T.mhat_s[k], a), a);
         gs += (u64)v[k] * T.mF[k];
     }
     const u32 gsh = 64 - T.gbits;

@@ -108,6 +108,63 @@ __global__ void __launch_bounds__(128) k_ks_mac32x(const u32* __restrict__ dig, 
     }
 }
 
+/// Slot-major key-switch MAC: thread = one NTT slot (j, n) of the K' aux primes.  Per slot the key
+/// is a [D][2L] matrix shared by every row b, so each thread keeps a CI-column block of it in
+/// registers (D x CI words) and streams the rows' D digit residues past it: D x CI products per
+/// D digit loads, the key read once per group of G rows instead of once per output.  Products are
+/// < 2^60 (residues < 2^30), accumulated 15 at a time in u64 before a Barrett reduction.
+/// Grid: (ceil(K' N / 128), row splits); rows [b0, b1) of this split in groups of G.
+template <int D, int CI, int G, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_ks_mac32s(const u32* __restrict__ dig, const u32* __restrict__ key, u32 B,
+                                                      u32 L, u32 N, const __grid_constant__ KsCrt C,
+                                                      const u64* __restrict__ abar, u32* __restrict__ out) {
+    const u32 K = C.K;
+    const u32 KN = K * N;  // < 2^32: plane offsets in 32-bit arithmetic (fewer live 64-bit addresses)
+    const u32 slot = blockIdx.x * 128 + threadIdx.x;  // j N + n
+    if (slot >= KN) return;
+    const u32 j = slot / N;
+    const u32 a = C.a[j];
+    const u64 mu = abar[j];
+    const u32 nci = 2 * L;
+    const u32 b0 = (u32)(((u64)B * blockIdx.y) / gridDim.y), b1 = (u32)(((u64)B * (blockIdx.y + 1)) / gridDim.y);
+#pragma unroll 1
+    for (u32 g0 = b0; g0 < b1; g0 += G) {
+        const u32 g1 = min(b1, g0 + G);
+#pragma unroll 1
+        for (u32 c0 = 0; c0 < nci; c0 += CI) {
+            u32 kr[D][CI];
+            const u32* kp = key + (size_t)c0 * KN + slot;
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+#pragma unroll
+                for (int c = 0; c < CI; ++c)
+                    kr[d][c] = (c0 + c < nci) ? __ldg(kp + ((u32)d * nci + (u32)c) * KN) : 0u;
+#pragma unroll 1
+            for (u32 b = g0; b < g1; ++b) {
+                const u32* dp = dig + (size_t)b * D * KN + slot;
+                u32 dr[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) dr[d] = dp[(u32)d * KN];
+                u32* op = out + ((size_t)b * nci + c0) * KN + slot;
+#pragma unroll
+                for (int c = 0; c < CI; ++c) {
+                    u64 s = 0;
+                    u32 r = 0;
+#pragma unroll
+                    for (int d = 0; d < D; ++d) {
+                        s += (u64)dr[d] * kr[d][c];
+                        if (d % 15 == 14 && d + 1 < D) {
+                            r += bar64(s, a, mu);  // < 2 a after two chunks
+                            s = 0;
+                        }
+                    }
+                    if (c0 + c < nci) op[(u32)c * KN] = bar64(s + r, a, mu);
+                }
+            }
+        }
+    }
+}
+
 /// ks[b][c][i][n] = (centred CRT of the K' residues x_j) mod q_i.  x: [B][2][L][K'][N] in [0, a_j).
 __global__ void k_ks_crt(const u32* __restrict__ x, u32 B, u32 L, u32 N, const __grid_constant__ KsCrt C, DevTab T,
                          u64* __restrict__ ks) {
