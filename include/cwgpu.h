@@ -123,6 +123,15 @@ int cwg_answer(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uin
                const uint64_t* galois, uint32_t h, uint32_t c, uint32_t m, const uint64_t* query,
                uint32_t op, uint64_t* out, cwg_timings* t);
 
+/* Multi-query answer: Q queries under one evaluation-key set (e.g. one client
+ * fetching Q rows) answered in one pass over the database -- every row tile's selection values are
+ * computed for all Q queries and the payload MAC reads the tile's database planes once for up to
+ * four of them.  queries: [Q][h][2][L][N]; out: [Q][s][2][L][N]; each response equals cwg_answer's.
+ * A multi-device context answers the queries one after another. */
+int cwg_answer_batch(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+                     const uint64_t* galois, uint32_t Q, uint32_t h, uint32_t c, uint32_t m, const uint64_t* queries,
+                     uint32_t op, uint64_t* out, cwg_timings* t);
+
 /* Row-sharded form (one process per GPU): the partial NTT-domain accumulators of this
  * device's rows, written to DEVICE memory (cwg_partial_words() u64 words, each < 2^31,
  * summable with a plain uint64 reduction), then cwg_finish on the root with the summed
@@ -153,6 +162,17 @@ int cwg_select(cwg_ctx* ctx, const uint64_t* relin, uint32_t n_galois, const uin
                const uint64_t* galois, uint32_t h, uint32_t c, uint32_t m, const uint64_t* query,
                uint32_t op, uint64_t* sel, uint32_t* comps, cwg_timings* t);
 
+/* ---- client side on the GPU, bit-identical to the reference client ---- */
+/* pack_query_bits (expansion.cpp:17-38): the m query bits packed 2^c per plaintext (scaled by
+ * 2^-c mod t) and encrypted (BfvBackend::encrypt, bfv.cpp:516-549) with the secret key sk (N ternary
+ * coefficients) under encryption indices first_index, first_index + 1, ...; sk_seed: the 4 words
+ * of the key's Seed256 (the reference's derive_seed domains 5 / 6).  out: [ceil(m / 2^c)][2][L][N]. */
+int cwg_encrypt_query(cwg_ctx* ctx, const uint64_t* sk_seed, const int8_t* sk, const uint8_t* bits, uint32_t m,
+                      uint32_t c, uint64_t first_index, uint64_t* out);
+/* BfvBackend::decrypt (bfv.cpp:551-595) of count ciphertexts [count][comps][L][N] (comps 2 or 3) ->
+ * out [count][N] plaintext coefficients mod t. */
+int cwg_decrypt(cwg_ctx* ctx, const int8_t* sk, uint32_t count, uint32_t comps, const uint64_t* cts, uint64_t* out);
+
 /* ---- stage entry points (the reference's unit-test surface) ---- */
 /* RingContext::ntt_forward/inverse (ring.cpp:78-144) on `count` polys of chain prime
  * idx (chain=1) or of aux prime idx (chain=0; our internal basis). */
@@ -170,7 +190,7 @@ int cwg_substitute(cwg_ctx* ctx, uint32_t count, const uint64_t* ct, uint64_t g,
  * read by the library).  key: "streams" (row-tile streams, 1-4), "tile_rows" (0 = auto),
  * "fuse_mac" (0: separate selection NTT + MAC kernels), "mac" (0: k_mac2 instead of the TMA
  * payload MAC for s >= 3), "round" (0: IMAD rounding instead of the tensor cores), "round_g2",
- * "round_ctas", "mac_waves", "mac_ck", "ntt_np", "prescale", "ks32" (0: 64-bit key switching), "ks_wide",
+ * "round_ctas", "mac_waves", "mac_ck", "ntt_np", "prescale", "ks32" (0: 64-bit key switching), "ks_wide", "prep_factors",
  * "force_exact" (every rounding / lift decision through the exact multiword path; tests).
  * Unknown keys return CWG_EINVAL. */
 int cwg_set_option(cwg_ctx* ctx, const char* key, int64_t value);

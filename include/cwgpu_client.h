@@ -30,6 +30,9 @@ int cwg_client_encrypt(const cwg_client* c, const uint64_t* plain, uint64_t inde
 int cwg_client_pack_query(const cwg_client* c, const uint8_t* bits, uint32_t m, uint32_t c_factor,
                           uint64_t first_index, uint64_t* out);
 int cwg_client_decrypt(const cwg_client* c, const uint64_t* ct, uint32_t comps, uint64_t* out);
+/* The secret key (N ternary coefficients) and its Seed256 words, for the GPU client calls of
+ * include/cwgpu.h (cwg_encrypt_query / cwg_decrypt). */
+int cwg_client_export_secret(const cwg_client* c, int8_t* s, uint64_t* seed_words);
 
 #ifdef __cplusplus
 }

@@ -33,6 +33,7 @@
 #include "ntt_mac.cuh"
 #include "ks32.cuh"
 #include "dbsetup.cuh"
+#include "client_gpu.cuh"
 
 namespace cwgpu {
 
@@ -92,6 +93,13 @@ struct Ctx {
     int round_kind = 2;               // 2 tensor-core (k_round_tma), 0 IMAD only (k_round_mac_t); option "round"
     DevBuf prep_s;                    // A-side prepared operands with the INTT output scale folded in
     bool prep_s_ok = false;           // prep_s valid for the current answer
+    const u32* prep_s_ptr = nullptr;  // the scaled A operands select_tile uses (prep_s or a batch query's)
+    // multi-query answers (cwg_answer_batch): per-query expanded entries, prepared operands, scaled
+    // A operands, D buffers and accumulators
+    std::vector<std::unique_ptr<DevBuf>> bq_ent, bq_prep, bq_preps, bq_D;
+    DevBuf bq_acc;
+    DevBuf prep_k, pair_idx;  // arithmetic-operator k' prepared once; product-tree pair indices
+    DevBuf cl_seeds, cl_lim, cl_s, cl_s2, cl_a, cl_b, cl_e, cl_bits, cl_out;  // GPU client scratch
     // tuning / test options (cwg_set_option; the defaults are the measured-fastest choices)
     bool prescale = true;             // "prescale": fold the INTT output scale into the A operands
     bool mac_tma = true;              // "mac": 1 TMA-fed payload MAC for s >= 3 (k_mac_tma), 0 k_mac2
@@ -110,6 +118,7 @@ struct Ctx {
     // key switching through the 30-bit aux primes ("ks32" = 0: the 64-bit NTT path)
     bool ks32 = true;
     bool ks_wide = true;  // "ks_wide": shared-load key-switch MAC also for 16 < D <= 32 digits
+    int prep_mode = 1;    // "prep_factors": 1 prepare k' once for the arithmetic factors, 0 each factor
     bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
     KsCrt ksC_r{}, ksC_g{};            // K' = 0: this key type keeps the 64-bit path
     DevBuf relinA, galoisA, ksdig, ksmac;  // keys re-based into the aux primes, digit / MAC scratch
@@ -728,6 +737,11 @@ struct Reg32 {
 static void set_smem_limits(u32 N) {
     CK(cudaFuncSetAttribute(k_mac_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 4 * kMacBlock * 4));
     CK(cudaFuncSetAttribute(k_mac_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 3 * kMacBlock * 4));
+#define MQ(NCv, QBv)                                                                                              \
+    CK(cudaFuncSetAttribute(k_mac_tma_q<NCv, QBv>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                            kMacStages * (1 + QBv * NCv) * kMacBlockQ * 4));
+    MQ(2, 1) MQ(2, 2) MQ(2, 3) MQ(2, 4) MQ(3, 1) MQ(3, 2) MQ(3, 3) MQ(3, 4)
+#undef MQ
 #define RTC(JMv, NCv)                                                                                                \
     CK(cudaFuncSetAttribute(k_round_tma<0, JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
     {                                                                                                                \
@@ -1012,10 +1026,10 @@ static void prepare(Ctx& c, const u64* src, size_t stride, const u32* sel, u32 c
 
 /// A-side copy of prepared operands with the INTT's output scale (N 2^32)^-1 (A/a_j)^-1 folded
 /// in: one pass per query instead of one Shoup product per tensor output coefficient.
-static u32* prepare_scaled(Ctx& c, const u32* prep, u32 count) {
+static u32* prepare_scaled(Ctx& c, const u32* prep, u32 count, u32* out = nullptr) {
     const u32 N = c.cp.N, J = c.ab.J;
     const size_t total = (size_t)count * 2 * J * N;
-    u32* out = c.prep_s.get<u32>(total);
+    if (!out) out = c.prep_s.get<u32>(total);
     launch(c, k_scale_planes, blocks(total, 256), 256, 0, prep, out, total, c.T.ninvRAc, c.T.ninvRAc_s, c.T);
     return out;
 }
@@ -1125,7 +1139,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
             nc = 3;
             return nullptr;
         }
-        u32* D = c.prep_s_ok ? mul_prepared(c, c.prep_s.ptr<u32>(), col(0), prep, col(1), R, true, nullptr, true)
+        u32* D = c.prep_s_ok ? mul_prepared(c, c.prep_s_ptr, col(0), prep, col(1), R, true, nullptr, true)
                              : mul_prepared(c, prep, col(0), prep, col(1), R, true, nullptr);
         nc = 3;
         zstride = c.zs_last;
@@ -1165,13 +1179,26 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
     }
     const bool lazy_root = (op == CWG_OP_FOLKLORE);
     // product_tree (eq_circuits.cpp:53-69)
+    bool first = true;
     while (cnt > 1) {
         const bool last = cnt == 2;
         const u32 np = cnt / 2, ncnt = np + (cnt % 2);
         // prepare every node of every row (entries keep their own prepared buffer)
         u32* np_prep = c.lift_tmp.get<u32>((size_t)R * cnt * 2 * J * N);
-        prepare(c, nodes, per, nullptr, R * cnt, np_prep);
-        u32* di = c.tmp_idx.get<u32>((size_t)2 * R * np);
+        if (first && op == CWG_OP_ARITH && c.prep_mode == 1) {
+            // the k factors of a row differ from k' only in coefficient 0 of component 0: prepare
+            // k' once (lift + NTT) and add each factor's lifted difference to every NTT slot
+            u32* pk = c.prep_k.get<u32>((size_t)R * 2 * J * N);
+            prepare(c, nodes, (size_t)cnt * per, nullptr, R, pk);
+            u32* dl = c.tmp_idx.get<u32>((size_t)R * cnt * J);
+            launch(c, k_arith_deltas, blocks((size_t)R * cnt, 128), 128, 0, (const u64*)nodes, R, cnt, c.T, dl);
+            launch(c, k_prep_factors, blocks((size_t)R * cnt * 2 * J * N, 256), 256, 0, (const u32*)pk, (const u32*)dl,
+                   R, cnt, c.T, np_prep);
+        } else {
+            prepare(c, nodes, per, nullptr, R * cnt, np_prep);
+        }
+        first = false;
+        u32* di = c.pair_idx.get<u32>((size_t)2 * R * np);
         launch(c, k_level_pairs, blocks((size_t)R * np, 256), 256, 0, R, cnt, di, di + (size_t)R * np);
         if (last && lazy_root) {
             if (chain_sel) {
@@ -1340,7 +1367,7 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         prep = c.prep.get<u32>((size_t)m * 2 * J * N);
         prepare(c, entries, 2 * LN, nullptr, m, prep);
         if (c.k == 2 && round_tc_on(c) && c.prescale) {
-            prepare_scaled(c, prep, m);
+            c.prep_s_ptr = prepare_scaled(c, prep, m);
             c.prep_s_ok = true;
         }
     }
@@ -1438,6 +1465,131 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
     launch(c, k_acc_mod, blocks(accw, 256), 256, 0, (const unsigned long long*)acc, accw, c.T, dev_partial);
     tm.mark(TM_MAC);
     return nc_all;
+}
+
+static void finish(Ctx& c, const u64* dev_partial, u32 nc, u64* out_host, Timer& tm);
+
+/// Multi-query answer (the reference answers one query per process_query,
+/// pir.cpp:337-347): Q queries under one evaluation-key set, each expanded and prepared once, then
+/// per row tile every query's selection is computed and the payload MAC reads the tile's database
+/// planes once for all of them (k_mac_tma_q for s >= 2 rows; the fused selection NTT + MAC of s <= 2
+/// rows streams the database per query, where it is a small part of the cost).  out: [Q][s][2][L][N].
+static void answer_batch(Ctx& c, u32 Q, u32 h, u32 comp, u32 m, const u64* queries, u32 op, u64* out, Timer& tm) {
+    if (!c.db_loaded) throw state_err("no database loaded");
+    if (m != c.m) throw std::invalid_argument("query code length does not match the database");  // pir.cpp:339-341
+    if (c.s == 0) throw state_err("database has no payload (selection-only); use cwg_select");
+    if (!c.have_keys) throw he_err("evaluation keys not set");
+    if (op != CWG_OP_FOLKLORE && op != CWG_OP_ARITH) throw std::invalid_argument("unknown equality operator");
+    if (op == CWG_OP_ARITH && c.k < 2) throw std::invalid_argument("arithmetic operator needs k >= 2");
+    if (Q == 0) throw std::invalid_argument("empty query batch");
+    const u32 N = c.cp.N, L = c.cp.L, J = c.ab.J, Mm = c.ab.Mm;
+    const size_t LN = (size_t)L * N;
+    const size_t per = 2 * LN;
+    CK(cudaMemsetAsync(c.d_fb, 0, 8, c.st));
+    auto grow = [](std::vector<std::unique_ptr<DevBuf>>& v, u32 n) {
+        while (v.size() < n) v.push_back(std::make_unique<DevBuf>());
+    };
+    grow(c.bq_ent, Q);
+    grow(c.bq_prep, Q);
+    grow(c.bq_preps, Q);
+    grow(c.bq_D, Q);
+    const bool folk = op == CWG_OP_FOLKLORE && c.k >= 2;
+    const bool scaled = c.k == 2 && folk && round_tc_on(c) && c.prescale;
+    // 1. expansion + preparation of every query (expand_query, prepare_cipher)
+    for (u32 q = 0; q < Q; ++q) {
+        Nvtx nv("cwgpu expand_query");
+        u64* dq = c.query.get<u64>((size_t)h * per);
+        CK(cudaMemcpyAsync(dq, queries + (size_t)q * h * per, (size_t)h * per * 8, cudaMemcpyDefault, c.st));
+        const u64* e = expand(c, dq, h, comp, m);
+        u64* ent = c.bq_ent[q]->get<u64>((size_t)m * per);
+        CK(cudaMemcpyAsync(ent, e, (size_t)m * per * 8, cudaMemcpyDeviceToDevice, c.st));
+        if (folk) {
+            u32* pr = c.bq_prep[q]->get<u32>((size_t)m * 2 * J * N);
+            prepare(c, ent, per, nullptr, m, pr);
+            if (scaled) prepare_scaled(c, pr, m, c.bq_preps[q]->get<u32>((size_t)m * 2 * J * N));
+        }
+    }
+    tm.mark(TM_EXPAND);
+    const size_t accw = (size_t)c.s * 3 * Mm * N;
+    auto* acc = reinterpret_cast<unsigned long long*>(c.bq_acc.get<u64>(accw * Q));
+    CK(cudaMemsetAsync(acc, 0, accw * Q * 8, c.st));
+    const u32 R = tile_rows(c);
+    c.fuse_now = c.fuse_mac != 0 && reg32_ok(c.cp.logN) && c.s <= 2;
+    struct Reset {
+        Ctx& c;
+        ~Reset() {
+            c.fuse_now = false;
+            c.prep_s_ok = false;
+            c.dcur = &c.Dbuf;
+        }
+    } reset{c};
+    u32 nc_all = 2;
+    std::vector<u32*> Z(Q);
+    std::vector<u32> zst(Q);
+    for (u64 r0 = 0; r0 < c.n_local; r0 += R) {
+        Nvtx nv("cwgpu row tile (batch)");
+        const u32 Rt = (u32)std::min<u64>(R, c.n_local - r0);
+        u32 nc = 0;
+        for (u32 q = 0; q < Q; ++q) {  // 2. every query's selection values for the tile
+            c.dcur = c.bq_D[q].get();
+            c.prep_s_ok = scaled;
+            c.prep_s_ptr = scaled ? c.bq_preps[q]->ptr<u32>() : nullptr;
+            Z[q] = select_tile(c, c.bq_ent[q]->ptr<u64>(), folk ? c.bq_prep[q]->ptr<u32>() : nullptr, op, r0, Rt, nc,
+                               zst[q], nullptr);
+        }
+        nc_all = std::max(nc_all, nc);
+        tm.mark(TM_SELECT);
+        const u32* dbt = c.db.ptr<u32>() + (size_t)r0 * c.s * Mm * N;
+        if (c.fuse_now) {  // 3a. fused selection NTT + MAC per query
+            for (u32 q = 0; q < Q; ++q) REG32_DISPATCH(c.cp.logN, ntt_mac(c, Z[q], zst[q], nc, dbt, Rt, acc + q * accw));
+        } else if (c.mac_tma && N >= (u32)kMacBlockQ) {  // 3b. one database pass per group of <= 4 queries
+            for (u32 q0 = 0; q0 < Q; q0 += 4) {
+                const u32 qb = std::min<u32>(4, Q - q0);
+                ZPtrs zp{};
+                for (u32 x = 0; x < qb; ++x) {
+                    if (zst[q0 + x] != zst[q0]) throw std::logic_error("batch selection strides differ");
+                    zp.z[x] = Z[q0 + x];
+                    zp.acc[x] = acc + (q0 + x) * accw;
+                }
+                const u32 blocksN = Mm * (N / kMacBlockQ) * c.s;
+                const u32 slots = 148 * 2 * 2;
+                u32 ck = std::max<u32>(1, std::min<u32>((Rt + 7) / 8, slots / blocksN));
+                const u32 crow = (Rt + ck - 1) / ck;
+                ck = (Rt + crow - 1) / crow;
+                const size_t smem = (size_t)kMacStages * (1 + qb * nc) * kMacBlockQ * 4;
+                c.next_units = (double)Rt * (c.s + (double)qb * nc) * Mm * N * 4;  // DB once + qb selections
+#define MACQ(NCv, QBv)                                                                                            \
+    launch_named(c, "k_mac_q", k_mac_tma_q<NCv, QBv>, (size_t)ck * blocksN, 288, smem, zp, zst[q0], dbt, Rt, c.s,   \
+                 crow, c.T)
+                if (nc == 3) {
+                    if (qb == 1) MACQ(3, 1); else if (qb == 2) MACQ(3, 2); else if (qb == 3) MACQ(3, 3); else MACQ(3, 4);
+                } else {
+                    if (qb == 1) MACQ(2, 1); else if (qb == 2) MACQ(2, 2); else if (qb == 3) MACQ(2, 3); else MACQ(2, 4);
+                }
+#undef MACQ
+            }
+        } else {
+            for (u32 q = 0; q < Q; ++q) {
+                const u32 chunks = (u32)std::max<size_t>(1, std::min<size_t>((size_t)(Rt + 15) / 16,
+                                                                             (148 * 2048 * 2) / ((size_t)c.s * Mm * (N / 4)) + 1));
+                const u32 chunk = (Rt + chunks - 1) / chunks;
+                const size_t threads = (size_t)c.s * Mm * ((N / 4 + 255) / 256) * 256 * ((Rt + chunk - 1) / chunk);
+                if (nc == 3)
+                    launch_named(c, "k_mac", k_mac2<3>, blocks(threads, 256), 256, 0, (const u32*)Z[q], zst[q], dbt, Rt,
+                                 c.s, chunk, c.T, acc + q * accw);
+                else
+                    launch_named(c, "k_mac", k_mac2<2>, blocks(threads, 256), 256, 0, (const u32*)Z[q], zst[q], dbt, Rt,
+                                 c.s, chunk, c.T, acc + q * accw);
+            }
+        }
+        tm.mark(TM_MAC);
+    }
+    // 4. finalize every query's response
+    u64* part = c.partial.get<u64>(accw);
+    for (u32 q = 0; q < Q; ++q) {
+        launch(c, k_acc_mod, blocks(accw, 256), 256, 0, (const unsigned long long*)(acc + q * accw), accw, c.T, part);
+        finish(c, part, nc_all, out + (size_t)q * c.s * per, tm);
+    }
 }
 
 /// summed partials -> responses: mod a_k, INTT, M -> chain, finalize (pir.cpp:345).
@@ -2097,6 +2249,131 @@ int cwg_answer(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint6
     });
 }
 
+int cwg_answer_batch(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g,
+                     const uint64_t* galois, uint32_t Q, uint32_t nq, uint32_t comp, uint32_t m,
+                     const uint64_t* queries, uint32_t op, uint64_t* out, cwg_timings* t) {
+    if (h->multi()) {  // several devices: one multi-device answer per query
+        const size_t qw = (size_t)nq * 2 * h->c.cp.L * h->c.cp.N, ow = (size_t)h->c.s * 2 * h->c.cp.L * h->c.cp.N;
+        for (uint32_t q = 0; q < Q; ++q) {
+            const int rc = cwg_answer(h, q ? nullptr : relin, n_galois, galois_g, galois, nq, comp, m, queries + q * qw,
+                                      op, out + q * ow, t);
+            if (rc != CWG_OK) return rc;
+        }
+        return CWG_OK;
+    }
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        auto t0 = std::chrono::steady_clock::now();
+        Timer tm(c, t != nullptr);
+        tm.mark(TM_START);
+        c.keys_cached = relin ? upload_keys(c, relin, n_galois, galois_g, galois) : false;
+        answer_batch(c, Q, nq, comp, m, queries, op, out, tm);
+        fill_timings(c, tm, t,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    });
+}
+
+/// NTT of the secret key (and its square) mod every chain prime, for the GPU client calls.
+static void client_secret(Ctx& c, const int8_t* sk, bool square) {
+    const u32 N = c.cp.N, L = c.cp.L;
+    const size_t LN = (size_t)L * N;
+    signed char* ds = reinterpret_cast<signed char*>(c.cl_bits.get<unsigned char>(std::max<size_t>(N, 16)));
+    CK(cudaMemcpyAsync(ds, sk, N, cudaMemcpyDefault, c.st));
+    u64* s1 = c.cl_s.get<u64>(LN);
+    launch(c, k_signed_to_chain, blocks(LN, 256), 256, 0, (const signed char*)ds, c.T, s1);
+    ntt64(c, s1, L, false);
+    if (square) {
+        u64* s2 = c.cl_s2.get<u64>(LN);
+        CK(cudaMemcpyAsync(s2, s1, LN * 8, cudaMemcpyDeviceToDevice, c.st));
+        launch(c, k_mul64, blocks(LN, 256), 256, 0, s2, (const u64*)s1, (size_t)1, c.T);
+    }
+}
+
+int cwg_encrypt_query(cwg_ctx* h, const uint64_t* sk_seed, const int8_t* sk, const uint8_t* bits, uint32_t m,
+                      uint32_t comp, uint64_t first_index, uint64_t* out) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        Nvtx nv("cwgpu encrypt_query");
+        const u32 N = c.cp.N, L = c.cp.L;
+        const size_t LN = (size_t)L * N;
+        if ((u64(1) << comp) > N) throw std::invalid_argument("compression factor exceeds log2(N)");
+        if (!sk || !sk_seed || (!bits && m)) throw std::invalid_argument("missing secret key or query bits");
+        const u64 t = c.cp.t;
+        const u64 scale = invmod64(((u64)1 << comp) % t, t);  // pack_query_bits' 2^-c mod t
+        const u32 hq = (u32)(((u64)m + (1u << comp) - 1) >> comp);
+        if (hq == 0) throw std::invalid_argument("empty query");
+        Seed4 seed;
+        for (int i = 0; i < 4; ++i) seed.w[i] = sk_seed[i];
+        Seed4* seeds = reinterpret_cast<Seed4*>(c.cl_seeds.get<u64>((size_t)8 * hq));
+        launch(c, k_enc_seeds, blocks(hq, 64), 64, 0, seed, (u64)first_index, hq, seeds, seeds + hq);
+        std::vector<u64> lim(L);
+        for (u32 i = 0; i < L; ++i) lim[i] = ~0ull - (~0ull % c.cp.q[i]);
+        u64* dlim = c.cl_lim.get<u64>(L);
+        CK(cudaMemcpyAsync(dlim, lim.data(), L * 8, cudaMemcpyHostToDevice, c.st));
+        u64* dout = c.cl_out.get<u64>((size_t)hq * 2 * LN);
+        // c1 = uniform_rns(derive_seed(sk.seed, 5, index)) straight into component 1
+        launch(c, k_uniform_rns, (size_t)hq * L, 1024, 0, (const Seed4*)seeds, c.T, (const u64*)dlim, dout + LN, 2 * LN);
+        // c1 s (negacyclic, per prime) through the chain NTT
+        client_secret(c, sk, false);
+        u64* prod = c.cl_a.get<u64>((size_t)hq * LN);
+        launch(c, k_gather_strided, blocks((size_t)hq * LN, 256), 256, 0, (const u64*)(dout + LN), 2 * LN,
+               (const u32*)nullptr, hq, LN, prod, LN);
+        ntt64(c, prod, hq * L, false);
+        launch(c, k_mul64, blocks((size_t)hq * LN, 256), 256, 0, prod, (const u64*)c.cl_s.ptr<u64>(), (size_t)hq, c.T);
+        ntt64(c, prod, hq * L, true);
+        int* e = c.cl_e.get<int>((size_t)hq * N);
+        launch(c, k_noise, blocks((size_t)hq * N, 256), 256, 0, (const Seed4*)(seeds + hq), hq, N, e);
+        unsigned char* db = c.cl_bits.get<unsigned char>(std::max<size_t>(m, N));
+        CK(cudaMemcpyAsync(db, bits, m, cudaMemcpyDefault, c.st));
+        launch(c, k_enc_combine, blocks((size_t)hq * LN, 256), 256, 0, (const u64*)prod, (const int*)e,
+               (const unsigned char*)db, m, comp, scale, hq, c.T, dout);
+        CK(cudaMemcpyAsync(out, dout, (size_t)hq * 2 * LN * 8, cudaMemcpyDefault, c.st));
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
+int cwg_decrypt(cwg_ctx* h, const int8_t* sk, uint32_t count, uint32_t comps, const uint64_t* cts, uint64_t* out) {
+    return guarded([&] {
+        Ctx& c = h->c;
+        std::lock_guard<std::mutex> g(c.mu);
+        CK(cudaSetDevice(c.device));
+        Nvtx nv("cwgpu decrypt");
+        if (comps < 2 || comps > 3) throw std::invalid_argument("ciphertext must have 2 or 3 components");
+        if (!sk) throw std::invalid_argument("decryption requires the secret key");
+        if (count == 0) return;
+        const u32 N = c.cp.N, L = c.cp.L;
+        const size_t LN = (size_t)L * N, per = (size_t)comps * LN;
+        u64* d = c.cl_out.get<u64>((size_t)count * per);
+        CK(cudaMemcpyAsync(d, cts, (size_t)count * per * 8, cudaMemcpyDefault, c.st));
+        client_secret(c, sk, comps == 3);
+        u64* v = c.cl_a.get<u64>((size_t)count * LN);
+        u64* w = c.cl_b.get<u64>((size_t)count * LN);
+        // v = c1 s (+ c2 s^2) in the NTT domain, back to coefficients, + c0 (bfv.cpp:556-568)
+        launch(c, k_gather_strided, blocks((size_t)count * LN, 256), 256, 0, (const u64*)(d + LN), per,
+               (const u32*)nullptr, count, LN, v, LN);
+        ntt64(c, v, count * L, false);
+        launch(c, k_mul64, blocks((size_t)count * LN, 256), 256, 0, v, (const u64*)c.cl_s.ptr<u64>(), (size_t)count, c.T);
+        if (comps == 3) {
+            launch(c, k_gather_strided, blocks((size_t)count * LN, 256), 256, 0, (const u64*)(d + 2 * LN), per,
+                   (const u32*)nullptr, count, LN, w, LN);
+            ntt64(c, w, count * L, false);
+            launch(c, k_mul64, blocks((size_t)count * LN, 256), 256, 0, w, (const u64*)c.cl_s2.ptr<u64>(), (size_t)count,
+                   c.T);
+            launch(c, k_add64_strided, blocks((size_t)count * LN, 256), 256, 0, v, (const u64*)w, LN, (size_t)count, c.T);
+        }
+        ntt64(c, v, count * L, true);
+        launch(c, k_add64_strided, blocks((size_t)count * LN, 256), 256, 0, v, (const u64*)d, per, (size_t)count, c.T);
+        u64* m = c.cl_b.get<u64>((size_t)count * N);
+        launch(c, k_dec_round, blocks((size_t)count * N, 128), 128, 0, (const u64*)v, (size_t)count, c.T, m);
+        CK(cudaMemcpyAsync(out, m, (size_t)count * N * 8, cudaMemcpyDefault, c.st));
+        CK(cudaStreamSynchronize(c.st));
+    });
+}
+
 int cwg_select(cwg_ctx* h, const uint64_t* relin, uint32_t n_galois, const uint64_t* galois_g, const uint64_t* galois,
                uint32_t nq, uint32_t comp, uint32_t m, const uint64_t* query, uint32_t op, uint64_t* sel,
                uint32_t* comps, cwg_timings* t) {
@@ -2258,6 +2535,7 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "ks32") { c.ks32 = v != 0; c.ksA_ok = false; }
         else if (k == "tile_rows") c.tile_rows_opt = (u32)std::max(0, v);
         else if (k == "ks_wide") c.ks_wide = v != 0;
+        else if (k == "prep_factors") c.prep_mode = v != 0;
         else if (k == "force_exact") {
             c.force_exact = v != 0;
             c.T.force_exact = c.force_exact ? 1u : 0u;

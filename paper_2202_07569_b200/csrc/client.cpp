@@ -419,4 +419,11 @@ int cwg_client_decrypt(const cwg_client* h, const uint64_t* ct, uint32_t comps, 
     return cguard([&] { h->c.decrypt(ct, comps, out); });
 }
 
+int cwg_client_export_secret(const cwg_client* h, int8_t* s, uint64_t* seed_words) {
+    return cguard([&] {
+        std::memcpy(s, h->c.s.data(), h->c.s.size());
+        for (int i = 0; i < 4; ++i) seed_words[i] = h->c.seed.w[i];
+    });
+}
+
 }  // extern "C"

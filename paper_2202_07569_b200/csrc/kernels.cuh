@@ -211,9 +211,12 @@ __device__ __forceinline__ bool mw_ge(const u32* X, const u32* src, u32 n) {
 __device__ __forceinline__ u32 crt_exact(const u64* y, u32 alpha_est, const DevTab& T, u32* X) {
 #pragma unroll
     for (u32 k = 0; k < kQW + 2; ++k) X[k] = 0;
-    for (u32 i = 0; i < T.L; ++i) {
-        mw_mac<0>(X, T.qov + (size_t)i * T.QW, T.QW, (u32)y[i]);
-        mw_mac<1>(X, T.qov + (size_t)i * T.QW, T.QW, (u32)(y[i] >> 32));
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) {  // unrolled with a uniform guard: y stays in registers
+        if (i < (int)T.L) {
+            mw_mac<0>(X, T.qov + (size_t)i * T.QW, T.QW, (u32)y[i]);
+            mw_mac<1>(X, T.qov + (size_t)i * T.QW, T.QW, (u32)(y[i] >> 32));
+        }
     }
     mw_msub(X, T.qw, T.QW, alpha_est);
     if (mw_ge(X, T.qw, T.QW)) {
@@ -228,12 +231,15 @@ __device__ __forceinline__ u32 crt_exact(const u64* y, u32 alpha_est, const DevT
 __device__ __forceinline__ u64 crt_prepare(const u64* res, const DevTab& T, u64* y, u32* ip) {
     u64 lo = 0;
     u32 carry = 0;
-    for (u32 i = 0; i < T.L; ++i) {
-        const u64 q = T.q[i];
-        y[i] = red64(shoup64(res[i], T.muq[i], T.muq_s[i], q), q);
-        const u64 f = frac64(y[i], T.q_gh[i], T.q_gl[i]);
-        lo += f;
-        carry += (lo < f);
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) {
+        if (i < (int)T.L) {
+            const u64 q = T.q[i];
+            y[i] = red64(shoup64(res[i], T.muq[i], T.muq_s[i], q), q);
+            const u64 f = frac64(y[i], T.q_gh[i], T.q_gl[i]);
+            lo += f;
+            carry += (lo < f);
+        }
     }
     *ip = carry;
     return lo;
@@ -241,7 +247,10 @@ __device__ __forceinline__ u64 crt_prepare(const u64* res, const DevTab& T, u64*
 
 /// rho = round(sum y_i / q_i): x > floor(q/2) decides (bfv.cpp:731).  Exact: the
 /// fractional estimate decides unless it lies within its error band below 1/2.
-__device__ __noinline__ u32 crt_round_exact(const u64* y, u32 ip, const DevTab& T) {
+__device__ __noinline__ u32 crt_round_exact(const u64* yin, u32 ip, const DevTab& T) {
+    u64 y[kMaxL];
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) y[i] = i < (int)T.L ? yin[i] : 0;
     u32 X[kQW + 2];
     const u32 alpha = crt_exact(y, ip, T, X);
     u32 c = 0;  // X <- 2X
@@ -284,10 +293,13 @@ __global__ void k_decompose_t(const u64* __restrict__ polys, size_t stride, u64 
         src = neg ? s - N : s;
     }
     u64 res[kMaxL];
-    for (u32 i = 0; i < T.L; ++i) {
-        u64 v = pb[(size_t)i * N + src];
-        if (neg && v) v = T.q[i] - v;
-        res[i] = v;
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) {
+        if (i < (int)T.L) {
+            u64 v = pb[(size_t)i * N + src];
+            if (neg && v) v = T.q[i] - v;
+            res[i] = v;
+        }
     }
     u64* out = digits + (size_t)b * D * N + n;
     auto put = [&](u32 d, u64 v) {
@@ -299,7 +311,9 @@ __global__ void k_decompose_t(const u64* __restrict__ polys, size_t stride, u64 
         }
     };
     if (bits == 0) {  // one RNS digit per chain prime (bfv.cpp:320-323)
-        for (u32 d = 0; d < D; ++d) put(d, res[d]);
+#pragma unroll
+        for (int d = 0; d < kMaxL; ++d)
+            if (d < (int)D) put(d, res[d]);
         return;
     }
     u64 y[kMaxL];
@@ -307,6 +321,12 @@ __global__ void k_decompose_t(const u64* __restrict__ polys, size_t stride, u64 
     crt_prepare(res, T, y, &ip);
     u32 X[kQW + 2];
     crt_exact(y, ip, T, X);
+    if (bits == 16) {  // the configured digit width: limb and shift are compile-time per unrolled digit
+#pragma unroll
+        for (int d = 0; d < 2 * kQW; ++d)
+            if (d < (int)D) put(d, (X[d >> 1] >> (16 * (d & 1))) & 0xffffu);
+        return;
+    }
     const u64 mask = (bits == 64) ? ~0ull : ((1ull << bits) - 1);
     for (u32 d = 0; d < D; ++d) {
         const u32 bit = d * bits, limb = bit >> 5, off = bit & 31;
@@ -447,25 +467,27 @@ __global__ void __launch_bounds__(256) k_lift(const u64* __restrict__ src, size_
     const u32 c = (u32)(idx / (2 * N)), k = (u32)((idx / N) % 2), n = (u32)(idx % N);
     const u64* s = src + (size_t)(sel ? sel[c] : c) * src_stride + (size_t)k * L * N + n;
     u64 res[kMaxL], y[kMaxL];
-    for (u32 i = 0; i < L; ++i) res[i] = s[(size_t)i * N];
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) res[i] = i < (int)L ? s[(size_t)i * N] : 0;
     u32 ip;
     const u64 fr = crt_prepare(res, T, y, &ip);
     const u32 rho = crt_round(y, ip, fr, T);
+    // y_i < 2^60 split 30 | 30 bits: sum_i ylo V + yhi V2 < L 2^61 (L <= 8: < 2^64), one reduction per prime
     u32 ylo[kMaxL], yhi[kMaxL];
-    for (u32 i = 0; i < L; ++i) {
-        ylo[i] = (u32)(y[i] & ((1u << 30) - 1));
-        yhi[i] = (u32)(y[i] >> 30);
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) {
+        ylo[i] = i < (int)L ? (u32)(y[i] & ((1u << 30) - 1)) : 0u;
+        yhi[i] = i < (int)L ? (u32)(y[i] >> 30) : 0u;
     }
     u32* o = out + ((size_t)c * 2 + k) * out_stride_j * N + n;
     for (u32 j = 0; j < nj; ++j) {
         const u32 a = sA[j];
-        u64 accA = 0, accB = (u64)rho * (a - sW[j]);
-        for (u32 i = 0; i < L; ++i) {
-            accA += (u64)ylo[i] * sV[i * nj + j];
-            accB += (u64)yhi[i] * sV2[i * nj + j];
-        }
+        u64 acc = 0;
+#pragma unroll
+        for (int i = 0; i < kMaxL; ++i)
+            if (i < (int)L) acc += (u64)ylo[i] * sV[i * nj + j] + (u64)yhi[i] * sV2[i * nj + j];
         const u64 ab = sAb[j];
-        o[(size_t)j * N] = red32(bar64(accA, a, ab) + bar64(accB, a, ab), a);
+        o[(size_t)j * N] = red32(bar64(acc, a, ab) + bar64((u64)rho * (a - sW[j]), a, ab), a);
     }
 }
 
@@ -721,27 +743,50 @@ __global__ void k_partial_mod(const u64* __restrict__ partial, size_t total, Dev
 
 /// MAC basis -> chain: X (coefficient form, centred |X| < M/2) -> out[g][i][n] mod q_i.
 /// X layout [G][xs][N] (the first Mm planes of each group of xs); out layout [G][L][N].
-__global__ void k_mac_to_chain(const u32* __restrict__ X, u32 xs, u32 G, DevTab T, u64* __restrict__ out) {
+__global__ void __launch_bounds__(128) k_mac_to_chain(const u32* __restrict__ X, u32 xs, u32 G, DevTab T,
+                                                      u64* __restrict__ out) {
+    // per-prime constants in shared memory (they were Mm L global loads per coefficient)
+    __shared__ u64 sMc[kMaxJ * kMaxL], sMF[kMaxJ], sQ[kMaxL], sMu[kMaxL], sNeg[kMaxL];
+    __shared__ u32 sA[kMaxJ], sH[kMaxJ], sHs[kMaxJ];
     const u32 N = T.N, Mm = T.Mm, L = T.L;
+    for (u32 x = threadIdx.x; x < Mm * L; x += blockDim.x) sMc[x] = T.Mconv[x];
+    for (u32 k = threadIdx.x; k < Mm; k += blockDim.x) {
+        sMF[k] = T.mF[k];
+        sA[k] = T.a[k];
+        sH[k] = T.mhat[k];
+        sHs[k] = T.mhat_s[k];
+    }
+    for (u32 i = threadIdx.x; i < L; i += blockDim.x) {
+        sQ[i] = T.q[i];
+        sMu[i] = T.q_mu96[i];
+        sNeg[i] = T.MnegQ[i];
+    }
+    __syncthreads();
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)G * N) return;
     const size_t g = idx / N;
     const u32 n = (u32)(idx % N);
-    u32 v[kMaxJ];
+    // acc_i = sum_k v_k (M / m_k mod q_i), 128-bit, gamma = round(sum_k v_k / m_k)
+    u64 hi[kMaxL], lo[kMaxL];
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) hi[i] = lo[i] = 0;
     u64 gs = 0;
     for (u32 k = 0; k < Mm; ++k) {
-        const u32 a = T.a[k];
-        v[k] = red32(shoup32(X[(g * xs + k) * N + n], T.mhat[k], T.mhat_s[k], a), a);
-        gs += (u64)v[k] * T.mF[k];
+        const u32 a = sA[k];
+        const u32 v = red32(shoup32(X[(g * xs + k) * N + n], sH[k], sHs[k], a), a);
+        gs += (u64)v * sMF[k];
+#pragma unroll
+        for (int i = 0; i < kMaxL; ++i)
+            if (i < (int)L) mac128(hi[i], lo[i], v, sMc[k * L + i]);
     }
     const u32 gsh = 64 - T.gbits;
     const u32 gamma = (u32)((gs + (1ull << (gsh - 1))) >> gsh);
-    for (u32 i = 0; i < L; ++i) {
-        const u64 q = T.q[i];
-        u64 hi = 0, lo = 0;
-        for (u32 k = 0; k < Mm; ++k) mac128(hi, lo, v[k], T.Mconv[(size_t)k * L + i]);
-        mac128(hi, lo, gamma, T.MnegQ[i]);
-        out[(g * L + i) * N + n] = reduce128(hi, lo, q, T.q_mu96[i]);
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) {
+        if (i < (int)L) {
+            mac128(hi[i], lo[i], gamma, sNeg[i]);
+            out[(g * L + i) * N + n] = reduce128(hi[i], lo[i], sQ[i], sMu[i]);
+        }
     }
 }
 
@@ -776,6 +821,61 @@ __global__ void k_arith_factors(const u64* __restrict__ entries, const u32* __re
         }
         out[(((size_t)r * k + f) * 2) * LN + rem] = v;
     }
+}
+
+/// Arithmetic-operator factors share everything but one coefficient: f_f = k' + Delta (t - f) only
+/// changes coefficient 0 of component 0 (add_plain, bfv.cpp:641-649), so the centred aux lift of
+/// f_f equals that of k' except there, and the NTT of that difference is the same constant in every
+/// slot.  delta[r][f][j] = (lift(f_f)_0 - lift(k')_0) mod a_j (Montgomery form, like the prepared
+/// operands) from the chain residues of coefficient 0 of each factor (nodes [R][k][2][L][N]).
+__global__ void k_arith_deltas(const u64* __restrict__ nodes, u32 R, u32 k, DevTab T, u32* __restrict__ delta) {
+    const u32 x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= R * k) return;
+    const u32 r = x / k, f = x % k;
+    const u32 L = T.L, N = T.N, J = T.J;
+    const size_t per = (size_t)2 * L * N;
+    u32 lf[kMaxJ];
+    for (int which = 0; which < 2; ++which) {  // 0: factor f, 1: factor 0 (= k')
+        const u64* s = nodes + ((size_t)r * k + (which ? 0 : f)) * per;
+        u64 res[kMaxL], y[kMaxL];
+#pragma unroll
+        for (int i = 0; i < kMaxL; ++i) res[i] = i < (int)L ? s[(size_t)i * N] : 0;
+        u32 ip;
+        const u64 fr = crt_prepare(res, T, y, &ip);
+        const u32 rho = crt_round(y, ip, fr, T);
+        for (u32 j = 0; j < J; ++j) {
+            const u32 a = T.a[j];
+            u64 acc = 0;
+#pragma unroll
+            for (int i = 0; i < kMaxL; ++i)
+                if (i < (int)L)
+                    acc += (u64)(u32)(y[i] & ((1u << 30) - 1)) * T.liftV_m[i * J + j] +
+                           (u64)(u32)(y[i] >> 30) * T.liftV2_m[i * J + j];
+            const u32 v = red32(bar64(acc, a, T.abar[j]) + bar64((u64)rho * (a - T.liftW_m[j]), a, T.abar[j]), a);
+            if (which == 0) lf[j] = v;
+            else delta[(size_t)x * J + j] = red32(lf[j] + a - v, a);
+        }
+    }
+}
+
+/// Prepared factors [R][k][2][J][N] from the prepared k' [R][2][J][N] (NTT form, Montgomery) and
+/// the per-factor constants delta (component 0 only).
+__global__ void k_prep_factors(const u32* __restrict__ pk, const u32* __restrict__ delta, u32 R, u32 k, DevTab T,
+                               u32* __restrict__ out) {
+    const u32 J = T.J, N = T.N;
+    const size_t JN = (size_t)J * N;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)R * k * 2 * JN) return;
+    const size_t x = idx % (2 * JN);
+    const size_t rf = idx / (2 * JN);
+    const u32 r = (u32)(rf / k);
+    const u32 comp = (u32)(x / JN), j = (u32)((x / N) % J);
+    u32 v = pk[(size_t)r * 2 * JN + x];
+    if (comp == 0) {
+        const u32 a = T.a[j];
+        v = red32(v + delta[rf * J + j], a);
+    }
+    out[idx] = v;
 }
 
 /// Multiply every coefficient of B 2-comp ciphertexts by c mod q_i (plain_mul by a

@@ -156,4 +156,115 @@ __global__ void __launch_bounds__(288, 3) k_mac_tma(const u32* __restrict__ Z, u
     }
 }
 
+
+/// Multi-query payload MAC: the k_mac_tma stream with QB queries' selection
+/// planes per database segment, so one pass over a row tile's database planes serves all of them
+/// (the DB read -- the HBM-bound part at s >= 3 -- is shared).  512-coefficient blocks (2 per
+/// consumer thread) keep the ring at 4 stages x (1 + QB NC) x 2 KB, 2 CTAs / SM at QB = 4.
+constexpr int kMacBlockQ = 512;
+struct ZPtrs {
+    const u32* z[4];
+    unsigned long long* acc[4];
+};
+template <int NC, int QB>
+__global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZPtrs Zp, u32 zstride,
+                                                     const u32* __restrict__ DB, u32 R, u32 s, u32 chunk, DevTab T) {
+    extern __shared__ __align__(128) uint2 ringq[];  // [stage][1 + QB NC][kMacBlockQ / 2]
+    __shared__ __align__(8) unsigned long long full[kMacStages], empty[kMacStages];
+    constexpr u32 NSEG = 1 + QB * NC;
+    constexpr u32 SEG = kMacBlockQ * 4;   // bytes per segment
+    constexpr u32 SEGV = kMacBlockQ / 2;  // uint2 per segment
+    const u32 N = T.N, Mm = T.Mm;
+    const u32 nblk = N / kMacBlockQ;
+    u32 b = blockIdx.x;
+    const u32 sj = b % s;
+    b /= s;
+    const u32 blk = b % nblk;
+    b /= nblk;
+    const u32 k = b % Mm;
+    const u32 ch = b / Mm;
+    const u32 r0 = ch * chunk, r1 = min(R, r0 + chunk);
+    const u32 rows = r1 > r0 ? r1 - r0 : 0;
+    const u32 tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0) {
+        for (int i = 0; i < kMacStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {  // producer
+        if ((tid & 31) == 0) {
+            const size_t dbs = (size_t)s * Mm * N;
+            const u32* dbase = DB + ((size_t)sj * Mm + k) * N + (size_t)blk * kMacBlockQ;
+            const size_t zs = (size_t)NC * zstride * N;
+            const size_t zoff = (size_t)k * N + (size_t)blk * kMacBlockQ;
+            for (u32 i = 0; i < rows; ++i) {
+                const u32 st = i % kMacStages;
+                if (i >= (u32)kMacStages) mbar_wait(&empty[st], ((i / kMacStages) - 1) & 1);
+                uint2* buf = ringq + (size_t)st * NSEG * SEGV;
+                mbar_expect_tx(&full[st], SEG * NSEG);
+                const size_t r = r0 + i;
+                tma_bulk_g2s(buf, dbase + r * dbs, SEG, &full[st]);
+#pragma unroll
+                for (int q = 0; q < QB; ++q)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        tma_bulk_g2s(buf + (1 + q * NC + c) * SEGV, Zp.z[q] + zoff + r * zs + (size_t)c * zstride * N,
+                                     SEG, &full[st]);
+            }
+        }
+        return;
+    }
+    const u32 p = T.a[k];
+    const u64 pb = T.abar[k];
+    u32 accr[QB][NC][2];
+#pragma unroll
+    for (int q = 0; q < QB; ++q)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) accr[q][c][0] = accr[q][c][1] = 0;
+    for (u32 g0 = 0; g0 < rows; g0 += 16) {
+        const u32 ge = min(rows, g0 + 16);
+        u64 g[QB][NC][2];
+#pragma unroll
+        for (int q = 0; q < QB; ++q)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) g[q][c][0] = g[q][c][1] = 0;
+        for (u32 i = g0; i < ge; ++i) {
+            const u32 st = i % kMacStages;
+            mbar_wait(&full[st], (i / kMacStages) & 1);
+            const uint2* buf = ringq + (size_t)st * NSEG * SEGV;
+            const uint2 d = buf[tid];
+#pragma unroll
+            for (int q = 0; q < QB; ++q)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const uint2 z = buf[(1 + q * NC + c) * SEGV + tid];
+                    g[q][c][0] += (u64)z.x * d.x;
+                    g[q][c][1] += (u64)z.y * d.y;
+                }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+        }
+#pragma unroll
+        for (int q = 0; q < QB; ++q)
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) accr[q][c][e] = red32(accr[q][c][e] + bar64(g[q][c][e], p, pb), p);
+    }
+    if (rows == 0) return;
+    const u32 n = blk * kMacBlockQ + 2 * tid;
+#pragma unroll
+    for (int q = 0; q < QB; ++q)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            unsigned long long* o = Zp.acc[q] + (((size_t)sj * 3 + c) * Mm + k) * N + n;
+            atomicAdd(o, (unsigned long long)accr[q][c][0]);
+            atomicAdd(o + 1, (unsigned long long)accr[q][c][1]);
+        }
+}
+
 }  // namespace cwgpu

@@ -39,11 +39,13 @@ EXPORTED_SYMBOLS = [
     "cwg_answer_partial_shards", "cwg_select", "cwg_ntt",
     "cwg_expand", "cwg_mul_lazy", "cwg_relinearize", "cwg_substitute", "cwg_kernel_launches",
     "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats", "cwg_kernel_units", "cwg_set_option",
-    "cwg_create_multi", "cwg_device_count", "cwg_load_db_file",
+    "cwg_create_multi", "cwg_device_count", "cwg_load_db_file", "cwg_answer_batch", "cwg_encrypt_query",
+    "cwg_decrypt",
 ]
 CLIENT_SYMBOLS = [
     "cwg_client_last_error", "cwg_client_create", "cwg_client_destroy", "cwg_client_digits",
     "cwg_client_export_keys", "cwg_client_encrypt", "cwg_client_pack_query", "cwg_client_decrypt",
+    "cwg_client_export_secret",
 ]
 
 
@@ -106,6 +108,12 @@ def load_library(path: str = LIB_PATH):
     keyargs = [_u64p, ctypes.c_uint32, _u64p, _u64p]
     qargs = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_uint32]
     lib.cwg_answer.argtypes = [ctypes.c_void_p, *keyargs, *qargs, ctypes.c_void_p, ctypes.POINTER(CwgTimings)]
+    lib.cwg_answer_batch.argtypes = [ctypes.c_void_p, *keyargs, ctypes.c_uint32, *qargs, ctypes.c_void_p,
+                                     ctypes.POINTER(CwgTimings)]
+    lib.cwg_encrypt_query.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
+                                      ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p]
+    lib.cwg_decrypt.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_void_p,
+                                ctypes.c_void_p]
     lib.cwg_answer_partial.argtypes = [ctypes.c_void_p, *keyargs, *qargs, ctypes.c_void_p,
                                        ctypes.POINTER(CwgTimings)]
     lib.cwg_partial_words.restype = ctypes.c_uint64
@@ -159,6 +167,7 @@ def load_client_library(path: str = CLIENT_LIB_PATH):
     lib.cwg_client_pack_query.argtypes = [ctypes.c_void_p, _u8p, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
                                           _u64p]
     lib.cwg_client_decrypt.argtypes = [ctypes.c_void_p, _u64p, ctypes.c_uint32, _u64p]
+    lib.cwg_client_export_secret.argtypes = [ctypes.c_void_p, ctypes.c_void_p, _u64p]
     _CLIENT_LIB = lib
     return lib
 
@@ -304,6 +313,19 @@ class Context:
         _raise(self.lib, rc)
         return (out, tm.as_dict()) if timings else out
 
+    def answer_batch(self, queries, c, m, op=OP_FOLKLORE, keys=None, timings=False):
+        """cwg_answer_batch: queries [Q][h][2][L][N] -> [Q][s][2][L][N] (one DB pass per tile)."""
+        queries = _c64(queries)
+        Q, h = queries.shape[0], queries.shape[1]
+        info = self.info()
+        out = np.zeros((Q, info.s, 2, self.L, self.N), np.uint64)
+        ka, keep = self._key_args(keys)
+        tm = CwgTimings()
+        rc = self.lib.cwg_answer_batch(self.h, *ka, Q, h, c, m, queries.ctypes.data, op, out.ctypes.data,
+                                       ctypes.byref(tm) if timings else None)
+        _raise(self.lib, rc)
+        return (out, tm.as_dict()) if timings else out
+
     def answer_ptr(self, query_ptr, h, c, m, op, out_ptr, keys_ptrs=(None, 0, None, None), timings=None):
         """Raw-pointer variant (pinned host buffers from torch) used by bench.py."""
         rc = self.lib.cwg_answer(self.h, *keys_ptrs, h, c, m, query_ptr, op, out_ptr,
@@ -375,6 +397,30 @@ class Context:
                                  ctypes.byref(tm) if timings else None)
         _raise(self.lib, rc)
         return (sel, comps, tm.as_dict()) if timings else (sel, comps)
+
+    def encrypt_query(self, secret, bits, c, first_index=1):
+        """cwg_encrypt_query: pack_query_bits + encrypt on the GPU.  secret = (s [N] int8, seed words [4])
+        (Client.secret()); returns [h][2][L][N], equal to Client.pack_query for the same indices."""
+        s, seed = secret
+        s = np.ascontiguousarray(s, dtype=np.int8)
+        seed = np.ascontiguousarray(seed, dtype=np.uint64)
+        bits = np.ascontiguousarray(bits, dtype=np.uint8)
+        h = -(-len(bits) // (1 << c))
+        out = np.zeros((max(h, 1), 2, self.L, self.N), np.uint64)
+        _raise(self.lib, self.lib.cwg_encrypt_query(self.h, _p64(seed), s.ctypes.data, bits.ctypes.data, len(bits), c,
+                                                    first_index, out.ctypes.data))
+        return out
+
+    def decrypt(self, secret, cts):
+        """cwg_decrypt: cts [count][comps][L][N] (or one [comps][L][N]) -> [count][N] (or [N])."""
+        s = np.ascontiguousarray(secret[0], dtype=np.int8)
+        cts = _c64(cts)
+        single = cts.ndim == 3
+        c4 = _c64(cts[None]) if single else cts
+        out = np.zeros((c4.shape[0], self.N), np.uint64)
+        _raise(self.lib, self.lib.cwg_decrypt(self.h, s.ctypes.data, c4.shape[0], c4.shape[1], c4.ctypes.data,
+                                              out.ctypes.data))
+        return out[0] if single else out
 
     def ntt(self, a, idx, chain=True, inverse=False):
         a = _c64(a).copy()
@@ -484,6 +530,13 @@ class Client:
         self._check(self.lib.cwg_client_pack_query(self.h, bits.ctypes.data_as(_u8p), len(bits), c, first_index,
                                                    _p64(out)))
         return out
+
+    def secret(self):
+        """(secret key coefficients [N] int8, Seed256 words [4]) for the GPU client calls."""
+        s = np.zeros(self.N, np.int8)
+        seed = np.zeros(4, np.uint64)
+        self._check(self.lib.cwg_client_export_secret(self.h, s.ctypes.data, _p64(seed)))
+        return s, seed
 
     def decrypt(self, ct):
         ct = _c64(ct)

@@ -110,3 +110,34 @@ def test_answer_path_variants_match_reference(gpu, reflib, opts, kernel):
     from paper_2202_07569_b200 import configs
 
     _run(reflib, configs.config("C4"), 40, expect_kernel=kernel, options={"tile_rows": 16, **opts})
+
+
+@pytest.mark.parametrize("name,rows,Q,opts", [
+    ("C3", 24, 5, {}),                 # s = 15: one database pass per group of <= 4 queries (k_mac_tma_q)
+    ("C3", 24, 2, {"mac": 0}),         # s = 15 through k_mac2 per query
+    ("C4", 40, 3, {"tile_rows": 16}),  # s = 1: fused selection NTT + MAC per query, ragged tiles
+])
+def test_answer_batch_matches_single_answers(gpu, reflib, name, rows, Q, opts):
+    """cwg_answer_batch (several queries of one client in one database pass) returns,
+    for every query, exactly the single-query answer -- and the first equals the reference's."""
+    from oracle import RefBackend
+    from paper_2202_07569_b200 import Client, Context, configs
+
+    cfg = configs.config(name)
+    client = Client(cfg.N, cfg.primes, cfg.t, seed=3, galois_levels=cfg.c)
+    keys = client.keys()
+    pos = configs.db_positions(cfg, 3)[:rows]
+    db = configs.db_payload(cfg, 3, 0, rows)
+    targets = [(5 * q + 1) % rows for q in range(Q)]
+    qs = np.stack([client.pack_query(configs.codeword_bits(pos[tg], cfg.m), cfg.c, first_index=1 + 10 * q)
+                   for q, tg in enumerate(targets)])
+    ctx = Context(cfg.N, cfg.primes, cfg.t, options=opts)
+    ctx.load_db(pos, db, n_total=rows, m=cfg.m)
+    got = ctx.answer_batch(qs, cfg.c, cfg.m, keys=keys)
+    for q in range(Q):
+        assert np.array_equal(got[q], ctx.answer(qs[q], cfg.c, cfg.m, keys=keys)), q
+        for j in range(cfg.s):
+            assert np.array_equal(client.decrypt(got[q, j]), db[targets[q], j])
+    be = RefBackend(reflib, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), keys=(keys.relin, keys.galois))
+    want, _ = be.answer(qs[0], cfg.c, cfg.m, pos, db)
+    assert np.array_equal(got[0], want)

@@ -524,3 +524,52 @@ def test_multi_device_context_matches_single(gpu, reflib, devices):
             assert np.array_equal(sel, sel_want) and np.array_equal(comps, comps_want)
         with pytest.raises(StateError):
             ctx.answer_partial(q, c, m, torch.zeros(8, dtype=torch.int64, device="cuda").data_ptr())
+
+
+@pytest.mark.parametrize("name", ["C1", "C4", "C5"])
+def test_gpu_client_matches_reference_client(gpu, reflib, name):
+    """SURVEY 8f-f4 on the GPU: pack_query_bits + encrypt (ChaCha20 streams, rejection-sampled
+    uniform_rns, centred-binomial noise) equal the CPU client's words (pinned to the reference's
+    bfv_keygen / pack_query_bits by test_cpu_host.py), for h = 1 and h = 2 query ciphertexts; decrypt
+    of 2- and 3-component ciphertexts equals the reference's BfvBackend::decrypt."""
+    from paper_2202_07569_b200 import Client, Context, configs
+
+    cfg = configs.config(name)
+    client = Client(cfg.N, cfg.primes, cfg.t, seed=7, galois_levels=1)
+    secret = client.secret()
+    ctx = Context(cfg.N, cfg.primes, cfg.t)
+    r = np.random.default_rng(8)
+    for m, first in ((cfg.m, 1), ((1 << cfg.c) + 5, 40)):  # h = 1, then h = 2 with a later index
+        bits = (r.random(m) < 0.3).astype(np.uint8)
+        want = client.pack_query(bits, cfg.c, first_index=first)
+        got = ctx.encrypt_query(secret, bits, cfg.c, first_index=first)
+        assert np.array_equal(got, want)
+    be = oracle_backend(reflib, cfg, seed=7)
+    ct2 = want
+    assert np.array_equal(ctx.decrypt(secret, ct2), np.stack([client.decrypt(x) for x in ct2]))
+    a, b = ct2[0], ct2[1]
+    ct3 = be.mul_lazy(a, b)
+    assert np.array_equal(ctx.decrypt(secret, ct3), be.decrypt(ct3))
+
+
+def oracle_backend(reflib, cfg, seed):
+    from oracle import RefBackend
+
+    return RefBackend(reflib, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), seed=seed, galois_levels=1)
+
+
+@pytest.mark.parametrize("k", [3, 4, 5])
+def test_arith_factor_preparation_variants(gpu, reflib, k):
+    """The arithmetic operator's factors prepared from k' once plus per-factor constants
+    (default) and prepared one by one (option prep_factors = 0) both equal the reference."""
+    from paper_2202_07569_b200 import configs
+
+    N, primes, t = small_params(2048, 4, 50, 65537)
+    n = 30
+    m = configs.min_code_length(n, k)
+    c = configs.default_compression(N, m)
+    for mode in (1, 0):
+        got, want, be, payload = _answer_case(reflib, N, primes, t, n, k, m, c, s=1, op=1, seed=80 + k,
+                                              options={"prep_factors": mode, "tile_rows": 7})
+        assert np.array_equal(got, want), mode
+        assert np.array_equal(be.decrypt(got[0]), payload[0])
