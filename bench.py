@@ -63,8 +63,12 @@ def imad_peak():
 # algorithmic units of the same launch, so `traffic` can be scaled to any launch of the kernel
 def ncu_traffic():
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic_C4.json")) as f:
-            return json.load(f)
+        for tag in ("r02", "r01"):
+            path = os.path.join(ROOT, "profiles", f"{tag}_ncu_traffic_C4.json")
+            if os.path.exists(path):
+                with open(path) as f:
+                    return json.load(f)
+        return {}
     except Exception:
         return {}
 

@@ -119,6 +119,7 @@ struct Ctx {
     bool ks32 = true;
     bool ks_wide = true;  // "ks_wide": shared-load key-switch MAC also for 16 < D <= 32 digits
     int prep_mode = 1;    // "prep_factors": 1 prepare k' once for the arithmetic factors, 0 each factor
+    bool mac_sg = true;   // "mac_sg": s >= 3 payload MAC with 3 or 5 slices per CTA (0: k_mac_tma, one slice)
     bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
     KsCrt ksC_r{}, ksC_g{};            // K' = 0: this key type keeps the 64-bit path
     DevBuf relinA, galoisA, ksdig, ksmac;  // keys re-based into the aux primes, digit / MAC scratch
@@ -737,10 +738,11 @@ struct Reg32 {
 static void set_smem_limits(u32 N) {
     CK(cudaFuncSetAttribute(k_mac_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 4 * kMacBlock * 4));
     CK(cudaFuncSetAttribute(k_mac_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMacStages * 3 * kMacBlock * 4));
-#define MQ(NCv, QBv)                                                                                              \
-    CK(cudaFuncSetAttribute(k_mac_tma_q<NCv, QBv>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
-                            kMacStages * (1 + QBv * NCv) * kMacBlockQ * 4));
-    MQ(2, 1) MQ(2, 2) MQ(2, 3) MQ(2, 4) MQ(3, 1) MQ(3, 2) MQ(3, 3) MQ(3, 4)
+#define MQ(NCv, QBv, SGv)                                                                                         \
+    CK(cudaFuncSetAttribute(k_mac_tma_q<NCv, QBv, SGv>, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                            kMacStages * (SGv + QBv * NCv) * kMacBlockQ * 4));
+    MQ(2, 1, 1) MQ(2, 2, 1) MQ(2, 3, 1) MQ(2, 4, 1) MQ(3, 1, 1) MQ(3, 2, 1) MQ(3, 3, 1) MQ(3, 4, 1)
+    MQ(2, 1, 3) MQ(3, 1, 3) MQ(2, 1, 5) MQ(3, 1, 5)
 #undef MQ
 #define RTC(JMv, NCv)                                                                                                \
     CK(cudaFuncSetAttribute(k_round_tma<0, JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
@@ -1431,6 +1433,25 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         // across the s payload slices); the register stream is as fast for s = 1 (C4: 22.9 ms)
         if (c.fuse_now) {
             REG32_DISPATCH(c.cp.logN, ntt_mac(c, Z, zs, nc, dbt, Rt, acc));
+        } else if (c.mac_sg && c.s >= 3 && (c.s % 5 == 0 || c.s % 3 == 0) && N >= (u32)kMacBlockQ) {
+            // several payload slices per CTA: the row's selection segments are read once per SG slices
+            const u32 SG = c.s % 3 == 0 ? 3 : 5;
+            ZPtrs zp{};
+            zp.z[0] = Z;
+            zp.acc[0] = acc;
+            const u32 blocksN = Mm * (N / kMacBlockQ) * (c.s / SG);
+            const u32 slots = 148 * 2 * 2;
+            u32 ck = std::max<u32>(1, std::min<u32>((Rt + 7) / 8, slots / blocksN));
+            const u32 crow = (Rt + ck - 1) / ck;
+            ck = (Rt + crow - 1) / crow;
+            const size_t smem = (size_t)kMacStages * (SG + nc) * kMacBlockQ * 4;
+            if (SG == 5) {
+                if (nc == 3) launch_named(c, "k_mac", k_mac_tma_q<3, 1, 5>, (size_t)ck * blocksN, 288, smem, zp, zs, dbt, Rt, c.s, crow, c.T);
+                else launch_named(c, "k_mac", k_mac_tma_q<2, 1, 5>, (size_t)ck * blocksN, 288, smem, zp, zs, dbt, Rt, c.s, crow, c.T);
+            } else {
+                if (nc == 3) launch_named(c, "k_mac", k_mac_tma_q<3, 1, 3>, (size_t)ck * blocksN, 288, smem, zp, zs, dbt, Rt, c.s, crow, c.T);
+                else launch_named(c, "k_mac", k_mac_tma_q<2, 1, 3>, (size_t)ck * blocksN, 288, smem, zp, zs, dbt, Rt, c.s, crow, c.T);
+            }
         } else if (c.mac_tma && c.s >= 2 && N >= (u32)kMacBlock) {
             // TMA-fed stream: whole waves of 3 CTAs / SM (no partial tail wave), >= 8 rows per chunk
             const u32 per = Mm * (N / kMacBlock) * c.s;
@@ -1551,7 +1572,7 @@ static void answer_batch(Ctx& c, u32 Q, u32 h, u32 comp, u32 m, const u64* queri
                     zp.z[x] = Z[q0 + x];
                     zp.acc[x] = acc + (q0 + x) * accw;
                 }
-                const u32 blocksN = Mm * (N / kMacBlockQ) * c.s;
+                const u32 blocksN = Mm * (N / kMacBlockQ) * c.s;  // SG = 1
                 const u32 slots = 148 * 2 * 2;
                 u32 ck = std::max<u32>(1, std::min<u32>((Rt + 7) / 8, slots / blocksN));
                 const u32 crow = (Rt + ck - 1) / ck;
@@ -1559,8 +1580,8 @@ static void answer_batch(Ctx& c, u32 Q, u32 h, u32 comp, u32 m, const u64* queri
                 const size_t smem = (size_t)kMacStages * (1 + qb * nc) * kMacBlockQ * 4;
                 c.next_units = (double)Rt * (c.s + (double)qb * nc) * Mm * N * 4;  // DB once + qb selections
 #define MACQ(NCv, QBv)                                                                                            \
-    launch_named(c, "k_mac_q", k_mac_tma_q<NCv, QBv>, (size_t)ck * blocksN, 288, smem, zp, zst[q0], dbt, Rt, c.s,   \
-                 crow, c.T)
+    launch_named(c, "k_mac_q", k_mac_tma_q<NCv, QBv, 1>, (size_t)ck * blocksN, 288, smem, zp, zst[q0], dbt, Rt,   \
+                 c.s, crow, c.T)
                 if (nc == 3) {
                     if (qb == 1) MACQ(3, 1); else if (qb == 2) MACQ(3, 2); else if (qb == 3) MACQ(3, 3); else MACQ(3, 4);
                 } else {
@@ -2536,6 +2557,7 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "tile_rows") c.tile_rows_opt = (u32)std::max(0, v);
         else if (k == "ks_wide") c.ks_wide = v != 0;
         else if (k == "prep_factors") c.prep_mode = v != 0;
+        else if (k == "mac_sg") c.mac_sg = v != 0;
         else if (k == "force_exact") {
             c.force_exact = v != 0;
             c.T.force_exact = c.force_exact ? 1u : 0u;

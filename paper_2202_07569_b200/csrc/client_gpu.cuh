@@ -219,46 +219,59 @@ __global__ void k_dec_round(const u64* __restrict__ v, size_t count, DevTab T, u
     const u32 n = (u32)(idx % N);
     const u64 t = T.t;
     u32 rem[kQW + 3];
-    for (u32 w = 0; w < QW + 3; ++w) rem[w] = 0;
+#pragma unroll
+    for (int w = 0; w < kQW + 3; ++w) rem[w] = 0;
     u64 qsum = 0;
-    for (u32 i = 0; i < L; ++i) {
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) {
+        if (i >= (int)L) break;
         const u64 qi = T.q[i];
         const u64 y = red64(shoup64(v[(b * L + i) * N + n], T.muq[i], T.muq_s[i], qi), qi);
-        const unsigned __int128 ty = (unsigned __int128)t * y;
-        qsum = (qsum + (u64)((ty / qi) % t)) % t;
-        const u64 r = (u64)(ty % qi);  // < 2^60
-        // rem += r * (q / q_i)  (multiword, 32-bit limbs)
+        // t y = fl q_i + r with fl < t: r by the 128-bit reduction, fl by exact division (q_i odd:
+        // fl = (t y - r) q_i^-1 mod 2^64, exact since fl < 2^64)
+        const u64 lo = t * y, hi = __umul64hi(t, y);
+        const u64 r = reduce128(hi, lo, qi, T.q_mu96[i]);
+        u64 qinv = qi;  // q_i^-1 mod 2^64 (Newton)
+#pragma unroll
+        for (int it = 0; it < 5; ++it) qinv *= 2 - qi * qinv;
+        const u64 fl = (lo - r) * qinv;
+        qsum = (qsum + fl % t) % t;
+        // rem += r (q / q_i), 32-bit limbs
         const u32 r0 = (u32)r, r1 = (u32)(r >> 32);
         const u32* qo = T.qov + (size_t)i * QW;
         u64 carry = 0;
-        for (u32 w = 0; w < QW + 2; ++w) {
-            const u64 lo = w < QW ? (u64)qo[w] * r0 : 0;
-            const u64 hi = (w >= 1 && w - 1 < QW) ? (u64)qo[w - 1] * r1 : 0;
-            const unsigned __int128 s = (unsigned __int128)rem[w] + (lo & 0xffffffffu) + (hi & 0xffffffffu) + carry;
+#pragma unroll
+        for (int w = 0; w < kQW + 2; ++w) {
+            const u64 a0 = w < (int)QW ? (u64)qo[w] * r0 : 0;
+            const u64 a1 = (w >= 1 && w - 1 < (int)QW) ? (u64)qo[w - 1] * r1 : 0;
+            const u64 s = (u64)rem[w] + (a0 & 0xffffffffu) + (a1 & 0xffffffffu) + (carry & 0xffffffffu);
             rem[w] = (u32)s;
-            carry = (u64)(s >> 32) + (lo >> 32) + (hi >> 32);
+            carry = (s >> 32) + (a0 >> 32) + (a1 >> 32) + (carry >> 32);
         }
-        rem[QW + 2] += (u32)carry;
+        rem[kQW + 2] += (u32)carry;
     }
     // 2 rem >= (2z - 1) q for z = 1, 2, ...: count them (rem < L q)
     u32 two[kQW + 3];
     u32 cy = 0;
-    for (u32 w = 0; w < QW + 3; ++w) {
+#pragma unroll
+    for (int w = 0; w < kQW + 3; ++w) {
         two[w] = (rem[w] << 1) | cy;
         cy = rem[w] >> 31;
     }
     u64 round_add = 0;
     for (u32 z = 1; z <= L; ++z) {
-        // (2z - 1) q
         u32 mq[kQW + 3];
         u64 c2 = 0;
-        for (u32 w = 0; w < QW + 3; ++w) {
-            const u64 s = (w < QW ? (u64)T.qw[w] * (2 * z - 1) : 0) + c2;
+#pragma unroll
+        for (int w = 0; w < kQW + 3; ++w) {
+            const u64 s = (w < (int)QW ? (u64)T.qw[w] * (2 * z - 1) : 0) + c2;
             mq[w] = (u32)s;
             c2 = s >> 32;
         }
         int cmp = 0;
-        for (int w = (int)QW + 2; w >= 0 && cmp == 0; --w) cmp = two[w] > mq[w] ? 1 : (two[w] < mq[w] ? -1 : 0);
+#pragma unroll
+        for (int w = kQW + 2; w >= 0; --w)
+            if (cmp == 0) cmp = two[w] > mq[w] ? 1 : (two[w] < mq[w] ? -1 : 0);
         if (cmp >= 0) ++round_add;
         else break;
     }

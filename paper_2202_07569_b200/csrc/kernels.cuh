@@ -247,10 +247,7 @@ __device__ __forceinline__ u64 crt_prepare(const u64* res, const DevTab& T, u64*
 
 /// rho = round(sum y_i / q_i): x > floor(q/2) decides (bfv.cpp:731).  Exact: the
 /// fractional estimate decides unless it lies within its error band below 1/2.
-__device__ __noinline__ u32 crt_round_exact(const u64* yin, u32 ip, const DevTab& T) {
-    u64 y[kMaxL];
-#pragma unroll
-    for (int i = 0; i < kMaxL; ++i) y[i] = i < (int)T.L ? yin[i] : 0;
+__device__ __noinline__ u32 crt_round_exact(const u64* y, u32 ip, const DevTab& T) {
     u32 X[kQW + 2];
     const u32 alpha = crt_exact(y, ip, T, X);
     u32 c = 0;  // X <- 2X

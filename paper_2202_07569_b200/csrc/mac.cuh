@@ -157,28 +157,31 @@ __global__ void __launch_bounds__(288, 3) k_mac_tma(const u32* __restrict__ Z, u
 }
 
 
-/// Multi-query payload MAC: the k_mac_tma stream with QB queries' selection
-/// planes per database segment, so one pass over a row tile's database planes serves all of them
-/// (the DB read -- the HBM-bound part at s >= 3 -- is shared).  512-coefficient blocks (2 per
-/// consumer thread) keep the ring at 4 stages x (1 + QB NC) x 2 KB, 2 CTAs / SM at QB = 4.
+/// Multi-query / multi-slice payload MAC: the k_mac_tma stream with QB queries' selection planes
+/// and SG payload slices per ring stage.  QB > 1: one pass over a row tile's
+/// database planes serves several queries.  SG > 1 (s >= 3 rows, e.g. C3's 15 plaintexts): the
+/// NC selection segments of a row are read once per SG slices instead of once per slice.
+/// 512-coefficient blocks (2 per consumer thread) keep the ring at 4 stages x (SG + QB NC) x 2 KB.
+/// Grid: chunks x Mm x (N / 512) x (s / SG); s must be a multiple of SG.
 constexpr int kMacBlockQ = 512;
 struct ZPtrs {
     const u32* z[4];
     unsigned long long* acc[4];
 };
-template <int NC, int QB>
+template <int NC, int QB, int SG>
 __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZPtrs Zp, u32 zstride,
                                                      const u32* __restrict__ DB, u32 R, u32 s, u32 chunk, DevTab T) {
-    extern __shared__ __align__(128) uint2 ringq[];  // [stage][1 + QB NC][kMacBlockQ / 2]
+    extern __shared__ __align__(128) uint2 ringq[];  // [stage][SG + QB NC][kMacBlockQ / 2]
     __shared__ __align__(8) unsigned long long full[kMacStages], empty[kMacStages];
-    constexpr u32 NSEG = 1 + QB * NC;
+    constexpr u32 NSEG = SG + QB * NC;
     constexpr u32 SEG = kMacBlockQ * 4;   // bytes per segment
     constexpr u32 SEGV = kMacBlockQ / 2;  // uint2 per segment
     const u32 N = T.N, Mm = T.Mm;
     const u32 nblk = N / kMacBlockQ;
+    const u32 ngrp = s / SG;
     u32 b = blockIdx.x;
-    const u32 sj = b % s;
-    b /= s;
+    const u32 sg0 = (b % ngrp) * SG;
+    b /= ngrp;
     const u32 blk = b % nblk;
     b /= nblk;
     const u32 k = b % Mm;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
     if (warp == 8) {  // producer
         if ((tid & 31) == 0) {
             const size_t dbs = (size_t)s * Mm * N;
-            const u32* dbase = DB + ((size_t)sj * Mm + k) * N + (size_t)blk * kMacBlockQ;
+            const u32* dbase = DB + ((size_t)sg0 * Mm + k) * N + (size_t)blk * kMacBlockQ;
             const size_t zs = (size_t)NC * zstride * N;
             const size_t zoff = (size_t)k * N + (size_t)blk * kMacBlockQ;
             for (u32 i = 0; i < rows; ++i) {
@@ -206,12 +209,14 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
                 uint2* buf = ringq + (size_t)st * NSEG * SEGV;
                 mbar_expect_tx(&full[st], SEG * NSEG);
                 const size_t r = r0 + i;
-                tma_bulk_g2s(buf, dbase + r * dbs, SEG, &full[st]);
+#pragma unroll
+                for (int g = 0; g < SG; ++g)
+                    tma_bulk_g2s(buf + g * SEGV, dbase + r * dbs + (size_t)g * Mm * N, SEG, &full[st]);
 #pragma unroll
                 for (int q = 0; q < QB; ++q)
 #pragma unroll
                     for (int c = 0; c < NC; ++c)
-                        tma_bulk_g2s(buf + (1 + q * NC + c) * SEGV, Zp.z[q] + zoff + r * zs + (size_t)c * zstride * N,
+                        tma_bulk_g2s(buf + (SG + q * NC + c) * SEGV, Zp.z[q] + zoff + r * zs + (size_t)c * zstride * N,
                                      SEG, &full[st]);
             }
         }
@@ -219,30 +224,39 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
     }
     const u32 p = T.a[k];
     const u64 pb = T.abar[k];
-    u32 accr[QB][NC][2];
+    u32 accr[QB][SG][NC][2];
 #pragma unroll
     for (int q = 0; q < QB; ++q)
 #pragma unroll
-        for (int c = 0; c < NC; ++c) accr[q][c][0] = accr[q][c][1] = 0;
+        for (int g = 0; g < SG; ++g)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) accr[q][g][c][0] = accr[q][g][c][1] = 0;
     for (u32 g0 = 0; g0 < rows; g0 += 16) {
         const u32 ge = min(rows, g0 + 16);
-        u64 g[QB][NC][2];
+        u64 acc64[QB][SG][NC][2];
 #pragma unroll
         for (int q = 0; q < QB; ++q)
 #pragma unroll
-            for (int c = 0; c < NC; ++c) g[q][c][0] = g[q][c][1] = 0;
+            for (int g = 0; g < SG; ++g)
+#pragma unroll
+                for (int c = 0; c < NC; ++c) acc64[q][g][c][0] = acc64[q][g][c][1] = 0;
         for (u32 i = g0; i < ge; ++i) {
             const u32 st = i % kMacStages;
             mbar_wait(&full[st], (i / kMacStages) & 1);
             const uint2* buf = ringq + (size_t)st * NSEG * SEGV;
-            const uint2 d = buf[tid];
+            uint2 d[SG];
+#pragma unroll
+            for (int g = 0; g < SG; ++g) d[g] = buf[g * SEGV + tid];
 #pragma unroll
             for (int q = 0; q < QB; ++q)
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
-                    const uint2 z = buf[(1 + q * NC + c) * SEGV + tid];
-                    g[q][c][0] += (u64)z.x * d.x;
-                    g[q][c][1] += (u64)z.y * d.y;
+                    const uint2 z = buf[(SG + q * NC + c) * SEGV + tid];
+#pragma unroll
+                    for (int g = 0; g < SG; ++g) {
+                        acc64[q][g][c][0] += (u64)z.x * d[g].x;
+                        acc64[q][g][c][1] += (u64)z.y * d[g].y;
+                    }
                 }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
@@ -251,20 +265,25 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
 #pragma unroll
         for (int q = 0; q < QB; ++q)
 #pragma unroll
-            for (int c = 0; c < NC; ++c)
+            for (int g = 0; g < SG; ++g)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) accr[q][c][e] = red32(accr[q][c][e] + bar64(g[q][c][e], p, pb), p);
+                for (int c = 0; c < NC; ++c)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        accr[q][g][c][e] = red32(accr[q][g][c][e] + bar64(acc64[q][g][c][e], p, pb), p);
     }
     if (rows == 0) return;
     const u32 n = blk * kMacBlockQ + 2 * tid;
 #pragma unroll
     for (int q = 0; q < QB; ++q)
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            unsigned long long* o = Zp.acc[q] + (((size_t)sj * 3 + c) * Mm + k) * N + n;
-            atomicAdd(o, (unsigned long long)accr[q][c][0]);
-            atomicAdd(o + 1, (unsigned long long)accr[q][c][1]);
-        }
+        for (int g = 0; g < SG; ++g)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                unsigned long long* o = Zp.acc[q] + (((size_t)(sg0 + g) * 3 + c) * Mm + k) * N + n;
+                atomicAdd(o, (unsigned long long)accr[q][g][c][0]);
+                atomicAdd(o + 1, (unsigned long long)accr[q][g][c][1]);
+            }
 }
 
 }  // namespace cwgpu

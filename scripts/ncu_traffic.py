@@ -32,8 +32,12 @@ first = {}
 for r in rows[2:]:
     name = r[h["Kernel Name"]].split("(")[0].split("<")[0].replace("void ", "").replace("cwgpu::", "").strip()
     first.setdefault(name, r)
-J = int(sys.argv[4]) if len(sys.argv) > 4 else 16
-Mm = int(sys.argv[5]) if len(sys.argv) > 5 else 11
+# the aux / MAC basis of this configuration, from the library itself (no stale labels)
+from paper_2202_07569_b200 import Context  # noqa: E402
+
+_info = Context(cfg.N, cfg.primes, cfg.t)
+_info.load_db(configs.perfect_map(range(2), cfg.m, cfg.k), None, n_total=cfg.n, m=cfg.m)
+J, Mm = _info.info().J, _info.info().Mm
 res = {"source": rep.split("/")[-1], "config": cname, "J": J, "Mm": Mm}
 P = None
 if "k_tensor_intt_r" in first:
@@ -46,7 +50,7 @@ for name, r in first.items():
     elif name == "k_ntt32r_sel3":
         key, units = name, grid
     elif name.startswith("k_round") and P:
-        key, units = "k_round_tc", P * 3 * cfg.N  # k_round_tma reports under the k_round_tc launch name
+        key, units = "k_round_tma", P * 3 * cfg.N
     elif name.startswith("k_mac2") and P:
         key, units = "k_mac", P * (cfg.s + 3) * Mm * cfg.N * 4
     elif name.startswith("k_ntt_mac"):

@@ -3,9 +3,11 @@
 # of the same bench command, and one ncu --set full capture of the hot kernels (4096-row run,
 # same per-launch sizes as the full C4 answer).  Everything is summarised on the box (the
 # .ncu-rep files are too large to bring back); outputs under gpurun_out/<tag>_*.
-TAG=${1:-r01}
+TAG=${1:-r02}
 mkdir -p gpurun_out
-python -m pytest tests -q -m gpu > gpurun_out/${TAG}_pytest_gpu.log 2>&1; tail -2 gpurun_out/${TAG}_pytest_gpu.log
+if [ -z "$SKIP_TESTS" ]; then
+    python -m pytest tests -q -m gpu > gpurun_out/${TAG}_pytest_gpu.log 2>&1; tail -2 gpurun_out/${TAG}_pytest_gpu.log
+fi
 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err || exit 1
 python scripts/bench_brief.py bench < gpurun_out/${TAG}_bench.json
 BCMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-verify"
