@@ -1194,8 +1194,8 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
             prepare(c, nodes, (size_t)cnt * per, nullptr, R, pk);
             u32* dl = c.tmp_idx.get<u32>((size_t)R * cnt * J);
             launch(c, k_arith_deltas, blocks((size_t)R * cnt, 128), 128, 0, (const u64*)nodes, R, cnt, c.T, dl);
-            launch(c, k_prep_factors, blocks((size_t)R * cnt * 2 * J * N, 256), 256, 0, (const u32*)pk, (const u32*)dl,
-                   R, cnt, c.T, np_prep);
+            launch(c, k_prep_factors, (size_t)R * cnt * 2 * J, 256, 0, (const u32*)pk, (const u32*)dl, cnt, c.T,
+                   np_prep);
         } else {
             prepare(c, nodes, per, nullptr, R * cnt, np_prep);
         }

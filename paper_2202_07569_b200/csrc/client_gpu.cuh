@@ -13,6 +13,7 @@
 #pragma once
 #include "devtab.h"
 #include "modarith.cuh"
+#include "kernels.cuh"
 
 namespace cwgpu {
 
@@ -212,69 +213,40 @@ __global__ void k_add64_strided(u64* __restrict__ a, const u64* __restrict__ src
 /// m_n = (sum_i floor(t y_i / q_i) + round(rem / q)) mod t, y_i = v_i (q / q_i)^-1 mod q_i,
 /// rem = sum_i (t y_i mod q_i) (q / q_i), rounding counted as the reference does (odd multiples).
 __global__ void k_dec_round(const u64* __restrict__ v, size_t count, DevTab T, u64* __restrict__ out) {
-    const u32 N = T.N, L = T.L, QW = T.QW;
+    const u32 N = T.N, L = T.L;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= count * N) return;
     const size_t b = idx / N;
     const u32 n = (u32)(idx % N);
     const u64 t = T.t;
-    u32 rem[kQW + 3];
-#pragma unroll
-    for (int w = 0; w < kQW + 3; ++w) rem[w] = 0;
-    u64 qsum = 0;
+    u64 r[kMaxL];
+    u64 qsum = 0, lo = 0;
+    u32 ip = 0;
 #pragma unroll
     for (int i = 0; i < kMaxL; ++i) {
-        if (i >= (int)L) break;
-        const u64 qi = T.q[i];
-        const u64 y = red64(shoup64(v[(b * L + i) * N + n], T.muq[i], T.muq_s[i], qi), qi);
-        // t y = fl q_i + r with fl < t: r by the 128-bit reduction, fl by exact division (q_i odd:
-        // fl = (t y - r) q_i^-1 mod 2^64, exact since fl < 2^64)
-        const u64 lo = t * y, hi = __umul64hi(t, y);
-        const u64 r = reduce128(hi, lo, qi, T.q_mu96[i]);
-        u64 qinv = qi;  // q_i^-1 mod 2^64 (Newton)
+        if (i < (int)L) {
+            const u64 qi = T.q[i];
+            const u64 y = red64(shoup64(v[(b * L + i) * N + n], T.muq[i], T.muq_s[i], qi), qi);
+            // t y = fl q_i + r_i with fl < t: r_i by the 128-bit reduction, fl by exact division
+            // (q_i odd: fl = (t y - r_i) q_i^-1 mod 2^64, exact since fl < 2^64)
+            const u64 tl = t * y, th = __umul64hi(t, y);
+            r[i] = reduce128(th, tl, qi, T.q_mu96[i]);
+            u64 qinv = qi;  // q_i^-1 mod 2^64 (Newton)
 #pragma unroll
-        for (int it = 0; it < 5; ++it) qinv *= 2 - qi * qinv;
-        const u64 fl = (lo - r) * qinv;
-        qsum = (qsum + fl % t) % t;
-        // rem += r (q / q_i), 32-bit limbs
-        const u32 r0 = (u32)r, r1 = (u32)(r >> 32);
-        const u32* qo = T.qov + (size_t)i * QW;
-        u64 carry = 0;
-#pragma unroll
-        for (int w = 0; w < kQW + 2; ++w) {
-            const u64 a0 = w < (int)QW ? (u64)qo[w] * r0 : 0;
-            const u64 a1 = (w >= 1 && w - 1 < (int)QW) ? (u64)qo[w - 1] * r1 : 0;
-            const u64 s = (u64)rem[w] + (a0 & 0xffffffffu) + (a1 & 0xffffffffu) + (carry & 0xffffffffu);
-            rem[w] = (u32)s;
-            carry = (s >> 32) + (a0 >> 32) + (a1 >> 32) + (carry >> 32);
+            for (int it = 0; it < 5; ++it) qinv *= 2 - qi * qinv;
+            qsum = (qsum + ((tl - r[i]) * qinv) % t) % t;
+            // fractional sum of r_i / q_i (the same estimate as the centred lift)
+            const u64 f = frac64(r[i], T.q_gh[i], T.q_gl[i]);
+            lo += f;
+            ip += (lo < f);
+        } else {
+            r[i] = 0;
         }
-        rem[kQW + 2] += (u32)carry;
     }
-    // 2 rem >= (2z - 1) q for z = 1, 2, ...: count them (rem < L q)
-    u32 two[kQW + 3];
-    u32 cy = 0;
-#pragma unroll
-    for (int w = 0; w < kQW + 3; ++w) {
-        two[w] = (rem[w] << 1) | cy;
-        cy = rem[w] >> 31;
-    }
-    u64 round_add = 0;
-    for (u32 z = 1; z <= L; ++z) {
-        u32 mq[kQW + 3];
-        u64 c2 = 0;
-#pragma unroll
-        for (int w = 0; w < kQW + 3; ++w) {
-            const u64 s = (w < (int)QW ? (u64)T.qw[w] * (2 * z - 1) : 0) + c2;
-            mq[w] = (u32)s;
-            c2 = s >> 32;
-        }
-        int cmp = 0;
-#pragma unroll
-        for (int w = kQW + 2; w >= 0; --w)
-            if (cmp == 0) cmp = two[w] > mq[w] ? 1 : (two[w] < mq[w] ? -1 : 0);
-        if (cmp >= 0) ++round_add;
-        else break;
-    }
+    // round(rem / q), rem = sum_i r_i (q / q_i): crt_round decides from the 64-bit fraction and
+    // falls back to the exact multiword comparison inside its error band (the reference counts
+    // odd multiples of q below 2 rem, bfv.cpp:581-590: the same round-half-up)
+    const u32 round_add = crt_round(r, ip, lo, T);
     out[idx] = (qsum + round_add) % t;
 }
 

@@ -742,11 +742,17 @@ __global__ void k_partial_mod(const u64* __restrict__ partial, size_t total, Dev
 /// X layout [G][xs][N] (the first Mm planes of each group of xs); out layout [G][L][N].
 __global__ void __launch_bounds__(128) k_mac_to_chain(const u32* __restrict__ X, u32 xs, u32 G, DevTab T,
                                                       u64* __restrict__ out) {
-    // per-prime constants in shared memory (they were Mm L global loads per coefficient)
-    __shared__ u64 sMc[kMaxJ * kMaxL], sMF[kMaxJ], sQ[kMaxL], sMu[kMaxL], sNeg[kMaxL];
+    // per-prime constants in shared memory, M / m_k mod q_i split into 30-bit halves: every product
+    // is a 32 x 32 -> 64-bit IMAD.WIDE (< 2^60) and 16 of them fit one u64 accumulator
+    __shared__ u32 sMl[kMaxJ * kMaxL], sMh[kMaxJ * kMaxL];
+    __shared__ u64 sMF[kMaxJ], sQ[kMaxL], sMu[kMaxL], sNeg[kMaxL];
     __shared__ u32 sA[kMaxJ], sH[kMaxJ], sHs[kMaxJ];
     const u32 N = T.N, Mm = T.Mm, L = T.L;
-    for (u32 x = threadIdx.x; x < Mm * L; x += blockDim.x) sMc[x] = T.Mconv[x];
+    for (u32 x = threadIdx.x; x < Mm * L; x += blockDim.x) {
+        const u64 v = T.Mconv[x];
+        sMl[x] = (u32)(v & ((1u << 30) - 1));
+        sMh[x] = (u32)(v >> 30);
+    }
     for (u32 k = threadIdx.x; k < Mm; k += blockDim.x) {
         sMF[k] = T.mF[k];
         sA[k] = T.a[k];
@@ -763,10 +769,10 @@ __global__ void __launch_bounds__(128) k_mac_to_chain(const u32* __restrict__ X,
     if (idx >= (size_t)G * N) return;
     const size_t g = idx / N;
     const u32 n = (u32)(idx % N);
-    // acc_i = sum_k v_k (M / m_k mod q_i), 128-bit, gamma = round(sum_k v_k / m_k)
-    u64 hi[kMaxL], lo[kMaxL];
+    // acc_i = sum_k v_k (M / m_k mod q_i) as lo + hi 2^30 (+ 128-bit spill every 16 terms)
+    u64 alo[kMaxL], ahi[kMaxL], shi[kMaxL], slo[kMaxL];
 #pragma unroll
-    for (int i = 0; i < kMaxL; ++i) hi[i] = lo[i] = 0;
+    for (int i = 0; i < kMaxL; ++i) alo[i] = ahi[i] = shi[i] = slo[i] = 0;
     u64 gs = 0;
     for (u32 k = 0; k < Mm; ++k) {
         const u32 a = sA[k];
@@ -774,15 +780,32 @@ __global__ void __launch_bounds__(128) k_mac_to_chain(const u32* __restrict__ X,
         gs += (u64)v * sMF[k];
 #pragma unroll
         for (int i = 0; i < kMaxL; ++i)
-            if (i < (int)L) mac128(hi[i], lo[i], v, sMc[k * L + i]);
+            if (i < (int)L) {
+                alo[i] += (u64)v * sMl[k * L + i];
+                ahi[i] += (u64)v * sMh[k * L + i];
+            }
+        if ((k & 15) == 15) {  // spill to 128 bits before the accumulators could overflow
+#pragma unroll
+            for (int i = 0; i < kMaxL; ++i)
+                if (i < (int)L) {
+                    u64 h2 = 0, l2 = alo[i];
+                    mac128(h2, l2, ahi[i], 1ull << 30);
+                    slo[i] += l2;
+                    shi[i] += h2 + (slo[i] < l2);
+                    alo[i] = ahi[i] = 0;
+                }
+        }
     }
     const u32 gsh = 64 - T.gbits;
     const u32 gamma = (u32)((gs + (1ull << (gsh - 1))) >> gsh);
 #pragma unroll
     for (int i = 0; i < kMaxL; ++i) {
         if (i < (int)L) {
-            mac128(hi[i], lo[i], gamma, sNeg[i]);
-            out[(g * L + i) * N + n] = reduce128(hi[i], lo[i], sQ[i], sMu[i]);
+            u64 hi = shi[i], lo = slo[i];
+            mac128(hi, lo, alo[i], 1ull);
+            mac128(hi, lo, ahi[i], 1ull << 30);
+            mac128(hi, lo, gamma, sNeg[i]);
+            out[(g * L + i) * N + n] = reduce128(hi, lo, sQ[i], sMu[i]);
         }
     }
 }
@@ -856,23 +879,27 @@ __global__ void k_arith_deltas(const u64* __restrict__ nodes, u32 R, u32 k, DevT
 }
 
 /// Prepared factors [R][k][2][J][N] from the prepared k' [R][2][J][N] (NTT form, Montgomery) and
-/// the per-factor constants delta (component 0 only).
-__global__ void k_prep_factors(const u32* __restrict__ pk, const u32* __restrict__ delta, u32 R, u32 k, DevTab T,
-                               u32* __restrict__ out) {
+/// the per-factor constants delta (component 0 only).  Block = one (row, factor, component, prime)
+/// plane (indices decoded once), threads copy it as uint4.
+__global__ void __launch_bounds__(256) k_prep_factors(const u32* __restrict__ pk, const u32* __restrict__ delta, u32 k,
+                                                      DevTab T, u32* __restrict__ out) {
     const u32 J = T.J, N = T.N;
-    const size_t JN = (size_t)J * N;
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (size_t)R * k * 2 * JN) return;
-    const size_t x = idx % (2 * JN);
-    const size_t rf = idx / (2 * JN);
-    const u32 r = (u32)(rf / k);
-    const u32 comp = (u32)(x / JN), j = (u32)((x / N) % J);
-    u32 v = pk[(size_t)r * 2 * JN + x];
-    if (comp == 0) {
-        const u32 a = T.a[j];
-        v = red32(v + delta[rf * J + j], a);
+    const u32 plane = blockIdx.x;  // ((r k + f) 2 + comp) J + j
+    const u32 j = plane % J, comp = (plane / J) % 2, rf = plane / (2 * J), r = rf / k;
+    const uint4* src = reinterpret_cast<const uint4*>(pk + (((size_t)r * 2 + comp) * J + j) * N);
+    uint4* dst = reinterpret_cast<uint4*>(out + (size_t)plane * N);
+    const u32 a = T.a[j];
+    const u32 d = comp == 0 ? delta[(size_t)rf * J + j] : 0u;
+    for (u32 x = threadIdx.x; x < N / 4; x += blockDim.x) {
+        uint4 v = src[x];
+        if (comp == 0) {
+            v.x = red32(v.x + d, a);
+            v.y = red32(v.y + d, a);
+            v.z = red32(v.z + d, a);
+            v.w = red32(v.w + d, a);
+        }
+        dst[x] = v;
     }
-    out[idx] = v;
 }
 
 /// Multiply every coefficient of B 2-comp ciphertexts by c mod q_i (plain_mul by a

@@ -148,17 +148,20 @@ __global__ void __launch_bounds__(128, MINB) k_ks_mac32s(const u32* __restrict__
                 u32* op = out + ((size_t)b * nci + c0) * KN + slot;
 #pragma unroll
                 for (int c = 0; c < CI; ++c) {
-                    u64 s = 0;
+                    // two independent chains (even / odd digits), each < 15 products < 2^64
+                    u64 s0 = 0, s1 = 0;
                     u32 r = 0;
 #pragma unroll
-                    for (int d = 0; d < D; ++d) {
-                        s += (u64)dr[d] * kr[d][c];
-                        if (d % 15 == 14 && d + 1 < D) {
-                            r += bar64(s, a, mu);  // < 2 a after two chunks
-                            s = 0;
+                    for (int d = 0; d < D; d += 2) {
+                        s0 += (u64)dr[d] * kr[d][c];
+                        if (d + 1 < D) s1 += (u64)dr[d + 1] * kr[d + 1][c];
+                        if (d % 28 == 26 && d + 2 < D) {  // 14 products per chain
+                            r += bar64(s0, a, mu);
+                            r += bar64(s1, a, mu);
+                            s0 = s1 = 0;
                         }
                     }
-                    if (c0 + c < nci) op[(u32)c * KN] = bar64(s + r, a, mu);
+                    if (c0 + c < nci) op[(u32)c * KN] = red32(bar64(s0, a, mu) + bar64(s1 + r, a, mu), a);
                 }
             }
         }

@@ -5,7 +5,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2202_07569_b200 import Client, Context, configs
 import oracle
 
-for name in ("C1", "C4"):
+for name in ("C1", "C4", "C5"):
     cfg = configs.config(name)
     client = Client(cfg.N, cfg.primes, cfg.t, seed=7, galois_levels=1)
     sec = client.secret()
