@@ -608,6 +608,13 @@ def main():
         verified = bool(dec_ok and e2e_eq)
         verify_detail = {"decrypt_equals_row": bool(dec_ok), "e2e_response_equals_device_response": e2e_eq}
 
+    # N > 1: per-rank phase times of one more answer (outside the timed region)
+    rank_rows = None
+    if world > 1:
+        mine = rs.phase_times(dq.data_ptr(), dout.data_ptr())
+        rank_rows = [None] * world
+        dist.all_gather_object(rank_rows, mine)
+
     # per-kernel device times (profiling pass, outside the timed region)
     ctx.set_profiling(True)
     tm = CwgTimings_type()
@@ -659,6 +666,8 @@ def main():
         "verify_detail": verify_detail,
         "db_load_s": t_load,
     }
+    if rank_rows:
+        line["ranks"] = rank_rows
     if world == 1 and not args.no_cpu_baseline:
         try:
             import oracle

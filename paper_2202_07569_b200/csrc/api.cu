@@ -854,8 +854,10 @@ static bool ks32_ready(Ctx& c) {
     return true;
 }
 
-static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B, const u64* key, u32 bits,
-                       u32 D, u64* ks) {
+/// add / add_stride / scale (aux-prime path only, see k_ks_crt): fused relinearisation add and
+/// constant scaling; returns true when they were applied.
+static bool key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B, const u64* key, u32 bits,
+                       u32 D, u64* ks, const u64* add = nullptr, size_t add_stride = 0, u64 scale = 0) {
     const u32 N = c.cp.N, L = c.cp.L;
     if (ks32_ready(c)) {
         const bool rel = key == c.relin.ptr<u64>();
@@ -900,8 +902,9 @@ static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
                 launch(c, k_ks_mac32, blocks((size_t)B * 2 * L * K * N, 256), 256, 0, (const u32*)dA, kA, B, D, L, N, C,
                        (const u64*)c.T.abar, mA);
             ntt32(c, mA, B * 2 * L * K, K, K, 0, true, 0);
-            launch(c, k_ks_crt, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u32*)mA, B, L, N, C, c.T, ks);
-            return;
+            launch(c, k_ks_crt, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u32*)mA, B, L, N, C, c.T, ks, add,
+                   add_stride, scale);
+            return true;
         }
     }
     u64* dig = c.digits.get<u64>((size_t)B * D * N);
@@ -911,6 +914,7 @@ static void key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
     launch_named(c, "k_ntt64_digits", k_ntt64<false, true>, (size_t)B * D * L, ntt_block(N), N * 8, dn, (const u64*)dig, c.T);
     launch(c, k_ks_mac, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u64*)dn, key, B, D, c.T, ks);
     ntt64(c, ks, B * 2 * L, true);
+    return false;
 }
 
 static size_t ks_chunk(const Ctx& c, u32 D) {
@@ -919,17 +923,23 @@ static size_t ks_chunk(const Ctx& c, u32 D) {
     return std::max<size_t>(1, (size_t(1536) << 20) / per);
 }
 
-/// relinearize count 3-comp cts (stride 3LN) into out2 [count][2][L][N].
-static void relinearize(Ctx& c, const u64* ct3, u32 count, u64* out2) {
+/// relinearize count 3-comp cts (stride 3LN) into out2 [count][2][L][N]; scale != 0 multiplies the
+/// result by that constant (fused into the key switch's CRT on the aux-prime path).
+static void relinearize(Ctx& c, const u64* ct3, u32 count, u64* out2, u64 scale = 0) {
     const size_t LN = (size_t)c.cp.L * c.cp.N;
     const size_t chunk = ks_chunk(c, c.cp.Dr);
     for (u32 b0 = 0; b0 < count; b0 += (u32)chunk) {
         const u32 B = (u32)std::min<size_t>(chunk, count - b0);
+        const u64* c3 = ct3 + (size_t)b0 * 3 * LN;
+        u64* o2 = out2 + (size_t)b0 * 2 * LN;
+        // the aux-prime key switch writes (c0 + ks0, c1 + ks1) straight into out2
+        if (key_switch(c, c3 + 2 * LN, 3 * LN, 0, B, c.relin.ptr<u64>(), c.cp.relin_bits, c.cp.Dr, o2, c3, 3 * LN,
+                       scale))
+            continue;
         u64* ks = c.ks.get<u64>((size_t)B * 2 * LN);
-        key_switch(c, ct3 + (size_t)b0 * 3 * LN + 2 * LN, 3 * LN, 0, B, c.relin.ptr<u64>(), c.cp.relin_bits,
-                   c.cp.Dr, ks);
-        launch(c, k_relin_add, blocks((size_t)B * 2 * LN, 256), 256, 0, ct3 + (size_t)b0 * 3 * LN, 3 * LN,
-               (const u64*)ks, B, c.T, out2 + (size_t)b0 * 2 * LN);
+        CK(cudaMemcpyAsync(ks, o2, (size_t)B * 2 * LN * 8, cudaMemcpyDeviceToDevice, c.st));
+        launch(c, k_relin_add, blocks((size_t)B * 2 * LN, 256), 256, 0, c3, 3 * LN, (const u64*)ks, B, c.T, o2);
+        if (scale) launch(c, k_scale_const, blocks((size_t)B * 2 * LN, 256), 256, 0, o2, B, scale, c.T);
     }
 }
 
@@ -1180,6 +1190,15 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
                nodes);
     }
     const bool lazy_root = (op == CWG_OP_FOLKLORE);
+    // arithmetic operator: the root gets plain_mul((k!)^-1) (eq_circuits.cpp:126), fused into the
+    // last relinearisation
+    u64 kinv = 0;
+    if (op == CWG_OP_ARITH) {
+        u64 f = 1;
+        for (u32 i = 2; i <= k; ++i) f = mulmod64(f, i % c.cp.t, c.cp.t);
+        if (f == 0) throw std::invalid_argument("k! is not invertible mod t");
+        kinv = invmod64(f, c.cp.t);
+    }
     // product_tree (eq_circuits.cpp:53-69)
     bool first = true;
     while (cnt > 1) {
@@ -1217,7 +1236,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         mul_prepared(c, np_prep, di, np_prep, di + (size_t)R * np, R * np, false, c3);
         u64* nn = nbuf[cur ^ 1]->get<u64>((size_t)R * ncnt * per);
         if (cnt % 2 == 0) {
-            relinearize(c, c3, R * np, nn);
+            relinearize(c, c3, R * np, nn, last ? kinv : 0);
         } else {
             u64* rl = c.resp3.get<u64>((size_t)R * np * per);
             relinearize(c, c3, R * np, rl);
@@ -1229,14 +1248,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         cur ^= 1;
         cnt = ncnt;
     }
-    // root is a 2-comp ciphertext: arithmetic operator -> plain_mul((k!)^-1) (eq_circuits.cpp:126)
-    if (op == CWG_OP_ARITH) {
-        u64 f = 1;
-        for (u32 i = 2; i <= k; ++i) f = mulmod64(f, i % c.cp.t, c.cp.t);
-        if (f == 0) throw std::invalid_argument("k! is not invertible mod t");
-        const u64 kinv = invmod64(f, c.cp.t);
-        launch(c, k_scale_const, blocks((size_t)R * 2 * LN, 256), 256, 0, nodes, R, kinv, c.T);
-    }
+    // (the arithmetic root's plain_mul((k!)^-1) was applied by the last relinearisation)
     if (chain_sel) {
         launch(c, k_gather_strided, blocks((size_t)R * per, 256), 256, 0, (const u64*)nodes, per, (const u32*)nullptr, R,
                per, chain_sel, 3 * LN);

@@ -740,10 +740,12 @@ __global__ void k_partial_mod(const u64* __restrict__ partial, size_t total, Dev
 
 /// MAC basis -> chain: X (coefficient form, centred |X| < M/2) -> out[g][i][n] mod q_i.
 /// X layout [G][xs][N] (the first Mm planes of each group of xs); out layout [G][L][N].
+constexpr int kMacToChainMm = 20;  // MAC-basis sizes handled with the residues in registers
 __global__ void __launch_bounds__(128) k_mac_to_chain(const u32* __restrict__ X, u32 xs, u32 G, DevTab T,
                                                       u64* __restrict__ out) {
     // per-prime constants in shared memory, M / m_k mod q_i split into 30-bit halves: every product
-    // is a 32 x 32 -> 64-bit IMAD.WIDE (< 2^60) and 16 of them fit one u64 accumulator
+    // is a 32 x 32 -> 64-bit IMAD.WIDE (< 2^60) and 16 of them fit one u64 accumulator.  The Mm
+    // residues stay in registers and each output prime is one short dot product (low register use).
     __shared__ u32 sMl[kMaxJ * kMaxL], sMh[kMaxJ * kMaxL];
     __shared__ u64 sMF[kMaxJ], sQ[kMaxL], sMu[kMaxL], sNeg[kMaxL];
     __shared__ u32 sA[kMaxJ], sH[kMaxJ], sHs[kMaxJ];
@@ -769,43 +771,62 @@ __global__ void __launch_bounds__(128) k_mac_to_chain(const u32* __restrict__ X,
     if (idx >= (size_t)G * N) return;
     const size_t g = idx / N;
     const u32 n = (u32)(idx % N);
-    // acc_i = sum_k v_k (M / m_k mod q_i) as lo + hi 2^30 (+ 128-bit spill every 16 terms)
-    u64 alo[kMaxL], ahi[kMaxL], shi[kMaxL], slo[kMaxL];
+    const u32 gsh = 64 - T.gbits;
+    if (Mm <= (u32)kMacToChainMm) {
+        u32 v[kMacToChainMm];
+        u64 gs = 0;
 #pragma unroll
-    for (int i = 0; i < kMaxL; ++i) alo[i] = ahi[i] = shi[i] = slo[i] = 0;
+        for (int k = 0; k < kMacToChainMm; ++k) {
+            if (k < (int)Mm) {
+                const u32 a = sA[k];
+                v[k] = red32(shoup32(X[(g * xs + k) * N + n], sH[k], sHs[k], a), a);
+                gs += (u64)v[k] * sMF[k];
+            } else {
+                v[k] = 0;
+            }
+        }
+        const u32 gamma = (u32)((gs + (1ull << (gsh - 1))) >> gsh);
+        for (u32 i = 0; i < L; ++i) {
+            u64 lo0 = 0, hi0 = 0, lo1 = 0, hi1 = 0;  // two chains of <= 10 products each
+#pragma unroll
+            for (int k = 0; k < kMacToChainMm; k += 2) {
+                if (k < (int)Mm) {
+                    lo0 += (u64)v[k] * sMl[k * L + i];
+                    hi0 += (u64)v[k] * sMh[k * L + i];
+                }
+                if (k + 1 < (int)Mm) {
+                    lo1 += (u64)v[k + 1] * sMl[(k + 1) * L + i];
+                    hi1 += (u64)v[k + 1] * sMh[(k + 1) * L + i];
+                }
+            }
+            u64 hi = 0, lo = lo0;
+            mac128(hi, lo, lo1, 1ull);
+            mac128(hi, lo, hi0, 1ull << 30);
+            mac128(hi, lo, hi1, 1ull << 30);
+            mac128(hi, lo, gamma, sNeg[i]);
+            out[(g * L + i) * N + n] = reduce128(hi, lo, sQ[i], sMu[i]);
+        }
+        return;
+    }
+    // larger MAC bases: accumulate per output prime in 128 bits
+    u64 hi[kMaxL], lo[kMaxL];
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) hi[i] = lo[i] = 0;
     u64 gs = 0;
     for (u32 k = 0; k < Mm; ++k) {
         const u32 a = sA[k];
-        const u32 v = red32(shoup32(X[(g * xs + k) * N + n], sH[k], sHs[k], a), a);
-        gs += (u64)v * sMF[k];
+        const u32 vk = red32(shoup32(X[(g * xs + k) * N + n], sH[k], sHs[k], a), a);
+        gs += (u64)vk * sMF[k];
 #pragma unroll
         for (int i = 0; i < kMaxL; ++i)
-            if (i < (int)L) {
-                alo[i] += (u64)v * sMl[k * L + i];
-                ahi[i] += (u64)v * sMh[k * L + i];
-            }
-        if ((k & 15) == 15) {  // spill to 128 bits before the accumulators could overflow
-#pragma unroll
-            for (int i = 0; i < kMaxL; ++i)
-                if (i < (int)L) {
-                    u64 h2 = 0, l2 = alo[i];
-                    mac128(h2, l2, ahi[i], 1ull << 30);
-                    slo[i] += l2;
-                    shi[i] += h2 + (slo[i] < l2);
-                    alo[i] = ahi[i] = 0;
-                }
-        }
+            if (i < (int)L) mac128(hi[i], lo[i], vk, ((u64)sMh[k * L + i] << 30) | sMl[k * L + i]);
     }
-    const u32 gsh = 64 - T.gbits;
     const u32 gamma = (u32)((gs + (1ull << (gsh - 1))) >> gsh);
 #pragma unroll
     for (int i = 0; i < kMaxL; ++i) {
         if (i < (int)L) {
-            u64 hi = shi[i], lo = slo[i];
-            mac128(hi, lo, alo[i], 1ull);
-            mac128(hi, lo, ahi[i], 1ull << 30);
-            mac128(hi, lo, gamma, sNeg[i]);
-            out[(g * L + i) * N + n] = reduce128(hi, lo, sQ[i], sMu[i]);
+            mac128(hi[i], lo[i], gamma, sNeg[i]);
+            out[(g * L + i) * N + n] = reduce128(hi[i], lo[i], sQ[i], sMu[i]);
         }
     }
 }

@@ -169,8 +169,11 @@ __global__ void __launch_bounds__(128, MINB) k_ks_mac32s(const u32* __restrict__
 }
 
 /// ks[b][c][i][n] = (centred CRT of the K' residues x_j) mod q_i.  x: [B][2][L][K'][N] in [0, a_j).
+/// add (optional): the result is (ks + add[b * add_stride + (c L + i) N + n]) mod q_i -- the
+/// relinearisation's (c0 + ks0, c1 + ks1), bfv.cpp:859-869 -- and scale (optional, != 0) then
+/// multiplies it by a constant mod q_i (the arithmetic operator's (k!)^-1, eq_circuits.cpp:126).
 __global__ void k_ks_crt(const u32* __restrict__ x, u32 B, u32 L, u32 N, const __grid_constant__ KsCrt C, DevTab T,
-                         u64* __restrict__ ks) {
+                         u64* __restrict__ ks, const u64* __restrict__ add, size_t add_stride, u64 scale) {
     const u32 K = C.K;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)B * 2 * L * N) return;
@@ -182,7 +185,8 @@ __global__ void k_ks_crt(const u32* __restrict__ x, u32 B, u32 L, u32 N, const _
     // Garner: y_j = ((x_j - y_0) c_0j - y_1) c_1j ... mod a_j
 #pragma unroll
     for (int jj = 0; jj < kMaxKs; ++jj) {
-        if (jj >= (int)K) break;
+        y[jj] = 0;
+        if (jj >= (int)K) continue;
         const u32 a = C.a[jj];
         u32 t = xp[(size_t)jj * N];
 #pragma unroll
@@ -196,12 +200,22 @@ __global__ void k_ks_crt(const u32* __restrict__ x, u32 B, u32 L, u32 N, const _
     }
     // centred: v > (A'-1)/2 <=> mixed-radix digits (top first) exceed the half digits
     int cmp = 0;
-    for (int jj = (int)K - 1; jj >= 0 && cmp == 0; --jj) cmp = y[jj] > C.half[jj] ? 1 : (y[jj] < C.half[jj] ? -1 : 0);
+#pragma unroll
+    for (int jj = kMaxKs - 1; jj >= 0; --jj)
+        if (jj < (int)K && cmp == 0) cmp = y[jj] > C.half[jj] ? 1 : (y[jj] < C.half[jj] ? -1 : 0);
     const u64 q = T.q[i];
     u64 hi = 0, lo = 0;
-    for (u32 jj = 0; jj < K; ++jj) mac128(hi, lo, (u64)y[jj], C.pmod[i][jj]);
+#pragma unroll
+    for (int jj = 0; jj < kMaxKs; ++jj)
+        if (jj < (int)K) mac128(hi, lo, (u64)y[jj], C.pmod[i][jj]);
     u64 v = reduce128(hi, lo, q, T.q_mu96[i]);
     if (cmp > 0) v = v >= C.amod[i] ? v - C.amod[i] : v + q - C.amod[i];
+    if (add) {
+        const size_t b = bci / (2 * L), ci = bci % (2 * L);
+        v += add[b * add_stride + ci * N + n];
+        if (v >= q) v -= q;
+    }
+    if (scale) v = reduce128(__umul64hi(v, scale), v * scale, q, T.q_mu96[i]);
     ks[idx] = v;
 }
 

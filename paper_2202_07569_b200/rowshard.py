@@ -81,6 +81,41 @@ class RowShardStep:
                                         keys_ptrs=keys_ptrs)
         self._reduce()
 
+    def phase_times(self, q_ptr, out_ptr):
+        """One answer with the phases timed on this rank (host wall clock around synchronised
+        phases; diagnostics outside the timed region): ms for expansion (shard), the all-gather,
+        the rows (selection + MAC), the reduction and, on rank 0, the finish."""
+        import time
+
+        cfg, t, torch = self.cfg, {}, self.torch
+
+        def mark(name, t0):
+            torch.cuda.synchronize()
+            t[name] = (time.perf_counter() - t0) * 1e3
+            return time.perf_counter()
+
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if self.shard:
+            self.ctx.expand_shard_ptr(q_ptr, cfg.c, self.world, self.rank, self.shard_local.data_ptr())
+            t0 = mark("expand_shard_ms", t0)
+            self._all_gather()
+            t0 = mark("all_gather_ms", t0)
+            self.ctx.answer_partial_shards_ptr(self.shards_all.data_ptr(), self.world, cfg.c, cfg.m, cfg.op,
+                                               self.partial.data_ptr())
+            t0 = mark("rows_ms", t0)
+        else:
+            self.ctx.answer_partial_ptr(q_ptr, self.h_q, cfg.c, cfg.m, cfg.op, self.partial.data_ptr())
+            t0 = mark("expand_and_rows_ms", t0)
+        self._reduce()
+        t0 = mark("reduce_ms", t0)
+        if self.rank == 0:
+            self.ctx.finish(self.partial.data_ptr(), cfg.op, out=out_ptr)
+            mark("finish_ms", t0)
+        info = self.ctx.info()
+        return {"rank": self.rank, "rows": int(info.n_local), "row_begin": int(info.row_begin),
+                **{k: round(v, 3) for k, v in t.items()}}
+
     def step(self, q_ptr, out_ptr, keys_ptrs=(None, 0, None, None)):
         """One whole answer; rank 0 writes the response to out_ptr (host or device)."""
         self.partial_step(q_ptr, keys_ptrs)
