@@ -117,7 +117,8 @@ struct Ctx {
     bool force_exact = false;  // "force_exact": every rounding / lift decision through the multiword path (tests)
     // key switching through the 30-bit aux primes ("ks32" = 0: the 64-bit NTT path)
     bool ks32 = true;
-    bool ks_wide = true;  // "ks_wide": shared-load key-switch MAC also for 16 < D <= 32 digits
+    bool ks_wide = true;  // "ks_wide": slot-major key-switch MAC (k_ks_mac32s) for D = 7 / 14 / 25
+    u32 ks_ci = 4;        // "ks_ci": key columns held per thread in k_ks_mac32s (2: smaller, unrolled rows)
     int prep_mode = 1;    // "prep_factors": 1 prepare k' once for the arithmetic factors, 0 each factor
     bool mac_sg = true;   // "mac_sg": s >= 3 payload MAC with 3 or 5 slices per CTA (0: k_mac_tma, one slice)
     bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
@@ -893,7 +894,9 @@ static bool key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
                 launch_grid(c, "k_ks_mac32", kern, cfg, (const u32*)dA, kA, B, L, N, C, (const u64*)c.T.abar, mA);
             };
             if (c.ks_wide && D == 7) ks_s(k_ks_mac32s<7, 6, 8, 3>);
+            else if (c.ks_wide && D == 14 && c.ks_ci == 2) ks_s(k_ks_mac32s<14, 2, 8, 4, 2>);
             else if (c.ks_wide && D == 14) ks_s(k_ks_mac32s<14, 5, 8, 2>);
+            else if (c.ks_wide && D == 25 && c.ks_ci == 2) ks_s(k_ks_mac32s<25, 2, 8, 3, 2>);
             else if (c.ks_wide && D == 25) ks_s(k_ks_mac32s<25, 4, 8, 2>);
             else if (D <= (u32)kKsDmax && B >= 64)
                 launch_named(c, "k_ks_mac32", k_ks_mac32x<kKsDmax>, blocks((size_t)((B + 1) / 2) * K * N, 128), 128, 0,
@@ -2568,6 +2571,7 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "ks32") { c.ks32 = v != 0; c.ksA_ok = false; }
         else if (k == "tile_rows") c.tile_rows_opt = (u32)std::max(0, v);
         else if (k == "ks_wide") c.ks_wide = v != 0;
+        else if (k == "ks_ci") c.ks_ci = v == 2 ? 2u : 4u;
         else if (k == "prep_factors") c.prep_mode = v != 0;
         else if (k == "mac_sg") c.mac_sg = v != 0;
         else if (k == "force_exact") {

@@ -274,10 +274,79 @@ __device__ __forceinline__ u32 crt_round(const u64* y, u32 ip, u64 frac, const D
 /// digits: [B][D][N].
 /// AUX (key switching through the aux primes, ks32.cuh): digit d is written as its residues
 /// mod the first K aux primes, u32 [B][D][K][N] at aux_out (digits < 2^29 need no reduction).
+/// crt_exact with the limb products accumulated column-wise (independent across limbs: no
+/// carry chain through the L x 2 x QW products, one carry pass at the end) and the q / q_i limbs
+/// read from shared memory (sqov [L][QW], sqw [QW]).
+__device__ __forceinline__ void crt_exact_cols(const u64* y, u32 alpha_est, const DevTab& T, const u32* sqov,
+                                               const u32* sqw, u32* X) {
+    const u32 QW = T.QW, L = T.L;
+    u64 col[kQW + 2];
+#pragma unroll
+    for (int w = 0; w < kQW + 2; ++w) col[w] = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxL; ++i) {
+        if (i >= (int)L) break;
+        const u32 y0 = (u32)y[i], y1 = (u32)(y[i] >> 32);
+#pragma unroll
+        for (int w = 0; w < kQW; ++w) {
+            if (w < (int)QW) {
+                const u32 qv = sqov[i * QW + w];
+                const u64 p0 = (u64)y0 * qv, p1 = (u64)y1 * qv;
+                col[w] += (u32)p0;
+                col[w + 1] += (p0 >> 32) + (u32)p1;
+                col[w + 2] += p1 >> 32;
+            }
+        }
+    }
+    // carried sum S, then X = S - alpha_est q (alpha_est < 2^8) and one correction
+    u32 S[kQW + 2];
+    u64 carry = 0;
+#pragma unroll
+    for (int w = 0; w < kQW + 2; ++w) {
+        const u64 s = col[w] + carry;
+        S[w] = (u32)s;
+        carry = s >> 32;
+    }
+    u64 c = 0;
+    u32 bb = 0;
+#pragma unroll
+    for (int w = 0; w < kQW + 2; ++w) {
+        const u64 pk = (w < (int)QW ? (u64)alpha_est * sqw[w] : 0) + c;
+        c = pk >> 32;
+        const u32 pl = (u32)pk, x = S[w];
+        const u32 r1 = x - pl, b1 = x < pl;
+        const u32 r2 = r1 - bb, b2 = r1 < bb;
+        X[w] = r2;
+        bb = b1 | b2;
+    }
+    // one correction: X >= q -> X - q (the fractional estimate is short by at most one)
+    int ge = 1;
+#pragma unroll
+    for (int w = kQW + 1; w >= 0; --w) {
+        const u32 qv = w < (int)QW ? sqw[w] : 0u;
+        if (ge == 1 && X[w] != qv) ge = X[w] > qv ? 2 : 0;
+    }
+    if (ge != 0) {
+        u32 b2 = 0;
+#pragma unroll
+        for (int w = 0; w < kQW + 2; ++w) {
+            const u32 qv = w < (int)QW ? sqw[w] : 0u;
+            const u32 r1 = X[w] - qv, c1 = X[w] < qv;
+            const u32 r2 = r1 - b2, c2 = r1 < b2;
+            X[w] = r2;
+            b2 = c1 | c2;
+        }
+    }
+}
+
 template <bool AUX = false>
 __global__ void k_decompose_t(const u64* __restrict__ polys, size_t stride, u64 ginv, u32 B, u32 bits,
                               u32 D, DevTab T, u64* __restrict__ digits, u32* __restrict__ aux_out, u32 K) {
     const u32 N = T.N;
+    __shared__ u32 sqov[kMaxL * kQW], sqw[kQW];
+    for (u32 x = threadIdx.x; x < T.L * T.QW; x += blockDim.x) sqov[x] = T.qov[x];
+    for (u32 x = threadIdx.x; x < T.QW; x += blockDim.x) sqw[x] = T.qw[x];
+    __syncthreads();
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)B * N) return;
     const u32 b = (u32)(idx / N), n = (u32)(idx % N);
@@ -317,7 +386,7 @@ __global__ void k_decompose_t(const u64* __restrict__ polys, size_t stride, u64 
     u32 ip;
     crt_prepare(res, T, y, &ip);
     u32 X[kQW + 2];
-    crt_exact(y, ip, T, X);
+    crt_exact_cols(y, ip, T, sqov, sqw, X);
     if (bits == 16) {  // the configured digit width: limb and shift are compile-time per unrolled digit
 #pragma unroll
         for (int d = 0; d < 2 * kQW; ++d)

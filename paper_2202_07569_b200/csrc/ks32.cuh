@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(128) k_ks_mac32x(const u32* __restrict__ dig, 
 /// D digit loads, the key read once per group of G rows instead of once per output.  Products are
 /// < 2^60 (residues < 2^30), accumulated 15 at a time in u64 before a Barrett reduction.
 /// Grid: (ceil(K' N / 128), row splits); rows [b0, b1) of this split in groups of G.
-template <int D, int CI, int G, int MINB>
+template <int D, int CI, int G, int MINB, int UB = 1>
 __global__ void __launch_bounds__(128, MINB) k_ks_mac32s(const u32* __restrict__ dig, const u32* __restrict__ key, u32 B,
                                                       u32 L, u32 N, const __grid_constant__ KsCrt C,
                                                       const u64* __restrict__ abar, u32* __restrict__ out) {
@@ -139,8 +139,8 @@ __global__ void __launch_bounds__(128, MINB) k_ks_mac32s(const u32* __restrict__
 #pragma unroll
                 for (int c = 0; c < CI; ++c)
                     kr[d][c] = (c0 + c < nci) ? __ldg(kp + ((u32)d * nci + (u32)c) * KN) : 0u;
-#pragma unroll 1
-            for (u32 b = g0; b < g1; ++b) {
+#pragma unroll UB
+            for (u32 b = g0; b < g1; ++b) {  // UB > 1: the next rows' digit loads overlap this row's MACs
                 const u32* dp = dig + (size_t)b * D * KN + slot;
                 u32 dr[D];
 #pragma unroll
