@@ -118,7 +118,7 @@ struct Ctx {
     // key switching through the 30-bit aux primes ("ks32" = 0: the 64-bit NTT path)
     bool ks32 = true;
     bool ks_wide = true;  // "ks_wide": slot-major key-switch MAC (k_ks_mac32s) for D = 7 / 14 / 25
-    u32 ks_ci = 4;        // "ks_ci": key columns held per thread in k_ks_mac32s (2: smaller, unrolled rows)
+    u32 ks_ci = 2;        // "ks_ci": key columns held per thread in k_ks_mac32s (2 default: 4 CTAs / SM, unrolled rows; 4: wider, 2 CTAs / SM)
     int prep_mode = 1;    // "prep_factors": 1 prepare k' once for the arithmetic factors, 0 each factor
     bool mac_sg = true;   // "mac_sg": s >= 3 payload MAC with 3 or 5 slices per CTA (0: k_mac_tma, one slice)
     bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
