@@ -125,6 +125,14 @@ def rooflines(kstats, cfg, info, hbm, hbm_kind):
             ach = byt / per_launch_s / 1e9
             r = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "peak_kind": hbm_kind,
                  "work_per_launch": f"{units / cnt:.0f} coefficients x (J + Mm) x 4 B"}
+        elif name in ("k_ks_mac32", "k_lift", "k_mac_to_chain"):
+            # IMAD-bound dot products of 30-bit residues: k_ks_mac32 one IMAD.WIDE per digit product
+            # (units = products), k_lift 2 L per (coefficient, output prime), k_mac_to_chain 2 per
+            # (coefficient, MAC prime, chain prime) -- IMAD.WIDE = 2.4 IMAD slots
+            per = {"k_ks_mac32": 1, "k_lift": 2 * cfg.L, "k_mac_to_chain": 2}[name]
+            ach = units / cnt * per * 2.4 / per_launch_s / 1e9
+            r = {"bound": "imad", "achieved": ach, "peak": ip, "unit": "G IMAD-slots/s", "frac": ach / ip,
+                 "peak_kind": ip_kind, "work_per_launch": f"{units / cnt:.3e} units x {per} IMAD.WIDE x 2.4 slots"}
         elif name == "k_mac":
             byt = units / cnt  # selection planes + database planes, each read once
             ach = byt / per_launch_s / 1e9

@@ -890,7 +890,7 @@ static bool key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
                 cfg.gridDim = dim3(gx, gy);
                 cfg.blockDim = dim3(128);
                 cfg.stream = c.st;
-                c.next_units = (double)B * 2 * L * K;  // output planes
+                c.next_units = (double)B * 2 * L * K * N * D;  // residue products (MACs)
                 launch_grid(c, "k_ks_mac32", kern, cfg, (const u32*)dA, kA, B, L, N, C, (const u64*)c.T.abar, mA);
             };
             if (c.ks_wide && D == 7) ks_s(k_ks_mac32s<7, 6, 8, 3>);
@@ -1035,6 +1035,7 @@ static void expand_shard(Ctx& c, const u64* dquery, u32 comp, u32 W, u32 rank, u
 /// out [count][2][J][N].
 static void prepare(Ctx& c, const u64* src, size_t stride, const u32* sel, u32 count, u32* out) {
     const u32 N = c.cp.N, J = c.ab.J;
+    c.next_units = (double)count * 2 * N * J;  // coefficient lifts x output primes
     launch(c, k_lift, blocks((size_t)count * 2 * N, 256), 256, 0, src, stride, sel, count, J, 1, c.T, out, J);
     ntt32(c, out, count * 2 * J, J, J, 0, false, 0);
 }
@@ -1109,6 +1110,7 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         else if (c.JM == 32) launch_named(c, "k_round_mac", k_round_mac_t<32>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else launch_named(c, "k_round_mac", k_round_mac_t<40>, grid, 256, sm, D, P, c.T, rj, rk, im);
         if (!to_mac) {
+            c.next_units = (double)items * c.ab.Mm * c.cp.L;  // residue x constant products
             launch(c, k_mac_to_chain, blocks(items, 128), 128, 0, (const u32*)D, c.T.DS, P * 3, c.T, chain_out);
         } else if (c.fuse_now) {
             // forward NTT happens inside k_ntt_mac
@@ -1142,6 +1144,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
             return nullptr;
         }
         u32* Z = c.dcur->get<u32>((size_t)R * 2 * Mm * N);  // the tile stream's own buffer
+        c.next_units = (double)R * 2 * N * Mm;
         launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, entries, 2 * LN, col(0), R, Mm, 0, c.T, Z, Mm);
         if (!c.fuse_now) ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
         nc = 2;
@@ -1259,6 +1262,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         return nullptr;
     }
     u32* Z = c.dcur->get<u32>((size_t)R * 2 * Mm * N);
+    c.next_units = (double)R * 2 * N * Mm;
     launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, (const u64*)nodes, 2 * LN, (const u32*)nullptr, R, Mm,
            0, c.T, Z, Mm);
     if (!c.fuse_now) ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
@@ -1638,6 +1642,7 @@ static void finish(Ctx& c, const u64* dev_partial, u32 nc, u64* out_host, Timer&
     launch(c, k_partial_mod, blocks(accw, 256), 256, 0, dev_partial, accw, c.T, X);
     ntt32(c, X, c.s * 3 * Mm, Mm, Mm, 0, true, 0);
     u64* r3 = c.resp3.get<u64>((size_t)c.s * 3 * LN);
+    c.next_units = (double)c.s * 3 * N * Mm * L;
     launch(c, k_mac_to_chain, blocks((size_t)c.s * 3 * N, 128), 128, 0, (const u32*)X, Mm, c.s * 3, c.T, r3);
     u64* o2 = c.out2.get<u64>((size_t)c.s * 2 * LN);
     if (nc == 3) {

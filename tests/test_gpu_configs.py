@@ -141,3 +141,33 @@ def test_answer_batch_matches_single_answers(gpu, reflib, name, rows, Q, opts):
     be = RefBackend(reflib, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), keys=(keys.relin, keys.galois))
     want, _ = be.answer(qs[0], cfg.c, cfg.m, pos, db)
     assert np.array_equal(got[0], want)
+
+
+def test_async_kernels_repeatable_and_exact(gpu, reflib):
+    """Stand-in for compute-sanitizer (closed on this GPU pool): the kernels with asynchronous
+    copies, mbarrier rings and tcgen05 (k_round_tma, k_mac_tma_q, k_mac_tma, k_ntt_mac) answer
+    the same small databases many times over ragged 16-row tiles on 3 streams, every response equal
+    to the reference's -- a missing fence or a ring race shows up as a differing word."""
+    from oracle import RefBackend
+    from paper_2202_07569_b200 import Client, Context, configs
+
+    cfg = configs.config("C1")
+    n, k, m, c = 64, 2, 12, 4
+    client = Client(cfg.N, cfg.primes, cfg.t, seed=2, galois_levels=c)
+    keys = client.keys()
+    be = RefBackend(reflib, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), keys=(keys.relin, keys.galois))
+    pos = configs.perfect_map(np.arange(n), m, k)
+    for s, opts in ((1, {}), (3, {}), (3, {"mac_sg": 0}), (15, {})):
+        db = np.random.default_rng(s).integers(0, cfg.t, (n, s, cfg.N), dtype=np.uint64)
+        qs = np.stack([client.pack_query(configs.codeword_bits(pos[tg], m), c, first_index=1 + 5 * i)
+                       for i, tg in enumerate((7, 40))])
+        want = be.answer(qs[0], c, m, pos, db)[0]
+        ctx = Context(cfg.N, cfg.primes, cfg.t, options={"tile_rows": 16, "streams": 3, **opts})
+        ctx.load_db(pos, db, m=m)
+        ctx.set_keys(keys)
+        for _ in range(8):
+            assert np.array_equal(ctx.answer(qs[0], c, m), want)
+        for _ in range(3):
+            both = ctx.answer_batch(qs, c, m)
+            assert np.array_equal(both[0], want)
+            assert np.array_equal(client.decrypt(both[1][0]), db[40, 0])
