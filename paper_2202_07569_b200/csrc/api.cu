@@ -121,6 +121,7 @@ struct Ctx {
     u32 ks_ci = 2;        // "ks_ci": key columns held per thread in k_ks_mac32s (2 default: 4 CTAs / SM, unrolled rows; 4: wider, 2 CTAs / SM)
     int prep_mode = 1;    // "prep_factors": 1 prepare k' once for the arithmetic factors, 0 each factor
     bool mac_sg = true;   // "mac_sg": s >= 3 payload MAC with 3 or 5 slices per CTA (0: k_mac_tma, one slice)
+    bool mac_stages8 = false;  // "mac_stages": 8 ring stages for the 3-slice MAC (default 4)
     bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
     KsCrt ksC_r{}, ksC_g{};            // K' = 0: this key type keeps the 64-bit path
     DevBuf relinA, galoisA, ksdig, ksmac;  // keys re-based into the aux primes, digit / MAC scratch
@@ -745,6 +746,8 @@ static void set_smem_limits(u32 N) {
     MQ(2, 1, 1) MQ(2, 2, 1) MQ(2, 3, 1) MQ(2, 4, 1) MQ(3, 1, 1) MQ(3, 2, 1) MQ(3, 3, 1) MQ(3, 4, 1)
     MQ(2, 1, 3) MQ(3, 1, 3) MQ(2, 1, 5) MQ(3, 1, 5)
 #undef MQ
+    CK(cudaFuncSetAttribute(k_mac_tma_q<2, 1, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (3 + 2) * kMacBlockQ * 4));
+    CK(cudaFuncSetAttribute(k_mac_tma_q<3, 1, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (3 + 3) * kMacBlockQ * 4));
 #define RTC(JMv, NCv)                                                                                                \
     CK(cudaFuncSetAttribute(k_round_tma<0, JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
     {                                                                                                                \
@@ -944,6 +947,20 @@ static void relinearize(Ctx& c, const u64* ct3, u32 count, u64* out2, u64 scale 
         launch(c, k_relin_add, blocks((size_t)B * 2 * LN, 256), 256, 0, c3, 3 * LN, (const u64*)ks, B, c.T, o2);
         if (scale) launch(c, k_scale_const, blocks((size_t)B * 2 * LN, 256), 256, 0, o2, B, scale, c.T);
     }
+}
+
+/// Relinearisation of R groups of np products whose third components are identical within a group
+/// (ct3 [R][np][3][L][N]): one key switch per group (product 0's c2) into ks [R][2][L][N], then
+/// out2[r][p] = (c0 + ks0, c1 + ks1) for every product of the group.
+static void relinearize_shared(Ctx& c, const u64* ct3, u32 R, u32 np, u64* ks, u64* out2) {
+    const size_t LN = (size_t)c.cp.L * c.cp.N;
+    const size_t chunk = ks_chunk(c, c.cp.Dr);
+    for (u32 r0 = 0; r0 < R; r0 += (u32)chunk) {
+        const u32 B = (u32)std::min<size_t>(chunk, R - r0);
+        key_switch(c, ct3 + (size_t)r0 * np * 3 * LN + 2 * LN, (size_t)np * 3 * LN, 0, B, c.relin.ptr<u64>(),
+                   c.cp.relin_bits, c.cp.Dr, ks + (size_t)r0 * 2 * LN);
+    }
+    launch(c, k_relin_add_shared, blocks((size_t)R * np * 2 * LN, 256), 256, 0, ct3, R, np, (const u64*)ks, c.T, out2);
 }
 
 static u64 inv_mod_2n(u64 g, u64 twoN) {
@@ -1224,6 +1241,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         } else {
             prepare(c, nodes, per, nullptr, R * cnt, np_prep);
         }
+        const bool arith_first = first && op == CWG_OP_ARITH && np > 1 && c.prep_mode == 1;
         first = false;
         u32* di = c.pair_idx.get<u32>((size_t)2 * R * np);
         launch(c, k_level_pairs, blocks((size_t)R * np, 256), 256, 0, R, cnt, di, di + (size_t)R * np);
@@ -1241,7 +1259,18 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         u64* c3 = c.chain3.get<u64>((size_t)R * np * 3 * LN);
         mul_prepared(c, np_prep, di, np_prep, di + (size_t)R * np, R * np, false, c3);
         u64* nn = nbuf[cur ^ 1]->get<u64>((size_t)R * ncnt * per);
-        if (cnt % 2 == 0) {
+        if (arith_first) {
+            // every first-level factor has component 1 = k'_1, so all of a row's first-level
+            // products have the same d2 = k'_1 x k'_1, the same rounded c2, and the same key switch:
+            // one key switch per row (product 0), added to each product's (c0, c1)
+            const size_t LN2 = 2 * LN;
+            u64* ks = c.ks.get<u64>((size_t)R * LN2);
+            relinearize_shared(c, c3, R, np, ks, cnt % 2 == 0 ? nn : c.resp3.get<u64>((size_t)R * np * per));
+            if (cnt % 2)
+                launch(c, k_tree_next, blocks((size_t)R * ncnt * per, 256), 256, 0, (const u64*)c.resp3.ptr<u64>(), R, np,
+                       ncnt, (const u64*)(nodes + (size_t)(cnt - 1) * per), (size_t)cnt * per, (const u32*)nullptr,
+                       (u64)0, 0u, per, nn);
+        } else if (cnt % 2 == 0) {
             relinearize(c, c3, R * np, nn, last ? kinv : 0);
         } else {
             u64* rl = c.resp3.get<u64>((size_t)R * np * per);
@@ -1463,8 +1492,11 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
             u32 ck = std::max<u32>(1, std::min<u32>((Rt + 7) / 8, slots / blocksN));
             const u32 crow = (Rt + ck - 1) / ck;
             ck = (Rt + crow - 1) / crow;
-            const size_t smem = (size_t)kMacStages * (SG + nc) * kMacBlockQ * 4;
-            if (SG == 5) {
+            const size_t smem = (size_t)(c.mac_stages8 ? 8 : kMacStages) * (SG + nc) * kMacBlockQ * 4;
+            if (SG == 3 && c.mac_stages8) {
+                if (nc == 3) launch_named(c, "k_mac", k_mac_tma_q<3, 1, 3, 8>, (size_t)ck * blocksN, 288, smem, zp, zs, dbt, Rt, c.s, crow, c.T);
+                else launch_named(c, "k_mac", k_mac_tma_q<2, 1, 3, 8>, (size_t)ck * blocksN, 288, smem, zp, zs, dbt, Rt, c.s, crow, c.T);
+            } else if (SG == 5) {
                 if (nc == 3) launch_named(c, "k_mac", k_mac_tma_q<3, 1, 5>, (size_t)ck * blocksN, 288, smem, zp, zs, dbt, Rt, c.s, crow, c.T);
                 else launch_named(c, "k_mac", k_mac_tma_q<2, 1, 5>, (size_t)ck * blocksN, 288, smem, zp, zs, dbt, Rt, c.s, crow, c.T);
             } else {
@@ -2579,6 +2611,7 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "ks_ci") c.ks_ci = v == 2 ? 2u : 4u;
         else if (k == "prep_factors") c.prep_mode = v != 0;
         else if (k == "mac_sg") c.mac_sg = v != 0;
+        else if (k == "mac_stages") c.mac_stages8 = v >= 8;
         else if (k == "force_exact") {
             c.force_exact = v != 0;
             c.T.force_exact = c.force_exact ? 1u : 0u;

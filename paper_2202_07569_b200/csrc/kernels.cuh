@@ -486,6 +486,21 @@ __global__ void k_expand_combine(const u64* __restrict__ in, const u64* __restri
     o1[LN + e] = v1;
 }
 
+/// out2[r][p] = (c0 + ks0, c1 + ks1) of product p of group r with the group's shared key switch
+/// ks[r] (ct3 [R][np][3][L][N], ks [R][2][L][N], out2 [R][np][2][L][N]).
+__global__ void k_relin_add_shared(const u64* __restrict__ ct3, u32 R, u32 np, const u64* __restrict__ ks, DevTab T,
+                                   u64* __restrict__ out2) {
+    const u32 N = T.N, L = T.L;
+    const size_t LN = (size_t)L * N;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)R * np * 2 * LN) return;
+    const size_t rp = idx / (2 * LN), x = idx % (2 * LN);
+    const size_t r = rp / np;
+    const u64 q = T.q[(x % LN) / N];
+    const u64 s = ct3[rp * 3 * LN + x] + ks[r * 2 * LN + x];
+    out2[idx] = s >= q ? s - q : s;
+}
+
 /// out2 = (c0 + ks0, c1 + ks1) for B ciphertexts; ct3 stride 3LN, ks stride 2LN (relinearize).
 __global__ void k_relin_add(const u64* __restrict__ ct3, size_t ct_stride, const u64* __restrict__ ks, u32 B,
                             DevTab T, u64* __restrict__ out2) {

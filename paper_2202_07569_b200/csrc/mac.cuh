@@ -168,11 +168,11 @@ struct ZPtrs {
     const u32* z[4];
     unsigned long long* acc[4];
 };
-template <int NC, int QB, int SG>
+template <int NC, int QB, int SG, int ST = kMacStages>
 __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZPtrs Zp, u32 zstride,
                                                      const u32* __restrict__ DB, u32 R, u32 s, u32 chunk, DevTab T) {
     extern __shared__ __align__(128) uint2 ringq[];  // [stage][SG + QB NC][kMacBlockQ / 2]
-    __shared__ __align__(8) unsigned long long full[kMacStages], empty[kMacStages];
+    __shared__ __align__(8) unsigned long long full[ST], empty[ST];
     constexpr u32 NSEG = SG + QB * NC;
     constexpr u32 SEG = kMacBlockQ * 4;   // bytes per segment
     constexpr u32 SEGV = kMacBlockQ / 2;  // uint2 per segment
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
     const u32 rows = r1 > r0 ? r1 - r0 : 0;
     const u32 tid = threadIdx.x, warp = tid >> 5;
     if (tid == 0) {
-        for (int i = 0; i < kMacStages; ++i) {
+        for (int i = 0; i < ST; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 8);
         }
@@ -204,8 +204,8 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
             const size_t zs = (size_t)NC * zstride * N;
             const size_t zoff = (size_t)k * N + (size_t)blk * kMacBlockQ;
             for (u32 i = 0; i < rows; ++i) {
-                const u32 st = i % kMacStages;
-                if (i >= (u32)kMacStages) mbar_wait(&empty[st], ((i / kMacStages) - 1) & 1);
+                const u32 st = i % ST;
+                if (i >= (u32)ST) mbar_wait(&empty[st], ((i / ST) - 1) & 1);
                 uint2* buf = ringq + (size_t)st * NSEG * SEGV;
                 mbar_expect_tx(&full[st], SEG * NSEG);
                 const size_t r = r0 + i;
@@ -241,8 +241,8 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
 #pragma unroll
                 for (int c = 0; c < NC; ++c) acc64[q][g][c][0] = acc64[q][g][c][1] = 0;
         for (u32 i = g0; i < ge; ++i) {
-            const u32 st = i % kMacStages;
-            mbar_wait(&full[st], (i / kMacStages) & 1);
+            const u32 st = i % ST;
+            mbar_wait(&full[st], (i / ST) & 1);
             const uint2* buf = ringq + (size_t)st * NSEG * SEGV;
             uint2 d[SG];
 #pragma unroll
