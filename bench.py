@@ -251,10 +251,14 @@ def cpu_reference_sample(cfg, be, ref, query, positions, seed=1, sample_rows=Non
                          "prepare_plain_untimed": t_plain}}
 
 
-def sample_rows_for(cfg, per_row_s, steps, budget_s=150.0):
-    """Rows per reference sample so that `steps` samples take about budget_s (>= 256 rows)."""
-    rows = int(budget_s / max(steps, 1) / max(per_row_s, 1e-6))
-    return int(min(cfg.n, max(256, min(rows, 8192))))
+def sample_rows_for(cfg, per_row_s, steps, budget_s=150.0, min_rows=4096):
+    """Rows per reference sample so that `steps` samples take about budget_s, at least min_rows
+    (4096 for the reference arm) and at most 8192 or the whole database."""
+    per_row_s = max(per_row_s, 1e-6)
+    rows = int(budget_s / max(steps, 1) / per_row_s)
+    # the floor yields when even that would run past ~8 minutes (C5: ~35 ms per row on 16 threads)
+    floor = min(min_rows, int(480.0 / max(steps, 1) / per_row_s))
+    return int(min(cfg.n, max(floor, 64, min(rows, 8192))))
 
 
 def cpu_model():
@@ -451,7 +455,8 @@ def run_select_bench(args, cfg):
             ref = oracle.RefLib()
             be = oracle.RefBackend(ref, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), keys=(keys.relin, keys.galois))
             probe = reference_select_sample(cfg, be, ref, query, positions, 64)
-            R = args.cpu_sample_rows or sample_rows_for(cfg, probe["stages_s"]["select_per_row"], 1, budget_s=20.0)
+            R = args.cpu_sample_rows or sample_rows_for(cfg, probe["stages_s"]["select_per_row"], 1, budget_s=20.0,
+                                                        min_rows=64)
             cb = reference_select_sample(cfg, be, ref, query, positions, R)
             line["cpu_baseline"] = {
                 "value": cfg.n / cb["seconds_full"], "unit": "equalities/s", "cores": cb["threads"], "kind": "reference",
@@ -685,7 +690,7 @@ def main():
                                    galois_bits=cfg.galois_bits, keys=(keys.relin, keys.galois))
             probe = cpu_reference_sample(cfg, be, ref, query, positions, sample_rows=min(cfg.n, 256))
             per_row = probe["stages_s"]["select_per_row"] + probe["stages_s"]["inner_per_row"]
-            R = args.cpu_sample_rows or sample_rows_for(cfg, per_row, 1, budget_s=20.0)
+            R = args.cpu_sample_rows or sample_rows_for(cfg, per_row, 1, budget_s=20.0, min_rows=256)
             cb = cpu_reference_sample(cfg, be, ref, query, positions, sample_rows=R)
             line["cpu_baseline"] = {
                 "value": db_bytes / cb["seconds_full"] / 1e9, "unit": "GB/s", "cores": cb["threads"],
