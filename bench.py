@@ -492,6 +492,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-rows", type=int, default=0)
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="also time cwg_answer_batch with this many queries (SURVEY 8f-f1; reported under 'batch')")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="N > 1 collectives: nccl (one GPU per rank) or gloo (host-staged; ranks may share a GPU)")
     ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
@@ -621,6 +623,18 @@ def main():
         verified = bool(dec_ok and e2e_eq)
         verify_detail = {"decrypt_equals_row": bool(dec_ok), "e2e_response_equals_device_response": e2e_eq}
 
+    # multi-query batch (f1): Q queries of one client per database pass, timed like `value`
+    batch_line = None
+    if args.batch > 1 and world == 1:
+        qb = np.stack([client.pack_query(configs.codeword_bits(positions[(target + 97 * b) % cfg.n], cfg.m), cfg.c,
+                                         first_index=100 + 10 * b) for b in range(args.batch)])
+        qb = np.ascontiguousarray(qb)
+        ctx.answer_batch(qb, cfg.c, cfg.m, op=cfg.op)
+        bms = timed(lambda: ctx.answer_batch(qb, cfg.c, cfg.m, op=cfg.op), max(1, args.steps // 2))
+        batch_line = {"queries": args.batch, "ms_per_batch": bms, "ms_per_query": bms / args.batch,
+                      "value_per_query": cfg.db_bytes() / (bms / args.batch / 1e3) / 1e9, "unit": "GB/s",
+                      "timing": "CUDA events around cwg_answer_batch (synchronous, host query buffers)"}
+
     # N > 1: per-rank phase times of one more answer (outside the timed region)
     rank_rows = None
     if world > 1:
@@ -681,6 +695,8 @@ def main():
     }
     if rank_rows:
         line["ranks"] = rank_rows
+    if batch_line:
+        line["batch"] = batch_line
     if world == 1 and not args.no_cpu_baseline:
         try:
             import oracle

@@ -152,3 +152,50 @@ def test_oracle_trees_match_reference(reflib, k, op):
     want, _ = be.answer(q, c, m, pos, db, op=op)
     assert np.array_equal(orc.answer(relin, galois, q, c, m, pos, db, op=op), want)
     assert np.array_equal(be.decrypt(want[0]), db[3, 0])
+
+
+def test_client_secret_export_and_reference_arm_inputs(reflib):
+    """The client's exported secret key decrypts what the reference encrypts with the same seed
+    (the GPU client calls take it), and the reference arm's own keys / query (oracle.RefBackend)
+    are word for word the repo client's, so both arms answer the same inputs."""
+    from oracle import RefBackend
+    from paper_2202_07569_b200 import Client, configs
+
+    import bench
+
+    N, primes, t = small_params()
+    cl = Client(N, primes, t, seed=9, galois_levels=2)
+    s, seed = cl.secret()
+    assert s.dtype == np.int8 and set(np.unique(s)) <= {-1, 0, 1}
+    assert list(seed[:1]) == [9]  # Seed256::from_u64(9) = {9, golden-ratio words} (prf.hpp:18-22)
+    be = RefBackend(reflib, N, t, np.array(primes, np.uint64), seed=9, galois_levels=2)
+    ct = be.encrypt(np.arange(N, dtype=np.uint64) % t)
+    assert np.array_equal(cl.decrypt(ct), np.arange(N) % t)
+    # the reference's encryption index is a process-global counter starting at 1 (bfv.cpp:518):
+    # the reference arm draws its query first thing in a fresh process, as here
+    import hashlib
+    import subprocess
+    import sys
+
+    code = ("import sys, hashlib; sys.path.insert(0, %r); import bench; from paper_2202_07569_b200 import configs; "
+            "cfg = configs.config('C1'); ref, be, q, pos = bench.reference_inputs(cfg); rk, gk = be.export_keys(); "
+            "print(hashlib.sha256(q.tobytes() + pos.tobytes() + rk.tobytes() + gk.tobytes()).hexdigest())") % ROOT
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    cfg = configs.config("C1")
+    client, keys, query, positions, target, lo, hi = bench.make_inputs(cfg, 0, 1)
+    want = hashlib.sha256(query.tobytes() + positions.tobytes() + keys.relin.tobytes() + keys.galois.tobytes())
+    assert out.stdout.strip().splitlines()[-1] == want.hexdigest()
+    assert bench.bench_config(cfg) == {"workload": bench.workload_desc(cfg), "db_bytes": cfg.db_bytes()}
+
+
+def test_reference_sample_bounds():
+    """Reference-arm samples: >= 4096 rows unless the whole run would pass ~8 minutes, <= 8192."""
+    import bench
+    from paper_2202_07569_b200 import configs
+
+    c4, c5, c1 = configs.config("C4"), configs.config("C5"), configs.config("C1")
+    assert bench.sample_rows_for(c4, 0.0027, 3) == 8192
+    assert bench.sample_rows_for(c4, 0.0027, 20) == 4096
+    assert 64 <= bench.sample_rows_for(c5, 0.035, 20) < 4096
+    assert bench.sample_rows_for(c1, 0.001, 3) == 1024  # whole database
