@@ -63,6 +63,11 @@ typedef struct cwg_timings {
 
 const char* cwg_last_error(void);
 
+/* Pinned (page-locked, portable) host memory for staging keys, queries and responses: copies
+ * from it run as asynchronous DMA at full PCIe / C2C speed.  NULL on failure. */
+void* cwg_pinned_alloc(uint64_t bytes);
+void cwg_pinned_free(void* p);
+
 /* Number of CUDA devices visible to this process (0 without a driver / device). */
 int cwg_device_count(void);
 

@@ -42,8 +42,25 @@ struct Shape {
     }
 };
 
+/// Pinned host staging buffer (cwg_pinned_alloc), grown on demand.
+struct Pinned {
+    std::uint64_t* p = nullptr;
+    std::size_t words = 0;
+    std::uint64_t* get(std::size_t n) {
+        if (n > words) {
+            cwg_pinned_free(p);
+            p = static_cast<std::uint64_t*>(cwg_pinned_alloc(n * 8));
+            words = p ? n : 0;
+            if (!p) throw std::runtime_error(cwg_last_error());
+        }
+        return p;
+    }
+    ~Pinned() { cwg_pinned_free(p); }
+};
+
 struct Resident {                            // device-resident DB (one per process)
     cwg_ctx* ctx = nullptr;
+    Pinned keys, query, out;                 // per-call staging in pinned memory
     Shape shape;
     std::uint64_t digest = 0;
     std::vector<int> devices;                // empty: all visible
@@ -153,40 +170,56 @@ std::vector<cwpir::CipherValue> process_query(const cwpir::HeBackend& be, const 
         fresh = true;
     }
     // evaluation keys (reference layout: rows[d][k][i] in NTT form, bfv.cpp:394-402)
+    // keys and query flattened straight into pinned staging buffers (asynchronous DMA to the devices)
     const EvalKeySet& keys = bfv->eval_keys();
-    auto flat = [&](const KeySwitchKey& key, std::vector<std::uint64_t>& out) {
-        for (const auto& row : key.rows)
-            for (int c = 0; c < 2; ++c)
-                for (std::size_t i = 0; i < L; ++i)
-                    out.insert(out.end(), row[c][i].coeffs().begin(), row[c][i].coeffs().end());
-    };
-    std::vector<std::uint64_t> relin, galois, gs;
-    flat(keys.relin, relin);
+    std::vector<const KeySwitchKey*> gkeys;
+    std::vector<std::uint64_t> gs;
     for (unsigned a = 0; a < query.compression; ++a) {
         const std::uint64_t g = N / (std::uint64_t(1) << a) + 1;
         auto it = keys.galois.find(g);
         if (it == keys.galois.end()) throw he_error("missing Galois key for requested exponent");
-        flat(it->second, galois);
+        gkeys.push_back(&it->second);
         gs.push_back(g);
     }
-    std::vector<std::uint64_t> q;
-    for (const auto& ct : query.cts)
-        for (const auto& comp : ct.comps)
-            for (const auto& e : comp) q.insert(q.end(), e.coeffs().begin(), e.coeffs().end());
+    auto words = [&](const KeySwitchKey& key) { return key.rows.size() * 2 * L * N; };
+    std::size_t gw = 0;
+    for (const auto* k : gkeys) gw += words(*k);
+    const std::size_t rw = words(keys.relin);
+    std::uint64_t* kbuf = R.keys.get(rw + gw);
+    auto flat = [&](const KeySwitchKey& key, std::uint64_t* dst) {
+        for (const auto& row : key.rows)
+            for (int c = 0; c < 2; ++c)
+                for (std::size_t i = 0; i < L; ++i) {
+                    std::memcpy(dst, row[c][i].coeffs().data(), N * 8);
+                    dst += N;
+                }
+        return dst;
+    };
+    flat(keys.relin, kbuf);
+    std::uint64_t* gp = kbuf + rw;
+    for (const auto* k : gkeys) gp = flat(*k, gp);
+    std::uint64_t* q = R.query.get(query.cts.size() * 2 * L * N);
+    {
+        std::uint64_t* dst = q;
+        for (const auto& ct : query.cts)
+            for (const auto& comp : ct.comps)
+                for (const auto& e : comp) {
+                    std::memcpy(dst, e.coeffs().data(), N * 8);
+                    dst += N;
+                }
+    }
     const std::size_t s = db.chunks_per_row();
-    std::vector<std::uint64_t> out(s * 2 * L * N);
+    std::uint64_t* out = R.out.get(s * 2 * L * N);
     auto answer = [&] {
-        check(cwg_answer(R.ctx, relin.data(), (uint32_t)gs.size(), gs.data(), galois.data(),
-                         (uint32_t)query.cts.size(), query.compression, query.code_length, q.data(),
-                         CWG_OP_FOLKLORE, out.data(), nullptr));
+        check(cwg_answer(R.ctx, kbuf, (uint32_t)gs.size(), gs.data(), kbuf + rw, (uint32_t)query.cts.size(),
+                         query.compression, query.code_length, q, CWG_OP_FOLKLORE, out, nullptr));
     };
     if (fresh) {
         answer();
     } else {  // verify the resident rows against the caller's database while the GPUs answer
         auto dig = std::async(std::launch::async, [&] { return db_digest(db); });
-        int rc = cwg_answer(R.ctx, relin.data(), (uint32_t)gs.size(), gs.data(), galois.data(),
-                            (uint32_t)query.cts.size(), query.compression, query.code_length, q.data(),
-                            CWG_OP_FOLKLORE, out.data(), nullptr);
+        int rc = cwg_answer(R.ctx, kbuf, (uint32_t)gs.size(), gs.data(), kbuf + rw, (uint32_t)query.cts.size(),
+                            query.compression, query.code_length, q, CWG_OP_FOLKLORE, out, nullptr);
         const std::uint64_t d = dig.get();
         if (d != R.digest) {  // different contents: reload and answer again
             load(R, hp, db, shape);
@@ -203,7 +236,7 @@ std::vector<cwpir::CipherValue> process_query(const cwpir::HeBackend& be, const 
         resp[j].comps.resize(2);
         for (int c = 0; c < 2; ++c)
             for (std::size_t i = 0; i < L; ++i) {
-                const std::uint64_t* src = out.data() + ((j * 2 + c) * L + i) * N;
+                const std::uint64_t* src = out + ((j * 2 + c) * L + i) * N;
                 resp[j].comps[c].push_back(RingElement::from_coeffs(bfv->chain_context(i),
                                                                     std::vector<std::uint64_t>(src, src + N)));
             }

@@ -1980,6 +1980,20 @@ extern "C" {
 
 const char* cwg_last_error(void) { return g_err.c_str(); }
 
+void* cwg_pinned_alloc(uint64_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, std::max<uint64_t>(bytes, 16), cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        g_err = "cwgpu: pinned host allocation failed";
+        return nullptr;
+    }
+    return p;
+}
+
+void cwg_pinned_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 int cwg_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {

@@ -40,7 +40,7 @@ EXPORTED_SYMBOLS = [
     "cwg_expand", "cwg_mul_lazy", "cwg_relinearize", "cwg_substitute", "cwg_kernel_launches",
     "cwg_stream", "cwg_set_profiling", "cwg_kernel_stats", "cwg_kernel_units", "cwg_set_option",
     "cwg_create_multi", "cwg_device_count", "cwg_load_db_file", "cwg_answer_batch", "cwg_encrypt_query",
-    "cwg_decrypt",
+    "cwg_decrypt", "cwg_pinned_alloc", "cwg_pinned_free",
 ]
 CLIENT_SYMBOLS = [
     "cwg_client_last_error", "cwg_client_create", "cwg_client_destroy", "cwg_client_digits",
@@ -96,6 +96,9 @@ def load_library(path: str = LIB_PATH):
     lib.cwg_create_multi.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u64p, ctypes.c_uint64, ctypes.c_uint32,
                                      ctypes.c_uint32, ctypes.POINTER(ctypes.c_int), ctypes.c_int]
     lib.cwg_device_count.restype = ctypes.c_int
+    lib.cwg_pinned_alloc.restype = ctypes.c_void_p
+    lib.cwg_pinned_alloc.argtypes = [ctypes.c_uint64]
+    lib.cwg_pinned_free.argtypes = [ctypes.c_void_p]
     lib.cwg_destroy.argtypes = [ctypes.c_void_p]
     lib.cwg_get_info.argtypes = [ctypes.c_void_p, ctypes.POINTER(CwgInfo)]
     lib.cwg_load_db.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32,
