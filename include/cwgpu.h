@@ -195,7 +195,7 @@ int cwg_substitute(cwg_ctx* ctx, uint32_t count, const uint64_t* ct, uint64_t g,
  * read by the library).  key: "streams" (row-tile streams, 1-4), "tile_rows" (0 = auto),
  * "fuse_mac" (0: separate selection NTT + MAC kernels), "mac" (0: k_mac2 instead of the TMA
  * payload MAC for s >= 3), "round" (0: IMAD rounding instead of the tensor cores), "round_g2",
- * "round_ctas", "mac_waves", "mac_ck", "ntt_np", "prescale", "ks32" (0: 64-bit key switching), "ks_wide", "ks_ci", "prep_factors", "mac_sg", "mac_stages",
+ * "round_ctas", "mac_waves", "mac_ck", "ntt_np", "prescale", "ks32" (0: 64-bit key switching), "ks_wide", "ks_ci", "prep_factors", "lift_tc", "mac_sg", "mac_stages",
  * "force_exact" (every rounding / lift decision through the exact multiword path; tests).
  * Unknown keys return CWG_EINVAL. */
 int cwg_set_option(cwg_ctx* ctx, const char* key, int64_t value);

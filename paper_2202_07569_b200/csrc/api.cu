@@ -89,6 +89,9 @@ struct Ctx {
     std::vector<unsigned char> rtc;   // RoundTcPar<JM, NC> (k_round_tma kernel-parameter block)
     DevBuf rtc_B;                     // k_round_tma B matrix (canonical UMMA K-major layout)
     DevBuf rtc_B2;                    // k_round_tma second-GEMM B matrix (gamma / rho / offset terms)
+    DevBuf lift_B;                    // k_lift_tc B matrices (plain, Montgomery)
+    u32 lift_nc = 0;                  // k_lift_tc GEMM width (0: not available)
+    bool lift_tc = true;              // "lift_tc": tensor-core centred lift (0: k_lift on the CUDA cores)
     u32 rtc_nc = 0;                   // k_round_tma GEMM width (0: no instance for this JM / Mm)
     int round_kind = 2;               // 2 tensor-core (k_round_tma), 0 IMAD only (k_round_mac_t); option "round"
     DevBuf prep_s;                    // A-side prepared operands with the INTT output scale folded in
@@ -620,6 +623,31 @@ static void build_tables(Ctx& c) {
             }
         }
     }
+    // tensor-core lift (k_lift_tc): B matrices [NC][K = 64] of byte b of (2^(8a) V_ij mod a_j) at
+    // column 4 j + b, K byte 8 i + a, for the Montgomery and the plain lift constants
+    c.lift_nc = 0;
+    if (L <= 8 && 4 * J <= 112) {
+        const u32 NCl = (4 * J + 15) / 16 * 16, K = 64;
+        std::vector<unsigned char> Bl((size_t)2 * NCl * K, 0);
+        for (int mont = 0; mont < 2; ++mont) {
+            unsigned char* B = Bl.data() + (size_t)mont * NCl * K;
+            auto put = [&](u32 n, u32 kb, unsigned char v) {
+                B[(size_t)(n / 8) * (K / 16 * 128) + (kb / 16) * 128 + (n % 8) * 16 + kb % 16] = v;
+            };
+            for (u32 j = 0; j < J; ++j)
+                for (u32 i = 0; i < L; ++i) {
+                    const u64 p = a[j];
+                    const u64 V = mont ? liftV_m[(size_t)i * J + j] : liftV_n[(size_t)i * J + j];
+                    for (u32 aa = 0; aa < 8; ++aa) {
+                        const u32 v = (u32)(((u128)V << (8 * aa)) % p);
+                        for (u32 b = 0; b < 4; ++b) put(4 * j + b, 8 * i + aa, (unsigned char)(v >> (8 * b)));
+                    }
+                }
+        }
+        c.lift_B.ensure(Bl.size());
+        CK(cudaMemcpy(c.lift_B.p, Bl.data(), Bl.size(), cudaMemcpyHostToDevice));
+        c.lift_nc = NCl;
+    }
     // device copy of the table itself (slow paths read it through T.self)
     c.tab_self.ensure(sizeof(DevTab));
     c.T.self = static_cast<const DevTab*>(c.tab_self.p);
@@ -1048,12 +1076,33 @@ static void expand_shard(Ctx& c, const u64* dquery, u32 comp, u32 W, u32 rank, u
 }
 
 // ------------------------------------------------------------------ per-row selection
+/// Centred lift of count 2-comp chain ciphertexts into nj aux / MAC residues (to_aux_basis,
+/// bfv.cpp:718-744): the tensor-core k_lift_tc when its tables exist, else k_lift.
+static void lift(Ctx& c, const u64* src, size_t stride, const u32* sel, u32 count, u32 nj, int mont, u32* out,
+                 u32 out_stride_j) {
+    const size_t items = (size_t)count * 2 * c.cp.N;
+    c.next_units = (double)items * nj;  // coefficient lifts x output primes
+    if (c.lift_tc && c.lift_nc && nj <= c.ab.J && reg32_ok(c.cp.logN)) {
+        const uint4* Bm = reinterpret_cast<const uint4*>(c.lift_B.ptr<unsigned char>() + (size_t)mont * c.lift_nc * kLiftK);
+        const u32* W = mont ? c.T.liftW_m : c.T.liftW_n;
+        const size_t grid = std::min<size_t>(blocks(items, 128), (size_t)148 * 4);
+#define LTC(NCv)                                                                                               \
+    if (c.lift_nc == NCv) {                                                                                     \
+        launch_named(c, "k_lift", k_lift_tc<NCv>, grid, 128, 0, src, stride, sel, count, nj, c.T, Bm, W, out,   \
+                     out_stride_j);                                                                            \
+        return;                                                                                                \
+    }
+        LTC(32) LTC(48) LTC(64) LTC(80) LTC(96) LTC(112)
+#undef LTC
+    }
+    launch(c, k_lift, blocks(items, 256), 256, 0, src, stride, sel, count, nj, mont, c.T, out, out_stride_j);
+}
+
 /// Lift count 2-comp chain cts (at src + sel[x]*stride) to the aux basis (Montgomery) and NTT:
 /// out [count][2][J][N].
 static void prepare(Ctx& c, const u64* src, size_t stride, const u32* sel, u32 count, u32* out) {
     const u32 N = c.cp.N, J = c.ab.J;
-    c.next_units = (double)count * 2 * N * J;  // coefficient lifts x output primes
-    launch(c, k_lift, blocks((size_t)count * 2 * N, 256), 256, 0, src, stride, sel, count, J, 1, c.T, out, J);
+    lift(c, src, stride, sel, count, J, 1, out, J);
     ntt32(c, out, count * 2 * J, J, J, 0, false, 0);
 }
 
@@ -1161,8 +1210,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
             return nullptr;
         }
         u32* Z = c.dcur->get<u32>((size_t)R * 2 * Mm * N);  // the tile stream's own buffer
-        c.next_units = (double)R * 2 * N * Mm;
-        launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, entries, 2 * LN, col(0), R, Mm, 0, c.T, Z, Mm);
+        lift(c, entries, 2 * LN, col(0), R, Mm, 0, Z, Mm);
         if (!c.fuse_now) ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
         nc = 2;
         zstride = Mm;
@@ -1291,9 +1339,7 @@ static u32* select_tile(Ctx& c, const u64* entries, const u32* prep, u32 op, u64
         return nullptr;
     }
     u32* Z = c.dcur->get<u32>((size_t)R * 2 * Mm * N);
-    c.next_units = (double)R * 2 * N * Mm;
-    launch(c, k_lift, blocks((size_t)R * 2 * N, 256), 256, 0, (const u64*)nodes, 2 * LN, (const u32*)nullptr, R, Mm,
-           0, c.T, Z, Mm);
+    lift(c, (const u64*)nodes, 2 * LN, (const u32*)nullptr, R, Mm, 0, Z, Mm);
     if (!c.fuse_now) ntt32(c, Z, R * 2 * Mm, Mm, Mm, 0, false, 0);
     nc = 2;
     zstride = Mm;
@@ -2624,6 +2670,7 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "ks_wide") c.ks_wide = v != 0;
         else if (k == "ks_ci") c.ks_ci = v == 2 ? 2u : 4u;
         else if (k == "prep_factors") c.prep_mode = v != 0;
+        else if (k == "lift_tc") c.lift_tc = v != 0;
         else if (k == "mac_sg") c.mac_sg = v != 0;
         else if (k == "mac_stages") c.mac_stages8 = v >= 8;
         else if (k == "force_exact") {

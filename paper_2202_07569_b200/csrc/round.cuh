@@ -318,4 +318,143 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(128));
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Centred lift chain -> aux basis on the tensor cores (to_aux_basis, bfv.cpp:718-744).
+//
+// x_j = (sum_i y_i (q / q_i mod a_j) - rho (q mod a_j)) mod a_j with y_i = res_i (q/q_i)^-1 mod q_i
+// (< 2^60, 8 bytes) and rho = round(sum_i y_i / q_i) (crt_round: 64-bit fraction, exact fallback).
+// The dot products over i are one int8 GEMM per 128 coefficients: A = the bytes of the L y_i
+// (K = 64 bytes, from TMEM), B = byte b of (2^(8a) V_ij mod a_j) at column 4 j + b (shared memory,
+// canonical K-major layout), so column group j sums to S_j = sum_b C 2^(8b) < 2^48 with
+// S_j = sum_i y_i V_ij (mod a_j).  The epilogue adds rho (a_j - W_j) and reduces once per prime.
+// V, W: the Montgomery (x 2^32) or plain lift constants, as k_lift.
+// ---------------------------------------------------------------------------------------
+constexpr int kLiftK = 64;  // 8 chain primes x 8 bytes
+template <int NC>
+__global__ void __launch_bounds__(128, 4) k_lift_tc(const u64* __restrict__ src, size_t src_stride,
+                                                   const u32* __restrict__ sel, u32 count, u32 nj, DevTab T,
+                                                   const uint4* __restrict__ Bglob, const u32* __restrict__ Wj,
+                                                   u32* __restrict__ out, u32 out_stride_j) {
+    constexpr int K = kLiftK, KSTEPS = K / 32, ACOLS = K / 4;
+    __shared__ __align__(128) uint4 Bs[NC * K / 16];
+    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ u32 tmem_base_sh;
+    __shared__ u32 sA[kMaxJ], sW[kMaxJ];
+    __shared__ u64 sAb[kMaxJ];
+    const u32 tid = threadIdx.x, warp = tid >> 5;
+    const u32 N = T.N, L = T.L;
+    for (u32 x = tid; x < NC * K / 16; x += blockDim.x) Bs[x] = Bglob[x];
+    for (u32 j = tid; j < nj; j += blockDim.x) {
+        sA[j] = T.a[j];
+        sW[j] = Wj[j];
+        sAb[j] = T.abar[j];
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                     "n"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // B visible to the tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const u32 tbase = tmem_base_sh;
+    const u32 ta = tbase + ((warp * 32u) << 16);  // A columns [0, 16), this warp's lanes
+    const u32 td = ta + ACOLS;                    // D columns [16, 16 + NC)
+    const u64 bdesc0 = ((u64)((smem_u32(Bs) >> 4) & 0x3fff)) | ((u64)(128 >> 4) << 16) |
+                       ((u64)((K / 16 * 128) >> 4) << 32) | (1ull << 46);
+    const u32 idesc = (2u << 4) | ((u32)(NC >> 3) << 17) | ((u32)(128 >> 4) << 24);  // D s32, A / B u8, M 128
+    const size_t total = (size_t)count * 2 * N;
+    u32 phase = 0;
+    for (size_t base = (size_t)blockIdx.x * 128; base < total; base += (size_t)gridDim.x * 128) {
+        const size_t idx = base + tid;
+        const bool live = idx < total;
+        u32* o = nullptr;
+        u32 rho = 0;
+        u32 w[ACOLS];
+#pragma unroll
+        for (int x = 0; x < ACOLS; ++x) w[x] = 0;
+        if (live) {
+            const u32 c = (u32)(idx / (2 * N)), k = (u32)((idx / N) % 2), n = (u32)(idx % N);
+            const u64* s = src + (size_t)(sel ? sel[c] : c) * src_stride + (size_t)k * L * N + n;
+            u64 res[kMaxL], y[kMaxL];
+#pragma unroll
+            for (int i = 0; i < kMaxL; ++i) res[i] = i < (int)L ? s[(size_t)i * N] : 0;
+            u32 ip;
+            const u64 fr = crt_prepare(res, T, y, &ip);
+            rho = crt_round(y, ip, fr, T);
+#pragma unroll
+            for (int i = 0; i < kMaxL; ++i) {
+                if (i < (int)L) {
+                    w[2 * i] = (u32)y[i];
+                    w[2 * i + 1] = (u32)(y[i] >> 32);
+                }
+            }
+            o = out + ((size_t)c * 2 + k) * out_stride_j * N + n;
+        }
+#pragma unroll
+        for (int x = 0; x < ACOLS; x += 8)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(ta + x),
+                         "r"(w[x]), "r"(w[x + 1]), "r"(w[x + 2]), "r"(w[x + 3]), "r"(w[x + 4]), "r"(w[x + 5]),
+                         "r"(w[x + 6]), "r"(w[x + 7])
+                         : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+            for (int st = 0; st < KSTEPS; ++st) {
+                const u64 bd = bdesc0 + (u64)((st * 2 * 128) >> 4);  // 2 K chunks of 16 B per step
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tbase + ACOLS),
+                    "r"(tbase + (u32)(st * 8)), "l"(bd), "r"(idesc), "r"(st)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                             smem_u32(&mbar))
+                         : "memory");
+        }
+        mbar_wait_sleep(&mbar, phase);
+        phase ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+        for (int j0 = 0; j0 < NC / 4; j0 += 4) {  // 4 primes (16 columns) per TMEM load
+            u32 C[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                "%14, %15}, [%16];\n"
+                : "=r"(C[0]), "=r"(C[1]), "=r"(C[2]), "=r"(C[3]), "=r"(C[4]), "=r"(C[5]), "=r"(C[6]), "=r"(C[7]),
+                  "=r"(C[8]), "=r"(C[9]), "=r"(C[10]), "=r"(C[11]), "=r"(C[12]), "=r"(C[13]), "=r"(C[14]), "=r"(C[15])
+                : "r"(td + 4 * j0)
+                : "memory");
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            if (o) {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const u32 j = j0 + jj;
+                    if (j < nj) {
+                        const u32 a = sA[j];
+                        const u64 S = (u64)C[4 * jj] + ((u64)C[4 * jj + 1] << 8) + ((u64)C[4 * jj + 2] << 16) +
+                                      ((u64)C[4 * jj + 3] << 24) + (u64)rho * (a - sW[j]);
+                        o[(size_t)j * N] = bar64(S, a, sAb[j]);
+                    }
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();  // D and A are rewritten by the next tile
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(128));
+}
+
 }  // namespace cwgpu

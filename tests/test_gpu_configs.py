@@ -100,9 +100,10 @@ def test_payload_mac_kernels_agree_under_repetition(gpu):
     ({"round_g2": 0}, "k_round_tma"),                   # one-GEMM rounding epilogue
     ({"round": 0}, "k_round_mac"),                      # IMAD-only rounding
     ({"ks32": 0}, "k_round_tma"),                       # 64-bit key switching in the expansion
+    ({"lift_tc": 0}, "k_round_tma"),                    # centred lift on the CUDA cores (k_lift)
     ({"force_exact": 1}, "k_round_tma"),                # every rounding through round_exact
     ({"force_exact": 1, "fuse_mac": 0}, "k_round_tma"),
-], ids=["unfused", "default", "one-stream", "one-gemm", "imad-round", "ks64", "exact", "exact-unfused"])
+], ids=["unfused", "default", "one-stream", "one-gemm", "imad-round", "ks64", "lift-cuda", "exact", "exact-unfused"])
 def test_answer_path_variants_match_reference(gpu, reflib, opts, kernel):
     """Every kernel variant of the answer path (tensor/rounding/NTT/MAC fusions, TMA feeds, the
     exact multiword rounding) against the reference at full C4 parameters, over ragged 16-row

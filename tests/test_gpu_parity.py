@@ -568,8 +568,8 @@ def test_arith_factor_preparation_variants(gpu, reflib, k):
     n = 30
     m = configs.min_code_length(n, k)
     c = configs.default_compression(N, m)
-    for mode in (1, 0):
+    for mode, ltc in ((1, 1), (0, 1), (1, 0)):
         got, want, be, payload = _answer_case(reflib, N, primes, t, n, k, m, c, s=1, op=1, seed=80 + k,
-                                              options={"prep_factors": mode, "tile_rows": 7})
+                                              options={"prep_factors": mode, "tile_rows": 7, "lift_tc": ltc})
         assert np.array_equal(got, want), mode
         assert np.array_equal(be.decrypt(got[0]), payload[0])
