@@ -693,6 +693,14 @@ def main():
         "verify_detail": verify_detail,
         "db_load_s": t_load,
     }
+    if "k_mac" in roof:  # north_star: the payload MAC against HBM bandwidth (separate kernel when s >= 3)
+        pm = roof["k_mac"]
+        line["payload_mac"] = {"kernel": "k_mac", "bound": "hbm", "achieved": pm["achieved"], "peak": pm["peak"],
+                               "unit": "GB/s", "frac": pm["frac"], "ms_per_answer": pm["ms_per_answer"],
+                               "what": "database planes + selection planes, each read once"}
+    elif "k_ntt_mac" in roof and "hbm_view" in roof["k_ntt_mac"]:
+        line["payload_mac"] = {"kernel": "k_ntt_mac (fused with the selection NTT, IMAD-bound)",
+                               **roof["k_ntt_mac"]["hbm_view"]}
     if rank_rows:
         line["ranks"] = rank_rows
     if batch_line:

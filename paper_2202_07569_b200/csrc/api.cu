@@ -125,6 +125,11 @@ struct Ctx {
     int prep_mode = 1;    // "prep_factors": 1 prepare k' once for the arithmetic factors, 0 each factor
     bool mac_sg = true;   // "mac_sg": s >= 3 payload MAC with 3 or 5 slices per CTA (0: k_mac_tma, one slice)
     bool mac_stages8 = false;  // "mac_stages": 8 ring stages for the 3-slice MAC (default 4)
+    bool mac_rows = true;      // "mac_rows": whole-row persistent payload MAC (k_mac_rows) when s is 3, 5 or 15
+    u32 mac_item_rows = 256;    // "mac_item_rows": rows per k_mac_rows work item
+    DevBuf mac_ctr;            // k_mac_rows work counters (one per launch in flight, rotating)
+    u32 mac_ctr_next = 0;
+    int n_sms = 148;
     bool ksA_ok = false;               // relinA / galoisA valid for the uploaded keys and aux basis
     KsCrt ksC_r{}, ksC_g{};            // K' = 0: this key type keeps the 64-bit path
     DevBuf relinA, galoisA, ksdig, ksmac;  // keys re-based into the aux primes, digit / MAC scratch
@@ -775,6 +780,12 @@ static void set_smem_limits(u32 N) {
     MQ(2, 1, 3) MQ(3, 1, 3) MQ(2, 1, 5) MQ(3, 1, 5)
 #undef MQ
     CK(cudaFuncSetAttribute(k_mac_tma_q<2, 1, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (3 + 2) * kMacBlockQ * 4));
+#define MAC_ROWS_ATTR(NCv, SGv, STv)                                                                         \
+    CK(cudaFuncSetAttribute(k_mac_rows<NCv, SGv, STv>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                            STv * (SGv + NCv) * kMacBlockS * 4));
+    MAC_ROWS_ATTR(3, 15, 10) MAC_ROWS_ATTR(2, 15, 10) MAC_ROWS_ATTR(3, 5, 16) MAC_ROWS_ATTR(2, 5, 16)
+    MAC_ROWS_ATTR(3, 3, 16) MAC_ROWS_ATTR(2, 3, 16)
+#undef MAC_ROWS_ATTR
     CK(cudaFuncSetAttribute(k_mac_tma_q<3, 1, 3, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * (3 + 3) * kMacBlockQ * 4));
 #define RTC(JMv, NCv)                                                                                                \
     CK(cudaFuncSetAttribute(k_round_tma<0, JMv, NCv>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)round_tma_smem<JMv>())); \
@@ -1352,8 +1363,37 @@ static u32 tile_rows(const Ctx& c) {
     // prepared-node buffers scale with it, ~12 GB in all at C5)
     const size_t per = (size_t)3 * c.T.DS * c.cp.N * 4 * std::max<u32>(1, c.k / 2);
     size_t r = std::max<size_t>(4, (size_t(c.k > 2 ? 2048 : 256) << 20) / per);
-    if (c.tile_rows_opt) r = c.tile_rows_opt;
+    if (c.tile_rows_opt) return (u32)std::min<size_t>(c.tile_rows_opt, 2048);
+    // rows of many plaintexts (whole-row payload MAC, k_mac_rows): large tiles keep its work items long
+    // (C3: 1,024-row tiles, 15.0 vs 18.4 ms of MAC per answer at 182 rows)
+    if (c.k <= 2 && c.s >= 3) return (u32)std::min<size_t>(std::max<size_t>(4, (size_t(1536) << 20) / per), 1024);
     return (u32)std::min<size_t>(r, 512);
+}
+
+/// Tiled tensor map of a u32 array viewed as [d3][d2][d1][d0] (d0 contiguous), box {box0, 1, box2, 1}:
+/// the operand of cp.async.bulk.tensor.4d in k_mac_rows.  cuTensorMapEncodeTiled is a host-side
+/// encoder; it is fetched through the runtime so the library does not link libcuda.
+static CUtensorMap tensor_map4(const u32* base, u64 d0, u64 d1, u64 d2, u64 d3, u32 box0, u32 box2) {
+    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                 const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+        if (!fn || qr != cudaDriverEntryPointSuccess) throw std::runtime_error("cwgpu: cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeFn>(fn);
+    }();
+    CUtensorMap tm;
+    const cuuint64_t dims[4] = {d0, d1, d2, d3};
+    const cuuint64_t strides[3] = {d0 * 4, d0 * d1 * 4, d0 * d1 * d2 * 4};
+    const cuuint32_t box[4] = {box0, 1, box2, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<u32*>(base), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cwgpu: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return tm;
 }
 
 // ------------------------------------------------------------------ answer
@@ -1527,6 +1567,29 @@ static u32 answer_partial(Ctx& c, u32 h, u32 comp, u32 m, const u64* query, u32 
         // across the s payload slices); the register stream is as fast for s = 1 (C4: 22.9 ms)
         if (c.fuse_now) {
             REG32_DISPATCH(c.cp.logN, ntt_mac(c, Z, zs, nc, dbt, Rt, acc));
+        } else if (c.mac_rows && c.mac_tma && (c.s == 15 || c.s == 5 || c.s == 3) && N >= (u32)kMacBlockS) {
+            // whole rows per CTA: every selection word is fetched once per row (persistent CTAs, work
+            // items from a global counter)
+            const u32 ck = std::max<u32>(1, (Rt + c.mac_item_rows / 2) / std::max<u32>(1, c.mac_item_rows));
+            const u32 crow = (Rt + ck - 1) / ck;
+            const u32 nch = (Rt + crow - 1) / crow;
+            const u32 items = nch * Mm * (N / kMacBlockS);
+            c.mac_ctr.ensure(64 * sizeof(u32));
+            u32* ctr = c.mac_ctr.ptr<u32>() + (c.mac_ctr_next++ % 64);
+            CK(cudaMemsetAsync(ctr, 0, sizeof(u32), c.st));
+            const size_t grid = std::min<size_t>(items, (size_t)c.n_sms);
+            // 4-D views [row][slice or component][prime plane][coefficient] of the tile's database rows
+            // and selection planes; one box per ring stage each
+            const CUtensorMap tmDB = tensor_map4(dbt, N, Mm, c.s, Rt, kMacBlockS, c.s);
+            const CUtensorMap tmZ = tensor_map4(Z, N, zs, nc, Rt, kMacBlockS, nc);
+#define MAC_ROWS(NCv, SGv)                                                                                         \
+    if (nc == NCv && c.s == SGv) {                                                                                 \
+        constexpr int STv = SGv == 15 ? 10 : 16;                                                                   \
+        launch_named(c, "k_mac", k_mac_rows<NCv, SGv, STv>, grid, 288, (size_t)STv*(SGv + NCv) * kMacBlockS * 4,   \
+                     tmDB, tmZ, Rt, crow, nch, c.T, acc, ctr);                                                     \
+    }
+            MAC_ROWS(3, 15) MAC_ROWS(2, 15) MAC_ROWS(3, 5) MAC_ROWS(2, 5) MAC_ROWS(3, 3) MAC_ROWS(2, 3)
+#undef MAC_ROWS
         } else if (c.mac_sg && c.s >= 3 && (c.s % 5 == 0 || c.s % 3 == 0) && N >= (u32)kMacBlockQ) {
             // several payload slices per CTA: the row's selection segments are read once per SG slices
             const u32 SG = c.s % 3 == 0 ? 3 : 5;
@@ -2011,6 +2074,8 @@ static void init_ctx(Ctx& c, uint32_t N, uint32_t L, const uint64_t* q, uint64_t
     CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) throw std::invalid_argument("cwgpu: device id out of range");
     c.device = device;
+    cudaDeviceGetAttribute(&c.n_sms, cudaDevAttrMultiProcessorCount, device);
+    if (c.n_sms <= 0) c.n_sms = 148;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
     CK(cudaMalloc(&c.d_fb, 8));
@@ -2673,6 +2738,8 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "lift_tc") c.lift_tc = v != 0;
         else if (k == "mac_sg") c.mac_sg = v != 0;
         else if (k == "mac_stages") c.mac_stages8 = v >= 8;
+        else if (k == "mac_rows") c.mac_rows = v != 0;
+        else if (k == "mac_item_rows") c.mac_item_rows = (u32)std::max(1, v);
         else if (k == "force_exact") {
             c.force_exact = v != 0;
             c.T.force_exact = c.force_exact ? 1u : 0u;

@@ -11,6 +11,7 @@
 // writer is the async proxy).  Loads in flight are bounded by the ring, not
 // by registers, so the stream runs at HBM rate.
 #pragma once
+#include <cuda.h>  // CUtensorMap (types only: the encoder is fetched through the runtime)
 #include "devtab.h"
 #include "modarith.cuh"
 
@@ -284,6 +285,131 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
                 atomicAdd(o, (unsigned long long)accr[q][g][c][0]);
                 atomicAdd(o + 1, (unsigned long long)accr[q][g][c][1]);
             }
+}
+
+
+/// Whole-row payload MAC for rows of many plaintexts (C3: s = 15): one persistent CTA per SM streams,
+/// per row, ALL SG payload segments and the NC selection segments of a 256-coefficient block of one
+/// MAC prime -- so each selection word is fetched once per row instead of once per slice group, and
+/// the ring (ST stages x (SG + NC) KB, ~180 KB) keeps enough bytes in flight per SM for the HBM
+/// stream on its own.  A stage is filled by TWO tensor-map copies (cp.async.bulk.tensor.4d: a
+/// {256, 1, SG, 1} box of the database viewed as [row][s][Mm][N] and a {256, 1, NC, 1} box of the
+/// selection planes): per-segment 1 KB cp.async.bulk copies were bound by the copy issue rate
+/// (~50 ns per copy and SM: 2.8 TB/s).  Work items (row chunk, prime, coefficient block) are handed
+/// out by a global counter: a CTA that starts late (the tile streams' other kernels still hold its
+/// SM) simply takes fewer items.  The item id travels with the ring stage (meta word; ~0 ends the
+/// stream).  Accumulation is lazy: 60-bit products summed in u64 and folded every 8 rows with
+/// x -> (x >> 32) (2^32 mod a) + (x & 2^32 - 1)  (< 2^62 + 2^32, one IMAD.WIDE), one Barrett
+/// reduction and one atomic add per output per item.
+/// Grid: <= SMs CTAs of 288 threads (8 consumer warps, 1 coefficient per thread, + a producer warp).
+constexpr int kMacBlockS = 256;
+__device__ __forceinline__ void tma_tensor4_g2s(void* dst, const void* tmap, u32 c0, u32 c1, u32 c2, u32 c3,
+                                                unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+            "r"(mac_smem(dst)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mac_smem(bar))
+        : "memory");
+}
+template <int NC, int SG, int ST>
+__global__ void __launch_bounds__(288, 1) k_mac_rows(const __grid_constant__ CUtensorMap tmDB,
+                                                    const __grid_constant__ CUtensorMap tmZ, u32 R, u32 chunk,
+                                                    u32 nchunks, DevTab T, unsigned long long* __restrict__ acc,
+                                                    u32* __restrict__ counter) {
+    extern __shared__ __align__(128) u32 rings[];  // [stage][SG + NC][kMacBlockS]
+    __shared__ __align__(8) unsigned long long full[ST], empty[ST];
+    __shared__ u32 meta[ST];
+    constexpr u32 NSEG = SG + NC;
+    constexpr u32 SEG = kMacBlockS * 4;  // bytes per segment
+    const u32 N = T.N, Mm = T.Mm;
+    const u32 nblk = N / kMacBlockS;
+    const u32 nitems = nchunks * Mm * nblk;
+    const u32 tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0) {
+        for (int i = 0; i < ST; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 8) {  // producer
+        if ((tid & 31) == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmDB) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmZ) : "memory");
+            u32 i = 0;
+            for (;;) {
+                const u32 it = atomicAdd(counter, 1u);
+                if (it >= nitems) break;
+                const u32 blk = it % nblk, k = (it / nblk) % Mm, ch = it / (nblk * Mm);
+                const u32 r0 = ch * chunk, r1 = min(R, r0 + chunk);
+                for (u32 r = r0; r < r1; ++r, ++i) {
+                    const u32 st = i % ST;
+                    if (i >= (u32)ST) mbar_wait(&empty[st], ((i / ST) - 1) & 1);
+                    u32* buf = rings + (size_t)st * NSEG * kMacBlockS;
+                    meta[st] = it;
+                    mbar_expect_tx(&full[st], SEG * NSEG);
+                    tma_tensor4_g2s(buf, &tmDB, blk * kMacBlockS, k, 0, r, &full[st]);
+                    tma_tensor4_g2s(buf + SG * kMacBlockS, &tmZ, blk * kMacBlockS, k, 0, r, &full[st]);
+                }
+            }
+            const u32 st = i % ST;  // end of stream
+            if (i >= (u32)ST) mbar_wait(&empty[st], ((i / ST) - 1) & 1);
+            meta[st] = 0xffffffffu;
+            mbar_arrive(&full[st]);
+        }
+        return;
+    }
+    u32 i = 0;
+    for (;;) {
+        mbar_wait(&full[i % ST], (i / ST) & 1);  // first row of the next item (waited for again below)
+        const u32 it = meta[i % ST];
+        if (it == 0xffffffffu) break;
+        const u32 blk = it % nblk, k = (it / nblk) % Mm, ch = it / (nblk * Mm);
+        const u32 r0 = ch * chunk, rows = min(R, r0 + chunk) - r0;
+        const u32 p = T.a[k];
+        const u64 pb = T.abar[k];
+        const u32 c32 = bar64(1ull << 32, p, pb);  // 2^32 mod a_k
+        u64 a64[SG][NC];
+#pragma unroll
+        for (int g = 0; g < SG; ++g)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) a64[g][c] = 0;
+        for (u32 g0 = 0; g0 < rows; g0 += 8) {
+            const u32 ge = min(rows, g0 + 8);
+            for (u32 r = g0; r < ge; ++r, ++i) {
+                const u32 st = i % ST;
+                mbar_wait(&full[st], (i / ST) & 1);
+                const u32* buf = rings + (size_t)st * NSEG * kMacBlockS + tid;
+                u32 z[NC];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) z[c] = buf[(SG + c) * kMacBlockS];
+#pragma unroll
+                for (int g = 0; g < SG; ++g) {
+                    const u32 d = buf[g * kMacBlockS];
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) a64[g][c] += (u64)z[c] * d;
+                }
+                // the stage is rewritten by TMA (async proxy): order this thread's generic-proxy reads
+                // of it before the release, then one arrival per warp
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if ((tid & 31) == 0) mbar_arrive(&empty[st]);
+            }
+            if (ge < rows) {
+#pragma unroll
+                for (int g = 0; g < SG; ++g)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) a64[g][c] = (u64)(u32)(a64[g][c] >> 32) * c32 + (u32)a64[g][c];
+            }
+        }
+        const u32 n = blk * kMacBlockS + tid;
+#pragma unroll
+        for (int g = 0; g < SG; ++g)
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                atomicAdd(acc + (((size_t)g * 3 + c) * Mm + k) * N + n, (unsigned long long)bar64(a64[g][c], p, pb));
+    }
 }
 
 }  // namespace cwgpu

@@ -78,19 +78,28 @@ def test_payload_mac_kernels_agree_under_repetition(gpu):
     _, keys, query, positions, _, _, _ = bench.make_inputs(cfg, 0, 1)
     payload = configs.db_payload(cfg, 1, 0, cfg.n)
     parts = {}
-    for mac in ("v2", "tma"):
-        ctx = Context(cfg.N, cfg.primes, cfg.t, options={"mac": int(mac == "tma")})
+    variants = {
+        "v2": {"mac": 0},                                  # k_mac2 (register stream)
+        "tma": {"mac_rows": 0},                            # k_mac_tma_q (3 slices per CTA)
+        "rows": {},                                        # k_mac_rows (whole rows, persistent CTAs)
+        "rows20": {"mac_item_rows": 20, "tile_rows": 100}, # ragged items: folds at rows 8 and 16, 5-row tail
+        "rows8": {"mac_item_rows": 8, "streams": 1},       # an item ends exactly on a fold boundary
+    }
+    for mac, opts in variants.items():
+        ctx = Context(cfg.N, cfg.primes, cfg.t, options=opts)
         ctx.load_db(positions, payload, n_total=cfg.n, m=cfg.m)
         ctx.set_keys(keys)
         runs = []
-        for _ in range(6 if mac == "tma" else 1):
+        for _ in range(1 if mac == "v2" else 4):
             dp = torch.zeros(ctx.partial_words(), dtype=torch.int64, device="cuda")
             ctx.answer_partial(query, cfg.c, cfg.m, dp.data_ptr())
             torch.cuda.synchronize()
             runs.append(dp.cpu().numpy())
         parts[mac] = runs
-    for r in parts["tma"]:
-        assert np.array_equal(r, parts["v2"][0])
+        del ctx
+    for mac, runs in parts.items():
+        for r in runs:
+            assert np.array_equal(r, parts["v2"][0]), mac
 
 
 @pytest.mark.parametrize("opts,kernel", [
@@ -146,7 +155,7 @@ def test_answer_batch_matches_single_answers(gpu, reflib, name, rows, Q, opts):
 
 def test_async_kernels_repeatable_and_exact(gpu, reflib):
     """Stand-in for compute-sanitizer (closed on this GPU pool): the kernels with asynchronous
-    copies, mbarrier rings and tcgen05 (k_round_tma, k_mac_tma_q, k_mac_tma, k_ntt_mac) answer
+    copies, mbarrier rings and tcgen05 (k_round_tma, k_mac_rows, k_mac_tma_q, k_mac_tma, k_ntt_mac) answer
     the same small databases many times over ragged 16-row tiles on 3 streams, every response equal
     to the reference's -- a missing fence or a ring race shows up as a differing word."""
     from oracle import RefBackend
@@ -158,7 +167,8 @@ def test_async_kernels_repeatable_and_exact(gpu, reflib):
     keys = client.keys()
     be = RefBackend(reflib, cfg.N, cfg.t, np.array(cfg.primes, np.uint64), keys=(keys.relin, keys.galois))
     pos = configs.perfect_map(np.arange(n), m, k)
-    for s, opts in ((1, {}), (3, {}), (3, {"mac_sg": 0}), (15, {})):
+    for s, opts in ((1, {}), (3, {}), (3, {"mac_rows": 0}), (3, {"mac_rows": 0, "mac_sg": 0}), (5, {}), (15, {}),
+                    (15, {"mac_item_rows": 5}), (15, {"mac_rows": 0})):
         db = np.random.default_rng(s).integers(0, cfg.t, (n, s, cfg.N), dtype=np.uint64)
         qs = np.stack([client.pack_query(configs.codeword_bits(pos[tg], m), c, first_index=1 + 5 * i)
                        for i, tg in enumerate((7, 40))])
