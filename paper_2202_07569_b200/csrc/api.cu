@@ -92,6 +92,9 @@ struct Ctx {
     DevBuf lift_B;                    // k_lift_tc B matrices (plain, Montgomery)
     u32 lift_nc = 0;                  // k_lift_tc GEMM width (0: not available)
     bool lift_tc = true;              // "lift_tc": tensor-core centred lift (0: k_lift on the CUDA cores)
+    DevBuf m2c_B;                     // k_mac_to_chain_tc B matrix
+    u32 m2c_kw = 0;                   // k_mac_to_chain_tc A words (0: not available)
+    bool m2c_tc = true;               // "m2c_tc": tensor-core MAC basis -> chain conversion (0: k_mac_to_chain)
     u32 rtc_nc = 0;                   // k_round_tma GEMM width (0: no instance for this JM / Mm)
     int round_kind = 2;               // 2 tensor-core (k_round_tma), 0 IMAD only (k_round_mac_t); option "round"
     DevBuf prep_s;                    // A-side prepared operands with the INTT output scale folded in
@@ -258,6 +261,44 @@ static void launch_named(Ctx& c, const char* name, K kern, size_t grid, unsigned
     c.next_units = 0;
 }
 #define launch(c, kern, ...) launch_named(c, #kern, kern, __VA_ARGS__)
+
+/// Tiled tensor map of a dense u32 array of `rank` dimensions (dims[0] contiguous) with the given box:
+/// the operand of cp.async.bulk.tensor in k_mac_rows and k_round_tma.  cuTensorMapEncodeTiled is a
+/// host-side encoder; it is fetched through the runtime so the library does not link libcuda.
+static CUtensorMap tensor_map(const u32* base, u32 rank, const u64* dims, const u32* box) {
+    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                                 const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
+        if (!fn || qr != cudaDriverEntryPointSuccess) throw std::runtime_error("cwgpu: cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeFn>(fn);
+    }();
+    CUtensorMap tm;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5], es[5];
+    u64 stride = 4;
+    for (u32 i = 0; i < rank; ++i) {
+        gd[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        stride *= dims[i];
+        if (i + 1 < rank) gs[i] = stride;
+    }
+    const CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, rank, const_cast<u32*>(base), gd, gs, bx, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cwgpu: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return tm;
+}
+static CUtensorMap tensor_map4(const u32* base, u64 d0, u64 d1, u64 d2, u64 d3, u32 box0, u32 box2) {
+    const u64 dims[4] = {d0, d1, d2, d3};
+    const u32 box[4] = {box0, 1, box2, 1};
+    return tensor_map(base, 4, dims, box);
+}
+
 
 /// launch_named for an explicit (multi-dimensional) launch configuration (cfg.stream is replaced by
 /// the context's stream); the same profiling / counting.
@@ -652,6 +693,27 @@ static void build_tables(Ctx& c) {
         c.lift_B.ensure(Bl.size());
         CK(cudaMemcpy(c.lift_B.p, Bl.data(), Bl.size(), cudaMemcpyHostToDevice));
         c.lift_nc = NCl;
+    }
+    // tensor-core MAC basis -> chain conversion (k_mac_to_chain_tc): B [64][K = 4 KW] of byte b of
+    // (2^(8a) (M/a_k) mod q_i) at column 8 i + b, K byte 4 k + a
+    c.m2c_kw = 0;
+    if (L <= 8 && Mm <= 24) {
+        const u32 KW = Mm <= 16 ? 16 : 24, K = 4 * KW, NCm = 64;
+        std::vector<unsigned char> Bm((size_t)NCm * K, 0);
+        auto put = [&](u32 n, u32 kb, unsigned char v) {
+            Bm[(size_t)(n / 8) * (K / 16 * 128) + (kb / 16) * 128 + (n % 8) * 16 + kb % 16] = v;
+        };
+        for (u32 k = 0; k < Mm; ++k)
+            for (u32 i = 0; i < L; ++i) {
+                const u64 qi = cp.q[i];
+                for (u32 aa = 0; aa < 4; ++aa) {
+                    const u64 v = (u64)(((u128)Mconv[(size_t)k * L + i] << (8 * aa)) % qi);
+                    for (u32 b = 0; b < 8; ++b) put(8 * i + b, 4 * k + aa, (unsigned char)(v >> (8 * b)));
+                }
+            }
+        c.m2c_B.ensure(Bm.size());
+        CK(cudaMemcpy(c.m2c_B.p, Bm.data(), Bm.size(), cudaMemcpyHostToDevice));
+        c.m2c_kw = KW;
     }
     // device copy of the table itself (slow paths read it through T.self)
     c.tab_self.ensure(sizeof(DevTab));
@@ -1086,6 +1148,20 @@ static void expand_shard(Ctx& c, const u64* dquery, u32 comp, u32 W, u32 rank, u
     CK(cudaMemcpyAsync(out, leaves, (full / W) * per * 8, cudaMemcpyDefault, c.st));
 }
 
+/// MAC basis -> chain (exact centred base conversion): X [G][xs][N] -> out [G][L][N].
+static void mac_to_chain(Ctx& c, const u32* X, u32 xs, u32 G, u64* out) {
+    const size_t items = (size_t)G * c.cp.N;
+    c.next_units = (double)items * c.ab.Mm * c.cp.L;  // residue x constant products
+    if (c.m2c_tc && c.m2c_kw) {
+        const size_t grid = std::min<size_t>(blocks(items, 128), (size_t)c.n_sms * 4);
+        const uint4* Bm = c.m2c_B.ptr<uint4>();
+        if (c.m2c_kw == 16) launch_named(c, "k_mac_to_chain", k_mac_to_chain_tc<16>, grid, 128, 0, X, xs, G, c.T, Bm, out);
+        else launch_named(c, "k_mac_to_chain", k_mac_to_chain_tc<24>, grid, 128, 0, X, xs, G, c.T, Bm, out);
+        return;
+    }
+    launch(c, k_mac_to_chain, blocks(items, 128), 128, 0, X, xs, G, c.T, out);
+}
+
 // ------------------------------------------------------------------ per-row selection
 /// Centred lift of count 2-comp chain ciphertexts into nj aux / MAC residues (to_aux_basis,
 /// bfv.cpp:718-744): the tensor-core k_lift_tc when its tables exist, else k_lift.
@@ -1157,6 +1233,10 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         const u32* im = reinterpret_cast<const u32*>(rk + kMaxJ);
         c.next_units = (double)items;  // coefficients rounded
         if (tc) {
+            // the producer warp fills a ring stage with ONE box copy: 128 coefficients x J planes of D[pc][j][n]
+            const u64 ddims[3] = {N, c.T.DS, (u64)P * 3};
+            const u32 dbox[3] = {128, J, 1};
+            const CUtensorMap tmD = tensor_map(D, 3, ddims, dbox);
             const uint4* Bm = c.rtc_B.ptr<uint4>();
             const uint4* B2m = c.round_g2 ? c.rtc_B2.ptr<uint4>() : nullptr;  // null: one-GEMM epilogue
 #define RTC(JMv, NCv)                                                                                             \
@@ -1167,16 +1247,16 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
             constexpr int LN = JMv == 16 ? 13 : JMv == 8 ? 12 : JMv == 32 ? 14 : 0;                              \
             if (LN == 13 && c.cp.logN == 13 && c.ab.Mm == 11)                                                    \
                 launch_named(c, "k_round_tma", k_round_tma<LN, JMv, NCv, 11>, gr, 160, round_tma_smem<JMv>(), D, P,  \
-                             c.T, rp, Bm, rk, B2m);                                                               \
+                             c.T, rp, Bm, rk, B2m, tmD);                                                               \
             else if (LN == 13 && c.cp.logN == 13 && c.ab.Mm == 10)                                               \
                 launch_named(c, "k_round_tma", k_round_tma<LN, JMv, NCv, 10>, gr, 160, round_tma_smem<JMv>(), D, P,  \
-                             c.T, rp, Bm, rk, B2m);                                                               \
+                             c.T, rp, Bm, rk, B2m, tmD);                                                               \
             else if (LN != 0 && c.cp.logN == (u32)LN)                                                             \
                 launch_named(c, "k_round_tma", k_round_tma<LN, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T, \
-                             rp, Bm, rk, B2m);                                                                    \
+                             rp, Bm, rk, B2m, tmD);                                                                    \
             else                                                                                                  \
                 launch_named(c, "k_round_tma", k_round_tma<0, JMv, NCv>, gr, 160, round_tma_smem<JMv>(), D, P, c.T,  \
-                             rp, Bm, rk, B2m);                                                                    \
+                             rp, Bm, rk, B2m, tmD);                                                                    \
         }                                                                                                         \
     }
             RTC(8, 48) RTC(8, 64) RTC(16, 64) RTC(16, 80) RTC(24, 80) RTC(24, 96) RTC(32, 96)
@@ -1187,8 +1267,7 @@ static u32* mul_prepared(Ctx& c, const u32* prepA, const u32* idxA, const u32* p
         else if (c.JM == 32) launch_named(c, "k_round_mac", k_round_mac_t<32>, grid, 256, sm, D, P, c.T, rj, rk, im);
         else launch_named(c, "k_round_mac", k_round_mac_t<40>, grid, 256, sm, D, P, c.T, rj, rk, im);
         if (!to_mac) {
-            c.next_units = (double)items * c.ab.Mm * c.cp.L;  // residue x constant products
-            launch(c, k_mac_to_chain, blocks(items, 128), 128, 0, (const u32*)D, c.T.DS, P * 3, c.T, chain_out);
+            mac_to_chain(c, (const u32*)D, c.T.DS, P * 3, chain_out);
         } else if (c.fuse_now) {
             // forward NTT happens inside k_ntt_mac
         } else if (reg32_ok(c.cp.logN)) {
@@ -1368,32 +1447,6 @@ static u32 tile_rows(const Ctx& c) {
     // (C3: 1,024-row tiles, 15.0 vs 18.4 ms of MAC per answer at 182 rows)
     if (c.k <= 2 && c.s >= 3) return (u32)std::min<size_t>(std::max<size_t>(4, (size_t(1536) << 20) / per), 1024);
     return (u32)std::min<size_t>(r, 512);
-}
-
-/// Tiled tensor map of a u32 array viewed as [d3][d2][d1][d0] (d0 contiguous), box {box0, 1, box2, 1}:
-/// the operand of cp.async.bulk.tensor.4d in k_mac_rows.  cuTensorMapEncodeTiled is a host-side
-/// encoder; it is fetched through the runtime so the library does not link libcuda.
-static CUtensorMap tensor_map4(const u32* base, u64 d0, u64 d1, u64 d2, u64 d3, u32 box0, u32 box2) {
-    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
-                                 const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static EncodeFn encode = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult qr;
-        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr));
-        if (!fn || qr != cudaDriverEntryPointSuccess) throw std::runtime_error("cwgpu: cuTensorMapEncodeTiled unavailable");
-        return reinterpret_cast<EncodeFn>(fn);
-    }();
-    CUtensorMap tm;
-    const cuuint64_t dims[4] = {d0, d1, d2, d3};
-    const cuuint64_t strides[3] = {d0 * 4, d0 * d1 * 4, d0 * d1 * d2 * 4};
-    const cuuint32_t box[4] = {box0, 1, box2, 1};
-    const cuuint32_t es[4] = {1, 1, 1, 1};
-    const CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 4, const_cast<u32*>(base), dims, strides, box, es,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) throw std::runtime_error("cwgpu: cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-    return tm;
 }
 
 // ------------------------------------------------------------------ answer
@@ -1784,7 +1837,7 @@ static void finish(Ctx& c, const u64* dev_partial, u32 nc, u64* out_host, Timer&
     ntt32(c, X, c.s * 3 * Mm, Mm, Mm, 0, true, 0);
     u64* r3 = c.resp3.get<u64>((size_t)c.s * 3 * LN);
     c.next_units = (double)c.s * 3 * N * Mm * L;
-    launch(c, k_mac_to_chain, blocks((size_t)c.s * 3 * N, 128), 128, 0, (const u32*)X, Mm, c.s * 3, c.T, r3);
+    mac_to_chain(c, (const u32*)X, Mm, c.s * 3, r3);
     u64* o2 = c.out2.get<u64>((size_t)c.s * 2 * LN);
     if (nc == 3) {
         relinearize(c, r3, c.s, o2);
@@ -2736,6 +2789,7 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "ks_ci") c.ks_ci = v == 2 ? 2u : 4u;
         else if (k == "prep_factors") c.prep_mode = v != 0;
         else if (k == "lift_tc") c.lift_tc = v != 0;
+        else if (k == "m2c_tc") c.m2c_tc = v != 0;
         else if (k == "mac_sg") c.mac_sg = v != 0;
         else if (k == "mac_stages") c.mac_stages8 = v >= 8;
         else if (k == "mac_rows") c.mac_rows = v != 0;

@@ -59,7 +59,8 @@ template <int LOGN, int JM, int NC, int MMT = 0>  // LOGN = 0: N at run time; MM
 __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P, DevTab T,
                                                      const __grid_constant__ RoundTcPar<JM, NC> RP,
                                                      const uint4* __restrict__ Bglob, const RoundK* __restrict__ gRK,
-                                                     const uint4* __restrict__ B2glob) {
+                                                     const uint4* __restrict__ B2glob,
+                                                     const __grid_constant__ CUtensorMap tmD) {
     using RPT = RoundTcPar<JM, NC>;
     constexpr int K = RPT::K, F0 = RPT::F0, G0 = RPT::G0;
     constexpr int KSTEPS = K / 32;
@@ -109,8 +110,13 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
                 const size_t pc = base >> logN;
                 const u32 n0 = (u32)(base & (N - 1));
                 mbar_expect_tx(&full[st], J * 512u);
-                const u32* src = D + pc * T.DS * N + n0;
-                for (u32 j = 0; j < J; ++j) tma_bulk_g2s(&ring[st][j][0], src + (size_t)j * N, 512u, &full[st]);
+                // one {128, J, 1} box of D viewed as [pc][plane][n]: per-plane 512 B bulk copies were
+                // bound by the copy issue rate (~30-50 ns per copy and SM)
+                asm volatile(
+                    "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+                        "r"(smem_u32(&ring[st][0][0])),
+                    "l"(&tmD), "r"(n0), "r"(0u), "r"((u32)pc), "r"(smem_u32(&full[st]))
+                    : "memory");
             }
         }
         return;
@@ -444,6 +450,145 @@ __global__ void __launch_bounds__(128, 4) k_lift_tc(const u64* __restrict__ src,
                         const u64 S = (u64)C[4 * jj] + ((u64)C[4 * jj + 1] << 8) + ((u64)C[4 * jj + 2] << 16) +
                                       ((u64)C[4 * jj + 3] << 24) + (u64)rho * (a - sW[j]);
                         o[(size_t)j * N] = bar64(S, a, sAb[j]);
+                    }
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();  // D and A are rewritten by the next tile
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(128));
+}
+
+// ---------------------------------------------------------------------------------------
+// MAC basis -> chain on the tensor cores (the exact centred base conversion of k_mac_to_chain).
+//
+// out_i = (sum_k v_k (M/a_k mod q_i) + gamma (-M mod q_i)) mod q_i with v_k = x_k (M/a_k)^-1 mod a_k
+// and gamma = round(sum_k v_k / a_k) (|X| < M/2 (1 - 2^-20): the 64-bit estimate decides).  The
+// Mm x L dot products are one int8 GEMM per 128 coefficients: A = the bytes of the v_k (K = 4 KW
+// bytes, from TMEM), B = byte b of (2^(8a) (M/a_k) mod q_i) at column 8 i + b, K byte 4 k + a, so
+// column group i sums to S_i = sum_b C_b 2^(8b) < 2^80 with S_i = sum_k v_k (M/a_k) (mod q_i); the
+// epilogue adds the gamma term and reduces once per chain prime (reduce96).  The CUDA-core kernel
+// spends ~4,800 instructions per coefficient at C5 (Mm = 17, L = 8) on the same sums.
+// X layout [G][xs][N] (the first Mm planes of each group of xs); out layout [G][L][N].
+// ---------------------------------------------------------------------------------------
+template <int KW>  // A words per coefficient (Mm <= KW, KW a multiple of 8)
+__global__ void __launch_bounds__(128, 4) k_mac_to_chain_tc(const u32* __restrict__ X, u32 xs, u32 G, DevTab T,
+                                                           const uint4* __restrict__ Bglob, u64* __restrict__ out) {
+    constexpr int K = 4 * KW, KSTEPS = K / 32, NC = 64;
+    __shared__ __align__(128) uint4 Bs[NC * K / 16];
+    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ u32 tmem_base_sh;
+    __shared__ u32 sA[KW], sH[KW], sHs[KW];
+    __shared__ u64 sMF[KW], sQ[kMaxL], sMu[kMaxL], sNeg[kMaxL];
+    const u32 tid = threadIdx.x, warp = tid >> 5;
+    const u32 N = T.N, L = T.L, Mm = T.Mm;
+    for (u32 x = tid; x < NC * K / 16; x += blockDim.x) Bs[x] = Bglob[x];
+    for (u32 k = tid; k < (u32)KW; k += blockDim.x) {
+        const bool on = k < Mm;
+        sA[k] = on ? T.a[k] : 1u;  // padded primes: v = 0
+        sH[k] = on ? T.mhat[k] : 0u;
+        sHs[k] = on ? T.mhat_s[k] : 0u;
+        sMF[k] = on ? T.mF[k] : 0ull;
+    }
+    for (u32 i = tid; i < L; i += blockDim.x) {
+        sQ[i] = T.q[i];
+        sMu[i] = T.q_mu96[i];
+        sNeg[i] = T.MnegQ[i];
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                     "n"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // B visible to the tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const u32 tbase = tmem_base_sh;
+    const u32 ta = tbase + ((warp * 32u) << 16);  // A columns [0, KW), this warp's lanes
+    const u32 td = ta + KW;                       // D columns [KW, KW + 64)
+    const u64 bdesc0 = ((u64)((smem_u32(Bs) >> 4) & 0x3fff)) | ((u64)(128 >> 4) << 16) |
+                       ((u64)((K / 16 * 128) >> 4) << 32) | (1ull << 46);
+    const u32 idesc = (2u << 4) | ((u32)(NC >> 3) << 17) | ((u32)(128 >> 4) << 24);  // D s32, A / B u8, M 128
+    const u32 gsh = 64 - T.gbits;
+    const size_t total = (size_t)G * N;
+    u32 phase = 0;
+    for (size_t base = (size_t)blockIdx.x * 128; base < total; base += (size_t)gridDim.x * 128) {
+        const size_t idx = base + tid;
+        const bool live = idx < total;
+        const size_t g = live ? idx / N : 0;
+        const u32 n = live ? (u32)(idx % N) : 0;
+        u32 v[KW];
+        {
+            u32 x[KW];
+#pragma unroll
+            for (int k = 0; k < KW; ++k) x[k] = (live && k < (int)Mm) ? __ldg(X + (g * xs + k) * N + n) : 0u;
+#pragma unroll
+            for (int k = 0; k < KW; ++k) v[k] = red32(shoup32(x[k], sH[k], sHs[k], sA[k]), sA[k]);
+        }
+        u64 gs = 0;
+#pragma unroll
+        for (int k = 0; k < KW; ++k) gs += (u64)v[k] * sMF[k];
+        const u32 gamma = (u32)((gs + (1ull << (gsh - 1))) >> gsh);
+#pragma unroll
+        for (int x = 0; x < KW; x += 8)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(ta + x),
+                         "r"(v[x]), "r"(v[x + 1]), "r"(v[x + 2]), "r"(v[x + 3]), "r"(v[x + 4]), "r"(v[x + 5]),
+                         "r"(v[x + 6]), "r"(v[x + 7])
+                         : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+            for (int st = 0; st < KSTEPS; ++st) {
+                const u64 bd = bdesc0 + (u64)((st * 2 * 128) >> 4);  // 2 K chunks of 16 B per step
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tbase + KW),
+                    "r"(tbase + (u32)(st * 8)), "l"(bd), "r"(idesc), "r"(st)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                             smem_u32(&mbar))
+                         : "memory");
+        }
+        mbar_wait_sleep(&mbar, phase);
+        phase ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+        for (int i0 = 0; i0 < kMaxL; i0 += 2) {  // 2 chain primes (16 columns) per TMEM load
+            if (i0 >= (int)L) break;  // warp-uniform
+            u32 C[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+                "%15}, [%16];\n"
+                : "=r"(C[0]), "=r"(C[1]), "=r"(C[2]), "=r"(C[3]), "=r"(C[4]), "=r"(C[5]), "=r"(C[6]), "=r"(C[7]),
+                  "=r"(C[8]), "=r"(C[9]), "=r"(C[10]), "=r"(C[11]), "=r"(C[12]), "=r"(C[13]), "=r"(C[14]), "=r"(C[15])
+                : "r"(td + 8 * i0)
+                : "memory");
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            if (live) {
+#pragma unroll
+                for (int ii = 0; ii < 2; ++ii) {
+                    const u32 i = i0 + ii;
+                    if (i < L) {
+                        const u32* c = C + 8 * ii;
+                        const u64 P = (u64)c[0] + ((u64)c[1] << 8) + ((u64)c[2] << 16) + ((u64)c[3] << 24);
+                        const u64 Q = (u64)c[4] + ((u64)c[5] << 8) + ((u64)c[6] << 16) + ((u64)c[7] << 24);
+                        u64 lo = P + (Q << 32);
+                        u64 hi = (Q >> 32) + (lo < P ? 1u : 0u);
+                        mac128(hi, lo, (u64)gamma, sNeg[i]);  // < 2^80 + 2^65
+                        out[(g * L + i) * N + n] = reduce96((u32)hi, lo, sQ[i], sMu[i]);
                     }
                 }
             }
