@@ -94,6 +94,7 @@ struct Ctx {
     bool lift_tc = true;              // "lift_tc": tensor-core centred lift (0: k_lift on the CUDA cores)
     DevBuf m2c_B;                     // k_mac_to_chain_tc B matrix
     u32 m2c_kw = 0;                   // k_mac_to_chain_tc A words (0: not available)
+    bool ks_fixed = true;             // "ks_fixed": compile-time-shape key-switch MAC (k_ks_mac32t) for the configured shapes
     bool m2c_tc = true;               // "m2c_tc": tensor-core MAC basis -> chain conversion (0: k_mac_to_chain)
     u32 rtc_nc = 0;                   // k_round_tma GEMM width (0: no instance for this JM / Mm)
     int round_kind = 2;               // 2 tensor-core (k_round_tma), 0 IMAD only (k_round_mac_t); option "round"
@@ -997,7 +998,23 @@ static bool key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
                 c.next_units = (double)B * 2 * L * K * N * D;  // residue products (MACs)
                 launch_grid(c, "k_ks_mac32", kern, cfg, (const u32*)dA, kA, B, L, N, C, (const u64*)c.T.abar, mA);
             };
-            if (c.ks_wide && D == 7) ks_s(k_ks_mac32s<7, 6, 8, 3>);
+            auto ks_t = [&](auto kern) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(gx, gy);
+                cfg.blockDim = dim3(128);
+                cfg.stream = c.st;
+                c.next_units = (double)B * 2 * L * K * N * D;  // residue products (MACs)
+                launch_grid(c, "k_ks_mac32", kern, cfg, (const u32*)dA, kA, B, c.T.a, c.T.apinv, c.T.a2_64, mA);
+            };
+            // every size at compile time (immediate plane offsets, Montgomery reductions) for the
+            // configured shapes: (log N, K', D, 2L)
+            const u32 lg = c.cp.logN;
+            if (c.ks_fixed && c.ks_wide && lg == 14 && K == 3 && D == 25 && L == 8 && c.ks_ci == 4) ks_t(k_ks_mac32t<14, 3, 25, 16, 4, 16, 2>);
+            else if (c.ks_fixed && c.ks_wide && lg == 14 && K == 3 && D == 25 && L == 8 && c.ks_ci == 8) ks_t(k_ks_mac32t<14, 3, 25, 16, 2, 16, 3>);
+            else if (c.ks_fixed && c.ks_wide && lg == 14 && K == 3 && D == 25 && L == 8) ks_t(k_ks_mac32t<14, 3, 25, 16, 2, 8, 3>);
+            else if (c.ks_fixed && c.ks_wide && lg == 13 && K == 3 && D == 14 && L == 5) ks_t(k_ks_mac32t<13, 3, 14, 10, 2, 8, 4>);
+            else if (c.ks_fixed && c.ks_wide && lg == 12 && K == 3 && D == 7 && L == 3) ks_t(k_ks_mac32t<12, 3, 7, 6, 6, 8, 3>);
+            else if (c.ks_wide && D == 7) ks_s(k_ks_mac32s<7, 6, 8, 3>);
             else if (c.ks_wide && D == 14 && c.ks_ci == 2) ks_s(k_ks_mac32s<14, 2, 8, 4, 2>);
             else if (c.ks_wide && D == 14) ks_s(k_ks_mac32s<14, 5, 8, 2>);
             else if (c.ks_wide && D == 25 && c.ks_ci == 2) ks_s(k_ks_mac32s<25, 2, 8, 3, 2>);
@@ -2786,10 +2803,11 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "ks32") { c.ks32 = v != 0; c.ksA_ok = false; }
         else if (k == "tile_rows") c.tile_rows_opt = (u32)std::max(0, v);
         else if (k == "ks_wide") c.ks_wide = v != 0;
-        else if (k == "ks_ci") c.ks_ci = v == 2 ? 2u : 4u;
+        else if (k == "ks_ci") c.ks_ci = (u32)v;
         else if (k == "prep_factors") c.prep_mode = v != 0;
         else if (k == "lift_tc") c.lift_tc = v != 0;
         else if (k == "m2c_tc") c.m2c_tc = v != 0;
+        else if (k == "ks_fixed") c.ks_fixed = v != 0;
         else if (k == "mac_sg") c.mac_sg = v != 0;
         else if (k == "mac_stages") c.mac_stages8 = v >= 8;
         else if (k == "mac_rows") c.mac_rows = v != 0;

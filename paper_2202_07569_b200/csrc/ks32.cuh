@@ -168,6 +168,70 @@ __global__ void __launch_bounds__(128, MINB) k_ks_mac32s(const u32* __restrict__
     }
 }
 
+/// (acc + m a) / 2^32 with m = -acc a^-1 mod 2^32: acc 2^-32 mod a, in [0, 3a) for acc < 2^63 + 2^62.
+__device__ __forceinline__ u32 ks_mont_red64(u64 acc, u32 a, u32 pinv) {
+    const u32 m = (u32)acc * pinv;
+    return (u32)((acc + (u64)m * a) >> 32);
+}
+
+/// Slot-major key-switch MAC with every size a compile-time constant (k_ks_mac32s spent ~9 issued
+/// instructions per product on 64-bit address arithmetic, tail predicates and two Barrett
+/// reductions per output): the digit and output planes of a row are read at immediate offsets
+/// d K'N from one base pointer, the key block of CI columns walks one pointer per digit, and each
+/// output is reduced by Montgomery steps -- chains of <= 12 products (< 2^63.6), one
+/// (acc + m a) >> 32 per chain, their sum times 2^64 mod a (one Montgomery product) restores the
+/// plain residue.  The key-switch primes are the first K' aux primes, so T.apinv / T.a2_64 apply.
+/// Grid: (K'N / 128, row splits); rows [b0, b1) of this split in groups of G.
+template <int LOGN, int KP, int D, int NCI, int CI, int G, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_ks_mac32t(const u32* __restrict__ dig, const u32* __restrict__ key, u32 B,
+                                                      const u32* __restrict__ ap, const u32* __restrict__ apinv,
+                                                      const u32* __restrict__ a2_64, u32* __restrict__ out) {
+    constexpr u32 N = 1u << LOGN, KN = KP * N;
+    constexpr int NCH = (D + 11) / 12;           // chains of <= 12 products
+    constexpr int CL = (D + NCH - 1) / NCH;      // products per chain
+    static_assert(NCI % CI == 0 && KN % 128 == 0, "k_ks_mac32t shape");
+    const u32 slot = blockIdx.x * 128 + threadIdx.x;  // j N + n
+    const u32 j = slot >> LOGN;
+    const u32 a = ap[j], pinv = apinv[j], r64 = a2_64[j];
+    const u32 b0 = (u32)(((u64)B * blockIdx.y) / gridDim.y), b1 = (u32)(((u64)B * (blockIdx.y + 1)) / gridDim.y);
+#pragma unroll 1
+    for (u32 g0 = b0; g0 < b1; g0 += G) {
+        const u32 g1 = min(b1, g0 + G);
+#pragma unroll 1
+        for (u32 c0 = 0; c0 < (u32)NCI; c0 += CI) {
+            u32 kr[D][CI];
+            const u32* kp = key + (size_t)c0 * KN + slot;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+#pragma unroll
+                for (int c = 0; c < CI; ++c) kr[d][c] = __ldg(kp + (u32)c * KN);
+                kp += (size_t)NCI * KN;
+            }
+#pragma unroll 2
+            for (u32 b = g0; b < g1; ++b) {
+                const u32* dp = dig + (size_t)b * D * KN + slot;
+                u32 dr[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) dr[d] = dp[(u32)d * KN];
+                u32* op = out + ((size_t)b * NCI + c0) * KN + slot;
+#pragma unroll
+                for (int c = 0; c < CI; ++c) {
+                    u32 r = 0;
+#pragma unroll
+                    for (int h = 0; h < NCH; ++h) {
+                        u64 s = 0;
+#pragma unroll
+                        for (int d = h * CL; d < (h + 1) * CL && d < D; ++d) s += (u64)dr[d] * kr[d][c];
+                        const u32 x = ks_mont_red64(s, a, pinv);  // [0, 3a)
+                        r += red32(red32(x, 2 * a), a);           // NCH <= 3: r < 3a < 2^32
+                    }
+                    op[(u32)c * KN] = red32(mont32(r, r64, a, pinv), a);
+                }
+            }
+        }
+    }
+}
+
 /// ks[b][c][i][n] = (centred CRT of the K' residues x_j) mod q_i.  x: [B][2][L][K'][N] in [0, a_j).
 /// add (optional): the result is (ks + add[b * add_stride + (c L + i) N + n]) mod q_i -- the
 /// relinearisation's (c0 + ks0, c1 + ks1), bfv.cpp:859-869 -- and scale (optional, != 0) then
