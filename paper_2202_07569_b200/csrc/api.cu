@@ -1026,8 +1026,12 @@ static bool key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
                 launch(c, k_ks_mac32, blocks((size_t)B * 2 * L * K * N, 256), 256, 0, (const u32*)dA, kA, B, D, L, N, C,
                        (const u64*)c.T.abar, mA);
             ntt32(c, mA, B * 2 * L * K, K, K, 0, true, 0);
-            launch(c, k_ks_crt, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u32*)mA, B, L, N, C, c.T, ks, add,
-                   add_stride, scale);
+            if (K == 3 && c.ks_fixed)
+                launch_named(c, "k_ks_crt", k_ks_crt3, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u32*)mA, B, L, N, C,
+                             c.T, ks, add, add_stride, scale);
+            else
+                launch(c, k_ks_crt, blocks((size_t)B * 2 * L * N, 256), 256, 0, (const u32*)mA, B, L, N, C, c.T, ks, add,
+                       add_stride, scale);
             return true;
         }
     }

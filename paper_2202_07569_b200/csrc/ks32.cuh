@@ -283,4 +283,50 @@ __global__ void k_ks_crt(const u32* __restrict__ x, u32 B, u32 L, u32 N, const _
     ks[idx] = v;
 }
 
+/// k_ks_crt for K' = 3 with the sums kept in 96 bits: y_j < 2^30 times (prod_{k<j} a_k mod q_i) < 2^60
+/// is two 32 x 32 products, and sum_j y_j P_ij < 2^92 needs one reduce96 (the generic kernel forms
+/// 64 x 64 -> 128-bit products and reduces twice: ~330 instructions per output at C5).
+__global__ void __launch_bounds__(256) k_ks_crt3(const u32* __restrict__ x, u32 B, u32 L, u32 N,
+                                                 const __grid_constant__ KsCrt C, DevTab T, u64* __restrict__ ks,
+                                                 const u64* __restrict__ add, size_t add_stride, u64 scale) {
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (size_t)B * 2 * L * N) return;
+    const size_t bci = idx / N;  // (b 2 + c) L + i
+    const u32 n = (u32)(idx % N);
+    const u32 i = (u32)(bci % L);
+    const u32* xp = x + bci * 3 * N + n;
+    const u32 x0 = xp[0], x1 = xp[N], x2 = xp[2 * (size_t)N];
+    const u32 a1 = C.a[1], a2 = C.a[2];
+    // Garner (mixed radix): v = y0 + y1 a0 + y2 a0 a1
+    const u32 y0 = x0;
+    u32 t = red32(x1 + a1 - red32(y0, a1), a1);
+    const u32 y1 = red32(shoup32(t, C.cinv[1][0], C.cinv_s[1][0], a1), a1);
+    t = red32(x2 + a2 - red32(y0, a2), a2);
+    t = red32(shoup32(t, C.cinv[2][0], C.cinv_s[2][0], a2), a2);
+    t = red32(t + a2 - red32(y1, a2), a2);
+    const u32 y2 = red32(shoup32(t, C.cinv[2][1], C.cinv_s[2][1], a2), a2);
+    // centred: v > (A'-1)/2 <=> mixed-radix digits (top first) exceed the half digits
+    const bool neg = y2 != C.half[2] ? y2 > C.half[2] : (y1 != C.half[1] ? y1 > C.half[1] : y0 > C.half[0]);
+    const u64 q = T.q[i];
+    const u64 P1 = C.pmod[i][1], P2 = C.pmod[i][2];  // P0 = 1
+    // 96-bit sum y0 + y1 P1 + y2 P2 (< 2^92)
+    u64 lo = (u64)y0 + (u64)y1 * (u32)P1;           // < 2^63
+    const u64 l2 = (u64)y2 * (u32)P2;
+    lo += l2;
+    u32 hi = lo < l2 ? 1u : 0u;
+    const u64 h = (u64)y1 * (u32)(P1 >> 32) + (u64)y2 * (u32)(P2 >> 32);  // < 2^59, weight 2^32
+    const u64 hs = h << 32;
+    lo += hs;
+    hi += (u32)(h >> 32) + (lo < hs ? 1u : 0u);
+    u64 v = reduce96(hi, lo, q, T.q_mu96[i]);
+    if (neg) v = v >= C.amod[i] ? v - C.amod[i] : v + q - C.amod[i];
+    if (add) {
+        const size_t b = bci / (2 * L), ci = bci % (2 * L);
+        v += add[b * add_stride + ci * N + n];
+        if (v >= q) v -= q;
+    }
+    if (scale) v = reduce128(__umul64hi(v, scale), v * scale, q, T.q_mu96[i]);
+    ks[idx] = v;
+}
+
 }  // namespace cwgpu

@@ -334,24 +334,16 @@ __global__ void __launch_bounds__(RegNtt<LOGN>::T, NP == 1 ? RegNtt<LOGN>::MINB 
             x[r] = __ldg(X + ((u32)r << (LOGN - WB)));
             y[r] = __ldg(Y + ((u32)r << (LOGN - WB)));
         }
+#pragma unroll
+        for (int r = 0; r < E; ++r) v[q][r] = red32(mont32(x[r], y[r], p, pinv), p);
         if (comp == 1) {
-            // A0 B1 + A1 B0: both 60-bit products in one u64, one Montgomery reduction for the sum
-            // (operands < 2p < 2^31: sum < 2^63), result in [0, 2p) as the INTT expects
-            u32 x2[E], y2[E];
 #pragma unroll
             for (int r = 0; r < E; ++r) {
-                x2[r] = __ldg(A + o1 + ((u32)r << (LOGN - WB)));
-                y2[r] = __ldg(B + ((u32)r << (LOGN - WB)));
+                x[r] = __ldg(A + o1 + ((u32)r << (LOGN - WB)));
+                y[r] = __ldg(B + ((u32)r << (LOGN - WB)));
             }
 #pragma unroll
-            for (int r = 0; r < E; ++r) {
-                const u64 t = (u64)x[r] * y[r] + (u64)x2[r] * y2[r];
-                const u32 m = (u32)t * pinv;
-                v[q][r] = red32((u32)((t + (u64)m * p) >> 32), 2 * p);  // operands < 2p: < 4p before
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < E; ++r) v[q][r] = red32(mont32(x[r], y[r], p, pinv), p);
+            for (int r = 0; r < E; ++r) v[q][r] += red32(mont32(x[r], y[r], p, pinv), p);
         }
     }
     nttw_inv<LOGN, WB, NP>(v, smd, T.airp + (size_t)j * N, T.airps + (size_t)j * N, p);
