@@ -94,6 +94,9 @@ struct Ctx {
     bool lift_tc = true;              // "lift_tc": tensor-core centred lift (0: k_lift on the CUDA cores)
     DevBuf m2c_B;                     // k_mac_to_chain_tc B matrix
     u32 m2c_kw = 0;                   // k_mac_to_chain_tc A words (0: not available)
+    DevBuf dec_B;                     // k_decompose_tc B matrix (bytes of q / q_i by column)
+    bool dec_ok = false;              // k_decompose_tc available (q below 448 bits)
+    bool dec_tc = true;               // "dec_tc": tensor-core digit decomposition (0: k_decompose_t)
     bool ks_fixed = true;             // "ks_fixed": compile-time-shape key-switch MAC (k_ks_mac32t) for the configured shapes
     bool m2c_tc = true;               // "m2c_tc": tensor-core MAC basis -> chain conversion (0: k_mac_to_chain)
     u32 rtc_nc = 0;                   // k_round_tma GEMM width (0: no instance for this JM / Mm)
@@ -716,6 +719,23 @@ static void build_tables(Ctx& c) {
         CK(cudaMemcpy(c.m2c_B.p, Bm.data(), Bm.size(), cudaMemcpyHostToDevice));
         c.m2c_kw = KW;
     }
+    // tensor-core digit decomposition (k_decompose_tc): B [64][K = 64], column s, K byte 8 i + a = byte
+    // s - a of q / q_i (32-bit limbs qov [L][QW])
+    c.dec_ok = false;
+    if (L <= 8 && 4 * T.QW + 7 < 64) {
+        const u32 K = 64, NCd = 64;
+        std::vector<unsigned char> Bd((size_t)NCd * K, 0);
+        auto put = [&](u32 n, u32 kb, unsigned char v) {
+            Bd[(size_t)(n / 8) * (K / 16 * 128) + (kb / 16) * 128 + (n % 8) * 16 + kb % 16] = v;
+        };
+        for (u32 i = 0; i < L; ++i)
+            for (u32 aa = 0; aa < 8; ++aa)
+                for (u32 sb = 0; sb < 4 * T.QW && sb + aa < NCd; ++sb)
+                    put(sb + aa, 8 * i + aa, (unsigned char)(qov[(size_t)i * T.QW + sb / 4] >> (8 * (sb % 4))));
+        c.dec_B.ensure(Bd.size());
+        CK(cudaMemcpy(c.dec_B.p, Bd.data(), Bd.size(), cudaMemcpyHostToDevice));
+        c.dec_ok = true;
+    }
     // device copy of the table itself (slow paths read it through T.self)
     c.tab_self.ensure(sizeof(DevTab));
     c.T.self = static_cast<const DevTab*>(c.tab_self.p);
@@ -980,8 +1000,12 @@ static bool key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
             }
             u32* dA = c.ksdig.get<u32>((size_t)B * D * K * N);
             u32* mA = c.ksmac.get<u32>((size_t)B * 2 * L * K * N);
-            launch_named(c, "k_decompose", k_decompose_t<true>, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv,
-                         B, bits, D, c.T, (u64*)nullptr, dA, K);
+            if (c.dec_tc && c.dec_ok && bits == 16)
+                launch_named(c, "k_decompose", k_decompose_tc, std::min<size_t>(blocks((size_t)B * N, 128), (size_t)c.n_sms * 4),
+                             128, 0, polys, stride, ginv, B, D, c.T, c.dec_B.ptr<uint4>(), dA, K);
+            else
+                launch_named(c, "k_decompose", k_decompose_t<true>, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv,
+                             B, bits, D, c.T, (u64*)nullptr, dA, K);
             ntt32(c, dA, B * D * K, K, K, 0, false, 0);
             // shared-load variant once the level is wide enough to fill the GPU (B >= 64 rows of
             // K N threads / 2); narrow levels and long digit chains keep one output per thread
@@ -2812,6 +2836,7 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "lift_tc") c.lift_tc = v != 0;
         else if (k == "m2c_tc") c.m2c_tc = v != 0;
         else if (k == "ks_fixed") c.ks_fixed = v != 0;
+        else if (k == "dec_tc") c.dec_tc = v != 0;
         else if (k == "mac_sg") c.mac_sg = v != 0;
         else if (k == "mac_stages") c.mac_stages8 = v >= 8;
         else if (k == "mac_rows") c.mac_rows = v != 0;

@@ -602,4 +602,183 @@ __global__ void __launch_bounds__(128, 4) k_mac_to_chain_tc(const u32* __restric
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(128));
 }
 
+// ---------------------------------------------------------------------------------------
+// Digit decomposition on the tensor cores (decompose_digits, bfv.cpp:316-339, 16-bit digits written
+// as key-switch aux residues): the exact CRT x = sum_i y_i (q/q_i) - alpha q in positional form.
+//
+// The L x QW limb products of crt_exact_cols are one int8 GEMM per 128 coefficients: A = the bytes
+// of the y_i (K = 64, from TMEM), B[8 i + a][s] = byte s - a of q / q_i, so column s is the base-256
+// column sum of sum_i y_i (q/q_i) (< 64 255^2 < 2^22); the epilogue carries the 64 columns into
+// 32-bit limbs, subtracts alpha q with one correction (as crt_exact_cols) and cuts the digits.
+// The CUDA-core kernel issues ~4,700 instructions per coefficient at C5 (unrolled limb products,
+// instruction-cache misses).  Requires 4 QW + 7 < 64 (q below 448 bits).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128, 4) k_decompose_tc(const u64* __restrict__ polys, size_t stride, u64 ginv, u32 B,
+                                                        u32 D, DevTab T, const uint4* __restrict__ Bglob,
+                                                        u32* __restrict__ aux_out, u32 K) {
+    constexpr int KB = 64, KSTEPS = KB / 32, ACOLS = KB / 4, NC = 64;
+    __shared__ __align__(128) uint4 Bs[NC * KB / 16];
+    __shared__ __align__(8) unsigned long long mbar;
+    __shared__ u32 tmem_base_sh;
+    __shared__ u32 sqw[kQW];
+    const u32 tid = threadIdx.x, warp = tid >> 5;
+    const u32 N = T.N, L = T.L, QW = T.QW;
+    for (u32 x = tid; x < NC * KB / 16; x += blockDim.x) Bs[x] = Bglob[x];
+    for (u32 x = tid; x < (u32)kQW; x += blockDim.x) sqw[x] = x < QW ? T.qw[x] : 0u;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
+                     "n"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // B visible to the tensor core
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const u32 tbase = tmem_base_sh;
+    const u32 ta = tbase + ((warp * 32u) << 16);  // A columns [0, 16), this warp's lanes
+    const u32 td = ta + ACOLS;                    // D columns [16, 80)
+    const u64 bdesc0 = ((u64)((smem_u32(Bs) >> 4) & 0x3fff)) | ((u64)(128 >> 4) << 16) |
+                       ((u64)((KB / 16 * 128) >> 4) << 32) | (1ull << 46);
+    const u32 idesc = (2u << 4) | ((u32)(NC >> 3) << 17) | ((u32)(128 >> 4) << 24);  // D s32, A / B u8, M 128
+    const size_t total = (size_t)B * N;
+    u32 phase = 0;
+    for (size_t base = (size_t)blockIdx.x * 128; base < total; base += (size_t)gridDim.x * 128) {
+        const size_t idx = base + tid;
+        const bool live = idx < total;
+        const u32 b = live ? (u32)(idx / N) : 0, n = live ? (u32)(idx % N) : 0;
+        u32 w[ACOLS];
+        u32 alpha = 0;
+        {
+            const u64* pb = polys + (size_t)b * stride;
+            u32 src = n;
+            bool neg = false;
+            if (ginv) {
+                const u32 sidx = (u32)(((u64)n * ginv) & (2 * N - 1));
+                neg = sidx >= N;
+                src = neg ? sidx - N : sidx;
+            }
+            u64 res[kMaxL], y[kMaxL];
+#pragma unroll
+            for (int i = 0; i < kMaxL; ++i) {
+                res[i] = 0;
+                if (live && i < (int)L) {
+                    u64 v = pb[(size_t)i * N + src];
+                    if (neg && v) v = T.q[i] - v;
+                    res[i] = v;
+                }
+            }
+            crt_prepare(res, T, y, &alpha);
+#pragma unroll
+            for (int i = 0; i < kMaxL; ++i) {
+                w[2 * i] = i < (int)L ? (u32)y[i] : 0u;
+                w[2 * i + 1] = i < (int)L ? (u32)(y[i] >> 32) : 0u;
+            }
+        }
+#pragma unroll
+        for (int x = 0; x < ACOLS; x += 8)
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(ta + x),
+                         "r"(w[x]), "r"(w[x + 1]), "r"(w[x + 2]), "r"(w[x + 3]), "r"(w[x + 4]), "r"(w[x + 5]),
+                         "r"(w[x + 6]), "r"(w[x + 7])
+                         : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+            for (int st = 0; st < KSTEPS; ++st) {
+                const u64 bd = bdesc0 + (u64)((st * 2 * 128) >> 4);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tbase + ACOLS),
+                    "r"(tbase + (u32)(st * 8)), "l"(bd), "r"(idesc), "r"(st)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                             smem_u32(&mbar))
+                         : "memory");
+        }
+        mbar_wait_sleep(&mbar, phase);
+        phase ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        // column sums -> carried 32-bit limbs S (16 limbs from the 64 columns, the carry in limb 16)
+        u32 S[kQW + 2];
+        u64 carry = 0;
+#pragma unroll
+        for (int c0 = 0; c0 < NC; c0 += 16) {
+            u32 C[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+                "%15}, [%16];\n"
+                : "=r"(C[0]), "=r"(C[1]), "=r"(C[2]), "=r"(C[3]), "=r"(C[4]), "=r"(C[5]), "=r"(C[6]), "=r"(C[7]),
+                  "=r"(C[8]), "=r"(C[9]), "=r"(C[10]), "=r"(C[11]), "=r"(C[12]), "=r"(C[13]), "=r"(C[14]), "=r"(C[15])
+                : "r"(td + c0)
+                : "memory");
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                const u64 s = carry + (u64)C[4 * l] + ((u64)C[4 * l + 1] << 8) + ((u64)C[4 * l + 2] << 16) +
+                              ((u64)C[4 * l + 3] << 24);
+                S[c0 / 4 + l] = (u32)s;
+                carry = s >> 32;
+            }
+        }
+        S[16] = (u32)carry;
+        S[17] = 0;
+        // X = S - alpha q (alpha: the fractional estimate, short by at most one) and one correction
+        u32 X[kQW + 2];
+        {
+            u64 c = 0;
+            u32 bb = 0;
+#pragma unroll
+            for (int x = 0; x < kQW + 2; ++x) {
+                const u64 pk = (x < kQW ? (u64)alpha * sqw[x] : 0) + c;
+                c = pk >> 32;
+                const u32 pl = (u32)pk, sx = S[x];
+                const u32 r1 = sx - pl, b1 = sx < pl;
+                const u32 r2 = r1 - bb, b2 = r1 < bb;
+                X[x] = r2;
+                bb = b1 | b2;
+            }
+            int ge = 1;
+#pragma unroll
+            for (int x = kQW + 1; x >= 0; --x) {
+                const u32 qv = x < kQW ? sqw[x] : 0u;
+                if (ge == 1 && X[x] != qv) ge = X[x] > qv ? 2 : 0;
+            }
+            if (ge != 0) {
+                u32 b2 = 0;
+#pragma unroll
+                for (int x = 0; x < kQW + 2; ++x) {
+                    const u32 qv = x < kQW ? sqw[x] : 0u;
+                    const u32 r1 = X[x] - qv, c1 = X[x] < qv;
+                    const u32 r2 = r1 - b2, c2 = r1 < b2;
+                    X[x] = r2;
+                    b2 = c1 | c2;
+                }
+            }
+        }
+        if (live) {
+            u32* o = aux_out + (size_t)b * D * K * N + n;
+#pragma unroll
+            for (int d = 0; d < 2 * kQW; ++d) {
+                if (d < (int)D) {
+                    const u32 v = (X[d >> 1] >> (16 * (d & 1))) & 0xffffu;
+                    for (u32 j = 0; j < K; ++j) o[((size_t)d * K + j) * N] = v;  // digits < 2^16 < a_j
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();  // D and A are rewritten by the next tile
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(128));
+}
+
 }  // namespace cwgpu

@@ -47,7 +47,7 @@ def test_config_full_params_reduced_rows(gpu, reflib, name, rows):
     _run(reflib, configs.config(name), rows)
 
 
-@pytest.mark.parametrize("opts", [{}, {"m2c_tc": 0, "lift_tc": 0, "ks_fixed": 0}], ids=["default", "cuda-core-conversions"])
+@pytest.mark.parametrize("opts", [{}, {"m2c_tc": 0, "lift_tc": 0, "ks_fixed": 0, "dec_tc": 0}], ids=["default", "cuda-core-conversions"])
 def test_config5_keyword_arith_reduced_rows(gpu, reflib, opts):
     """Config 5: N = 16384, 8 x 50-bit primes (400-bit q), t = 786433, arithmetic operator
     k = 4 over CW(569, 4) keyword codewords, s = 2, c = 10 (1023 substitutions).  Default: the chain
@@ -115,9 +115,10 @@ def test_payload_mac_kernels_agree_under_repetition(gpu):
     ({"lift_tc": 0}, "k_round_tma"),                    # centred lift on the CUDA cores (k_lift)
     ({"m2c_tc": 0}, "k_round_tma"),                     # MAC basis -> chain on the CUDA cores (k_mac_to_chain)
     ({"ks_fixed": 0}, "k_round_tma"),                   # run-time-shape key-switch MAC (k_ks_mac32s)
+    ({"dec_tc": 0}, "k_round_tma"),                     # digit decomposition on the CUDA cores (k_decompose_t)
     ({"force_exact": 1}, "k_round_tma"),                # every rounding through round_exact
     ({"force_exact": 1, "fuse_mac": 0}, "k_round_tma"),
-], ids=["unfused", "default", "one-stream", "one-gemm", "imad-round", "ks64", "lift-cuda", "m2c-cuda", "ks-runtime-shape", "exact",
+], ids=["unfused", "default", "one-stream", "one-gemm", "imad-round", "ks64", "lift-cuda", "m2c-cuda", "ks-runtime-shape", "decompose-cuda", "exact",
         "exact-unfused"])
 def test_answer_path_variants_match_reference(gpu, reflib, opts, kernel):
     """Every kernel variant of the answer path (tensor/rounding/NTT/MAC fusions, TMA feeds, the
