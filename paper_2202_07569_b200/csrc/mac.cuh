@@ -225,22 +225,19 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
     }
     const u32 p = T.a[k];
     const u64 pb = T.abar[k];
-    u32 accr[QB][SG][NC][2];
+    // lazy accumulation: 60-bit products summed in u64, folded every 8 rows with
+    // x -> (x >> 32) (2^32 mod a) + (x & 2^32 - 1) (< 2^62 + 2^32: one IMAD.WIDE instead of a Barrett
+    // reduction), one Barrett reduction per output at the end of the chunk
+    const u32 c32 = bar64(1ull << 32, p, pb);
+    u64 acc64[QB][SG][NC][2];
 #pragma unroll
     for (int q = 0; q < QB; ++q)
 #pragma unroll
         for (int g = 0; g < SG; ++g)
 #pragma unroll
-            for (int c = 0; c < NC; ++c) accr[q][g][c][0] = accr[q][g][c][1] = 0;
-    for (u32 g0 = 0; g0 < rows; g0 += 16) {
-        const u32 ge = min(rows, g0 + 16);
-        u64 acc64[QB][SG][NC][2];
-#pragma unroll
-        for (int q = 0; q < QB; ++q)
-#pragma unroll
-            for (int g = 0; g < SG; ++g)
-#pragma unroll
-                for (int c = 0; c < NC; ++c) acc64[q][g][c][0] = acc64[q][g][c][1] = 0;
+            for (int c = 0; c < NC; ++c) acc64[q][g][c][0] = acc64[q][g][c][1] = 0;
+    for (u32 g0 = 0; g0 < rows; g0 += 8) {
+        const u32 ge = min(rows, g0 + 8);
         for (u32 i = g0; i < ge; ++i) {
             const u32 st = i % ST;
             mbar_wait(&full[st], (i / ST) & 1);
@@ -263,15 +260,17 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
             __syncwarp();
             if ((tid & 31) == 0) mbar_arrive(&empty[st]);
         }
+        if (ge < rows) {
 #pragma unroll
-        for (int q = 0; q < QB; ++q)
+            for (int q = 0; q < QB; ++q)
 #pragma unroll
-            for (int g = 0; g < SG; ++g)
+                for (int g = 0; g < SG; ++g)
 #pragma unroll
-                for (int c = 0; c < NC; ++c)
+                    for (int c = 0; c < NC; ++c)
 #pragma unroll
-                    for (int e = 0; e < 2; ++e)
-                        accr[q][g][c][e] = red32(accr[q][g][c][e] + bar64(acc64[q][g][c][e], p, pb), p);
+                        for (int e = 0; e < 2; ++e)
+                            acc64[q][g][c][e] = (u64)(u32)(acc64[q][g][c][e] >> 32) * c32 + (u32)acc64[q][g][c][e];
+        }
     }
     if (rows == 0) return;
     const u32 n = blk * kMacBlockQ + 2 * tid;
@@ -282,8 +281,8 @@ __global__ void __launch_bounds__(288, 2) k_mac_tma_q(const __grid_constant__ ZP
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 unsigned long long* o = Zp.acc[q] + (((size_t)(sg0 + g) * 3 + c) * Mm + k) * N + n;
-                atomicAdd(o, (unsigned long long)accr[q][g][c][0]);
-                atomicAdd(o + 1, (unsigned long long)accr[q][g][c][1]);
+                atomicAdd(o, (unsigned long long)bar64(acc64[q][g][c][0], p, pb));
+                atomicAdd(o + 1, (unsigned long long)bar64(acc64[q][g][c][1], p, pb));
             }
 }
 

@@ -33,6 +33,15 @@ for r in rows[2:]:
     if pat and not pat.search(name):
         continue
     vals = {k: r[col[v]] for k, v in want.items() if v in col}
+    # ncu prints each metric in its own unit (row 1 of the CSV): bring bytes to MB and times to us
+    units = rows[1]
+    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6}
+    tscale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}
+    for k in ("dram_rd_MB", "dram_wr_MB"):
+        if k in vals:
+            vals[k] = f"{float(vals[k].replace(',', '')) * scale.get(units[col[want[k]]], 1.0):.1f}"
+    if "dur_us" in vals:
+        vals["dur_us"] = f"{float(vals['dur_us'].replace(',', '')) * tscale.get(units[col[want['dur_us']]], 1.0):.1f}"
     st = sorted(((float(r[col[h]] or 0), h.split("stalled_")[1].split("_per")[0]) for h in stall), reverse=True)[:5]
     print(name[:60])
     print("   " + "  ".join(f"{k}={v}" for k, v in vals.items()))
