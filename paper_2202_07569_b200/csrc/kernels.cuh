@@ -450,8 +450,8 @@ __global__ void k_expand_combine(const u64* __restrict__ in, const u64* __restri
     const u32 N = T.N, L = T.L;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)B * L * N) return;
-    const u32 b = (u32)(idx / ((size_t)L * N));
-    const u32 i = (u32)((idx / N) % L), e = (u32)(idx % N);
+    const u32 plane = (u32)(idx >> T.logN), e = (u32)idx & (N - 1);  // N is a power of two
+    const u32 b = plane / L, i = plane % L;
     const u64 q = T.q[i];
     const size_t LN = (size_t)L * N;
     const u64* c0 = in + (size_t)b * 2 * LN + (size_t)i * N;
@@ -494,10 +494,13 @@ __global__ void k_relin_add_shared(const u64* __restrict__ ct3, u32 R, u32 np, c
     const size_t LN = (size_t)L * N;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)R * np * 2 * LN) return;
-    const size_t rp = idx / (2 * LN), x = idx % (2 * LN);
-    const size_t r = rp / np;
-    const u64 q = T.q[(x % LN) / N];
-    const u64 s = ct3[rp * 3 * LN + x] + ks[r * 2 * LN + x];
+    // N is a power of two: plane index by shift, then 32-bit divisions (no 64-bit div / mod)
+    const u32 plane = (u32)(idx >> T.logN), n = (u32)idx & (N - 1);
+    const u32 rp = plane / (2 * L), xp = plane % (2 * L);
+    const u32 r = rp / np;
+    const size_t x = (size_t)xp * N + n;
+    const u64 q = T.q[xp % L];
+    const u64 s = ct3[(size_t)rp * 3 * LN + x] + ks[(size_t)r * 2 * LN + x];
     out2[idx] = s >= q ? s - q : s;
 }
 
@@ -925,9 +928,11 @@ __global__ void k_arith_factors(const u64* __restrict__ entries, const u32* __re
     const size_t LN = (size_t)L * N;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)R * 2 * LN) return;
-    const u32 r = (u32)(idx / (2 * LN));
-    const size_t rem = idx % (2 * LN);
-    const u32 comp = (u32)(rem / LN), i = (u32)((rem / N) % L), n = (u32)(rem % N);
+    // N is a power of two: plane index by shift, then 32-bit divisions (no 64-bit div / mod)
+    const u32 plane = (u32)(idx >> T.logN), n = (u32)idx & (N - 1);
+    const u32 r = plane / (2 * L), pl = plane % (2 * L);
+    const u32 comp = pl / L, i = pl % L;
+    const size_t rem = (size_t)pl * N + n;
     const u64 q = T.q[i];
     u64 s = 0;
     for (u32 p = 0; p < k; ++p) {
@@ -1127,8 +1132,9 @@ __global__ void k_subst_combine(const u64* __restrict__ in, const u64* __restric
     const size_t LN = (size_t)L * N;
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)B * LN) return;
-    const size_t b = idx / LN;
-    const u32 i = (u32)((idx / N) % L), e = (u32)(idx % N);
+    const u32 plane = (u32)(idx >> T.logN), e = (u32)idx & (N - 1);  // N is a power of two
+    const size_t b = plane / L;
+    const u32 i = plane % L;
     const u64 q = T.q[i];
     const u64* c0 = in + b * 2 * LN + (size_t)i * N;
     const u32 s = (u32)(((u64)e * ginv) & (2 * N - 1));

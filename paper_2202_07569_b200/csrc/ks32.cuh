@@ -291,10 +291,10 @@ __global__ void __launch_bounds__(256) k_ks_crt3(const u32* __restrict__ x, u32 
                                                  const u64* __restrict__ add, size_t add_stride, u64 scale) {
     const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (size_t)B * 2 * L * N) return;
-    const size_t bci = idx / N;  // (b 2 + c) L + i
-    const u32 n = (u32)(idx % N);
-    const u32 i = (u32)(bci % L);
-    const u32* xp = x + bci * 3 * N + n;
+    const u32 bci = (u32)(idx >> T.logN);  // (b 2 + c) L + i  (N is a power of two: no 64-bit div / mod)
+    const u32 n = (u32)idx & (N - 1);
+    const u32 i = bci % L;
+    const u32* xp = x + (size_t)bci * 3 * N + n;
     const u32 x0 = xp[0], x1 = xp[N], x2 = xp[2 * (size_t)N];
     const u32 a1 = C.a[1], a2 = C.a[2];
     // Garner (mixed radix): v = y0 + y1 a0 + y2 a0 a1
@@ -321,8 +321,8 @@ __global__ void __launch_bounds__(256) k_ks_crt3(const u32* __restrict__ x, u32 
     u64 v = reduce96(hi, lo, q, T.q_mu96[i]);
     if (neg) v = v >= C.amod[i] ? v - C.amod[i] : v + q - C.amod[i];
     if (add) {
-        const size_t b = bci / (2 * L), ci = bci % (2 * L);
-        v += add[b * add_stride + ci * N + n];
+        const u32 b = bci / (2 * L), ci = bci % (2 * L);
+        v += add[(size_t)b * add_stride + (size_t)ci * N + n];
         if (v >= q) v -= q;
     }
     if (scale) v = reduce128(__umul64hi(v, scale), v * scale, q, T.q_mu96[i]);

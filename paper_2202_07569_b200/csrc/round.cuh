@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(128, 4) k_lift_tc(const u64* __restrict__ src,
     __shared__ u32 sA[kMaxJ], sW[kMaxJ];
     __shared__ u64 sAb[kMaxJ];
     const u32 tid = threadIdx.x, warp = tid >> 5;
-    const u32 N = T.N, L = T.L;
+    const u32 N = T.N, L = T.L, logN = T.logN;  // N is a power of two: no 64-bit divisions
     for (u32 x = tid; x < NC * K / 16; x += blockDim.x) Bs[x] = Bglob[x];
     for (u32 j = tid; j < nj; j += blockDim.x) {
         sA[j] = T.a[j];
@@ -377,6 +377,22 @@ __global__ void __launch_bounds__(128, 4) k_lift_tc(const u64* __restrict__ src,
     const u32 idesc = (2u << 4) | ((u32)(NC >> 3) << 17) | ((u32)(128 >> 4) << 24);  // D s32, A / B u8, M 128
     const size_t total = (size_t)count * 2 * N;
     u32 phase = 0;
+    // the next tile's residues are loaded before this tile's GEMM round trip and epilogue (the
+    // kernel is bound by the per-tile latency chain: 4 CTAs / SM by the TMEM allocation)
+    u64 resn[kMaxL];
+    auto fetch = [&](size_t base) {
+        const size_t idx = base + tid;
+#pragma unroll
+        for (int i = 0; i < kMaxL; ++i) resn[i] = 0;
+        if (idx < total) {
+            const u32 c = (u32)(idx >> (logN + 1)), k = (u32)(idx >> logN) & 1u, n = (u32)(idx & (N - 1));
+            const u64* s = src + (size_t)(sel ? sel[c] : c) * src_stride + (size_t)k * L * N + n;
+#pragma unroll
+            for (int i = 0; i < kMaxL; ++i)
+                if (i < (int)L) resn[i] = s[(size_t)i * N];
+        }
+    };
+    fetch((size_t)blockIdx.x * 128);
     for (size_t base = (size_t)blockIdx.x * 128; base < total; base += (size_t)gridDim.x * 128) {
         const size_t idx = base + tid;
         const bool live = idx < total;
@@ -385,12 +401,13 @@ __global__ void __launch_bounds__(128, 4) k_lift_tc(const u64* __restrict__ src,
         u32 w[ACOLS];
 #pragma unroll
         for (int x = 0; x < ACOLS; ++x) w[x] = 0;
-        if (live) {
-            const u32 c = (u32)(idx / (2 * N)), k = (u32)((idx / N) % 2), n = (u32)(idx % N);
-            const u64* s = src + (size_t)(sel ? sel[c] : c) * src_stride + (size_t)k * L * N + n;
-            u64 res[kMaxL], y[kMaxL];
+        u64 res[kMaxL];
 #pragma unroll
-            for (int i = 0; i < kMaxL; ++i) res[i] = i < (int)L ? s[(size_t)i * N] : 0;
+        for (int i = 0; i < kMaxL; ++i) res[i] = resn[i];
+        if (base + (size_t)gridDim.x * 128 < total) fetch(base + (size_t)gridDim.x * 128);
+        if (live) {
+            const u32 c = (u32)(idx >> (logN + 1)), k = (u32)(idx >> logN) & 1u, n = (u32)(idx & (N - 1));
+            u64 y[kMaxL];
             u32 ip;
             const u64 fr = crt_prepare(res, T, y, &ip);
             rho = crt_round(y, ip, fr, T);
@@ -485,7 +502,7 @@ __global__ void __launch_bounds__(128, 4) k_mac_to_chain_tc(const u32* __restric
     __shared__ u32 sA[KW], sH[KW], sHs[KW];
     __shared__ u64 sMF[KW], sQ[kMaxL], sMu[kMaxL], sNeg[kMaxL];
     const u32 tid = threadIdx.x, warp = tid >> 5;
-    const u32 N = T.N, L = T.L, Mm = T.Mm;
+    const u32 N = T.N, L = T.L, Mm = T.Mm, logN = T.logN;
     for (u32 x = tid; x < NC * K / 16; x += blockDim.x) Bs[x] = Bglob[x];
     for (u32 k = tid; k < (u32)KW; k += blockDim.x) {
         const bool on = k < Mm;
@@ -521,19 +538,27 @@ __global__ void __launch_bounds__(128, 4) k_mac_to_chain_tc(const u32* __restric
     const u32 gsh = 64 - T.gbits;
     const size_t total = (size_t)G * N;
     u32 phase = 0;
+    // the next tile's residues are loaded before this tile's GEMM round trip and epilogue (the
+    // kernel is bound by the per-tile latency chain: 4 CTAs / SM by the TMEM allocation)
+    u32 xn[KW];
+    auto fetch = [&](size_t base) {
+        const size_t idx = base + tid;
+        const bool live = idx < total;
+        const size_t g = live ? idx >> logN : 0;  // N is a power of two: no 64-bit divisions
+        const u32 n = live ? (u32)(idx & (N - 1)) : 0;
+#pragma unroll
+        for (int k = 0; k < KW; ++k) xn[k] = (live && k < (int)Mm) ? __ldg(X + (g * xs + k) * N + n) : 0u;
+    };
+    fetch((size_t)blockIdx.x * 128);
     for (size_t base = (size_t)blockIdx.x * 128; base < total; base += (size_t)gridDim.x * 128) {
         const size_t idx = base + tid;
         const bool live = idx < total;
-        const size_t g = live ? idx / N : 0;
-        const u32 n = live ? (u32)(idx % N) : 0;
+        const size_t g = live ? idx >> logN : 0;
+        const u32 n = live ? (u32)(idx & (N - 1)) : 0;
         u32 v[KW];
-        {
-            u32 x[KW];
 #pragma unroll
-            for (int k = 0; k < KW; ++k) x[k] = (live && k < (int)Mm) ? __ldg(X + (g * xs + k) * N + n) : 0u;
-#pragma unroll
-            for (int k = 0; k < KW; ++k) v[k] = red32(shoup32(x[k], sH[k], sHs[k], sA[k]), sA[k]);
-        }
+        for (int k = 0; k < KW; ++k) v[k] = red32(shoup32(xn[k], sH[k], sHs[k], sA[k]), sA[k]);
+        if (base + (size_t)gridDim.x * 128 < total) fetch(base + (size_t)gridDim.x * 128);
         u64 gs = 0;
 #pragma unroll
         for (int k = 0; k < KW; ++k) gs += (u64)v[k] * sMF[k];
@@ -622,7 +647,7 @@ __global__ void __launch_bounds__(128, 4) k_decompose_tc(const u64* __restrict__
     __shared__ u32 tmem_base_sh;
     __shared__ u32 sqw[kQW];
     const u32 tid = threadIdx.x, warp = tid >> 5;
-    const u32 N = T.N, L = T.L, QW = T.QW;
+    const u32 N = T.N, L = T.L, QW = T.QW, logN = T.logN;
     for (u32 x = tid; x < NC * KB / 16; x += blockDim.x) Bs[x] = Bglob[x];
     for (u32 x = tid; x < (u32)kQW; x += blockDim.x) sqw[x] = x < QW ? T.qw[x] : 0u;
     if (warp == 0) {
@@ -646,31 +671,42 @@ __global__ void __launch_bounds__(128, 4) k_decompose_tc(const u64* __restrict__
     const u32 idesc = (2u << 4) | ((u32)(NC >> 3) << 17) | ((u32)(128 >> 4) << 24);  // D s32, A / B u8, M 128
     const size_t total = (size_t)B * N;
     u32 phase = 0;
+    // the next tile's residues are loaded before this tile's GEMM round trip and epilogue
+    u64 resn[kMaxL];
+    auto fetch = [&](size_t base) {
+        const size_t idx = base + tid;
+        const bool live = idx < total;
+        const u32 b = live ? (u32)(idx >> logN) : 0, n = live ? (u32)(idx & (N - 1)) : 0;
+        const u64* pb = polys + (size_t)b * stride;
+        u32 src = n;
+        bool neg = false;
+        if (ginv) {
+            const u32 sidx = (u32)(((u64)n * ginv) & (2 * N - 1));
+            neg = sidx >= N;
+            src = neg ? sidx - N : sidx;
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxL; ++i) {
+            resn[i] = 0;
+            if (live && i < (int)L) {
+                u64 v = pb[(size_t)i * N + src];
+                if (neg && v) v = T.q[i] - v;
+                resn[i] = v;
+            }
+        }
+    };
+    fetch((size_t)blockIdx.x * 128);
     for (size_t base = (size_t)blockIdx.x * 128; base < total; base += (size_t)gridDim.x * 128) {
         const size_t idx = base + tid;
         const bool live = idx < total;
-        const u32 b = live ? (u32)(idx / N) : 0, n = live ? (u32)(idx % N) : 0;
+        const u32 b = live ? (u32)(idx >> logN) : 0, n = live ? (u32)(idx & (N - 1)) : 0;
         u32 w[ACOLS];
         u32 alpha = 0;
         {
-            const u64* pb = polys + (size_t)b * stride;
-            u32 src = n;
-            bool neg = false;
-            if (ginv) {
-                const u32 sidx = (u32)(((u64)n * ginv) & (2 * N - 1));
-                neg = sidx >= N;
-                src = neg ? sidx - N : sidx;
-            }
             u64 res[kMaxL], y[kMaxL];
 #pragma unroll
-            for (int i = 0; i < kMaxL; ++i) {
-                res[i] = 0;
-                if (live && i < (int)L) {
-                    u64 v = pb[(size_t)i * N + src];
-                    if (neg && v) v = T.q[i] - v;
-                    res[i] = v;
-                }
-            }
+            for (int i = 0; i < kMaxL; ++i) res[i] = resn[i];
+            if (base + (size_t)gridDim.x * 128 < total) fetch(base + (size_t)gridDim.x * 128);
             crt_prepare(res, T, y, &alpha);
 #pragma unroll
             for (int i = 0; i < kMaxL; ++i) {
