@@ -90,6 +90,7 @@ struct Ctx {
     DevBuf rtc_B;                     // k_round_tma B matrix (canonical UMMA K-major layout)
     DevBuf rtc_B2;                    // k_round_tma second-GEMM B matrix (gamma / rho / offset terms)
     DevBuf lift_B;                    // k_lift_tc B matrices (plain, Montgomery)
+    DevBuf lift_W2;                   // k_lift_tc rho constants (a_j - W_j) 2^32 mod a_j (plain, Montgomery)
     u32 lift_nc = 0;                  // k_lift_tc GEMM width (0: not available)
     bool lift_tc = true;              // "lift_tc": tensor-core centred lift (0: k_lift on the CUDA cores)
     DevBuf m2c_B;                     // k_mac_to_chain_tc B matrix
@@ -687,7 +688,8 @@ static void build_tables(Ctx& c) {
             for (u32 j = 0; j < J; ++j)
                 for (u32 i = 0; i < L; ++i) {
                     const u64 p = a[j];
-                    const u64 V = mont ? liftV_m[(size_t)i * J + j] : liftV_n[(size_t)i * J + j];
+                    // with one more factor 2^32: the epilogue reduces by a Montgomery step (x 2^-32)
+                    const u64 V = (((u64)(mont ? liftV_m[(size_t)i * J + j] : liftV_n[(size_t)i * J + j])) << 32) % p;
                     for (u32 aa = 0; aa < 8; ++aa) {
                         const u32 v = (u32)(((u128)V << (8 * aa)) % p);
                         for (u32 b = 0; b < 4; ++b) put(4 * j + b, 8 * i + aa, (unsigned char)(v >> (8 * b)));
@@ -696,6 +698,16 @@ static void build_tables(Ctx& c) {
         }
         c.lift_B.ensure(Bl.size());
         CK(cudaMemcpy(c.lift_B.p, Bl.data(), Bl.size(), cudaMemcpyHostToDevice));
+        // rho term of the lift in the same form: (a_j - W_j) 2^32 mod a_j, [plain | Montgomery][J]
+        std::vector<u32> W2((size_t)2 * J);
+        for (int mont = 0; mont < 2; ++mont)
+            for (u32 j = 0; j < J; ++j) {
+                const u64 p = a[j];
+                const u64 w = mont ? liftW_m[j] : liftW_n[j];
+                W2[(size_t)mont * J + j] = (u32)((((p - w % p) % p) << 32) % p);
+            }
+        c.lift_W2.ensure(W2.size() * 4);
+        CK(cudaMemcpy(c.lift_W2.p, W2.data(), W2.size() * 4, cudaMemcpyHostToDevice));
         c.lift_nc = NCl;
     }
     // tensor-core MAC basis -> chain conversion (k_mac_to_chain_tc): B [64][K = 4 KW] of byte b of
@@ -1216,7 +1228,7 @@ static void lift(Ctx& c, const u64* src, size_t stride, const u32* sel, u32 coun
     c.next_units = (double)items * nj;  // coefficient lifts x output primes
     if (c.lift_tc && c.lift_nc && nj <= c.ab.J && reg32_ok(c.cp.logN)) {
         const uint4* Bm = reinterpret_cast<const uint4*>(c.lift_B.ptr<unsigned char>() + (size_t)mont * c.lift_nc * kLiftK);
-        const u32* W = mont ? c.T.liftW_m : c.T.liftW_n;
+        const u32* W = c.lift_W2.ptr<u32>() + (size_t)mont * c.ab.J;
         const size_t grid = std::min<size_t>(blocks(items, 128), (size_t)148 * 4);
 #define LTC(NCv)                                                                                               \
     if (c.lift_nc == NCv) {                                                                                     \

@@ -333,8 +333,9 @@ __global__ void __launch_bounds__(160, 4) k_round_tma(u32* __restrict__ D, u32 P
 // The dot products over i are one int8 GEMM per 128 coefficients: A = the bytes of the L y_i
 // (K = 64 bytes, from TMEM), B = byte b of (2^(8a) V_ij mod a_j) at column 4 j + b (shared memory,
 // canonical K-major layout), so column group j sums to S_j = sum_b C 2^(8b) < 2^48 with
-// S_j = sum_i y_i V_ij (mod a_j).  The epilogue adds rho (a_j - W_j) and reduces once per prime.
-// V, W: the Montgomery (x 2^32) or plain lift constants, as k_lift.
+// S_j = sum_i y_i V_ij (mod a_j).  The epilogue adds rho (a_j - W_j) and reduces once per prime by a
+// Montgomery step: V and (a_j - W_j) are stored with one more factor 2^32 (on top of the Montgomery
+// (x 2^32) or plain lift constants of k_lift).
 // ---------------------------------------------------------------------------------------
 constexpr int kLiftK = 64;  // 8 chain primes x 8 bytes
 template <int NC>
@@ -346,15 +347,14 @@ __global__ void __launch_bounds__(128, 4) k_lift_tc(const u64* __restrict__ src,
     __shared__ __align__(128) uint4 Bs[NC * K / 16];
     __shared__ __align__(8) unsigned long long mbar;
     __shared__ u32 tmem_base_sh;
-    __shared__ u32 sA[kMaxJ], sW[kMaxJ];
-    __shared__ u64 sAb[kMaxJ];
+    __shared__ u32 sA[kMaxJ], sW[kMaxJ], sPi[kMaxJ];
     const u32 tid = threadIdx.x, warp = tid >> 5;
     const u32 N = T.N, L = T.L, logN = T.logN;  // N is a power of two: no 64-bit divisions
     for (u32 x = tid; x < NC * K / 16; x += blockDim.x) Bs[x] = Bglob[x];
     for (u32 j = tid; j < nj; j += blockDim.x) {
         sA[j] = T.a[j];
-        sW[j] = Wj[j];
-        sAb[j] = T.abar[j];
+        sW[j] = Wj[j];      // (a_j - W_j) 2^32 mod a_j
+        sPi[j] = T.apinv[j];
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
@@ -464,9 +464,11 @@ __global__ void __launch_bounds__(128, 4) k_lift_tc(const u64* __restrict__ src,
                     const u32 j = j0 + jj;
                     if (j < nj) {
                         const u32 a = sA[j];
+                        // the constants carry one more factor 2^32: S < 2^48 + 2^34 a, one Montgomery step
+                        // (x 2^-32) leaves the residue in [0, 2a)
                         const u64 S = (u64)C[4 * jj] + ((u64)C[4 * jj + 1] << 8) + ((u64)C[4 * jj + 2] << 16) +
-                                      ((u64)C[4 * jj + 3] << 24) + (u64)rho * (a - sW[j]);
-                        o[(size_t)j * N] = bar64(S, a, sAb[j]);
+                                      ((u64)C[4 * jj + 3] << 24) + (u64)rho * sW[j];
+                        o[(size_t)j * N] = red32(mont_red64(S, a, sPi[j]), a);
                     }
                 }
             }
