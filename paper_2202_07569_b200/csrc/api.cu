@@ -1012,10 +1012,15 @@ static bool key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
             }
             u32* dA = c.ksdig.get<u32>((size_t)B * D * K * N);
             u32* mA = c.ksmac.get<u32>((size_t)B * 2 * L * K * N);
-            if (c.dec_tc && c.dec_ok && bits == 16)
-                launch_named(c, "k_decompose", k_decompose_tc, std::min<size_t>(blocks((size_t)B * N, 128), (size_t)c.n_sms * 4),
-                             128, 0, polys, stride, ginv, B, D, c.T, c.dec_B.ptr<uint4>(), dA, K);
-            else
+            if (c.dec_tc && c.dec_ok && bits == 16) {
+                const size_t gr = std::min<size_t>(blocks((size_t)B * N, 128), (size_t)c.n_sms * 4);
+                const uint4* Bd = c.dec_B.ptr<uint4>();
+                const u32 QW = c.T.QW;  // limb count of q: the kernel's multiword loops are sized for it
+                if (QW <= 4) launch_named(c, "k_decompose", k_decompose_tc<4>, gr, 128, 0, polys, stride, ginv, B, D, c.T, Bd, dA, K);
+                else if (QW <= 7) launch_named(c, "k_decompose", k_decompose_tc<7>, gr, 128, 0, polys, stride, ginv, B, D, c.T, Bd, dA, K);
+                else if (QW <= 10) launch_named(c, "k_decompose", k_decompose_tc<10>, gr, 128, 0, polys, stride, ginv, B, D, c.T, Bd, dA, K);
+                else launch_named(c, "k_decompose", k_decompose_tc<14>, gr, 128, 0, polys, stride, ginv, B, D, c.T, Bd, dA, K);
+            } else
                 launch_named(c, "k_decompose", k_decompose_t<true>, blocks((size_t)B * N, 256), 256, 0, polys, stride, ginv,
                              B, bits, D, c.T, (u64*)nullptr, dA, K);
             ntt32(c, dA, B * D * K, K, K, 0, false, 0);

@@ -640,6 +640,7 @@ __global__ void __launch_bounds__(128, 4) k_mac_to_chain_tc(const u32* __restric
 // The CUDA-core kernel issues ~4,700 instructions per coefficient at C5 (unrolled limb products,
 // instruction-cache misses).  Requires 4 QW + 7 < 64 (q below 448 bits).
 // ---------------------------------------------------------------------------------------
+template <int QWT>  // 32-bit limbs of q (T.QW <= QWT <= 14): the carry / subtract / compare loops stop there
 __global__ void __launch_bounds__(128, 4) k_decompose_tc(const u64* __restrict__ polys, size_t stride, u64 ginv, u32 B,
                                                         u32 D, DevTab T, const uint4* __restrict__ Bglob,
                                                         u32* __restrict__ aux_out, u32 K) {
@@ -647,6 +648,8 @@ __global__ void __launch_bounds__(128, 4) k_decompose_tc(const u64* __restrict__
     __shared__ __align__(128) uint4 Bs[NC * KB / 16];
     __shared__ __align__(8) unsigned long long mbar;
     __shared__ u32 tmem_base_sh;
+    constexpr int SW = QWT + 2;  // limbs of the column sums (sum_i y_i q/q_i < 2^61 q 2^3)
+    constexpr int NCU = (4 * SW + 15) / 16 * 16 < NC ? (4 * SW + 15) / 16 * 16 : NC;  // columns that can be non-zero
     __shared__ u32 sqw[kQW];
     const u32 tid = threadIdx.x, warp = tid >> 5;
     const u32 N = T.N, L = T.L, QW = T.QW, logN = T.logN;
@@ -744,10 +747,10 @@ __global__ void __launch_bounds__(128, 4) k_decompose_tc(const u64* __restrict__
         phase ^= 1u;
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         // column sums -> carried 32-bit limbs S (16 limbs from the 64 columns, the carry in limb 16)
-        u32 S[kQW + 2];
+        u32 S[SW];
         u64 carry = 0;
 #pragma unroll
-        for (int c0 = 0; c0 < NC; c0 += 16) {
+        for (int c0 = 0; c0 < NCU; c0 += 16) {
             u32 C[16];
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -759,22 +762,22 @@ __global__ void __launch_bounds__(128, 4) k_decompose_tc(const u64* __restrict__
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
             for (int l = 0; l < 4; ++l) {
-                const u64 s = carry + (u64)C[4 * l] + ((u64)C[4 * l + 1] << 8) + ((u64)C[4 * l + 2] << 16) +
-                              ((u64)C[4 * l + 3] << 24);
-                S[c0 / 4 + l] = (u32)s;
-                carry = s >> 32;
+                if (c0 / 4 + l < SW) {
+                    const u64 s = carry + (u64)C[4 * l] + ((u64)C[4 * l + 1] << 8) + ((u64)C[4 * l + 2] << 16) +
+                                  ((u64)C[4 * l + 3] << 24);
+                    S[c0 / 4 + l] = (u32)s;
+                    carry = s >> 32;
+                }
             }
         }
-        S[16] = (u32)carry;
-        S[17] = 0;
         // X = S - alpha q (alpha: the fractional estimate, short by at most one) and one correction
-        u32 X[kQW + 2];
+        u32 X[SW];
         {
             u64 c = 0;
             u32 bb = 0;
 #pragma unroll
-            for (int x = 0; x < kQW + 2; ++x) {
-                const u64 pk = (x < kQW ? (u64)alpha * sqw[x] : 0) + c;
+            for (int x = 0; x < SW; ++x) {
+                const u64 pk = (x < QWT ? (u64)alpha * sqw[x] : 0) + c;
                 c = pk >> 32;
                 const u32 pl = (u32)pk, sx = S[x];
                 const u32 r1 = sx - pl, b1 = sx < pl;
@@ -784,15 +787,15 @@ __global__ void __launch_bounds__(128, 4) k_decompose_tc(const u64* __restrict__
             }
             int ge = 1;
 #pragma unroll
-            for (int x = kQW + 1; x >= 0; --x) {
-                const u32 qv = x < kQW ? sqw[x] : 0u;
+            for (int x = SW - 1; x >= 0; --x) {
+                const u32 qv = x < QWT ? sqw[x] : 0u;
                 if (ge == 1 && X[x] != qv) ge = X[x] > qv ? 2 : 0;
             }
             if (ge != 0) {
                 u32 b2 = 0;
 #pragma unroll
-                for (int x = 0; x < kQW + 2; ++x) {
-                    const u32 qv = x < kQW ? sqw[x] : 0u;
+                for (int x = 0; x < SW; ++x) {
+                    const u32 qv = x < QWT ? sqw[x] : 0u;
                     const u32 r1 = X[x] - qv, c1 = X[x] < qv;
                     const u32 r2 = r1 - b2, c2 = r1 < b2;
                     X[x] = r2;
@@ -803,7 +806,7 @@ __global__ void __launch_bounds__(128, 4) k_decompose_tc(const u64* __restrict__
         if (live) {
             u32* o = aux_out + (size_t)b * D * K * N + n;
 #pragma unroll
-            for (int d = 0; d < 2 * kQW; ++d) {
+            for (int d = 0; d < 2 * QWT; ++d) {
                 if (d < (int)D) {
                     const u32 v = (X[d >> 1] >> (16 * (d & 1))) & 0xffffu;
                     for (u32 j = 0; j < K; ++j) o[((size_t)d * K + j) * N] = v;  // digits < 2^16 < a_j
