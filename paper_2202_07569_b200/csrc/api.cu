@@ -1217,7 +1217,10 @@ static void mac_to_chain(Ctx& c, const u32* X, u32 xs, u32 G, u64* out) {
     if (c.m2c_tc && c.m2c_kw) {
         const size_t grid = std::min<size_t>(blocks(items, 128), (size_t)c.n_sms * 4);
         const uint4* Bm = c.m2c_B.ptr<uint4>();
-        if (c.m2c_kw == 16) launch_named(c, "k_mac_to_chain", k_mac_to_chain_tc<16>, grid, 128, 0, X, xs, G, c.T, Bm, out);
+        if (c.m2c_kw == 16 && c.cp.L <= 6) {  // 48 D columns: 64 TMEM columns per CTA, 6 CTAs / SM
+            const size_t g6 = std::min<size_t>(blocks(items, 128), (size_t)c.n_sms * 6);
+            launch_named(c, "k_mac_to_chain", k_mac_to_chain_tc<16, 48>, g6, 128, 0, X, xs, G, c.T, Bm, out);
+        } else if (c.m2c_kw == 16) launch_named(c, "k_mac_to_chain", k_mac_to_chain_tc<16>, grid, 128, 0, X, xs, G, c.T, Bm, out);
         else launch_named(c, "k_mac_to_chain", k_mac_to_chain_tc<24>, grid, 128, 0, X, xs, G, c.T, Bm, out);
         return;
     }

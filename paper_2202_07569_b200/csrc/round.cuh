@@ -494,10 +494,13 @@ __global__ void __launch_bounds__(128, 4) k_lift_tc(const u64* __restrict__ src,
 // spends ~4,800 instructions per coefficient at C5 (Mm = 17, L = 8) on the same sums.
 // X layout [G][xs][N] (the first Mm planes of each group of xs); out layout [G][L][N].
 // ---------------------------------------------------------------------------------------
-template <int KW>  // A words per coefficient (Mm <= KW, KW a multiple of 8)
-__global__ void __launch_bounds__(128, 4) k_mac_to_chain_tc(const u32* __restrict__ X, u32 xs, u32 G, DevTab T,
+// NC = 48 (L <= 6) keeps A + D within a 64-column TMEM allocation: 6 CTAs per SM instead of 4 (the
+// kernel is bound by the per-tile latency chain).
+template <int KW, int NC = 64>  // A words per coefficient (Mm <= KW, KW a multiple of 8); D columns 8 L <= NC
+__global__ void __launch_bounds__(128, (KW + NC <= 64) ? 6 : 4) k_mac_to_chain_tc(const u32* __restrict__ X, u32 xs, u32 G, DevTab T,
                                                            const uint4* __restrict__ Bglob, u64* __restrict__ out) {
-    constexpr int K = 4 * KW, KSTEPS = K / 32, NC = 64;
+    constexpr int K = 4 * KW, KSTEPS = K / 32;
+    constexpr int TCOLS = (KW + NC <= 64) ? 64 : 128;  // TMEM allocation (power of two)
     __shared__ __align__(128) uint4 Bs[NC * K / 16];
     __shared__ __align__(8) unsigned long long mbar;
     __shared__ u32 tmem_base_sh;
@@ -520,7 +523,7 @@ __global__ void __launch_bounds__(128, 4) k_mac_to_chain_tc(const u32* __restric
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_sh)),
-                     "n"(128));
+                     "n"(TCOLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 0) {
@@ -594,7 +597,7 @@ __global__ void __launch_bounds__(128, 4) k_mac_to_chain_tc(const u32* __restric
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
         for (int i0 = 0; i0 < kMaxL; i0 += 2) {  // 2 chain primes (16 columns) per TMEM load
-            if (i0 >= (int)L) break;  // warp-uniform
+            if (i0 >= (int)L || 8 * i0 >= NC) break;  // warp-uniform
             u32 C[16];
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -626,7 +629,7 @@ __global__ void __launch_bounds__(128, 4) k_mac_to_chain_tc(const u32* __restric
     }
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(128));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tbase), "n"(TCOLS));
 }
 
 // ---------------------------------------------------------------------------------------
