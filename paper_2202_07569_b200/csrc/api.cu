@@ -98,6 +98,7 @@ struct Ctx {
     DevBuf dec_B;                     // k_decompose_tc B matrix (bytes of q / q_i by column)
     bool dec_ok = false;              // k_decompose_tc available (q below 448 bits)
     bool dec_tc = true;               // "dec_tc": tensor-core digit decomposition (0: k_decompose_t)
+    u32 ks_chunk_mb = 3072;           // "ks_chunk_mb": key-switch scratch bound (rows per key-switch launch)
     bool ks_fixed = true;             // "ks_fixed": compile-time-shape key-switch MAC (k_ks_mac32t) for the configured shapes
     bool m2c_tc = true;               // "m2c_tc": tensor-core MAC basis -> chain conversion (0: k_mac_to_chain)
     u32 rtc_nc = 0;                   // k_round_tma GEMM width (0: no instance for this JM / Mm)
@@ -1087,9 +1088,9 @@ static bool key_switch(Ctx& c, const u64* polys, size_t stride, u64 ginv, u32 B,
 }
 
 static size_t ks_chunk(const Ctx& c, u32 D) {
-    // bound the digit / digit-NTT scratch to ~1.5 GB
+    // bound the digit / digit-NTT scratch (3 GB by default: C5 96 rows per key-switch launch, 409 vs 417 ms per 4,096 rows at 1.5 GB; option "ks_chunk_mb")
     const size_t per = (size_t)D * (c.cp.L + 1) * c.cp.N * 8 + 2 * (size_t)c.cp.L * c.cp.N * 8;
-    return std::max<size_t>(1, (size_t(1536) << 20) / per);
+    return std::max<size_t>(1, (size_t(c.ks_chunk_mb) << 20) / per);
 }
 
 /// relinearize count 3-comp cts (stride 3LN) into out2 [count][2][L][N]; scale != 0 multiplies the
@@ -2856,6 +2857,7 @@ int cwg_set_option(cwg_ctx* h, const char* key, int64_t value) {
         else if (k == "lift_tc") c.lift_tc = v != 0;
         else if (k == "m2c_tc") c.m2c_tc = v != 0;
         else if (k == "ks_fixed") c.ks_fixed = v != 0;
+        else if (k == "ks_chunk_mb") c.ks_chunk_mb = (u32)std::max(64, v);
         else if (k == "dec_tc") c.dec_tc = v != 0;
         else if (k == "mac_sg") c.mac_sg = v != 0;
         else if (k == "mac_stages") c.mac_stages8 = v >= 8;
