@@ -196,7 +196,8 @@ int cwg_substitute(cwg_ctx* ctx, uint32_t count, const uint64_t* ct, uint64_t g,
  * "fuse_mac" (0: separate selection NTT + MAC kernels), "mac" (0: k_mac2 instead of the TMA
  * payload MAC for s >= 3), "round" (0: IMAD rounding instead of the tensor cores), "round_g2",
  * "round_ctas", "mac_waves", "mac_ck", "ntt_np", "prescale", "ks32" (0: 64-bit key switching),
- * "ks_wide", "ks_ci", "ks_fixed" (0: run-time-shape key-switch MAC / CRT kernels), "prep_factors",
+ * "ks_wide", "ks_ci", "ks_fixed" (0: run-time-shape key-switch MAC / CRT kernels), "ks_chunk_mb"
+ * (scratch bound of one key-switch launch, default 3072), "prep_factors",
  * "lift_tc", "m2c_tc", "dec_tc" (0: the centred lift / MAC-basis -> chain conversion / digit
  * decomposition on the CUDA cores instead of the tensor cores), "mac_rows" (0: per-slice-group
  * payload MAC instead of the whole-row persistent kernel for s = 3, 5, 15), "mac_item_rows" (rows
